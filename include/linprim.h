@@ -1,0 +1,189 @@
+/*
+ * include/linprim.h -- C-ABI of liblinprim.so, the B200 (sm_100a) implementation of
+ * LinPrim's differentiable tile rasterizer for transparent octahedra and tetrahedra
+ * (arXiv 2501.16312).  P:n = PAPER.md line n, S:n = SPEC.md line n.
+ *
+ * Conventions for every entry point
+ *   - extern "C", plain pointers and sizes; no C++ or torch types cross the ABI.
+ *   - Device pointers are CUDA device memory owned by the CALLER (PyTorch tensors in the
+ *     binding).  The library allocates no persistent memory and keeps no global mutable
+ *     state; a frame's scratch lives in a caller-provided workspace (lp_frame_init).
+ *   - Every call enqueues asynchronously on the given stream (cudaStream_t passed as void*;
+ *     NULL = legacy default stream).  Only lp_bin_sort with a non-NULL n_entries and
+ *     lp_frame_counters synchronise that stream.
+ *   - Arguments are validated BEFORE anything is enqueued; on LP_ERR_ARG nothing ran.
+ *     LP_ERR_CUDA reports a launch error (cudaGetLastError); asynchronous faults surface at
+ *     the caller's next synchronisation.
+ *   - Per-primitive bad data (non-finite features, |q| = 0, any distance <= 0) is not an
+ *     error: such primitives are culled, get zero gradient and are counted (#23).
+ *   - Gradients ACCUMULATE (+=) so views and calls sum; the caller zeroes them.
+ *   - Images are fp32, channel-major [3][H][W] per view (CHW).
+ */
+#ifndef LINPRIM_H
+#define LINPRIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LP_ABI_VERSION 1
+#define LP_TILE 16            /* 16 x 16 pixel tiles */
+
+typedef enum {
+  LP_OK = 0,
+  LP_ERR_ARG = 1,             /* null / inconsistent argument; nothing enqueued */
+  LP_ERR_CAPACITY = 2,        /* tile list longer than the frame's capacity (never truncate silently) */
+  LP_ERR_CUDA = 3,            /* CUDA launch / runtime error */
+  LP_ERR_UNSUPPORTED = 4      /* valid request this build does not implement */
+} lp_status;
+
+typedef enum { LP_OCTAHEDRON = 0, LP_TETRAHEDRON = 1 } lp_kind;
+
+/* Primitive features, device fp32, structure-of-arrays, component-major (N contiguous per
+ * component).  P:111-139: octahedron 11 floats (c, q, d_x d_y d_z, opacity), tetrahedron 12
+ * (c, q, d_0..d_3, opacity), plus (deg+1)^2 x 3 SH coefficients (48 at degree 3). */
+typedef struct {
+  int32_t kind;               /* lp_kind */
+  int32_t n;                  /* number of primitives, >= 0 */
+  int32_t sh_degree;          /* 0..3: storage AND evaluation degree */
+  const float *pos;           /* [3][n] world centre c */
+  const float *rot;           /* [4][n] quaternion (w,x,y,z), need not be unit (normalised inside) */
+  const float *dist;          /* [3][n] octa | [4][n] tetra, raw world distances > 0 (reading 2) */
+  const float *opacity;       /* [n] logit; alpha = sigmoid (reading 1) */
+  const float *sh;            /* [(deg+1)^2][3][n] SH coefficients, 3DGS basis order */
+  const float *filter3d;      /* [n] 3D smoothing filter size s (d -> sqrt(d^2+s^2)) or NULL */
+} lp_prims;
+
+/* Pinhole camera, host POD passed by value to the kernels.  x_cam = W x_world + t. */
+typedef struct {
+  float W[9];                 /* world->camera rotation, row-major */
+  float t[3];
+  float fx, fy, cx, cy;       /* pixels; pixel (x, y) has its centre at (x + 0.5, y + 0.5) (reading 12) */
+  float znear;                /* cull iff p_z <= znear (reading 5) */
+  int32_t width, height;      /* > 0 */
+} lp_camera;
+
+typedef struct {
+  float aa_kernel;            /* 2D anti-aliasing filter kernel kappa in pixels (0.1), 0 disables */
+  float t_stop;               /* stop once transmittance T < t_stop (1e-3), 0 disables */
+  float bg[3];                /* background colour (reading 14) */
+  int32_t count_stats;        /* 1: count iterated / intersected pairs into the frame counters */
+} lp_raster_cfg;
+
+/* Per-view scratch carved from one caller-allocated device workspace by lp_frame_init.
+ * All pointers are device pointers into that workspace; callers treat them as read-only
+ * results (the layout is the library's). */
+typedef struct {
+  int32_t kind, n, width, height, tiles_x, tiles_y;
+  int64_t capacity;           /* maximum tile-list entries */
+  int32_t record_words;       /* floats per raster record (20 octa, 24 tetra) */
+  int32_t rgrad_words;        /* floats per primitive in rgrad (20 octa, 22 tetra) */
+  uint32_t *tiles_touched;    /* [n] */
+  uint16_t *rect;             /* [n][4] tile rect tx0, ty0, tx1, ty1 (inclusive), zeros if none */
+  uint32_t *depth_key;        /* [n] float bits of l = |p| (0 if culled / invalid) */
+  float    *record;           /* [n][record_words] raster records */
+  uint32_t *prim_key, *prim_key_alt;     /* [n] depth-sort keys */
+  uint32_t *prim_order, *prim_order_alt; /* [n] depth-sorted primitive ids */
+  uint32_t *offsets;          /* [n + 1] exclusive scan of tiles_touched in depth order */
+  uint32_t *tile_key, *tile_key_alt;     /* [capacity] */
+  uint32_t *entry_val, *entry_val_alt;   /* [capacity] */
+  uint32_t *sorted_tile;      /* [E] after lp_bin_sort: tile of each entry, ascending (points into the above) */
+  uint32_t *sorted_val;       /* [E] after lp_bin_sort: primitive id of each entry */
+  uint32_t *ranges;           /* [tiles][2] [start, end) into the sorted list */
+  uint32_t *sort_hist;        /* radix-sort histogram scratch */
+  uint32_t *scan_tmp;         /* scan scratch */
+  uint32_t *counters;         /* [16] device counters, see LP_CNT_* */
+  float    *T_final;          /* [H][W] final transmittance */
+  uint32_t *n_proc;           /* [H][W] tile-list entries processed per pixel (from the tile's start) */
+  float    *rgrad;            /* [rgrad_words][n] raster-gradient scratch of the backward */
+  float    *canon;            /* [n][2 + 3K] canonical fp32 cr_x, cr_y, offsets (debug; NULL unless requested) */
+} lp_frame;
+
+enum {
+  LP_CNT_ENTRIES = 0,         /* E, tile-list length */
+  LP_CNT_OVERFLOW = 1,        /* 1 if E > capacity (entries beyond capacity were not written) */
+  LP_CNT_INVALID = 2,         /* primitives with invalid features */
+  LP_CNT_FRUSTUM = 3,         /* primitives with p_z > znear and valid features */
+  LP_CNT_VISIBLE = 4,         /* primitives with tiles_touched > 0 */
+  LP_CNT_ITERATED = 8,        /* words 8-9: u64 (pixel, entry) pairs evaluated by the forward (count_stats) */
+  LP_CNT_INTERSECTED = 10,    /* words 10-11: u64 pairs with chord > 0 (count_stats) */
+  LP_NUM_COUNTERS = 16
+};
+
+/* C5 helpers: per-parameter-group learning rates for the fused Adam. */
+typedef struct {
+  int64_t begin, end;         /* element range [begin, end) of the flat parameter buffer */
+  float lr;
+} lp_adam_group;
+
+/* Gradient sinks, device fp32, same layout as lp_prims; += semantics.  Any may be NULL. */
+typedef struct {
+  float *pos, *rot, *dist, *opacity, *sh;
+  float *mean2d_abs;          /* [n] += |dL/d c_ray.xy| per view (densification statistic) or NULL */
+} lp_grads;
+
+int32_t     lp_abi_version(void);
+const char *lp_status_string(lp_status s);
+
+/* Bytes of device workspace for one frame (256-byte aligned inside). */
+size_t lp_frame_bytes(int32_t kind, int32_t n, int32_t width, int32_t height, int64_t capacity,
+                      int32_t with_canon);
+
+/* Carve a frame out of `workspace` (device, >= lp_frame_bytes, 256-byte aligned). Host-only. */
+lp_status lp_frame_init(lp_frame *frame, void *workspace, size_t bytes, int32_t kind, int32_t n,
+                        int32_t width, int32_t height, int64_t capacity, int32_t with_canon);
+
+/* a1-a3: per primitive, for each view v:
+ * vertices from features, view transform, EWA ray space, 2D filter, bbox -> tile rect,
+ * depth key, raster record (slab / plane form), sigma (Eq. 1) and SH colour.
+ * Also resets the frame's counters.  frames[v].n must equal prims->n. */
+lp_status lp_preprocess(const lp_prims *prims, const lp_camera *cams, int32_t n_views,
+                        const lp_raster_cfg *cfg, lp_frame *frames, void *stream);
+
+/* a4-a7: depth sort of the primitives, exclusive scan of tiles_touched, emission
+ * of (tile, id) entries in depth order, stable radix sort by tile, per-tile ranges.
+ * n_entries: NULL -> fully asynchronous (overflow is flagged in LP_CNT_OVERFLOW and must be
+ * checked by the caller after synchronising); non-NULL [n_views] host array -> the stream is
+ * synchronised after the scan, E is written per view and LP_ERR_CAPACITY is returned (with
+ * nothing truncated and the sort not run) if any E exceeds its frame's capacity. */
+lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, int64_t *n_entries,
+                      void *stream);
+
+/* a8-a9: per-pixel chord through each primitive of the pixel's
+ * tile list (slab / Cyrus-Beck form of the ray-face intersection), opacity
+ * 1 - exp(-sigma chord), front-to-back compositing with include-then-stop at T < t_stop.
+ * image: device [n_views][3][H][W]; T_final / n_proc are kept in the frame for the backward. */
+lp_status lp_render_fwd(const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg,
+                        lp_frame *frames, float *image, void *stream);
+
+/* a10-a12 (App. E): reverse replay of each tile list, blend backward,
+ * chord -> entry/exit -> slab/plane moments reduced per (warp, primitive) -> rgrad, then the
+ * preprocess backward to world features (+= into grads).  Requires the frames filled by
+ * lp_preprocess / lp_bin_sort / lp_render_fwd with the same prims, cams and cfg.
+ * dL_dimage: device [n_views][3][H][W]. */
+lp_status lp_render_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_views,
+                        const lp_raster_cfg *cfg, lp_frame *frames, const float *dL_dimage,
+                        const lp_grads *grads, void *stream);
+
+/* Copy the frame's counters to host (synchronises the stream). */
+lp_status lp_frame_counters(const lp_frame *frame, uint32_t *host_counters /* [LP_NUM_COUNTERS] words */,
+                            void *stream);
+
+/* C5 (north_star): L1 loss gradient dL/dC = scale * sign(C - target) over n elements
+ * (written, not accumulated) and loss_sum[0] += scale * sum |C - target| (device float). */
+lp_status lp_l1_grad(const float *image, const float *target, float *dL_dimage, float *loss_sum,
+                     int64_t n, float scale, void *stream);
+
+/* C5: one fused Adam step over a flat fp32 parameter buffer with per-group learning
+ * rates; elements outside every group are left unchanged.  step >= 1 (bias correction). */
+lp_status lp_adam_step(float *param, const float *grad, float *m, float *v,
+                       const lp_adam_group *groups, int32_t n_groups, float beta1, float beta2,
+                       float eps, int32_t step, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LINPRIM_H */

@@ -1,0 +1,275 @@
+// lp_api.cu -- the C-ABI of liblinprim.so (include/linprim.h): argument validation, frame
+// workspace layout, and the per-view launch sequences of the four hot-path calls.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "../../include/linprim.h"
+#include "lp_kernels.h"
+
+namespace {
+
+using namespace lp;
+
+constexpr size_t ALIGN = 256;
+inline size_t up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
+
+inline int record_words(int kind) { return kind == LP_OCTAHEDRON ? 20 : 24; }
+inline int rgrad_words(int kind) { return kind == LP_OCTAHEDRON ? 20 : 22; }
+inline int offsets_k(int kind) { return kind == LP_OCTAHEDRON ? 3 : 4; }
+
+struct Layout {
+  size_t tiles_touched, rect, depth_key, record, prim_key, prim_key_alt, prim_order, prim_order_alt, offsets, tile_key,
+      tile_key_alt, entry_val, entry_val_alt, ranges, sort_hist, scan_tmp, counters, T_final, n_proc, rgrad, canon,
+      total;
+};
+
+Layout layout(int kind, int64_t n, int w, int h, int64_t cap, int canon) {
+  Layout L;
+  const int64_t tiles = (int64_t)((w + LP_TILE - 1) / LP_TILE) * ((h + LP_TILE - 1) / LP_TILE);
+  const int64_t hw = (int64_t)w * h;
+  const int64_t nn = n > 0 ? n : 1, cc = cap > 0 ? cap : 1;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { const size_t at = o; o += up(bytes); return at; };
+  L.tiles_touched = take(4 * nn);
+  L.rect = take(8 * nn);
+  L.depth_key = take(4 * nn);
+  L.record = take(4 * (size_t)record_words(kind) * nn);
+  L.prim_key = take(4 * nn);
+  L.prim_key_alt = take(4 * nn);
+  L.prim_order = take(4 * nn);
+  L.prim_order_alt = take(4 * nn);
+  L.offsets = take(4 * (nn + 1));
+  L.tile_key = take(4 * cc);
+  L.tile_key_alt = take(4 * cc);
+  L.entry_val = take(4 * cc);
+  L.entry_val_alt = take(4 * cc);
+  L.ranges = take(8 * tiles);
+  L.sort_hist = take(4 * radix_hist_words(nn > cc ? nn : cc));
+  L.scan_tmp = take(4 * scan_tmp_words(nn));
+  L.counters = take(4 * LP_NUM_COUNTERS);
+  L.T_final = take(4 * hw);
+  L.n_proc = take(4 * hw);
+  L.rgrad = take(4 * (size_t)rgrad_words(kind) * nn);
+  L.canon = canon ? take(4 * (size_t)(2 + 3 * offsets_k(kind)) * nn) : 0;
+  L.total = o;
+  return L;
+}
+
+bool valid_kind(int k) { return k == LP_OCTAHEDRON || k == LP_TETRAHEDRON; }
+
+bool valid_cam(const lp_camera &c) {
+  return c.width > 0 && c.height > 0 && c.width <= 65535 * LP_TILE && c.height <= 65535 * LP_TILE &&
+         c.fx > 0.f && c.fy > 0.f;
+}
+
+bool frame_matches(const lp_frame &F, const lp_camera &c) {
+  return F.counters && F.width == c.width && F.height == c.height;
+}
+
+lp_status check_prims(const lp_prims *P) {
+  if (!P || !valid_kind(P->kind) || P->n < 0 || P->sh_degree < 0 || P->sh_degree > 3) return LP_ERR_ARG;
+  if (P->n > 0 && (!P->pos || !P->rot || !P->dist || !P->opacity || !P->sh)) return LP_ERR_ARG;
+  return LP_OK;
+}
+
+lp_status last_error() { return cudaGetLastError() == cudaSuccess ? LP_OK : LP_ERR_CUDA; }
+
+int bits_for(int64_t v) {   // bits needed to represent values in [0, v)
+  int b = 1;
+  while ((int64_t(1) << b) < v) ++b;
+  return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t lp_abi_version(void) { return LP_ABI_VERSION; }
+
+const char *lp_status_string(lp_status s) {
+  switch (s) {
+    case LP_OK: return "ok";
+    case LP_ERR_ARG: return "invalid argument";
+    case LP_ERR_CAPACITY: return "tile list exceeds frame capacity";
+    case LP_ERR_CUDA: return "CUDA error";
+    case LP_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+size_t lp_frame_bytes(int32_t kind, int32_t n, int32_t width, int32_t height, int64_t capacity, int32_t with_canon) {
+  if (!valid_kind(kind) || n < 0 || width <= 0 || height <= 0 || capacity < 0) return 0;
+  return layout(kind, n, width, height, capacity, with_canon).total;
+}
+
+lp_status lp_frame_init(lp_frame *F, void *workspace, size_t bytes, int32_t kind, int32_t n, int32_t width,
+                        int32_t height, int64_t capacity, int32_t with_canon) {
+  if (!F || !workspace || !valid_kind(kind) || n < 0 || width <= 0 || height <= 0 || capacity < 0) return LP_ERR_ARG;
+  if ((reinterpret_cast<uintptr_t>(workspace) & (ALIGN - 1)) != 0) return LP_ERR_ARG;
+  if (capacity > (int64_t)0xFFFFFFF0u) return LP_ERR_ARG;   // entries are indexed with u32
+  const Layout L = layout(kind, n, width, height, capacity, with_canon);
+  if (bytes < L.total) return LP_ERR_ARG;
+  char *b = static_cast<char *>(workspace);
+  memset(F, 0, sizeof(*F));
+  F->kind = kind;
+  F->n = n;
+  F->width = width;
+  F->height = height;
+  F->tiles_x = (width + LP_TILE - 1) / LP_TILE;
+  F->tiles_y = (height + LP_TILE - 1) / LP_TILE;
+  F->capacity = capacity;
+  F->record_words = record_words(kind);
+  F->rgrad_words = rgrad_words(kind);
+  F->tiles_touched = reinterpret_cast<uint32_t *>(b + L.tiles_touched);
+  F->rect = reinterpret_cast<uint16_t *>(b + L.rect);
+  F->depth_key = reinterpret_cast<uint32_t *>(b + L.depth_key);
+  F->record = reinterpret_cast<float *>(b + L.record);
+  F->prim_key = reinterpret_cast<uint32_t *>(b + L.prim_key);
+  F->prim_key_alt = reinterpret_cast<uint32_t *>(b + L.prim_key_alt);
+  F->prim_order = reinterpret_cast<uint32_t *>(b + L.prim_order);
+  F->prim_order_alt = reinterpret_cast<uint32_t *>(b + L.prim_order_alt);
+  F->offsets = reinterpret_cast<uint32_t *>(b + L.offsets);
+  F->tile_key = reinterpret_cast<uint32_t *>(b + L.tile_key);
+  F->tile_key_alt = reinterpret_cast<uint32_t *>(b + L.tile_key_alt);
+  F->entry_val = reinterpret_cast<uint32_t *>(b + L.entry_val);
+  F->entry_val_alt = reinterpret_cast<uint32_t *>(b + L.entry_val_alt);
+  F->sorted_tile = nullptr;
+  F->sorted_val = nullptr;
+  F->ranges = reinterpret_cast<uint32_t *>(b + L.ranges);
+  F->sort_hist = reinterpret_cast<uint32_t *>(b + L.sort_hist);
+  F->scan_tmp = reinterpret_cast<uint32_t *>(b + L.scan_tmp);
+  F->counters = reinterpret_cast<uint32_t *>(b + L.counters);
+  F->T_final = reinterpret_cast<float *>(b + L.T_final);
+  F->n_proc = reinterpret_cast<uint32_t *>(b + L.n_proc);
+  F->rgrad = reinterpret_cast<float *>(b + L.rgrad);
+  F->canon = with_canon ? reinterpret_cast<float *>(b + L.canon) : nullptr;
+  return LP_OK;
+}
+
+lp_status lp_preprocess(const lp_prims *prims, const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg,
+                        lp_frame *frames, void *stream) {
+  if (check_prims(prims) != LP_OK || !cams || !cfg || !frames || n_views < 0) return LP_ERR_ARG;
+  if (!(cfg->aa_kernel >= 0.f)) return LP_ERR_ARG;
+  for (int v = 0; v < n_views; ++v) {
+    if (!valid_cam(cams[v]) || !frame_matches(frames[v], cams[v])) return LP_ERR_ARG;
+    if (frames[v].kind != prims->kind || frames[v].n != prims->n) return LP_ERR_ARG;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int v = 0; v < n_views; ++v) {
+    lp_frame &F = frames[v];
+    F.sorted_tile = F.sorted_val = nullptr;
+    cudaMemsetAsync(F.counters, 0, 4 * LP_NUM_COUNTERS, st);
+    launch_preprocess(*prims, cams[v], cfg->aa_kernel, F, st);
+  }
+  return last_error();
+}
+
+lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, int64_t *n_entries, void *stream) {
+  if (!cams || !frames || n_views < 0) return LP_ERR_ARG;
+  for (int v = 0; v < n_views; ++v)
+    if (!valid_cam(cams[v]) || !frame_matches(frames[v], cams[v])) return LP_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  lp_status status = LP_OK;
+  for (int v = 0; v < n_views; ++v) {
+    lp_frame &F = frames[v];
+    const int n = F.n;
+    // 1. depth sort of the primitives (stable: ties keep ascending id, reading 11)
+    const int flip = radix_sort_pairs(F.prim_key, F.prim_key_alt, F.prim_order, F.prim_order_alt, n, nullptr, 32,
+                                      F.sort_hist, st);
+    lp_frame Fv = F;
+    if (flip) {
+      Fv.prim_key = F.prim_key_alt;
+      Fv.prim_order = F.prim_order_alt;
+    }
+    // 2. exclusive scan of tiles_touched in depth order -> offsets, E
+    launch_scan_tiles(Fv, n, st);
+    int64_t E_host = -1;
+    if (n_entries) {
+      uint32_t e32 = 0;
+      cudaMemcpyAsync(&e32, F.counters + LP_CNT_ENTRIES, 4, cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) return LP_ERR_CUDA;
+      E_host = e32;
+      n_entries[v] = E_host;
+      if (E_host > F.capacity) {
+        status = LP_ERR_CAPACITY;
+        continue;
+      }
+    }
+    // 3. emission in depth order
+    launch_emit(Fv, n, st);
+    // 4. stable sort by tile id
+    const int tiles = F.tiles_x * F.tiles_y;
+    const int64_t nmax = E_host >= 0 ? E_host : F.capacity;
+    const uint32_t *ndev = E_host >= 0 ? nullptr : F.counters + LP_CNT_ENTRIES;
+    const int tflip = radix_sort_pairs(F.tile_key, F.tile_key_alt, F.entry_val, F.entry_val_alt, nmax, ndev,
+                                       bits_for(tiles), F.sort_hist, st);
+    F.sorted_tile = tflip ? F.tile_key_alt : F.tile_key;
+    F.sorted_val = tflip ? F.entry_val_alt : F.entry_val;
+    // 5. ranges
+    lp_frame Fr = F;
+    if (E_host >= 0) Fr.capacity = E_host;
+    launch_ranges(Fr, F.sorted_tile, tiles, st);
+  }
+  const lp_status e = last_error();
+  return status != LP_OK ? status : e;
+}
+
+lp_status lp_render_fwd(const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg, lp_frame *frames,
+                        float *image, void *stream) {
+  if (!cams || !cfg || !frames || !image || n_views < 0) return LP_ERR_ARG;
+  for (int v = 0; v < n_views; ++v)
+    if (!valid_cam(cams[v]) || !frame_matches(frames[v], cams[v]) || !frames[v].sorted_val) return LP_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  size_t off = 0;
+  for (int v = 0; v < n_views; ++v) {
+    launch_raster_fwd(frames[v], *cfg, image + off, st);
+    off += (size_t)3 * cams[v].width * cams[v].height;
+  }
+  return last_error();
+}
+
+lp_status lp_render_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg,
+                        lp_frame *frames, const float *dL_dimage, const lp_grads *grads, void *stream) {
+  if (check_prims(prims) != LP_OK || !cams || !cfg || !frames || !dL_dimage || !grads || n_views < 0) return LP_ERR_ARG;
+  for (int v = 0; v < n_views; ++v) {
+    if (!valid_cam(cams[v]) || !frame_matches(frames[v], cams[v]) || !frames[v].sorted_val) return LP_ERR_ARG;
+    if (frames[v].kind != prims->kind || frames[v].n != prims->n) return LP_ERR_ARG;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  size_t off = 0;
+  for (int v = 0; v < n_views; ++v) {
+    const lp_frame &F = frames[v];
+    cudaMemsetAsync(F.rgrad, 0, 4 * (size_t)F.rgrad_words * (F.n > 0 ? F.n : 1), st);
+    launch_raster_bwd(F, *cfg, dL_dimage + off, st);
+    launch_preprocess_bwd(*prims, cams[v], cfg->aa_kernel, F, *grads, st);
+    off += (size_t)3 * cams[v].width * cams[v].height;
+  }
+  return last_error();
+}
+
+lp_status lp_frame_counters(const lp_frame *F, uint32_t *host, void *stream) {
+  if (!F || !F->counters || !host) return LP_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(host, F->counters, 4 * LP_NUM_COUNTERS, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return LP_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? LP_OK : LP_ERR_CUDA;
+}
+
+lp_status lp_l1_grad(const float *image, const float *target, float *dL_dimage, float *loss_sum, int64_t n,
+                     float scale, void *stream) {
+  if (!image || !target || !dL_dimage || !loss_sum || n < 0) return LP_ERR_ARG;
+  launch_l1_grad(image, target, dL_dimage, loss_sum, n, scale, static_cast<cudaStream_t>(stream));
+  return last_error();
+}
+
+lp_status lp_adam_step(float *param, const float *grad, float *m, float *v, const lp_adam_group *groups,
+                       int32_t n_groups, float beta1, float beta2, float eps, int32_t step, void *stream) {
+  if (!param || !grad || !m || !v || (n_groups > 0 && !groups) || n_groups < 0 || step < 1) return LP_ERR_ARG;
+  for (int g = 0; g < n_groups; ++g)
+    if (groups[g].begin < 0 || groups[g].end < groups[g].begin) return LP_ERR_ARG;
+  launch_adam(param, grad, m, v, groups, n_groups, beta1, beta2, eps, step, static_cast<cudaStream_t>(stream));
+  return last_error();
+}
+
+}  // extern "C"

@@ -1,0 +1,373 @@
+// lp_device.cuh -- device-side building blocks shared by the liblinprim kernels (sm_100a).
+//
+//   * canonical_geometry<KIND>: the integer-producing preprocess geometry in the canonical fp32
+//     op order of DESIGN.md §3 (one __f*_rn intrinsic per operation: no FMA contraction).
+//   * build_record<KIND>: the raster record (slab form for octahedra, plane form for
+//     tetrahedra) computed in fp64 from the canonical offsets, stored fp32.
+//   * chord<KIND>: per-pixel entry/exit/chord from a record; the SAME function (bitwise) is used
+//     by the forward and the backward raster so transmittance recovery is exact.
+//
+// P:n = PAPER.md line n.  This header is product code: it shares nothing with
+// oracle/ (the CPU oracle implements the same paper independently).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/linprim.h"
+
+namespace lp {
+
+constexpr int OCTA = LP_OCTAHEDRON;
+constexpr int TETRA = LP_TETRAHEDRON;
+
+template <int KIND> struct Kind;
+template <> struct Kind<LP_OCTAHEDRON> {
+  static constexpr int K = 3;          // offset vectors (vertices are c +- o_j)
+  static constexpr int RW = 20;        // record words: cx cy (b g h)x4 sigma rgb pad2
+  static constexpr int RG = 20;        // raster-gradient words: (Mb Mg Mc Mh)x4 dsigma drgb
+};
+template <> struct Kind<LP_TETRAHEDRON> {
+  static constexpr int K = 4;          // vertices c + o_k
+  static constexpr int RW = 24;        // cx cy (A B C)x6 slots sigma rgb
+  static constexpr int RG = 22;        // (MA MB MC)x6 slots dsigma drgb
+};
+
+// record word offsets
+constexpr int REC_OCTA_SIGMA = 14, REC_OCTA_RGB = 15;
+constexpr int REC_TETRA_SIGMA = 20, REC_TETRA_RGB = 21;
+
+__device__ __forceinline__ float fm(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fa(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fs(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fdv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float fq(float a) { return __fsqrt_rn(a); }
+
+// fp32(1/sqrt(3)) = 0x3F13CD3A (tetrahedron basis b_k = (+-1,+-1,+-1)/sqrt(3))
+__device__ __forceinline__ float tetra_k() { return __uint_as_float(0x3F13CD3Au); }
+
+struct Geom {
+  int flag;                  // 0 in frustum, 1 invalid input, 2 culled by znear
+  float crx, cry, l;         // ray-space centre (l = |p|, the depth key source)
+  float off[4][3];           // post-filter ray-space offsets
+  uint32_t tiles;            // tiles_touched
+  int rect[4];               // tx0 ty0 tx1 ty1
+};
+
+// Canonical fp32 geometry.  Also returns the fp32 inputs used downstream.
+template <int KIND>
+__device__ __forceinline__ void canonical_geometry(const lp_prims &P, int i, const lp_camera &cam, float kappa,
+                                                   Geom &g, float dh[4], float q_out[4], float c_out[3]) {
+  constexpr int K = Kind<KIND>::K;
+  const int n = P.n;
+  g.flag = 0;
+  g.tiles = 0;
+  g.rect[0] = g.rect[1] = g.rect[2] = g.rect[3] = 0;
+  g.crx = g.cry = g.l = 0.f;
+  float c[3], q[4], d[4], op = P.opacity[i];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) c[a] = P.pos[a * n + i];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) q[a] = P.rot[a * n + i];
+#pragma unroll
+  for (int a = 0; a < K; ++a) d[a] = P.dist[a * n + i];
+  bool fin = isfinite(c[0]) && isfinite(c[1]) && isfinite(c[2]) && isfinite(q[0]) && isfinite(q[1]) &&
+             isfinite(q[2]) && isfinite(q[3]) && isfinite(op);
+  bool pos_d = true;
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    fin = fin && isfinite(d[a]);
+    pos_d = pos_d && (d[a] > 0.f);
+  }
+  float f3 = 0.f;
+  if (P.filter3d) {
+    f3 = P.filter3d[i];
+    fin = fin && isfinite(f3);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) c_out[a] = c[a];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) q_out[a] = q[a];
+  if (!fin || !pos_d) { g.flag = 1; return; }
+#pragma unroll
+  for (int a = 0; a < K; ++a) dh[a] = P.filter3d ? fq(fa(fm(d[a], d[a]), fm(f3, f3))) : d[a];
+
+  // quaternion -> R (3DGS w-first formula), canonical order
+  const float n2 = fa(fa(fa(fm(q[0], q[0]), fm(q[1], q[1])), fm(q[2], q[2])), fm(q[3], q[3]));
+  if (n2 == 0.f) { g.flag = 1; return; }
+  const float nq = fq(n2);
+  const float w = fdv(q[0], nq), x = fdv(q[1], nq), y = fdv(q[2], nq), z = fdv(q[3], nq);
+  const float xx = fm(x, x), yy = fm(y, y), zz = fm(z, z);
+  const float xy = fm(x, y), xz = fm(x, z), yz = fm(y, z), wx = fm(w, x), wy = fm(w, y), wz = fm(w, z);
+  float R[3][3];
+  R[0][0] = fs(1.f, fm(2.f, fa(yy, zz)));
+  R[0][1] = fm(2.f, fs(xy, wz));
+  R[0][2] = fm(2.f, fa(xz, wy));
+  R[1][0] = fm(2.f, fa(xy, wz));
+  R[1][1] = fs(1.f, fm(2.f, fa(xx, zz)));
+  R[1][2] = fm(2.f, fs(yz, wx));
+  R[2][0] = fm(2.f, fs(xz, wy));
+  R[2][1] = fm(2.f, fa(yz, wx));
+  R[2][2] = fs(1.f, fm(2.f, fa(xx, yy)));
+
+  // view transform
+  float p[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    p[r] = fa(fa(fa(fm(cam.W[3 * r + 0], c[0]), fm(cam.W[3 * r + 1], c[1])), fm(cam.W[3 * r + 2], c[2])), cam.t[r]);
+  if (!(p[2] > cam.znear)) { g.flag = 2; return; }
+
+  // EWA ray space
+  const float l = fq(fa(fa(fm(p[0], p[0]), fm(p[1], p[1])), fm(p[2], p[2])));
+  g.l = l;
+  g.crx = fa(fm(cam.fx, fdv(p[0], p[2])), cam.cx);
+  g.cry = fa(fm(cam.fy, fdv(p[1], p[2])), cam.cy);
+  const float pz2 = fm(p[2], p[2]);
+  const float J00 = fdv(cam.fx, p[2]);
+  const float J02 = -fdv(fm(cam.fx, p[0]), pz2);
+  const float J11 = fdv(cam.fy, p[2]);
+  const float J12 = -fdv(fm(cam.fy, p[1]), pz2);
+  const float J20 = fdv(p[0], l), J21 = fdv(p[1], l), J22 = fdv(p[2], l);
+
+  // world offsets -> camera -> ray space
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    float ow[3];
+    if (KIND == OCTA) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r) ow[r] = fm(dh[j], R[r][j]);
+    } else {
+      const float k = tetra_k();
+      const float b0 = (j == 0 || j == 1) ? k : -k;
+      const float b1 = (j == 0 || j == 2) ? k : -k;
+      const float b2 = (j == 0 || j == 3) ? k : -k;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) ow[r] = fm(dh[j], fa(fa(fm(R[r][0], b0), fm(R[r][1], b1)), fm(R[r][2], b2)));
+    }
+    float oc[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+      oc[r] = fa(fa(fm(cam.W[3 * r + 0], ow[0]), fm(cam.W[3 * r + 1], ow[1])), fm(cam.W[3 * r + 2], ow[2]));
+    g.off[j][0] = fa(fm(J00, oc[0]), fm(J02, oc[2]));
+    g.off[j][1] = fa(fm(J11, oc[1]), fm(J12, oc[2]));
+    g.off[j][2] = fa(fa(fm(J20, oc[0]), fm(J21, oc[1])), fm(J22, oc[2]));
+  }
+
+  // 2D anti-aliasing filter (readings 19-20)
+  const float h = fm(0.5f, kappa);
+#pragma unroll
+  for (int ax = 0; ax < 2; ++ax) {
+    if (KIND == OCTA) {
+      int jm = 0;
+#pragma unroll
+      for (int j = 1; j < 3; ++j)
+        if (fabsf(g.off[j][ax]) > fabsf(g.off[jm][ax])) jm = j;
+      const float v = g.off[jm][ax];
+      const float nv = fa(v, v >= 0.f ? h : -h);
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (j == jm) g.off[j][ax] = nv;
+    } else {
+      int kmin = 0, kmax = 0;
+#pragma unroll
+      for (int k = 1; k < 4; ++k) {
+        if (g.off[k][ax] < g.off[kmin][ax]) kmin = k;
+        if (g.off[k][ax] > g.off[kmax][ax]) kmax = k;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k == kmin) g.off[k][ax] = fs(g.off[k][ax], h);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k == kmax) g.off[k][ax] = fa(g.off[k][ax], h);
+    }
+  }
+
+  // bbox -> pixel rect -> tile rect
+  const int dims[2] = {cam.width, cam.height};
+  const float cr[2] = {g.crx, g.cry};
+  int pmin[2], pmax[2];
+#pragma unroll
+  for (int ax = 0; ax < 2; ++ax) {
+    float lo, hi;
+    if (KIND == OCTA) {
+      float m = fabsf(g.off[0][ax]);
+#pragma unroll
+      for (int j = 1; j < 3; ++j) m = fabsf(g.off[j][ax]) > m ? fabsf(g.off[j][ax]) : m;
+      lo = fs(cr[ax], m);
+      hi = fa(cr[ax], m);
+    } else {
+      float mn = g.off[0][ax], mx = g.off[0][ax];
+#pragma unroll
+      for (int k = 1; k < 4; ++k) {
+        mn = g.off[k][ax] < mn ? g.off[k][ax] : mn;
+        mx = g.off[k][ax] > mx ? g.off[k][ax] : mx;
+      }
+      lo = fa(cr[ax], mn);
+      hi = fa(cr[ax], mx);
+    }
+    float a = fs(lo, 0.5f), b = fs(hi, 0.5f);
+    const float top = (float)(dims[ax] + 2);
+    a = a < -2.f ? -2.f : (a > top ? top : a);
+    b = b < -2.f ? -2.f : (b > top ? top : b);
+    const int i0 = (int)ceilf(a), i1 = (int)floorf(b);
+    pmin[ax] = i0 < 0 ? 0 : i0;
+    pmax[ax] = i1 > dims[ax] - 1 ? dims[ax] - 1 : i1;
+  }
+  if (pmin[0] > pmax[0] || pmin[1] > pmax[1]) return;
+  g.rect[0] = pmin[0] >> 4;
+  g.rect[1] = pmin[1] >> 4;
+  g.rect[2] = pmax[0] >> 4;
+  g.rect[3] = pmax[1] >> 4;
+  g.tiles = (uint32_t)((g.rect[2] - g.rect[0] + 1) * (g.rect[3] - g.rect[1] + 1));
+}
+
+// ---------------------------------------------------------------------------------------------
+// raster records
+// ---------------------------------------------------------------------------------------------
+// Octahedron = {c + M lam : |lam|_1 <= 1}, M = [o0 o1 o2] (post-filter ray-space offsets).
+// |lam|_1 <= 1  <=>  |s . G (x - c)| <= 1 for the 4 sign vectors s (up to sign), G = M^-1.
+// For the vertical pixel ray x = (r, c_z + t):  t in [L_s - h_s, L_s + h_s] with
+// L_s = b_s dx + g_s dy,  b = -row.x/row.z,  g = -row.y/row.z,  h = 1/|row.z|,  row = s^T G.
+// entry = max_s (L_s - h_s), exit = min_s (L_s + h_s)   (equals MTIA's i2 - i1).
+__device__ __constant__ static const signed char kSlabSign[4][3] = {{1, 1, 1}, {1, 1, -1}, {1, -1, 1}, {-1, 1, 1}};
+
+// Tetrahedron faces, outward for the S:102 basis (DESIGN.md conventions).
+__device__ __constant__ static const unsigned char kTetraFace[4][3] = {{1, 3, 2}, {0, 2, 3}, {0, 3, 1}, {0, 1, 2}};
+
+__device__ __forceinline__ void inverse3(const double M[3][3], double G[3][3], double &det) {
+  const double a00 = M[1][1] * M[2][2] - M[1][2] * M[2][1];
+  const double a01 = M[0][2] * M[2][1] - M[0][1] * M[2][2];
+  const double a02 = M[0][1] * M[1][2] - M[0][2] * M[1][1];
+  const double a10 = M[1][2] * M[2][0] - M[1][0] * M[2][2];
+  const double a11 = M[0][0] * M[2][2] - M[0][2] * M[2][0];
+  const double a12 = M[0][2] * M[1][0] - M[0][0] * M[1][2];
+  const double a20 = M[1][0] * M[2][1] - M[1][1] * M[2][0];
+  const double a21 = M[0][1] * M[2][0] - M[0][0] * M[2][1];
+  const double a22 = M[0][0] * M[1][1] - M[0][1] * M[1][0];
+  det = M[0][0] * a00 + M[0][1] * a10 + M[0][2] * a20;
+  const double id = 1.0 / det;
+  G[0][0] = a00 * id; G[0][1] = a01 * id; G[0][2] = a02 * id;
+  G[1][0] = a10 * id; G[1][1] = a11 * id; G[1][2] = a12 * id;
+  G[2][0] = a20 * id; G[2][1] = a21 * id; G[2][2] = a22 * id;
+}
+
+// clamp a near-zero depth coefficient away from 0 (vertical face / slab seen edge-on): the
+// slab/plane then acts as the lateral constraint in the limit
+__device__ __forceinline__ double clamp_away(double qz, double lateral) {
+  const double lim = 1e-25 * lateral + 1e-300;
+  if (fabs(qz) < lim) return qz < 0.0 ? -lim : lim;
+  return qz;
+}
+
+struct SlabRows {     // octahedron: rows r_s = s^T G (fp64) and the clamped row.z
+  double r[4][3];
+  bool ok;
+};
+
+__device__ __forceinline__ void octa_slabs(const float off[4][3], SlabRows &S) {
+  double M[3][3], G[3][3], det;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) M[a][j] = (double)off[j][a];   // columns are the offsets
+  inverse3(M, G, det);
+  S.ok = isfinite(det) && det != 0.0;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      S.r[s][c] = kSlabSign[s][0] * G[0][c] + kSlabSign[s][1] * G[1][c] + kSlabSign[s][2] * G[2][c];
+    S.r[s][2] = clamp_away(S.r[s][2], fmax(fabs(S.r[s][0]), fabs(S.r[s][1])));
+  }
+}
+
+struct TetraPlanes {  // plane of each face: z = A + B dx + C dy relative to the centre
+  double n[4][3];     // face normals (outward, n.z clamped away from 0)
+  double A[4], B[4], C[4];
+  int slot_face[6];   // slots 0..2 front (entry), 3..5 back (exit)
+  bool ok;
+};
+
+__device__ __forceinline__ void tetra_planes(const float off[4][3], TetraPlanes &T) {
+  double v[4][3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) v[k][a] = (double)off[k][a];
+  int nf = 0, nb = 0, fr[4], bk[4];
+  T.ok = true;
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const double *pa = v[kTetraFace[f][0]], *pb = v[kTetraFace[f][1]], *pc = v[kTetraFace[f][2]];
+    const double e1[3] = {pb[0] - pa[0], pb[1] - pa[1], pb[2] - pa[2]};
+    const double e2[3] = {pc[0] - pa[0], pc[1] - pa[1], pc[2] - pa[2]};
+    double nx = e1[1] * e2[2] - e1[2] * e2[1];
+    double ny = e1[2] * e2[0] - e1[0] * e2[2];
+    double nz = e1[0] * e2[1] - e1[1] * e2[0];
+    if (nx == 0.0 && ny == 0.0 && nz == 0.0) T.ok = false;
+    nz = clamp_away(nz, fmax(fabs(nx), fabs(ny)));
+    T.n[f][0] = nx; T.n[f][1] = ny; T.n[f][2] = nz;
+    T.B[f] = -nx / nz;
+    T.C[f] = -ny / nz;
+    T.A[f] = pa[2] - T.B[f] * pa[0] - T.C[f] * pa[1];
+    if (nz < 0.0) fr[nf++] = f; else bk[nb++] = f;   // outward normal towards the camera = entry face
+  }
+  if (nf == 0 || nb == 0) { T.ok = false; nf = nf ? nf : 1; nb = nb ? nb : 1; fr[0] = fr[0]; }
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    T.slot_face[s] = (nf > 0) ? fr[s < nf ? s : nf - 1] : 0;
+    T.slot_face[3 + s] = (nb > 0) ? bk[s < nb ? s : nb - 1] : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// chord evaluation (a8).  TRACK: also return the entry / exit slab (octa) or slot (tetra).
+// ---------------------------------------------------------------------------------------------
+template <bool TRACK>
+__device__ __forceinline__ float octa_chord(const float *rec, float px, float py, int &se, int &sx) {
+  const float dx = fs(px, rec[0]), dy = fs(py, rec[1]);
+  float L = __fmaf_rn(rec[2], dx, fm(rec[3], dy));
+  float en = fs(L, rec[4]), ex = fa(L, rec[4]);
+  if (TRACK) { se = 0; sx = 0; }
+#pragma unroll
+  for (int s = 1; s < 4; ++s) {
+    L = __fmaf_rn(rec[2 + 3 * s], dx, fm(rec[3 + 3 * s], dy));
+    const float a = fs(L, rec[4 + 3 * s]), b = fa(L, rec[4 + 3 * s]);
+    if (TRACK) {
+      if (a > en) se = s;
+      if (b < ex) sx = s;
+    }
+    en = fmaxf(en, a);
+    ex = fminf(ex, b);
+  }
+  return fs(ex, en);
+}
+
+template <bool TRACK>
+__device__ __forceinline__ float tetra_chord(const float *rec, float px, float py, int &se, int &sx) {
+  const float dx = fs(px, rec[0]), dy = fs(py, rec[1]);
+  float z[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) z[s] = __fmaf_rn(rec[4 + 3 * s], dy, __fmaf_rn(rec[3 + 3 * s], dx, rec[2 + 3 * s]));
+  float en = z[0], ex = z[3];
+  if (TRACK) { se = 0; sx = 3; }
+#pragma unroll
+  for (int s = 1; s < 3; ++s) {
+    if (TRACK) {
+      if (z[s] > en) se = s;
+      if (z[3 + s] < ex) sx = 3 + s;
+    }
+    en = fmaxf(en, z[s]);
+    ex = fminf(ex, z[3 + s]);
+  }
+  return fs(ex, en);
+}
+
+// opacity transmittance factor E = exp(-sigma chord); identical in forward and backward.
+// sigma*chord is capped at 80 so E stays a normal fp32 (>= 1.8e-35) and the backward can divide
+// by it; the cap changes o by < 1e-34.
+__device__ __forceinline__ float transmit(float sigma, float chord) {
+  return __expf(-fminf(fm(sigma, chord), 80.f));
+}
+
+}  // namespace lp

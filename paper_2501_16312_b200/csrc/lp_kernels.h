@@ -1,0 +1,40 @@
+// lp_kernels.h -- internal launch wrappers (host side) of liblinprim; not part of the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/linprim.h"
+
+namespace lp {
+
+// K1 / K5 (lp_preprocess.cu)
+void launch_preprocess(const lp_prims &P, const lp_camera &cam, float kappa, const lp_frame &F, cudaStream_t st);
+void launch_preprocess_bwd(const lp_prims &P, const lp_camera &cam, float kappa, const lp_frame &F,
+                           const lp_grads &G, cudaStream_t st);
+
+// K2 (lp_sort.cu)
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_ITEMS = 16;
+constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;   // keys per radix block
+constexpr int SCAN_TILE = 2048;                        // elements per scan block
+size_t radix_hist_words(int64_t max_items);
+size_t scan_tmp_words(int64_t max_items);
+// stable LSD radix sort of (key, val) u32 pairs over key bits [0, bits); n from n_dev if non-null
+// else n_host; returns 1 if the result lives in the *_alt buffers.
+int radix_sort_pairs(uint32_t *keys, uint32_t *keys_alt, uint32_t *vals, uint32_t *vals_alt, int64_t n_max,
+                     const uint32_t *n_dev, int bits, uint32_t *hist, cudaStream_t st);
+void launch_scan_tiles(const lp_frame &F, int n, cudaStream_t st);   // offsets + E -> counters
+void launch_emit(const lp_frame &F, int n, cudaStream_t st);
+void launch_ranges(const lp_frame &F, const uint32_t *sorted_tile, int tiles, cudaStream_t st);
+
+// K3 / K4 (lp_raster.cu)
+void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image, cudaStream_t st);
+void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL_dimage, cudaStream_t st);
+
+// C5 helpers (lp_train.cu)
+void launch_l1_grad(const float *img, const float *tgt, float *dL, float *loss, int64_t n, float scale,
+                    cudaStream_t st);
+void launch_adam(float *p, const float *g, float *m, float *v, const lp_adam_group *groups, int ng, float b1,
+                 float b2, float eps, int step, cudaStream_t st);
+
+}  // namespace lp

@@ -1,0 +1,404 @@
+// lp_preprocess.cu -- K1 (forward preprocess, rows a1-a3) and K5 (preprocess backward, row a12).
+//
+// One thread per primitive.  Feature loads are SoA and coalesced across the warp (thread i reads
+// element i of each component array).  HBM-bound: see DESIGN.md §7 for the algorithmic bytes.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lp_device.cuh"
+#include "lp_kernels.h"
+#include "lp_sh.cuh"
+
+namespace lp {
+
+__device__ __forceinline__ void warp_count(uint32_t *ctr, bool pred) {
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(ctr, (uint32_t)__popc(b));
+}
+
+// unclamped SH colour exactly as the forward computes it (fp32), shared by K1 and K5
+__device__ __forceinline__ void sh_colour_fp32(const lp_prims &P, int i, const lp_camera &cam, const float c[3],
+                                               float raw[3]) {
+  const float cpx = -(cam.W[0] * cam.t[0] + cam.W[3] * cam.t[1] + cam.W[6] * cam.t[2]);
+  const float cpy = -(cam.W[1] * cam.t[0] + cam.W[4] * cam.t[1] + cam.W[7] * cam.t[2]);
+  const float cpz = -(cam.W[2] * cam.t[0] + cam.W[5] * cam.t[1] + cam.W[8] * cam.t[2]);
+  float vx = c[0] - cpx, vy = c[1] - cpy, vz = c[2] - cpz;
+  const float inv = rsqrtf(vx * vx + vy * vy + vz * vz);
+  vx *= inv;
+  vy *= inv;
+  vz *= inv;
+  float Y[16];
+  sh_basis<float>(P.sh_degree, vx, vy, vz, Y);
+  const int ncoef = (P.sh_degree + 1) * (P.sh_degree + 1);
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    float acc = 0.5f;
+    for (int k = 0; k < ncoef; ++k) acc += P.sh[((size_t)k * 3 + ch) * P.n + i] * Y[k];
+    raw[ch] = acc;
+  }
+}
+
+// =============================================================================================
+// K1: features -> canonical geometry -> record, sigma (Eq. 1), SH colour
+// =============================================================================================
+template <int KIND>
+__global__ void __launch_bounds__(256) k_preprocess(lp_prims P, lp_camera cam, float kappa, lp_frame F) {
+  constexpr int K = Kind<KIND>::K, RW = Kind<KIND>::RW;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool inb = i < P.n;
+  Geom g;
+  float dh[4], q[4], c[3];
+  g.flag = 1;
+  g.tiles = 0;
+  if (inb) canonical_geometry<KIND>(P, i, cam, kappa, g, dh, q, c);
+  warp_count(F.counters + LP_CNT_INVALID, inb && g.flag == 1);
+  warp_count(F.counters + LP_CNT_FRUSTUM, inb && g.flag == 0);
+  warp_count(F.counters + LP_CNT_VISIBLE, inb && g.tiles > 0);
+  if (!inb) return;
+
+  const bool ok = g.flag == 0;
+  F.tiles_touched[i] = g.tiles;
+  reinterpret_cast<ushort4 *>(F.rect)[i] =
+      make_ushort4((unsigned short)g.rect[0], (unsigned short)g.rect[1], (unsigned short)g.rect[2],
+                   (unsigned short)g.rect[3]);
+  const uint32_t key = ok ? __float_as_uint(g.l) : 0u;
+  F.depth_key[i] = key;
+  F.prim_key[i] = g.tiles > 0 ? key : 0xFFFFFFFFu;   // invisible primitives sort last (emit nothing)
+  F.prim_order[i] = (uint32_t)i;
+  if (F.canon) {
+    float *cn = F.canon + (size_t)i * (2 + 3 * K);
+    cn[0] = ok ? g.crx : 0.f;
+    cn[1] = ok ? g.cry : 0.f;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) cn[2 + 3 * j + a] = ok ? g.off[j][a] : 0.f;
+  }
+  if (g.tiles == 0) return;   // only visible primitives need a record
+
+  // ---- density, Eq. 1: sigma = -log(1 - 0.99 alpha) / (2 min dhat)
+  const float alpha = 1.f / (1.f + expf(-P.opacity[i]));
+  float md = dh[0];
+#pragma unroll
+  for (int a = 1; a < K; ++a) md = fminf(md, dh[a]);
+  const float sigma = -log1pf(-0.99f * alpha) / (2.f * md);
+
+  // ---- SH colour
+  float rgb[3];
+  sh_colour_fp32(P, i, cam, c, rgb);
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) rgb[ch] = fmaxf(rgb[ch], 0.f);
+
+  // ---- raster record
+  float rec[RW];
+  rec[0] = g.crx;
+  rec[1] = g.cry;
+  if (KIND == OCTA) {
+    SlabRows S;
+    octa_slabs(g.off, S);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const double rz = S.r[s][2];
+      rec[2 + 3 * s] = S.ok ? (float)(-S.r[s][0] / rz) : 0.f;
+      rec[3 + 3 * s] = S.ok ? (float)(-S.r[s][1] / rz) : 0.f;
+      rec[4 + 3 * s] = S.ok ? (float)(1.0 / fabs(rz)) : -1.f;   // h = -1: never intersected
+    }
+    rec[REC_OCTA_SIGMA] = sigma;
+    rec[REC_OCTA_RGB + 0] = rgb[0];
+    rec[REC_OCTA_RGB + 1] = rgb[1];
+    rec[REC_OCTA_RGB + 2] = rgb[2];
+    rec[18] = rec[19] = 0.f;
+  } else {
+    TetraPlanes T;
+    tetra_planes(g.off, T);
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int f = T.slot_face[s];
+      rec[2 + 3 * s] = T.ok ? (float)T.A[f] : (s < 3 ? 1.f : -1.f);   // empty: entry 1 > exit -1
+      rec[3 + 3 * s] = T.ok ? (float)T.B[f] : 0.f;
+      rec[4 + 3 * s] = T.ok ? (float)T.C[f] : 0.f;
+    }
+    rec[REC_TETRA_SIGMA] = sigma;
+    rec[REC_TETRA_RGB + 0] = rgb[0];
+    rec[REC_TETRA_RGB + 1] = rgb[1];
+    rec[REC_TETRA_RGB + 2] = rgb[2];
+  }
+  float4 *dst = reinterpret_cast<float4 *>(F.record + (size_t)i * RW);
+#pragma unroll
+  for (int w = 0; w < RW / 4; ++w) dst[w] = make_float4(rec[4 * w], rec[4 * w + 1], rec[4 * w + 2], rec[4 * w + 3]);
+}
+
+// =============================================================================================
+// K5: raster moments -> ray-space geometry -> world features
+// =============================================================================================
+template <int KIND>
+__global__ void __launch_bounds__(128) k_preprocess_bwd(lp_prims P, lp_camera cam, float kappa, lp_frame F,
+                                                        lp_grads Gs) {
+  constexpr int K = Kind<KIND>::K, RG = Kind<KIND>::RG;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  if (F.tiles_touched[i] == 0) return;
+  const int n = P.n;
+  float m[RG];
+  bool any = false;
+#pragma unroll
+  for (int a = 0; a < RG; ++a) {
+    m[a] = F.rgrad[(size_t)a * n + i];
+    any |= (m[a] != 0.f);
+  }
+  if (!any) return;
+
+  Geom g;
+  float dhf[4], qf[4], cf[3];
+  canonical_geometry<KIND>(P, i, cam, kappa, g, dhf, qf, cf);
+
+  // ---- raster moments -> d/d(ray-space offsets) and d/d(ray-space centre xy)
+  double go[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  double gcr[2] = {0, 0};
+  double dsig, drgb[3];
+  if (KIND == OCTA) {
+    double M[3][3], G[3][3], det;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) M[a][j] = (double)g.off[j][a];
+    inverse3(M, G, det);
+    SlabRows S;
+    octa_slabs(g.off, S);
+    double gG[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const double rx = S.r[s][0], ry = S.r[s][1], rz = S.r[s][2];
+      const double b = -rx / rz, gg = -ry / rz;
+      const double db = m[4 * s + 0], dg = m[4 * s + 1], mc = m[4 * s + 2], dhh = m[4 * s + 3];
+      // L_s = b dx + g dy with dx = px - c.x: d/dc.x = -b (summed weights M_c)
+      gcr[0] -= b * mc;
+      gcr[1] -= gg * mc;
+      const double rz2 = rz * rz;
+      const double drx = -db / rz, dry = -dg / rz;
+      const double drz = db * rx / rz2 + dg * ry / rz2 - dhh * (rz > 0 ? 1.0 : -1.0) / rz2;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double sa = kSlabSign[s][a];
+        gG[a][0] += sa * drx;
+        gG[a][1] += sa * dry;
+        gG[a][2] += sa * drz;
+      }
+    }
+    // G = M^-1  =>  dM = -G^T dG G^T
+    double t1[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) t1[a][b] = G[0][a] * gG[0][b] + G[1][a] * gG[1][b] + G[2][a] * gG[2][b];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const double dM = -(t1[a][0] * G[j][0] + t1[a][1] * G[j][1] + t1[a][2] * G[j][2]);
+        go[j][a] += dM;   // column j of M is offset j
+      }
+    dsig = m[16];
+    drgb[0] = m[17]; drgb[1] = m[18]; drgb[2] = m[19];
+  } else {
+    TetraPlanes T;
+    tetra_planes(g.off, T);
+    double v[4][3];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) v[k][a] = (double)g.off[k][a];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const double dA = m[3 * s], dB = m[3 * s + 1], dC = m[3 * s + 2];
+      if (dA == 0.0 && dB == 0.0 && dC == 0.0) continue;
+      const int f = T.slot_face[s];
+      const int ia = kTetraFace[f][0], ib = kTetraFace[f][1], ic = kTetraFace[f][2];
+      const double B = T.B[f], C = T.C[f];
+      gcr[0] -= B * dA;
+      gcr[1] -= C * dA;
+      // A = va.z - B va.x - C va.y
+      go[ia][2] += dA;
+      go[ia][0] -= B * dA;
+      go[ia][1] -= C * dA;
+      const double dBt = dB - dA * v[ia][0], dCt = dC - dA * v[ia][1];
+      const double nx = T.n[f][0], ny = T.n[f][1], nz = T.n[f][2];
+      const double gn[3] = {-dBt / nz, -dCt / nz, dBt * nx / (nz * nz) + dCt * ny / (nz * nz)};
+      const double e1[3] = {v[ib][0] - v[ia][0], v[ib][1] - v[ia][1], v[ib][2] - v[ia][2]};
+      const double e2[3] = {v[ic][0] - v[ia][0], v[ic][1] - v[ia][1], v[ic][2] - v[ia][2]};
+      // n = e1 x e2:  dL/de1 = e2 x gn,  dL/de2 = gn x e1
+      const double ge1[3] = {e2[1] * gn[2] - e2[2] * gn[1], e2[2] * gn[0] - e2[0] * gn[2], e2[0] * gn[1] - e2[1] * gn[0]};
+      const double ge2[3] = {gn[1] * e1[2] - gn[2] * e1[1], gn[2] * e1[0] - gn[0] * e1[2], gn[0] * e1[1] - gn[1] * e1[0]};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        go[ib][a] += ge1[a];
+        go[ic][a] += ge2[a];
+        go[ia][a] -= ge1[a] + ge2[a];
+      }
+    }
+    dsig = m[18];
+    drgb[0] = m[19]; drgb[1] = m[20]; drgb[2] = m[21];
+  }
+  if (Gs.mean2d_abs) Gs.mean2d_abs[i] += (float)sqrt(gcr[0] * gcr[0] + gcr[1] * gcr[1]);
+
+  // ---- the 2D filter adds constants (fixed extreme index): identity.
+  // ---- o_j = J W (dh_j R b_j); c_ray = phi(p), p = W c + t  (fp64 chain)
+  double q[4] = {qf[0], qf[1], qf[2], qf[3]};
+  const double nq = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  const double w = q[0] / nq, x = q[1] / nq, y = q[2] / nq, z = q[3] / nq;
+  const double R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+                          {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
+                          {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
+  double Wm[3][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) Wm[r][cc] = cam.W[3 * r + cc];
+  double p[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) p[r] = Wm[r][0] * cf[0] + Wm[r][1] * cf[1] + Wm[r][2] * cf[2] + (double)cam.t[r];
+  const double l = sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+  const double fx = cam.fx, fy = cam.fy, pz = p[2], pz2 = pz * pz, pz3 = pz2 * pz;
+  const double J[3][3] = {{fx / pz, 0, -fx * p[0] / pz2}, {0, fy / pz, -fy * p[1] / pz2}, {p[0] / l, p[1] / l, p[2] / l}};
+  double gJ[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, gR[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  double gdh[4] = {0, 0, 0, 0};
+  const double kk = 0.57735026918962576451;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double bj[3];
+    if (KIND == OCTA) {
+      bj[0] = j == 0; bj[1] = j == 1; bj[2] = j == 2;
+    } else {
+      bj[0] = (j == 0 || j == 1) ? kk : -kk;
+      bj[1] = (j == 0 || j == 2) ? kk : -kk;
+      bj[2] = (j == 0 || j == 3) ? kk : -kk;
+    }
+    double Rb[3], ow[3], oc[3], goc[3], gow[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) Rb[r] = R[r][0] * bj[0] + R[r][1] * bj[1] + R[r][2] * bj[2];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) ow[r] = (double)dhf[j] * Rb[r];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) oc[r] = Wm[r][0] * ow[0] + Wm[r][1] * ow[1] + Wm[r][2] * ow[2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) goc[a] = J[0][a] * go[j][0] + J[1][a] * go[j][1] + J[2][a] * go[j][2];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) gJ[r][a] += go[j][r] * oc[a];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) gow[a] = Wm[0][a] * goc[0] + Wm[1][a] * goc[1] + Wm[2][a] * goc[2];
+    gdh[j] = Rb[0] * gow[0] + Rb[1] * gow[1] + Rb[2] * gow[2];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc) gR[r][cc] += (double)dhf[j] * gow[r] * bj[cc];
+  }
+  double gp[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) gp[a] = J[0][a] * gcr[0] + J[1][a] * gcr[1];   // c_ray.z gets no gradient
+  gp[2] += gJ[0][0] * (-fx / pz2);
+  gp[0] += gJ[0][2] * (-fx / pz2);
+  gp[2] += gJ[0][2] * (2.0 * fx * p[0] / pz3);
+  gp[2] += gJ[1][1] * (-fy / pz2);
+  gp[1] += gJ[1][2] * (-fy / pz2);
+  gp[2] += gJ[1][2] * (2.0 * fy * p[1] / pz3);
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int mm = 0; mm < 3; ++mm) gp[mm] += gJ[2][k] * (((k == mm) ? 1.0 : 0.0) - p[k] * p[mm] / (l * l)) / l;
+  double gc[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) gc[a] = Wm[0][a] * gp[0] + Wm[1][a] * gp[1] + Wm[2][a] * gp[2];
+
+  // ---- distances (through the optional 3D filter)
+  if (Gs.dist) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      double gd = gdh[j];
+      if (P.filter3d) gd *= (double)P.dist[j * n + i] / (double)dhf[j];
+      Gs.dist[(size_t)j * n + i] += (float)gd;
+    }
+  }
+  // ---- rotation: R(q_hat) -> q_hat -> q
+  if (Gs.rot) {
+    const double dR[4][3][3] = {
+        {{0, -2 * z, 2 * y}, {2 * z, 0, -2 * x}, {-2 * y, 2 * x, 0}},
+        {{0, 2 * y, 2 * z}, {2 * y, -4 * x, -2 * w}, {2 * z, 2 * w, -4 * x}},
+        {{-4 * y, 2 * x, 2 * w}, {2 * x, 0, 2 * z}, {-2 * w, 2 * z, -4 * y}},
+        {{-4 * z, -2 * w, 2 * x}, {2 * w, -4 * z, 2 * y}, {2 * x, 2 * y, 0}}};
+    double gq[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) gq[a] += gR[r][cc] * dR[a][r][cc];
+    const double qh[4] = {w, x, y, z};
+    const double dot = qh[0] * gq[0] + qh[1] * gq[1] + qh[2] * gq[2] + qh[3] * gq[3];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) Gs.rot[(size_t)a * n + i] += (float)((gq[a] - qh[a] * dot) / nq);
+  }
+  // ---- opacity: Eq. 1 with the denominator frozen, alpha = sigmoid(logit)
+  if (Gs.opacity) {
+    const double alpha = 1.0 / (1.0 + exp(-(double)P.opacity[i]));
+    double md = dhf[0];
+#pragma unroll
+    for (int a = 1; a < K; ++a) md = fmin(md, (double)dhf[a]);
+    const double dsda = 0.99 / ((1.0 - 0.99 * alpha) * 2.0 * md);
+    Gs.opacity[i] += (float)(dsig * dsda * alpha * (1.0 - alpha));
+  }
+  // ---- SH coefficients and the view-direction term of the centre
+  {
+    const double cp[3] = {-(Wm[0][0] * cam.t[0] + Wm[1][0] * cam.t[1] + Wm[2][0] * cam.t[2]),
+                          -(Wm[0][1] * cam.t[0] + Wm[1][1] * cam.t[1] + Wm[2][1] * cam.t[2]),
+                          -(Wm[0][2] * cam.t[0] + Wm[1][2] * cam.t[1] + Wm[2][2] * cam.t[2])};
+    double v[3] = {cf[0] - cp[0], cf[1] - cp[1], cf[2] - cp[2]};
+    const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    const double dir[3] = {v[0] / nv, v[1] / nv, v[2] / nv};
+    double Y[16];
+    sh_basis<double>(P.sh_degree, dir[0], dir[1], dir[2], Y);
+    const int ncoef = (P.sh_degree + 1) * (P.sh_degree + 1);
+    double wsum[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) wsum[k] = 0.0;
+    float raw[3];
+    sh_colour_fp32(P, i, cam, cf, raw);   // the forward's exact fp32 value decides the clamp
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      if (raw[ch] < 0.f) continue;
+      const double gr = drgb[ch];
+      for (int k = 0; k < ncoef; ++k) {
+        if (Gs.sh) Gs.sh[((size_t)k * 3 + ch) * n + i] += (float)(Y[k] * gr);
+        wsum[k] += gr * (double)P.sh[((size_t)k * 3 + ch) * n + i];
+      }
+    }
+    double gdir[3];
+    sh_basis_grad_dot<double>(P.sh_degree, dir[0], dir[1], dir[2], wsum, gdir);
+    const double dd = dir[0] * gdir[0] + dir[1] * gdir[1] + dir[2] * gdir[2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) gc[a] += (gdir[a] - dir[a] * dd) / nv;
+  }
+  if (Gs.pos) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += (float)gc[a];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+void launch_preprocess(const lp_prims &P, const lp_camera &cam, float kappa, const lp_frame &F, cudaStream_t st) {
+  if (P.n == 0) return;
+  const int grid = (P.n + 255) / 256;
+  if (P.kind == LP_OCTAHEDRON) k_preprocess<LP_OCTAHEDRON><<<grid, 256, 0, st>>>(P, cam, kappa, F);
+  else k_preprocess<LP_TETRAHEDRON><<<grid, 256, 0, st>>>(P, cam, kappa, F);
+}
+
+void launch_preprocess_bwd(const lp_prims &P, const lp_camera &cam, float kappa, const lp_frame &F,
+                           const lp_grads &G, cudaStream_t st) {
+  if (P.n == 0) return;
+  const int grid = (P.n + 127) / 128;
+  if (P.kind == LP_OCTAHEDRON) k_preprocess_bwd<LP_OCTAHEDRON><<<grid, 128, 0, st>>>(P, cam, kappa, F, G);
+  else k_preprocess_bwd<LP_TETRAHEDRON><<<grid, 128, 0, st>>>(P, cam, kappa, F, G);
+}
+
+}  // namespace lp

@@ -1,0 +1,338 @@
+// lp_raster.cu -- K3 forward raster (rows a8-a9) and K4 backward raster (rows a10-a11).
+//
+// One CTA per 16x16 tile.  A CTA walks its tile's sorted list in batches of NT records: each
+// thread stages one record (80 B octa / 96 B tetra, gathered by primitive id) into shared
+// memory, then every thread evaluates the whole batch for its PPT pixels, reading each record
+// with broadcast LDS.128.  The per-pair work is the slab / Cyrus-Beck chord:
+// ~26 FP32 instructions per (pixel, octahedron), ~19 per (pixel, tetrahedron), plus ~10 per
+// intersected pair for the opacity and compositing.
+//
+// Backward: the same lists in reverse.  Per (pixel, entry) with chord > 0 it recovers T_k = T/E,
+// runs the blend backward and the chord backward (App. E, in slab/plane
+// moment form), accumulates <= 22 moments per thread, then a warp transpose-reduce (24 SHFL)
+// and one RED.F32 per moment per (warp, primitive) into rgrad[moment][n].
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lp_device.cuh"
+#include "lp_kernels.h"
+
+namespace lp {
+
+// pixel (x, y) of thread `tid`, slot k, inside the 16x16 tile (warps cover compact squares)
+template <int NT>
+__device__ __forceinline__ void pixel_of(int tid, int k, int &x, int &y) {
+  const int w = tid >> 5, lane = tid & 31;
+  if (NT == 128) {          // PPT 2: warp = 8x8 square, lane = 8x4, second pixel 4 rows down
+    x = (w & 1) * 8 + (lane & 7);
+    y = (w >> 1) * 8 + (lane >> 3) + 4 * k;
+  } else if (NT == 64) {    // PPT 4: warp = 16x8, lane = 16x2, pixels 2 rows apart
+    x = lane & 15;
+    y = w * 8 + (lane >> 4) + 2 * k;
+  } else {                  // PPT 1 (NT 256): warp = 8x4
+    x = (w & 1) * 8 + (lane & 7);
+    y = (w >> 1) * 4 + (lane >> 3);
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ float chord_of(const float *rec, float px, float py, int &se, int &sx) {
+  if (KIND == OCTA) return octa_chord<false>(rec, px, py, se, sx);
+  return tetra_chord<false>(rec, px, py, se, sx);
+}
+
+// =============================================================================================
+// K3 forward
+// =============================================================================================
+template <int KIND, int NT>
+__global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg, float *__restrict__ image) {
+  constexpr int RW = Kind<KIND>::RW, RW4 = RW / 4, PPT = 256 / NT;
+  constexpr int SIG = KIND == OCTA ? REC_OCTA_SIGMA : REC_TETRA_SIGMA;
+  constexpr int RGB = KIND == OCTA ? REC_OCTA_RGB : REC_TETRA_RGB;
+  __shared__ float4 s_rec[NT * RW4];
+  __shared__ unsigned long long s_stat[2];
+
+  const int tile = blockIdx.x;
+  const int tx = tile % F.tiles_x, ty = tile / F.tiles_x;
+  const uint32_t start = F.ranges[2 * tile], end = F.ranges[2 * tile + 1];
+  const int W = F.width, H = F.height;
+  if (threadIdx.x < 2) s_stat[threadIdx.x] = 0ull;
+
+  float fx[PPT], fy[PPT], T[PPT], C[PPT][3];
+  uint32_t nproc[PPT];
+  bool done[PPT], inside[PPT];
+  uint32_t nhit = 0;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    int x, y;
+    pixel_of<NT>(threadIdx.x, k, x, y);
+    x += tx * LP_TILE;
+    y += ty * LP_TILE;
+    inside[k] = x < W && y < H;
+    fx[k] = (float)x + 0.5f;
+    fy[k] = (float)y + 0.5f;
+    T[k] = 1.f;
+    C[k][0] = C[k][1] = C[k][2] = 0.f;
+    done[k] = !inside[k];
+    nproc[k] = end - start;
+  }
+
+  for (uint32_t b = start; b < end; b += NT) {
+    bool mine = true;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) mine = mine && done[k];
+    if (__syncthreads_and(mine)) break;   // also protects s_rec from the previous batch
+    const uint32_t e = b + threadIdx.x;
+    if (e < end) {
+      const uint32_t v = F.sorted_val[e];
+      const float4 *src = reinterpret_cast<const float4 *>(F.record + (size_t)v * RW);
+#pragma unroll
+      for (int w = 0; w < RW4; ++w) s_rec[threadIdx.x * RW4 + w] = __ldg(src + w);
+    }
+    __syncthreads();
+    if (__all_sync(0xffffffffu, mine)) continue;
+    const int cnt = (int)min((uint32_t)NT, end - b);
+    for (int j = 0; j < cnt; ++j) {
+      const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        if (done[k]) continue;
+        int se, sx;
+        const float ch = chord_of<KIND>(rec, fx[k], fy[k], se, sx);
+        if (ch > 0.f) {
+          const float E = transmit(rec[SIG], ch);
+          const float o = 1.f - E;
+          const float wgt = T[k] * o;
+          C[k][0] = fmaf(wgt, rec[RGB + 0], C[k][0]);
+          C[k][1] = fmaf(wgt, rec[RGB + 1], C[k][1]);
+          C[k][2] = fmaf(wgt, rec[RGB + 2], C[k][2]);
+          T[k] = T[k] * E;
+          ++nhit;
+          if (T[k] < cfg.t_stop) {       // include-then-stop (reading 9)
+            done[k] = true;
+            nproc[k] = b + (uint32_t)j - start + 1;
+          }
+        }
+      }
+    }
+  }
+
+  const size_t HW = (size_t)W * H;
+  unsigned long long it = 0;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    if (!inside[k]) continue;
+    const int x = (int)fx[k], y = (int)fy[k];
+    const size_t p = (size_t)y * W + x;
+    image[p] = fmaf(T[k], cfg.bg[0], C[k][0]);
+    image[HW + p] = fmaf(T[k], cfg.bg[1], C[k][1]);
+    image[2 * HW + p] = fmaf(T[k], cfg.bg[2], C[k][2]);
+    F.T_final[p] = T[k];
+    F.n_proc[p] = nproc[k];
+    it += nproc[k];
+  }
+  if (cfg.count_stats) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      it += __shfl_xor_sync(0xffffffffu, it, o);
+      nhit += __shfl_xor_sync(0xffffffffu, nhit, o);
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&s_stat[0], it);
+      atomicAdd(&s_stat[1], (unsigned long long)nhit);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long *>(F.counters + LP_CNT_ITERATED), s_stat[0]);
+      atomicAdd(reinterpret_cast<unsigned long long *>(F.counters + LP_CNT_INTERSECTED), s_stat[1]);
+    }
+  }
+}
+
+// =============================================================================================
+// warp transpose-reduce: every lane holds N partials; afterwards lane l holds the warp sum of
+// partial idx(l) (valid when `valid`).  5 steps, sum_l ceil(N_l / 2) shuffles.
+// =============================================================================================
+template <int N, int OFF>
+__device__ __forceinline__ void tr_step(const float (&in)[N], float (&out)[(N + 1) / 2], bool upper) {
+  constexpr int H = (N + 1) / 2;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const float lo = in[i];
+    const float hi = (i + H < N) ? in[i + H] : 0.f;
+    const float send = upper ? lo : hi;
+    const float keep = upper ? hi : lo;
+    out[i] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ float warp_transpose_reduce(const float (&a)[N], int lane, int &idx, bool &valid) {
+  constexpr int N1 = (N + 1) / 2, N2 = (N1 + 1) / 2, N3 = (N2 + 1) / 2, N4 = (N3 + 1) / 2;
+  float b1[N1], b2[N2], b3[N3], b4[N4], b5[(N4 + 1) / 2];
+  tr_step<N, 16>(a, b1, lane & 16);
+  tr_step<N1, 8>(b1, b2, lane & 8);
+  tr_step<N2, 4>(b2, b3, lane & 4);
+  tr_step<N3, 2>(b3, b4, lane & 2);
+  tr_step<N4, 1>(b4, b5, lane & 1);
+  // which partial did this lane end up with?
+  const int Ns[5] = {N, N1, N2, N3, N4};
+  int base = 0, size = N;
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int Hs = (Ns[s] + 1) / 2;
+    if (lane & (16 >> s)) {
+      base += Hs;
+      size -= Hs;
+    } else {
+      size = size < Hs ? size : Hs;
+    }
+  }
+  idx = base;
+  valid = size >= 1;
+  return b5[0];
+}
+
+// =============================================================================================
+// K4 backward
+// =============================================================================================
+template <int KIND, int NT>
+__global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg, const float *__restrict__ dL) {
+  constexpr int RW = Kind<KIND>::RW, RW4 = RW / 4, PPT = 256 / NT, RG = Kind<KIND>::RG;
+  constexpr int SIG = KIND == OCTA ? REC_OCTA_SIGMA : REC_TETRA_SIGMA;
+  constexpr int RGB = KIND == OCTA ? REC_OCTA_RGB : REC_TETRA_RGB;
+  __shared__ float4 s_rec[NT * RW4];
+  __shared__ uint32_t s_id[NT];
+  __shared__ uint32_t s_last;
+
+  const int tile = blockIdx.x;
+  const int tx = tile % F.tiles_x, ty = tile / F.tiles_x;
+  const uint32_t start = F.ranges[2 * tile], end = F.ranges[2 * tile + 1];
+  if (end <= start) return;
+  const int W = F.width, H = F.height;
+  const size_t HW = (size_t)W * H;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_last = start;
+  __syncthreads();
+
+  float fx[PPT], fy[PPT], T[PPT], S[PPT][3], G[PPT][3];
+  uint32_t last[PPT];
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    int x, y;
+    pixel_of<NT>(threadIdx.x, k, x, y);
+    x += tx * LP_TILE;
+    y += ty * LP_TILE;
+    const bool in = x < W && y < H;
+    fx[k] = (float)x + 0.5f;
+    fy[k] = (float)y + 0.5f;
+    const size_t p = in ? (size_t)y * W + x : 0;
+    T[k] = in ? F.T_final[p] : 1.f;
+    last[k] = in ? start + F.n_proc[p] : start;     // entries [start, last) were processed
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      S[k][c] = cfg.bg[c];
+      G[k][c] = in ? dL[c * HW + p] : 0.f;
+    }
+    if (last[k] > start) atomicMax(&s_last, last[k]);
+  }
+  __syncthreads();
+  const uint32_t lmax = s_last;
+
+  for (uint32_t bend = lmax; bend > start; bend = (bend - start > NT) ? bend - NT : start) {
+    const uint32_t bstart = (bend - start > NT) ? bend - NT : start;
+    __syncthreads();
+    const uint32_t e = bstart + threadIdx.x;
+    if (e < bend) {
+      const uint32_t v = F.sorted_val[e];
+      s_id[threadIdx.x] = v;
+      const float4 *src = reinterpret_cast<const float4 *>(F.record + (size_t)v * RW);
+#pragma unroll
+      for (int w = 0; w < RW4; ++w) s_rec[threadIdx.x * RW4 + w] = __ldg(src + w);
+    }
+    __syncthreads();
+    bool act = false;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) act = act || (last[k] > bstart);
+    if (!__any_sync(0xffffffffu, act)) continue;
+
+    for (int j = (int)(bend - bstart) - 1; j >= 0; --j) {
+      const uint32_t ej = bstart + (uint32_t)j;
+      const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
+      float acc[RG];
+#pragma unroll
+      for (int a = 0; a < RG; ++a) acc[a] = 0.f;
+      bool hit = false;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        if (ej >= last[k]) continue;
+        int se, sx;
+        const float ch = KIND == OCTA ? octa_chord<true>(rec, fx[k], fy[k], se, sx)
+                                      : tetra_chord<true>(rec, fx[k], fy[k], se, sx);
+        if (!(ch > 0.f)) continue;
+        hit = true;
+        const float sig = rec[SIG];
+        const float E = transmit(sig, ch);
+        const float o = 1.f - E;
+        const float Tk = T[k] / E;                       // transmittance in front of this entry
+        float dLdo = 0.f;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          acc[RG - 3 + c] = fmaf(Tk * o, G[k][c], acc[RG - 3 + c]);   // dL/drgb
+          dLdo = fmaf(rec[RGB + c] - S[k][c], G[k][c], dLdo);
+          S[k][c] = fmaf(o, rec[RGB + c], E * S[k][c]);               // colour behind the previous entry
+        }
+        dLdo *= Tk;
+        T[k] = Tk;
+        const float gE = E * dLdo;
+        acc[RG - 4] = fmaf(ch, gE, acc[RG - 4]);          // dL/dsigma = chord E dL/do
+        const float g = sig * gE;                          // dL/d exit = g, dL/d entry = -g
+        const float dx = fx[k] - rec[0], dy = fy[k] - rec[1];
+        if (KIND == OCTA) {
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const float gx = (s == sx) ? g : 0.f, gn = (s == se) ? g : 0.f;
+            const float ws = gx - gn, us = gx + gn;
+            acc[4 * s + 0] = fmaf(ws, dx, acc[4 * s + 0]);
+            acc[4 * s + 1] = fmaf(ws, dy, acc[4 * s + 1]);
+            acc[4 * s + 2] += ws;
+            acc[4 * s + 3] += us;
+          }
+        } else {
+#pragma unroll
+          for (int s = 0; s < 6; ++s) {
+            const float ws = (s == sx) ? g : ((s == se) ? -g : 0.f);
+            acc[3 * s + 0] += ws;
+            acc[3 * s + 1] = fmaf(ws, dx, acc[3 * s + 1]);
+            acc[3 * s + 2] = fmaf(ws, dy, acc[3 * s + 2]);
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, hit)) {
+        int idx;
+        bool valid;
+        const float val = warp_transpose_reduce<RG>(acc, lane, idx, valid);
+        if (valid && val != 0.f) atomicAdd(F.rgrad + (size_t)idx * F.n + s_id[j], val);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+constexpr int FWD_NT = 128;
+constexpr int BWD_NT = 128;
+
+void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image, cudaStream_t st) {
+  const int tiles = F.tiles_x * F.tiles_y;
+  if (F.kind == LP_OCTAHEDRON) k_raster_fwd<LP_OCTAHEDRON, FWD_NT><<<tiles, FWD_NT, 0, st>>>(F, cfg, image);
+  else k_raster_fwd<LP_TETRAHEDRON, FWD_NT><<<tiles, FWD_NT, 0, st>>>(F, cfg, image);
+}
+
+void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL, cudaStream_t st) {
+  const int tiles = F.tiles_x * F.tiles_y;
+  if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, BWD_NT><<<tiles, BWD_NT, 0, st>>>(F, cfg, dL);
+  else k_raster_bwd<LP_TETRAHEDRON, BWD_NT><<<tiles, BWD_NT, 0, st>>>(F, cfg, dL);
+}
+
+}  // namespace lp

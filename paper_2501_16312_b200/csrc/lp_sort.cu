@@ -1,0 +1,340 @@
+// lp_sort.cu -- K2: tiling and global sort (rows a4-a7).
+//
+// The method orders every tile's list by (depth key, primitive id) (readings 8, 10, 11).
+// Instead of one 64-bit (tile|depth) radix sort over all E entries we
+//   1. sort the N primitives by depth key (stable LSD radix, 4 x 8-bit passes over N, ties by id),
+//   2. exclusive-scan tiles_touched in that order,
+//   3. emit (tile, id) entries in depth order (warp-cooperative),
+//   4. stable LSD radix sort of the entries by tile id only (ceil(log2 T / 8) passes over E),
+//   5. per-tile [start, end) ranges.
+// The output equals the full (tile|depth, id) sort bit for bit (stable sorts compose), but the
+// E-sized work drops from ~6 passes to 1-2.
+//
+// Radix pass = histogram kernel + per-digit scan kernel + scatter kernel.  The scatter ranks keys
+// stably inside a 4096-key block with warp match_any (order = element index), stages the block in
+// shared memory in sorted order and writes it out digit-run by digit-run (coalesced).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lp_kernels.h"
+
+namespace lp {
+
+constexpr int RADIX = 256;
+constexpr int WARPS = SORT_THREADS / 32;
+
+__device__ __forceinline__ int64_t item_count(const uint32_t *n_dev, int64_t n_host) {
+  if (!n_dev) return n_host;
+  const int64_t n = (int64_t)*n_dev;
+  return n < n_host ? n : n_host;   // n_host is the capacity when n_dev is given
+}
+
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(SORT_THREADS) k_radix_hist(const uint32_t *__restrict__ keys, const uint32_t *n_dev,
+                                                             int64_t n_host, int shift, uint32_t *__restrict__ hist,
+                                                             int nblk) {
+  __shared__ uint32_t s_h[WARPS][RADIX];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int d = tid; d < WARPS * RADIX; d += SORT_THREADS) (&s_h[0][0])[d] = 0;
+  __syncthreads();
+  const int64_t n = item_count(n_dev, n_host);
+  const int64_t start = (int64_t)blockIdx.x * SORT_TILE;
+  if (start < n) {
+    const int64_t end = start + SORT_TILE < n ? start + SORT_TILE : n;
+    for (int64_t e = start + tid; e < end; e += SORT_THREADS) atomicAdd(&s_h[warp][(keys[e] >> shift) & 0xFF], 1u);
+  }
+  __syncthreads();
+  uint32_t s = 0;
+#pragma unroll
+  for (int w = 0; w < WARPS; ++w) s += s_h[w][tid];
+  hist[(size_t)tid * nblk + blockIdx.x] = s;
+}
+
+// block-wide exclusive scan of one value per thread (blockDim multiple of 32, <= 1024)
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *s_warp, uint32_t &total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) s_warp[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t wbase = warp ? s_warp[warp - 1] : 0;
+  total = s_warp[nw - 1];
+  __syncthreads();
+  return wbase + x - v;
+}
+
+// one block per digit: exclusive scan over the blocks of hist[d][*]; digit total -> tot[d]
+__global__ void __launch_bounds__(1024) k_radix_scan(uint32_t *__restrict__ hist, int nblk, uint32_t *__restrict__ tot) {
+  __shared__ uint32_t s_warp[32];
+  uint32_t *row = hist + (size_t)blockIdx.x * nblk;
+  uint32_t carry = 0;
+  for (int base = 0; base < nblk; base += 1024) {
+    const int i = base + threadIdx.x;
+    const uint32_t v = i < nblk ? row[i] : 0;
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan(v, s_warp, total);
+    if (i < nblk) row[i] = carry + ex;
+    carry += total;
+  }
+  if (threadIdx.x == 0) tot[blockIdx.x] = carry;
+}
+
+__global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(const uint32_t *__restrict__ keys_in,
+                                                                const uint32_t *__restrict__ vals_in,
+                                                                uint32_t *__restrict__ keys_out,
+                                                                uint32_t *__restrict__ vals_out, const uint32_t *n_dev,
+                                                                int64_t n_host, int shift,
+                                                                const uint32_t *__restrict__ hist,
+                                                                const uint32_t *__restrict__ tot, int nblk) {
+  __shared__ uint32_t s_keys[SORT_TILE];
+  __shared__ uint32_t s_vals[SORT_TILE];
+  __shared__ uint32_t s_wcnt[WARPS][RADIX];
+  __shared__ uint32_t s_base[RADIX];    // global position of this block's first key of digit d
+  __shared__ uint32_t s_local[RADIX];   // start of digit d inside the block's sorted tile
+  __shared__ uint32_t s_warp[32];
+  const int64_t n = item_count(n_dev, n_host);
+  const int64_t start = (int64_t)blockIdx.x * SORT_TILE;
+  if (start >= n) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cnt = (int)(n - start < SORT_TILE ? n - start : SORT_TILE);
+
+  for (int d = lane; d < RADIX; d += 32) s_wcnt[warp][d] = 0;
+  __syncwarp();
+  // ---- stable rank within (warp, digit): element index = start + warp*32*ITEMS + r*32 + lane
+  uint32_t key[SORT_ITEMS], val[SORT_ITEMS], rank[SORT_ITEMS];
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int r = 0; r < SORT_ITEMS; ++r) {
+    const int li = warp * 32 * SORT_ITEMS + r * 32 + lane;
+    const bool valid = li < cnt;
+    key[r] = valid ? keys_in[start + li] : 0u;
+    val[r] = valid ? vals_in[start + li] : 0u;
+    const uint32_t d = (key[r] >> shift) & 0xFF;
+    const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0x100u + lane);
+    const int leader = __ffs(peers) - 1;
+    uint32_t b = 0;
+    if (valid && lane == leader) {
+      b = s_wcnt[warp][d];
+      s_wcnt[warp][d] = b + __popc(peers);
+    }
+    b = __shfl_sync(0xffffffffu, b, leader);
+    rank[r] = b + __popc(peers & lt);
+    __syncwarp();
+  }
+  __syncthreads();
+  // ---- per digit: exclusive prefix over warps; block digit counts -> local digit starts
+  {
+    const int d = tid;   // SORT_THREADS == RADIX
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      const uint32_t c = s_wcnt[w][d];
+      s_wcnt[w][d] = run;
+      run += c;
+    }
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan(run, s_warp, total);
+    s_local[d] = ex;
+    // global start of digit d = (keys of smaller digits, all blocks) + (digit d, earlier blocks)
+    const uint32_t tsum = tot[d];
+    uint32_t gtotal;
+    const uint32_t gex = block_exclusive_scan(tsum, s_warp, gtotal);
+    s_base[d] = gex + hist[(size_t)d * nblk + blockIdx.x];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < SORT_ITEMS; ++r) {
+    const int li = warp * 32 * SORT_ITEMS + r * 32 + lane;
+    if (li < cnt) {
+      const uint32_t d = (key[r] >> shift) & 0xFF;
+      const uint32_t lp = s_local[d] + s_wcnt[warp][d] + rank[r];
+      s_keys[lp] = key[r];
+      s_vals[lp] = val[r];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < cnt; i += SORT_THREADS) {
+    const uint32_t k = s_keys[i];
+    const uint32_t d = (k >> shift) & 0xFF;
+    const uint32_t g = s_base[d] + (uint32_t)i - s_local[d];
+    keys_out[g] = k;
+    vals_out[g] = s_vals[i];
+  }
+}
+
+size_t radix_hist_words(int64_t max_items) {
+  const int64_t nblk = (max_items + SORT_TILE - 1) / SORT_TILE;
+  return (size_t)(nblk > 0 ? nblk : 1) * RADIX + RADIX;
+}
+
+int radix_sort_pairs(uint32_t *keys, uint32_t *keys_alt, uint32_t *vals, uint32_t *vals_alt, int64_t n_max,
+                     const uint32_t *n_dev, int bits, uint32_t *hist, cudaStream_t st) {
+  if (n_max <= 0 || bits <= 0) return 0;
+  const int nblk = (int)((n_max + SORT_TILE - 1) / SORT_TILE);
+  uint32_t *tot = hist + (size_t)nblk * RADIX;
+  int flip = 0;
+  for (int shift = 0; shift < bits; shift += 8) {
+    uint32_t *ki = flip ? keys_alt : keys, *vi = flip ? vals_alt : vals;
+    uint32_t *ko = flip ? keys : keys_alt, *vo = flip ? vals : vals_alt;
+    k_radix_hist<<<nblk, SORT_THREADS, 0, st>>>(ki, n_dev, n_max, shift, hist, nblk);
+    k_radix_scan<<<RADIX, 1024, 0, st>>>(hist, nblk, tot);
+    k_radix_scatter<<<nblk, SORT_THREADS, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, hist, tot, nblk);
+    flip ^= 1;
+  }
+  return flip;
+}
+
+// ---------------------------------------------------------------------------------------------
+// exclusive scan of tiles_touched in depth order (a4)
+// ---------------------------------------------------------------------------------------------
+size_t scan_tmp_words(int64_t max_items) { return (size_t)((max_items + SCAN_TILE - 1) / SCAN_TILE) + 32; }
+
+__global__ void __launch_bounds__(256) k_scan_reduce(const uint32_t *__restrict__ order, const uint32_t *__restrict__ tt,
+                                                     int n, uint32_t *__restrict__ part) {
+  __shared__ uint32_t s_warp[32];
+  const int base = blockIdx.x * SCAN_TILE;
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_TILE / 256; ++k) {
+    const int j = base + k * 256 + threadIdx.x;
+    if (j < n) s += tt[order[j]];
+  }
+  uint32_t total;
+  block_exclusive_scan(s, s_warp, total);
+  if (threadIdx.x == 0) part[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_top(uint32_t *__restrict__ part, int nb, uint32_t *__restrict__ offsets,
+                                                   int n, uint32_t *__restrict__ counters, int64_t capacity) {
+  __shared__ uint32_t s_warp[32];
+  uint32_t carry = 0;
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    const uint32_t v = i < nb ? part[i] : 0;
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan(v, s_warp, total);
+    if (i < nb) part[i] = carry + ex;
+    carry += total;
+  }
+  if (threadIdx.x == 0) {
+    offsets[n] = carry;
+    counters[LP_CNT_ENTRIES] = carry;
+    counters[LP_CNT_OVERFLOW] = (int64_t)carry > capacity ? 1u : 0u;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_scan_down(const uint32_t *__restrict__ order, const uint32_t *__restrict__ tt,
+                                                   int n, const uint32_t *__restrict__ part,
+                                                   uint32_t *__restrict__ offsets) {
+  __shared__ uint32_t s_warp[32];
+  const int base = blockIdx.x * SCAN_TILE;
+  // thread t owns 8 consecutive elements: base + 8t .. 8t+7
+  uint32_t v[SCAN_TILE / 256];
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_TILE / 256; ++k) {
+    const int j = base + threadIdx.x * (SCAN_TILE / 256) + k;
+    v[k] = j < n ? tt[order[j]] : 0;
+    s += v[k];
+  }
+  uint32_t total;
+  uint32_t run = part[blockIdx.x] + block_exclusive_scan(s, s_warp, total);
+#pragma unroll
+  for (int k = 0; k < SCAN_TILE / 256; ++k) {
+    const int j = base + threadIdx.x * (SCAN_TILE / 256) + k;
+    if (j < n) offsets[j] = run;
+    run += v[k];
+  }
+}
+
+void launch_scan_tiles(const lp_frame &F, int n, cudaStream_t st) {
+  const int nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+  if (n > 0) k_scan_reduce<<<nb, 256, 0, st>>>(F.prim_order, F.tiles_touched, n, F.scan_tmp);
+  k_scan_top<<<1, 1024, 0, st>>>(F.scan_tmp, nb, F.offsets, n, F.counters, F.capacity);
+  if (n > 0) k_scan_down<<<nb, 256, 0, st>>>(F.prim_order, F.tiles_touched, n, F.scan_tmp, F.offsets);
+}
+
+// ---------------------------------------------------------------------------------------------
+// emission (a5): entries of sorted primitive j at [offsets[j], offsets[j] + tiles_touched)
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ order, const uint32_t *__restrict__ tt,
+                                              const uint32_t *__restrict__ offsets, const ushort4 *__restrict__ rect,
+                                              int n, int tiles_x, int64_t capacity, uint32_t *__restrict__ tile_key,
+                                              uint32_t *__restrict__ entry_val) {
+  const int lane = threadIdx.x & 31;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31;
+  const int j = j0 + lane;
+  uint32_t my_i = 0, my_tt = 0, my_off = 0;
+  ushort4 my_r = make_ushort4(0, 0, 0, 0);
+  if (j < n) {
+    my_i = order[j];
+    my_tt = tt[my_i];
+    if (my_tt) {
+      my_off = offsets[j];
+      my_r = rect[my_i];
+    }
+  }
+  unsigned todo = __ballot_sync(0xffffffffu, my_tt != 0);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const uint32_t i = __shfl_sync(0xffffffffu, my_i, src);
+    const uint32_t cntt = __shfl_sync(0xffffffffu, my_tt, src);
+    const uint32_t off = __shfl_sync(0xffffffffu, my_off, src);
+    const uint32_t tx0 = __shfl_sync(0xffffffffu, (uint32_t)my_r.x, src);
+    const uint32_t ty0 = __shfl_sync(0xffffffffu, (uint32_t)my_r.y, src);
+    const uint32_t tx1 = __shfl_sync(0xffffffffu, (uint32_t)my_r.z, src);
+    const uint32_t rw = tx1 - tx0 + 1;
+    for (uint32_t k = lane; k < cntt; k += 32) {
+      const uint32_t ty = ty0 + k / rw, tx = tx0 + k % rw;
+      const int64_t pos = (int64_t)off + k;
+      if (pos < capacity) {
+        tile_key[pos] = ty * (uint32_t)tiles_x + tx;
+        entry_val[pos] = i;
+      }
+    }
+  }
+}
+
+void launch_emit(const lp_frame &F, int n, cudaStream_t st) {
+  if (n == 0) return;
+  k_emit<<<(n + 255) / 256, 256, 0, st>>>(F.prim_order, F.tiles_touched, F.offsets,
+                                          reinterpret_cast<const ushort4 *>(F.rect), n, F.tiles_x, F.capacity,
+                                          F.tile_key, F.entry_val);
+}
+
+// ---------------------------------------------------------------------------------------------
+// per-tile ranges (a7)
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t *__restrict__ tile, const uint32_t *n_dev,
+                                                int64_t capacity, uint32_t *__restrict__ ranges) {
+  const int64_t E = item_count(n_dev, capacity);
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const uint32_t t = tile[e];
+  if (e == 0 || tile[e - 1] != t) ranges[2 * (size_t)t] = (uint32_t)e;
+  if (e == E - 1 || tile[e + 1] != t) ranges[2 * (size_t)t + 1] = (uint32_t)(e + 1);
+}
+
+void launch_ranges(const lp_frame &F, const uint32_t *sorted_tile, int tiles, cudaStream_t st) {
+  cudaMemsetAsync(F.ranges, 0, sizeof(uint32_t) * 2 * (size_t)tiles, st);
+  if (F.capacity <= 0) return;
+  const int64_t grid = (F.capacity + 255) / 256;
+  k_ranges<<<(unsigned)grid, 256, 0, st>>>(sorted_tile, F.counters + LP_CNT_ENTRIES, F.capacity, F.ranges);
+}
+
+}  // namespace lp

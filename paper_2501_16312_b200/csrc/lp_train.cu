@@ -1,0 +1,106 @@
+// lp_train.cu -- C5 helpers: L1 loss gradient and fused multi-group Adam.
+// Both are HBM-bound elementwise kernels: float4 vectorised, grid-stride over 148 x k CTAs.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lp_kernels.h"
+
+namespace lp {
+
+__global__ void __launch_bounds__(256) k_l1_grad(const float *__restrict__ img, const float *__restrict__ tgt,
+                                                 float *__restrict__ dL, float *__restrict__ loss, int64_t n,
+                                                 float scale) {
+  float s = 0.f;
+  const int64_t n4 = n / 4;
+  const float4 *i4 = reinterpret_cast<const float4 *>(img);
+  const float4 *t4 = reinterpret_cast<const float4 *>(tgt);
+  float4 *d4 = reinterpret_cast<float4 *>(dL);
+  const bool vec = ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(tgt) |
+                     reinterpret_cast<uintptr_t>(dL)) & 15) == 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec) {
+    for (int64_t i = i0; i < n4; i += stride) {
+      const float4 a = i4[i], b = t4[i];
+      const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z, dw = a.w - b.w;
+      s += fabsf(dx) + fabsf(dy) + fabsf(dz) + fabsf(dw);
+      d4[i] = make_float4(scale * (float)((dx > 0.f) - (dx < 0.f)), scale * (float)((dy > 0.f) - (dy < 0.f)),
+                          scale * (float)((dz > 0.f) - (dz < 0.f)), scale * (float)((dw > 0.f) - (dw < 0.f)));
+    }
+    i0 += n4 * 4;   // tail handled below
+    for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      const float d = img[i] - tgt[i];
+      s += fabsf(d);
+      dL[i] = scale * (float)((d > 0.f) - (d < 0.f));
+    }
+  } else {
+    for (int64_t i = i0; i < n; i += stride) {
+      const float d = img[i] - tgt[i];
+      s += fabsf(d);
+      dL[i] = scale * (float)((d > 0.f) - (d < 0.f));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ float sw[8];
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sw[w];
+    atomicAdd(loss, scale * t);
+  }
+}
+
+void launch_l1_grad(const float *img, const float *tgt, float *dL, float *loss, int64_t n, float scale,
+                    cudaStream_t st) {
+  if (n <= 0) return;
+  const int64_t want = (n / 4 + 255) / 256;
+  const int grid = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
+  k_l1_grad<<<grid, 256, 0, st>>>(img, tgt, dL, loss, n, scale);
+}
+
+struct AdamGroups {
+  int64_t begin[8], end[8];
+  float lr[8];
+  int n;
+};
+
+__global__ void __launch_bounds__(256) k_adam(float *__restrict__ p, const float *__restrict__ g, float *__restrict__ m,
+                                              float *__restrict__ v, AdamGroups G, float b1, float b2, float eps,
+                                              float bc1, float bc2) {
+  const int gi = blockIdx.y;
+  const int64_t b = G.begin[gi], e = G.end[gi];
+  const float lr = G.lr[gi];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += stride) {
+    const float gg = g[i];
+    const float mm = fmaf(b1, m[i], (1.f - b1) * gg);
+    const float vv = fmaf(b2, v[i], (1.f - b2) * gg * gg);
+    m[i] = mm;
+    v[i] = vv;
+    p[i] -= lr * (mm / bc1) / (sqrtf(vv / bc2) + eps);
+  }
+}
+
+void launch_adam(float *p, const float *g, float *m, float *v, const lp_adam_group *groups, int ng, float b1, float b2,
+                 float eps, int step, cudaStream_t st) {
+  for (int base = 0; base < ng; base += 8) {
+    AdamGroups G;
+    G.n = ng - base < 8 ? ng - base : 8;
+    int64_t longest = 1;
+    for (int k = 0; k < G.n; ++k) {
+      G.begin[k] = groups[base + k].begin;
+      G.end[k] = groups[base + k].end;
+      G.lr[k] = groups[base + k].lr;
+      if (G.end[k] - G.begin[k] > longest) longest = G.end[k] - G.begin[k];
+    }
+    for (int k = G.n; k < 8; ++k) { G.begin[k] = G.end[k] = 0; G.lr[k] = 0.f; }
+    const float bc1 = 1.f - powf(b1, (float)step), bc2 = 1.f - powf(b2, (float)step);
+    int64_t want = (longest + 255) / 256;
+    const int gx = (int)(want < 148 * 4 ? want : 148 * 4);
+    k_adam<<<dim3(gx, G.n), 256, 0, st>>>(p, g, m, v, G, b1, b2, eps, bc1, bc2);
+  }
+}
+
+}  // namespace lp

@@ -1,0 +1,207 @@
+"""Thin ctypes binding of liblinprim.so (include/linprim.h) -- argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C-ABI; this module only turns
+torch tensors / dicts into the C structs and calls the entry points with the same names.
+There is NO CPU fallback: importing this module without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblinprim.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(no CPU fallback exists)")
+_lib = C.CDLL(LIB_PATH)
+
+LP_OK, LP_ERR_ARG, LP_ERR_CAPACITY, LP_ERR_CUDA, LP_ERR_UNSUPPORTED = range(5)
+LP_OCTAHEDRON, LP_TETRAHEDRON = 0, 1
+LP_TILE = 16
+LP_CNT_ENTRIES, LP_CNT_OVERFLOW, LP_CNT_INVALID, LP_CNT_FRUSTUM, LP_CNT_VISIBLE = 0, 1, 2, 3, 4
+LP_CNT_ITERATED, LP_CNT_INTERSECTED, LP_NUM_COUNTERS = 8, 10, 16
+
+_p = C.c_void_p
+
+
+class lp_prims(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int32), ("sh_degree", C.c_int32),
+                ("pos", _p), ("rot", _p), ("dist", _p), ("opacity", _p), ("sh", _p), ("filter3d", _p)]
+
+
+class lp_camera(C.Structure):
+    _fields_ = [("W", C.c_float * 9), ("t", C.c_float * 3), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("znear", C.c_float),
+                ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class lp_raster_cfg(C.Structure):
+    _fields_ = [("aa_kernel", C.c_float), ("t_stop", C.c_float), ("bg", C.c_float * 3),
+                ("count_stats", C.c_int32)]
+
+
+class lp_frame(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
+                ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("capacity", C.c_int64),
+                ("record_words", C.c_int32), ("rgrad_words", C.c_int32)] + \
+        [(f, _p) for f in ("tiles_touched", "rect", "depth_key", "record", "prim_key", "prim_key_alt",
+                           "prim_order", "prim_order_alt", "offsets", "tile_key", "tile_key_alt", "entry_val",
+                           "entry_val_alt", "sorted_tile", "sorted_val", "ranges", "sort_hist", "scan_tmp",
+                           "counters", "T_final", "n_proc", "rgrad", "canon")]
+
+
+class lp_adam_group(C.Structure):
+    _fields_ = [("begin", C.c_int64), ("end", C.c_int64), ("lr", C.c_float)]
+
+
+class lp_grads(C.Structure):
+    _fields_ = [(f, _p) for f in ("pos", "rot", "dist", "opacity", "sh", "mean2d_abs")]
+
+
+_sig = {
+    "lp_abi_version": (C.c_int32, []),
+    "lp_status_string": (C.c_char_p, [C.c_int]),
+    "lp_frame_bytes": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32]),
+    "lp_frame_init": (C.c_int, [C.POINTER(lp_frame), _p, C.c_size_t, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                C.c_int64, C.c_int32]),
+    "lp_preprocess": (C.c_int, [C.POINTER(lp_prims), C.POINTER(lp_camera), C.c_int32, C.POINTER(lp_raster_cfg),
+                                C.POINTER(lp_frame), _p]),
+    "lp_bin_sort": (C.c_int, [C.POINTER(lp_camera), C.c_int32, C.POINTER(lp_frame), C.POINTER(C.c_int64), _p]),
+    "lp_render_fwd": (C.c_int, [C.POINTER(lp_camera), C.c_int32, C.POINTER(lp_raster_cfg), C.POINTER(lp_frame),
+                                _p, _p]),
+    "lp_render_bwd": (C.c_int, [C.POINTER(lp_prims), C.POINTER(lp_camera), C.c_int32, C.POINTER(lp_raster_cfg),
+                                C.POINTER(lp_frame), _p, C.POINTER(lp_grads), _p]),
+    "lp_frame_counters": (C.c_int, [C.POINTER(lp_frame), C.POINTER(C.c_uint32), _p]),
+    "lp_l1_grad": (C.c_int, [_p, _p, _p, _p, C.c_int64, C.c_float, _p]),
+    "lp_adam_step": (C.c_int, [_p, _p, _p, _p, C.POINTER(lp_adam_group), C.c_int32, C.c_float, C.c_float,
+                               C.c_float, C.c_int32, _p]),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTS = tuple(_sig)
+
+
+class LinPrimError(RuntimeError):
+    pass
+
+
+def _check(status, what):
+    if status != LP_OK:
+        raise LinPrimError(f"{what}: {lp_status_string(status)} ({status})")
+    return status
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    return C.c_void_p(stream) if isinstance(stream, int) else C.c_void_p(stream.cuda_stream)
+
+
+# ------------------------------------------------------------------ raw entry points (same names)
+
+def lp_abi_version() -> int:
+    return _lib.lp_abi_version()
+
+
+def lp_status_string(s) -> str:
+    return _lib.lp_status_string(int(s)).decode()
+
+
+def lp_frame_bytes(kind, n, width, height, capacity, with_canon=0) -> int:
+    return int(_lib.lp_frame_bytes(kind, n, width, height, capacity, with_canon))
+
+
+def lp_frame_init(frame, workspace, nbytes, kind, n, width, height, capacity, with_canon=0):
+    return _check(_lib.lp_frame_init(C.byref(frame), _ptr(workspace), nbytes, kind, n, width, height, capacity,
+                                     with_canon), "lp_frame_init")
+
+
+def lp_preprocess(prims, cams, cfg, frames, stream):
+    return _check(_lib.lp_preprocess(C.byref(prims), cams, len(cams), C.byref(cfg), frames, _stream(stream)),
+                  "lp_preprocess")
+
+
+def lp_bin_sort(cams, frames, stream, n_entries=None):
+    """n_entries: None (async) or a ctypes c_int64 array of len(cams) (synchronising, capacity checked)."""
+    st = _lib.lp_bin_sort(cams, len(cams), frames, n_entries, _stream(stream))
+    if st == LP_ERR_CAPACITY:
+        return st
+    return _check(st, "lp_bin_sort")
+
+
+def lp_render_fwd(cams, cfg, frames, image, stream):
+    return _check(_lib.lp_render_fwd(cams, len(cams), C.byref(cfg), frames, _ptr(image), _stream(stream)),
+                  "lp_render_fwd")
+
+
+def lp_render_bwd(prims, cams, cfg, frames, dL_dimage, grads, stream):
+    return _check(_lib.lp_render_bwd(C.byref(prims), cams, len(cams), C.byref(cfg), frames, _ptr(dL_dimage),
+                                     C.byref(grads), _stream(stream)), "lp_render_bwd")
+
+
+def lp_frame_counters(frame, stream) -> np.ndarray:
+    out = (C.c_uint32 * LP_NUM_COUNTERS)()
+    _check(_lib.lp_frame_counters(C.byref(frame), out, _stream(stream)), "lp_frame_counters")
+    return np.frombuffer(out, dtype=np.uint32).copy()
+
+
+def lp_l1_grad(image, target, dL, loss_sum, scale, stream):
+    return _check(_lib.lp_l1_grad(_ptr(image), _ptr(target), _ptr(dL), _ptr(loss_sum), image.numel(),
+                                  C.c_float(scale), _stream(stream)), "lp_l1_grad")
+
+
+def lp_adam_step(param, grad, m, v, groups, beta1, beta2, eps, step, stream):
+    arr = (lp_adam_group * len(groups))(*[lp_adam_group(int(b), int(e), float(lr)) for b, e, lr in groups])
+    return _check(_lib.lp_adam_step(_ptr(param), _ptr(grad), _ptr(m), _ptr(v), arr, len(groups), C.c_float(beta1),
+                                    C.c_float(beta2), C.c_float(eps), int(step), _stream(stream)), "lp_adam_step")
+
+
+# ------------------------------------------------------------------ struct builders
+
+def camera(cam) -> lp_camera:
+    c = lp_camera()
+    c.W[:] = [float(v) for v in np.asarray(cam["W"], np.float32).reshape(9)]
+    c.t[:] = [float(v) for v in np.asarray(cam["t"], np.float32).reshape(3)]
+    for k in ("fx", "fy", "cx", "cy", "znear"):
+        setattr(c, k, float(np.float32(cam[k])))
+    c.width, c.height = int(cam["width"]), int(cam["height"])
+    return c
+
+
+def cameras(cams):
+    arr = (lp_camera * len(cams))()
+    for i, c in enumerate(cams):
+        arr[i] = camera(c)
+    return arr
+
+
+def raster_cfg(aa_kernel=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), count_stats=False) -> lp_raster_cfg:
+    c = lp_raster_cfg()
+    c.aa_kernel, c.t_stop = float(aa_kernel), float(t_stop)
+    c.bg[:] = [float(b) for b in bg]
+    c.count_stats = 1 if count_stats else 0
+    return c
+
+
+def prims_struct(kind, n, sh_degree, pos, rot, dist, opacity, sh, filter3d=None) -> lp_prims:
+    p = lp_prims()
+    p.kind, p.n, p.sh_degree = int(kind), int(n), int(sh_degree)
+    p.pos, p.rot, p.dist, p.opacity, p.sh = (t.data_ptr() for t in (pos, rot, dist, opacity, sh))
+    p.filter3d = None if filter3d is None else filter3d.data_ptr()
+    return p
+
+
+def grads_struct(pos=None, rot=None, dist=None, opacity=None, sh=None, mean2d_abs=None) -> lp_grads:
+    g = lp_grads()
+    for f, t in (("pos", pos), ("rot", rot), ("dist", dist), ("opacity", opacity), ("sh", sh),
+                 ("mean2d_abs", mean2d_abs)):
+        setattr(g, f, None if t is None else t.data_ptr())
+    return g

@@ -1,0 +1,187 @@
+"""Device-resident scene + frame management around the C-ABI (marshalling and memory only).
+
+PyTorch provides device memory and streams; every computation is a liblinprim kernel.
+Features (and their gradients) live in ONE flat fp32 buffer laid out
+[pos 3N | rot 4N | dist KN | opacity N | sh (deg+1)^2*3N] so the C5 step can allreduce and Adam
+it as a single tensor.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import linprim as L
+
+
+def section_sizes(kind, n, sh_degree):
+    K = 3 if kind == L.LP_OCTAHEDRON else 4
+    return [("pos", 3 * n), ("rot", 4 * n), ("dist", K * n), ("opacity", n), ("sh", (sh_degree + 1) ** 2 * 3 * n)]
+
+
+class DeviceScene:
+    """Primitive features + gradient sinks in flat device buffers."""
+
+    def __init__(self, scene: dict, device="cuda", filter3d=None):
+        self.kind = int(scene["kind"])
+        self.sh_degree = int(scene["sh_degree"])
+        self.n = int(scene["pos"].shape[1])
+        self.K = 3 if self.kind == L.LP_OCTAHEDRON else 4
+        secs = section_sizes(self.kind, self.n, self.sh_degree)
+        total = sum(s for _, s in secs)
+        self.flat = torch.empty(total, dtype=torch.float32, device=device)
+        self.grad = torch.zeros(total, dtype=torch.float32, device=device)
+        self.offsets = {}
+        o = 0
+        for name, size in secs:
+            self.offsets[name] = (o, o + size)
+            src = torch.from_numpy(np.ascontiguousarray(scene[name], np.float32).reshape(-1))
+            self.flat[o:o + size].copy_(src)
+            o += size
+        self.filter3d = None if filter3d is None else torch.as_tensor(filter3d, dtype=torch.float32, device=device)
+        self.mean2d = None
+        self._rebuild()
+
+    def view(self, name, grad=False):
+        b, e = self.offsets[name]
+        return (self.grad if grad else self.flat)[b:e]
+
+    def _rebuild(self):
+        v = {k: self.view(k) for k in self.offsets}
+        self.prims = L.prims_struct(self.kind, self.n, self.sh_degree, v["pos"], v["rot"], v["dist"], v["opacity"],
+                                    v["sh"], self.filter3d)
+        g = {k: self.view(k, grad=True) for k in self.offsets}
+        self.grads = L.grads_struct(g["pos"], g["rot"], g["dist"], g["opacity"], g["sh"],
+                                    None if self.mean2d is None else self.mean2d)
+
+    def track_mean2d(self):
+        self.mean2d = torch.zeros(self.n, dtype=torch.float32, device=self.flat.device)
+        self._rebuild()
+
+    def grad_dict(self):
+        return {k: self.view(k, grad=True) for k in self.offsets}
+
+
+class Frame:
+    """One view's scratch: a device workspace carved by lp_frame_init."""
+
+    def __init__(self, kind, n, width, height, capacity, device="cuda", with_canon=False):
+        self.args = (kind, n, width, height, int(capacity), 1 if with_canon else 0)
+        nbytes = L.lp_frame_bytes(*self.args)
+        if nbytes == 0:
+            raise L.LinPrimError("lp_frame_bytes: invalid frame arguments")
+        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+        base = self.ws.data_ptr()
+        self.shift = (-base) % 256
+        self.c = L.lp_frame()
+        L._check(L._lib.lp_frame_init(C.byref(self.c), C.c_void_p(base + self.shift), nbytes, *self.args),
+                 "lp_frame_init")
+
+    @property
+    def capacity(self):
+        return self.c.capacity
+
+    def buf(self, field, count, dtype=torch.int32):
+        """Torch view of a frame buffer (device pointer inside the workspace)."""
+        ptr = getattr(self.c, field)
+        if ptr is None:
+            return None
+        off = ptr - self.ws.data_ptr()
+        item = torch.empty((), dtype=dtype).element_size()
+        return self.ws[off:off + count * item].view(dtype)
+
+
+def frames_array(frames):
+    arr = (L.lp_frame * len(frames))()
+    for i, f in enumerate(frames):
+        arr[i] = f.c
+    return arr
+
+
+def _store_back(frames, arr):
+    for i, f in enumerate(frames):
+        f.c = arr[i]
+
+
+def estimate_capacity(n, width, height):
+    return max(1 << 16, 8 * n + 4 * width * height)
+
+
+class Renderer:
+    """Forward / backward of the LinPrim tile rasterizer over a list of views (C-ABI calls only)."""
+
+    def __init__(self, scene: DeviceScene, cams, aa_kernel=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), capacity=None,
+                 with_canon=False, count_stats=False, sync_capacity=True):
+        self.scene = scene
+        self.cam_dicts = list(cams)
+        self.cams = L.cameras(self.cam_dicts)
+        self.cfg = L.raster_cfg(aa_kernel, t_stop, bg, count_stats)
+        self.with_canon = with_canon
+        self.sync_capacity = sync_capacity
+        dev = scene.flat.device
+        self.frames = []
+        for c in self.cam_dicts:
+            cap = capacity or estimate_capacity(scene.n, c["width"], c["height"])
+            self.frames.append(Frame(scene.kind, scene.n, c["width"], c["height"], cap, dev, with_canon))
+        self.sizes = [3 * c["width"] * c["height"] for c in self.cam_dicts]
+
+    def stream(self):
+        return torch.cuda.current_stream(self.scene.flat.device)
+
+    def _cams(self, views):
+        arr = (L.lp_camera * len(views))()
+        for i, v in enumerate(views):
+            arr[i] = self.cams[v]
+        return arr
+
+    def preprocess_and_sort(self, views=None):
+        views = list(range(len(self.frames))) if views is None else list(views)
+        st = self.stream()
+        for v in views:
+            cams = self._cams([v])
+            while True:
+                fa = frames_array([self.frames[v]])
+                L.lp_preprocess(self.scene.prims, cams, self.cfg, fa, st)
+                if self.sync_capacity:
+                    ne = (C.c_int64 * 1)()
+                    status = L.lp_bin_sort(cams, fa, st, ne)
+                    _store_back([self.frames[v]], fa)
+                    if status == L.LP_ERR_CAPACITY:
+                        c = self.cam_dicts[v]
+                        self.frames[v] = Frame(self.scene.kind, self.scene.n, c["width"], c["height"],
+                                               int(ne[0] * 1.25) + 1024, self.scene.flat.device, self.with_canon)
+                        continue
+                else:
+                    L.lp_bin_sort(cams, fa, st, None)
+                    _store_back([self.frames[v]], fa)
+                break
+
+    def render_views(self, image, views=None):
+        views = list(range(len(self.frames))) if views is None else list(views)
+        st = self.stream()
+        for i, v in enumerate(views):
+            fa = frames_array([self.frames[v]])
+            L.lp_render_fwd(self._cams([v]), self.cfg, fa, image[i], st)
+            _store_back([self.frames[v]], fa)
+
+    def forward(self, views=None, image=None):
+        views = list(range(len(self.frames))) if views is None else list(views)
+        if image is None:
+            c = self.cam_dicts[views[0]]
+            image = torch.empty((len(views), 3, c["height"], c["width"]), dtype=torch.float32,
+                                device=self.scene.flat.device)
+        self.preprocess_and_sort(views)
+        self.render_views(image, views)
+        return image
+
+    def backward(self, dL_dimage, views=None):
+        views = list(range(len(self.frames))) if views is None else list(views)
+        st = self.stream()
+        dL_dimage = dL_dimage.contiguous()
+        for i, v in enumerate(views):
+            fa = frames_array([self.frames[v]])
+            L.lp_render_bwd(self.scene.prims, self._cams([v]), self.cfg, fa, dL_dimage[i], self.scene.grads, st)
+
+    def counters(self, v=0):
+        return L.lp_frame_counters(self.frames[v].c, self.stream())

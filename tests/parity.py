@@ -1,0 +1,70 @@
+"""GPU-vs-oracle parity helpers (test-only).  Both sides get the same seeded inputs; the oracle
+supplies the decision margins used for masking."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+from tests.helpers import oscene
+
+STOP_MARGIN = 1e-4      # |ln(T/t_stop)| below this: the stop index may flip -> pixel masked
+FACE_MARGIN = 2e-5      # min barycentric below this: entry/exit face may switch -> primitive flagged
+IMG_TOL = 1e-4          # north_star: images within 1e-4 max abs (fp32)
+GRAD_RTOL = 1e-3        # north_star: gradients within 1e-3 relative ...
+GRAD_ATOL_REL = 1e-5    # ... or 1e-5 absolute, in units of the group's largest |gradient|
+
+
+def gpu_run(scene, cams, G=None, kappa=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), with_canon=True, capacity=None,
+            count_stats=True, filter3d=None):
+    import torch
+
+    from paper_2501_16312_b200 import render
+    ds = render.DeviceScene(scene, filter3d=filter3d)
+    r = render.Renderer(ds, cams, aa_kernel=kappa, t_stop=t_stop, bg=bg, with_canon=with_canon,
+                        capacity=capacity, count_stats=count_stats)
+    img = r.forward()
+    if G is not None:
+        r.backward(torch.as_tensor(G, device="cuda").reshape(img.shape))
+    torch.cuda.synchronize()
+    return ds, r, img
+
+
+def frame_arrays(r, v, n, K):
+    f = r.frames[v]
+    import torch
+    W, H = f.c.width, f.c.height
+    cnt = r.counters(v)
+    E = int(cnt[0])
+    out = {
+        "tiles_touched": f.buf("tiles_touched", n, torch.int32).cpu().numpy().view(np.uint32),
+        "rect": f.buf("rect", 4 * n, torch.int16).cpu().numpy().view(np.uint16).reshape(n, 4).astype(np.int32),
+        "depth_key": f.buf("depth_key", n, torch.int32).cpu().numpy().view(np.uint32),
+        "E": E,
+        "sorted_val": f.buf("sorted_val", E, torch.int32).cpu().numpy().view(np.uint32),
+        "sorted_tile": f.buf("sorted_tile", E, torch.int32).cpu().numpy().view(np.uint32),
+        "ranges": f.buf("ranges", 2 * f.c.tiles_x * f.c.tiles_y, torch.int32).cpu().numpy().view(np.uint32).reshape(-1, 2),
+        "T_final": f.buf("T_final", W * H, torch.float32).cpu().numpy().reshape(H, W),
+        "n_proc": f.buf("n_proc", W * H, torch.int32).cpu().numpy().reshape(H, W),
+        "counters": cnt,
+    }
+    if f.c.canon:
+        out["canon"] = f.buf("canon", n * (2 + 3 * K), torch.float32).cpu().numpy().reshape(n, 2 + 3 * K)
+    return out
+
+
+def grad_close(name, got, ref, flagged=None, rtol=GRAD_RTOL, atol_rel=GRAD_ATOL_REL, loose=1e-1):
+    """Element-wise |got - ref| <= rtol |ref| + atol_rel * max|ref|; flagged primitives (last axis)
+    only at the loose bound.  Returns (ok, worst ratio, report)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    scale = np.abs(ref).max() if ref.size else 0.0
+    if scale == 0.0:
+        return np.abs(got).max() == 0.0 if got.size else True, 0.0, f"{name}: all zero"
+    tol = rtol * np.abs(ref) + atol_rel * scale
+    ratio = np.abs(got - ref) / tol
+    if flagged is not None and flagged.any():
+        lt = loose * (np.abs(ref) + 1e-2 * scale)
+        ratio[..., flagged] = (np.abs(got - ref) / lt)[..., flagged]
+    worst = float(ratio.max())
+    idx = np.unravel_index(int(np.argmax(ratio)), ratio.shape)
+    return worst <= 1.0, worst, f"{name}: worst {worst:.3g} at {idx} got {got[idx]:.6g} ref {ref[idx]:.6g} scale {scale:.3g}"

@@ -1,0 +1,92 @@
+"""C-ABI boundary checks that need no GPU: the library builds/loads, exports every symbol that
+include/linprim.h declares, and validates arguments before touching the device."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "linprim.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2501_16312_b200 import _build
+    _build.build()
+    import paper_2501_16312_b200.linprim as L
+    return L
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lp_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_four_hot_path_calls():
+    names = declared_functions()
+    for f in ("lp_preprocess", "lp_bin_sort", "lp_render_fwd", "lp_render_bwd"):
+        assert f in names
+
+
+def test_library_exports_every_declared_symbol(L):
+    lib = C.CDLL(L.LIB_PATH)
+    names = declared_functions()
+    assert names, "no declarations parsed"
+    for name in names:
+        assert hasattr(lib, name), f"{name} declared in linprim.h but not exported"
+    assert set(names) == set(L.EXPORTS), "binding and header disagree"
+
+
+def test_abi_version_and_status_strings(L):
+    assert L.lp_abi_version() == 1
+    assert L.lp_status_string(L.LP_OK) == "ok"
+    assert "capacity" in L.lp_status_string(L.LP_ERR_CAPACITY)
+
+
+def test_struct_sizes_match_header_layout(L):
+    # lp_camera: 9+3+5 floats + 2 ints = 76 B; lp_raster_cfg: 5 floats + 1 int = 24 B
+    assert C.sizeof(L.lp_camera) == 76
+    assert C.sizeof(L.lp_raster_cfg) == 24
+    assert C.sizeof(L.lp_prims) == 12 + 4 + 6 * 8
+    assert C.sizeof(L.lp_adam_group) == 24
+
+
+def test_frame_bytes(L):
+    a = L.lp_frame_bytes(L.LP_OCTAHEDRON, 1000, 128, 128, 100000, 0)
+    b = L.lp_frame_bytes(L.LP_OCTAHEDRON, 1000, 128, 128, 200000, 0)
+    c = L.lp_frame_bytes(L.LP_TETRAHEDRON, 1000, 128, 128, 100000, 1)
+    assert 0 < a < b and c > a
+    assert L.lp_frame_bytes(7, 1000, 128, 128, 100, 0) == 0          # bad kind
+    assert L.lp_frame_bytes(L.LP_OCTAHEDRON, 10, 0, 128, 100, 0) == 0  # bad size
+
+
+def test_arguments_validated_before_any_launch(L):
+    """Null / inconsistent arguments return LP_ERR_ARG without touching the device."""
+    lib = L._lib
+    cfg = L.raster_cfg()
+    cams = L.cameras([{"W": [[1, 0, 0], [0, 1, 0], [0, 0, 1]], "t": [0, 0, 0], "fx": 10, "fy": 10, "cx": 8,
+                       "cy": 8, "znear": 0.2, "width": 16, "height": 16}])
+    p = L.lp_prims()
+    p.kind, p.n, p.sh_degree = 5, 1, 0                        # bad kind
+    frames = (L.lp_frame * 1)()
+    assert lib.lp_preprocess(C.byref(p), cams, 1, C.byref(cfg), frames, None) == L.LP_ERR_ARG
+    p.kind, p.sh_degree = 0, 4                                # bad SH degree
+    assert lib.lp_preprocess(C.byref(p), cams, 1, C.byref(cfg), frames, None) == L.LP_ERR_ARG
+    p.sh_degree = 0                                           # null feature pointers
+    assert lib.lp_preprocess(C.byref(p), cams, 1, C.byref(cfg), frames, None) == L.LP_ERR_ARG
+    assert lib.lp_bin_sort(cams, 1, frames, None, None) == L.LP_ERR_ARG          # frame not initialised
+    assert lib.lp_render_fwd(cams, 1, C.byref(cfg), frames, None, None) == L.LP_ERR_ARG
+    assert lib.lp_frame_init(C.byref(frames[0]), None, 0, 0, 1, 16, 16, 10, 0) == L.LP_ERR_ARG
+    assert lib.lp_adam_step(None, None, None, None, None, 0, 0.9, 0.999, 1e-15, 1, None) == L.LP_ERR_ARG
+
+
+def test_no_oracle_in_product_path():
+    """The product package never imports the oracle (no CPU fallback)."""
+    pkg = os.path.join(ROOT, "paper_2501_16312_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "lpo_" not in txt, f

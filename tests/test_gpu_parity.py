@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Bit-exact: tiles_touched, tile rect, depth key, canonical geometry bits, sorted (tile, id) list,
+per-tile ranges.  Tolerances (north_star): image max |err| <= 1e-4; gradients |err| <= 1e-3 |g| +
+1e-5 * max|g| per group.  Stop-index flips and entry/exit-face switches are masked / flagged from
+the oracle's margins; the counts are asserted to stay small.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2501_16312_b200 import scenegen
+from tests import parity as PT
+from tests.canonical_np import canonical
+from tests.helpers import oscene
+
+pytestmark = pytest.mark.gpu
+
+OCTA, TETRA = scenegen.OCTA, scenegen.TETRA
+K_OF = {OCTA: 3, TETRA: 4}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    assert torch.cuda.is_available(), "gpu tests need CUDA"
+    from paper_2501_16312_b200 import _build
+    _build.build()
+    torch.cuda.set_device(0)
+
+
+def check_preprocess(scene, cam, r, v=0, kappa=0.1, filter3d=None):
+    n = scene["pos"].shape[1]
+    K = K_OF[scene["kind"]]
+    got = PT.frame_arrays(r, v, n, K)
+    pre = oracle.preprocess(oscene(scene, filter3d), cam, kappa=kappa, mode=0)
+    assert np.array_equal(got["tiles_touched"], pre.tiles_touched), "tiles_touched"
+    assert np.array_equal(got["rect"], pre.rect), "rect"
+    assert np.array_equal(got["depth_key"], pre.depth_key), "depth key"
+    if "canon" in got:
+        assert np.array_equal(got["canon"].view(np.uint32), pre.canon.view(np.uint32)), "canonical geometry bits"
+    c = got["counters"]
+    assert c[2] == int((pre.flag == 1).sum()) and c[3] == int((pre.flag == 0).sum())
+    assert c[4] == int((pre.tiles_touched > 0).sum())
+    return got, pre
+
+
+def check_binning(got, pre, cam):
+    keys, vals, ranges = oracle.bin_tiles(pre, cam["width"], cam["height"])
+    assert got["E"] == len(vals)
+    assert np.array_equal(got["sorted_val"], vals), "sorted ids"
+    assert np.array_equal(got["sorted_tile"].astype(np.uint64), keys >> np.uint64(32)), "sorted tiles"
+    assert np.array_equal(got["ranges"].astype(np.int64), ranges), "ranges"
+    # the full 64-bit (tile | depth) key of every entry, reconstructed
+    k64 = (got["sorted_tile"].astype(np.uint64) << np.uint64(32)) | got["depth_key"][got["sorted_val"]].astype(np.uint64)
+    assert np.array_equal(k64, keys)
+    return keys, vals, ranges
+
+
+def full_parity(scene, cam, kappa=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), seed=0, grads=True, filter3d=None,
+                max_masked=0.01, max_flagged=0.05):
+    W, H = cam["width"], cam["height"]
+    osc = oscene(scene, filter3d)
+    f0 = oracle.forward(osc, cam, kappa=kappa, t_stop=t_stop, bg=bg)
+    mask = f0.out.m_stop < PT.STOP_MARGIN
+    assert mask.mean() <= max_masked, f"too many stop-margin pixels {mask.mean()}"
+    G = scenegen.upstream_grad(W, H, seed=seed)[0] * (~mask)[None].astype(np.float32) if grads else None
+    ds, r, img = PT.gpu_run(scene, [cam], G=G, kappa=kappa, t_stop=t_stop, bg=bg, filter3d=filter3d)
+    got, pre = check_preprocess(scene, cam, r, kappa=kappa, filter3d=filter3d)
+    check_binning(got, pre, cam)
+    im = img[0].cpu().numpy()
+    err = np.abs(im - f0.out.image)[:, ~mask]
+    assert err.max(initial=0.0) <= PT.IMG_TOL, f"image max err {err.max()}"
+    assert np.abs(got["T_final"] - f0.out.T_final)[~mask].max(initial=0.0) <= PT.IMG_TOL
+    assert np.array_equal(got["n_proc"][~mask], f0.out.n_proc[~mask]), "n_proc"
+    assert got["counters"][8] == int(f0.out.n_proc.sum()) or mask.any()
+    if not grads:
+        return
+    fb, g = oracle.forward_backward(osc, cam, G, kappa=kappa, t_stop=t_stop, bg=bg)
+    flagged = fb.out.face_margin < PT.FACE_MARGIN
+    touched = np.isfinite(fb.out.face_margin)
+    assert flagged.sum() <= max(2, max_flagged * touched.sum()), f"flagged {flagged.sum()} of {touched.sum()}"
+    gd = ds.grad_dict()
+    n = scene["pos"].shape[1]
+    reports = []
+    for name, ref, fl in (("pos", g.pos, flagged), ("rot", g.rot, flagged), ("dist", g.dist, flagged),
+                          ("opacity", g.opacity, None), ("sh", g.sh, None)):
+        got_g = gd[name].cpu().numpy().reshape(ref.shape)
+        ok, worst, rep = PT.grad_close(name, got_g, ref, fl)
+        reports.append(rep)
+        assert ok, "; ".join(reports)
+    return reports
+
+
+# ------------------------------------------------------------------------------------------------
+
+def test_c1_full_forward_backward():
+    """configs[0]: 1k random octahedra, SH deg 0, 128x128, fwd+bwd vs the oracle."""
+    scene, cams = scenegen.make_scene("C1", seed=0)
+    full_parity(scene, cams[0])
+
+
+@pytest.mark.parametrize("kind", [OCTA, TETRA])
+@pytest.mark.parametrize("seed", range(6))
+def test_random_small_scenes(kind, seed):
+    scene, cam = scenegen.small_scene(kind, 300, seed=seed, width=96, height=72, sh_degree=seed % 4,
+                                      opacity_mu=0.5 * (seed % 3))
+    full_parity(scene, cam, seed=seed, bg=(0.1, 0.2, 0.3) if seed % 2 else (0, 0, 0))
+
+
+@pytest.mark.parametrize("kind", [OCTA, TETRA])
+@pytest.mark.parametrize("kappa,t_stop", [(0.0, 1e-3), (0.1, 0.0), (0.5, 1e-2)])
+def test_filter_and_stop_variants(kind, kappa, t_stop):
+    scene, cam = scenegen.small_scene(kind, 250, seed=11, width=80, height=64, sh_degree=2, opacity_mu=1.0)
+    full_parity(scene, cam, kappa=kappa, t_stop=t_stop, seed=3)
+
+
+@pytest.mark.parametrize("kind", [OCTA, TETRA])
+def test_3d_filter(kind):
+    scene, cam = scenegen.small_scene(kind, 200, seed=12, width=64, height=48, sh_degree=1)
+    f3 = np.random.default_rng(0).uniform(0.0, 0.05, 200).astype(np.float32)
+    full_parity(scene, cam, filter3d=f3, seed=4)
+
+
+@pytest.mark.parametrize("kind", [OCTA, TETRA])
+@pytest.mark.parametrize("seed", range(3))
+def test_edge_scenes(kind, seed):
+    """Tile-border stragglers, off-screen, behind camera, znear, sub-pixel, huge, alpha ~ 0,
+    duplicate depths, zero quaternion, d <= 0, NaN; image size not a multiple of 16."""
+    scene, cam = scenegen.edge_scene(kind, seed=seed)
+    full_parity(scene, cam, seed=seed)
+
+
+def test_canonical_matches_numpy_arbiter_on_gpu():
+    scene, cam = scenegen.small_scene(OCTA, 5000, seed=5, width=333, height=211)
+    ds, r, img = PT.gpu_run(scene, [cam])
+    got = PT.frame_arrays(r, 0, 5000, 3)
+    ref = canonical(scene, cam, kappa=0.1)
+    assert np.array_equal(got["canon"].view(np.uint32), ref["canon"].view(np.uint32))
+    assert np.array_equal(got["tiles_touched"], ref["tiles_touched"])
+
+
+def test_empty_and_degenerate_inputs():
+    import torch
+    # all primitives culled
+    scene, cam = scenegen.small_scene(OCTA, 50, seed=1, width=40, height=30)
+    scene["pos"][2] = -5.0
+    ds, r, img = PT.gpu_run(scene, [cam], G=np.ones((3, 30, 40), np.float32), bg=(0.25, 0.5, 0.75))
+    assert torch.allclose(img[0, 0], torch.full_like(img[0, 0], 0.25))
+    assert float(ds.grad.abs().max()) == 0.0
+    # a single primitive, 1x1 image
+    scene, cam = scenegen.small_scene(TETRA, 1, seed=2, width=1, height=1)
+    full_parity(scene, cam, seed=1)
+
+
+def test_multi_view_call_and_accumulation():
+    """Two views in one Renderer: gradients accumulate (+=) over views."""
+    import torch
+    scene, cams = scenegen.make_scene("C5", seed=0, n=3000)
+    cams = [dict(c, width=96, height=64, cx=np.float32(48), cy=np.float32(32),
+                 fx=np.float32(83.1), fy=np.float32(83.1)) for c in cams[:2]]
+    G = scenegen.upstream_grad(96, 64, seed=0, n_views=2)
+    ds, r, img = PT.gpu_run(scene, cams, G=G)
+    osc = oscene(scene)
+    tot = None
+    for v in range(2):
+        f, g = oracle.forward_backward(osc, cams[v], G[v])
+        assert np.abs(img[v].cpu().numpy() - f.out.image).max() <= PT.IMG_TOL
+        tot = g.opacity if tot is None else tot + g.opacity
+    ok, worst, rep = PT.grad_close("opacity", ds.grad_dict()["opacity"].cpu().numpy(), tot)
+    assert ok, rep
+
+
+def test_capacity_error_and_async_overflow_flag():
+    import ctypes as C
+
+    import torch
+
+    from paper_2501_16312_b200 import linprim as L
+    from paper_2501_16312_b200 import render
+    scene, cam = scenegen.small_scene(OCTA, 400, seed=3, width=64, height=48)
+    ds = render.DeviceScene(scene)
+    fr = render.Frame(ds.kind, ds.n, 64, 48, capacity=16)
+    cams = L.cameras([cam])
+    cfg = L.raster_cfg()
+    fa = render.frames_array([fr])
+    st = torch.cuda.current_stream()
+    L.lp_preprocess(ds.prims, cams, cfg, fa, st)
+    ne = (C.c_int64 * 1)()
+    assert L.lp_bin_sort(cams, fa, st, ne) == L.LP_ERR_CAPACITY
+    pre = oracle.preprocess(oscene(scene), cam)
+    assert ne[0] == int(pre.tiles_touched.sum())
+    L.lp_preprocess(ds.prims, cams, cfg, fa, st)
+    L.lp_bin_sort(cams, fa, st, None)                     # async: no truncation is silent
+    cnt = L.lp_frame_counters(fa[0], st)
+    assert cnt[L.LP_CNT_OVERFLOW] == 1 and cnt[L.LP_CNT_ENTRIES] == ne[0]
+
+
+def test_l1_grad_and_adam_vs_torch():
+    import torch
+
+    from paper_2501_16312_b200 import linprim as L
+    g = torch.Generator(device="cuda").manual_seed(0)
+    a = torch.rand(3 * 37 * 29 + 3, device="cuda", generator=g)
+    b = torch.rand(a.numel(), device="cuda", generator=g)
+    dL = torch.empty_like(a)
+    loss = torch.zeros(1, device="cuda")
+    st = torch.cuda.current_stream()
+    L.lp_l1_grad(a, b, dL, loss, 0.5, st)
+    assert torch.equal(dL, 0.5 * torch.sign(a - b))
+    assert torch.allclose(loss, 0.5 * (a - b).abs().sum(), rtol=1e-5)
+    p = torch.randn(1000, device="cuda", generator=g)
+    gr = torch.randn(1000, device="cuda", generator=g)
+    m = torch.zeros_like(p)
+    v = torch.zeros_like(p)
+    p_ref, m_ref, v_ref = p.clone(), m.clone(), v.clone()
+    groups = [(0, 300, 1e-3), (300, 900, 2.5e-2)]
+    for step in (1, 2, 3):
+        L.lp_adam_step(p, gr, m, v, groups, 0.9, 0.999, 1e-15, step, st)
+        m_ref = 0.9 * m_ref + 0.1 * gr
+        v_ref = 0.999 * v_ref + 0.001 * gr * gr
+        for b0, e0, lr in groups:
+            mh = m_ref[b0:e0] / (1 - 0.9 ** step)
+            vh = v_ref[b0:e0] / (1 - 0.999 ** step)
+            p_ref[b0:e0] -= lr * mh / (vh.sqrt() + 1e-15)
+        m_ref[900:] = 0
+        v_ref[900:] = 0
+    assert torch.allclose(p, p_ref, rtol=1e-5, atol=1e-6)
+    assert torch.equal(p[900:], p_ref[900:])
