@@ -1,0 +1,443 @@
+#!/usr/bin/env python
+"""bench.py -- LinPrim (arXiv 2501.16312) training-step benchmark on B200.
+
+Workload (BASELINE.json configs[4], the config its metric "fwd+bwd Mpixel/s and train iters/s at
+1/2/4/8 B200" is quoted on): 1M octahedra, SH degree 3, a batch of 8 views at 1600x1060, one
+training step = for each local view: lp_preprocess -> lp_bin_sort -> lp_render_fwd -> lp_l1_grad
+-> lp_raster_bwd -> lp_preprocess_bwd; then (N > 1) one NCCL allreduce of the flat gradient; then
+one fused Adam (lp_adam_step, also zeroing the gradient).  Views are sharded views[r::N] over
+ranks (strong scaling, fixed global batch of 8).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+--impl reference times the CPU oracle (oracle/, plain C fp64) on a bounded pixel sample of the
+same workload on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOAD = "C5"
+PAPER_FPS_CONTEXT = "paper (RTX 3090, forward only): octahedra 14.6 ms ScanNet++ 1752x1168, 34.6 ms Mip-NeRF360"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=None, help="override the primitive count (debug)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ clocks sampler
+
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.idx), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if r[4 + k].lower() == "active":
+                    reasons.add(nm)
+        load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------ work model
+
+def fp32_ops(kind, iterated, intersected, backward):
+    """Algorithmic FP32-pipe lane instructions: octahedron chord 26 per iterated pair,
+    tetrahedron 20; opacity + compositing 11 per intersected pair (forward); the backward replays the
+    chord (+6 argmax selects) and spends 61 per intersected pair (blend + moments)."""
+    chord = 26 if kind == 0 else 20
+    if not backward:
+        return chord * iterated + 11 * intersected
+    return (chord + 6) * iterated + 61 * intersected
+
+
+def launches_per_view(n, tiles):
+    bits = max(1, math.ceil(math.log2(tiles)))
+    tile_passes = math.ceil(bits / 8)
+    sort_prims = 4 * 3
+    return 1 + sort_prims + 3 + 1 + 3 * tile_passes + 1 + 1 + 1 + 1 + 1   # K1 | depth sort | scan | emit | tile sort | ranges | fwd | l1 | raster bwd | pre bwd
+
+
+# ------------------------------------------------------------------------------ our implementation
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_16312_b200 import linprim as L
+    from paper_2501_16312_b200 import render, scenegen
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    scene, cams = scenegen.make_scene(WORKLOAD, seed=args.seed, n=args.n)
+    n_views = len(cams)
+    W, H = cams[0]["width"], cams[0]["height"]
+    my_views = list(range(rank, n_views, world))
+    ds = render.DeviceScene(scene, device=dev)
+
+    # synthetic targets: the same scene with jittered centres, rendered once at setup
+    rng = np.random.default_rng(1234)
+    tgt_scene = dict(scene)
+    tgt_scene["pos"] = (scene["pos"] + rng.normal(0, 0.01, scene["pos"].shape) *
+                        scene["dist"].mean(0, keepdims=True)).astype(np.float32)
+    tds = render.DeviceScene(tgt_scene, device=dev)
+    trend = render.Renderer(tds, [cams[v] for v in my_views])
+    targets = trend.forward()
+    torch.cuda.synchronize()
+    del trend, tds
+
+    # counters pass (untimed): per-view E, iterated and intersected pairs
+    rr = render.Renderer(ds, [cams[v] for v in my_views], count_stats=True)
+    img = torch.empty((len(my_views), 3, H, W), dtype=torch.float32, device=dev)
+    rr.forward(image=img)
+    torch.cuda.synchronize()
+    stats = [rr.counters(i) for i in range(len(my_views))]
+    caps = [rr.frames[i].capacity for i in range(len(my_views))]
+    del rr
+    E = [int(s[L.LP_CNT_ENTRIES]) for s in stats]
+    it = [int(s[8]) | (int(s[9]) << 32) for s in stats]
+    hit = [int(s[10]) | (int(s[11]) << 32) for s in stats]
+    frustum = [int(s[L.LP_CNT_FRUSTUM]) for s in stats]
+
+    # the timed renderer: async binning (no host sync), capacity sized from the counters pass
+    rend = render.Renderer(ds, [cams[v] for v in my_views], capacity=int(max(E) * 1.3) + 4096,
+                           sync_capacity=False)
+    st = torch.cuda.current_stream(dev)
+    dL = torch.empty_like(img)
+    n_local = len(my_views)
+    total_steps = args.warmup + args.steps
+    loss_buf = torch.zeros(2 * total_steps + 64, dtype=torch.float32, device=dev)
+    m = torch.zeros_like(ds.flat)
+    v = torch.zeros_like(ds.flat)
+    # paper's learning rates; position 1.6e-4 x extent (3DGS), distances 2.6^-1 1e-4 x extent
+    extent = 4.0
+    off = ds.offsets
+    n = ds.n
+    groups = [(off["pos"][0], off["pos"][1], 1.6e-4 * extent), (off["rot"][0], off["rot"][1], 1e-3),
+              (off["dist"][0], off["dist"][1], 1e-4 / 2.6 * extent), (off["opacity"][0], off["opacity"][1], 2.5e-2),
+              (off["sh"][0], off["sh"][0] + 3 * n, 2.5e-3), (off["sh"][0] + 3 * n, off["sh"][1], 1.25e-4)]
+    scale = 1.0 / (3.0 * W * H * n_views)
+    cams_c = rend.cams
+    ev_names = ["pre", "sort", "fwd", "l1", "rbwd", "pbwd"]
+
+    def step(si, events=None):
+        for i in range(n_local):
+            ca = rend._cams([i])
+            fa = render.frames_array([rend.frames[i]])
+            if events is not None:
+                events[i][0].record(st)
+            L.lp_preprocess(ds.prims, ca, rend.cfg, fa, st)
+            if events is not None:
+                events[i][1].record(st)
+            L.lp_bin_sort(ca, fa, st, None)
+            if events is not None:
+                events[i][2].record(st)
+            L.lp_render_fwd(ca, rend.cfg, fa, img[i], st)
+            if events is not None:
+                events[i][3].record(st)
+            L.lp_l1_grad(img[i], targets[i], dL[i], loss_buf[si:si + 1], scale, st)
+            if events is not None:
+                events[i][4].record(st)
+            L.lp_raster_bwd(ca, rend.cfg, fa, dL[i], st)
+            if events is not None:
+                events[i][5].record(st)
+            L.lp_preprocess_bwd(ds.prims, ca, rend.cfg, fa, ds.grads, st)
+            if events is not None:
+                events[i][6].record(st)
+            render._store_back([rend.frames[i]], fa)
+        if world > 1:
+            dist.all_reduce(ds.grad)
+        if events is not None:
+            events[n_local][0].record(st)
+        L.lp_adam_step(ds.flat, ds.grad, m, v, groups, 0.9, 0.999, 1e-15, si + 1, st, zero_grad=True)
+        if events is not None:
+            events[n_local][1].record(st)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for s in range(args.warmup):
+        step(s)
+    barrier()
+    # overflow check after warm-up (async binning must not have truncated)
+    for i in range(n_local):
+        c = rend.counters(i)
+        assert c[L.LP_CNT_OVERFLOW] == 0, "tile-list capacity overflow in the timed renderer"
+
+    vis = [s for s in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if s.strip().isdigit()]
+    clocks = ClockSampler(int(vis[local_rank]) if local_rank < len(vis) else local_rank)
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(n_local)] + [
+        [torch.cuda.Event(enable_timing=True) for _ in range(2)]] for _ in range(args.steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    wall0 = time.perf_counter()
+    t0.record(st)
+    for k in range(args.steps):
+        step(args.warmup + k, evs[k])
+    t1.record(st)
+    barrier()
+    wall = time.perf_counter() - wall0
+    clocks.stop()
+    ms = t0.elapsed_time(t1)
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    ms_step = ms_max / args.steps
+
+    # per-stage averages (ms per view-call) from the timed region's events
+    stage = {nm: [] for nm in ev_names}
+    ar_adam = []
+    for k in range(args.steps):
+        for i in range(n_local):
+            e = evs[k][i]
+            for j, nm in enumerate(ev_names):
+                stage[nm].append(e[j].elapsed_time(e[j + 1]))
+        ar_adam.append(evs[k][n_local][0].elapsed_time(evs[k][n_local][1]))
+    stage_ms = {nm: statistics.mean(vals) for nm, vals in stage.items()}
+    stage_ms["adam"] = statistics.mean(ar_adam)
+
+    # roofline of the dominant kernel (raster forward or backward; both FP32-pipe bound)
+    kind = ds.kind
+    I_tot, X_tot = sum(it), sum(hit)
+    dom = "rbwd" if stage_ms["rbwd"] >= stage_ms["fwd"] else "fwd"
+    ops_per_launch = fp32_ops(kind, I_tot / n_local, X_tot / n_local, backward=(dom == "rbwd"))
+    achieved = ops_per_launch / (stage_ms[dom] * 1e-3) / 1e12          # T lane-instr / s
+    sm_max = 1965.0
+    peak = 148 * 128 * sm_max * 1e6 / 1e12                              # FP32 issue: 148 SM x 128 lanes x clock
+    traffic = None
+    prof_path = os.path.join(ROOT, "profiles", "latest_traffic.json")
+    if os.path.exists(prof_path):
+        try:
+            traffic = json.load(open(prof_path)).get("k_raster_bwd" if dom == "rbwd" else "k_raster_fwd")
+        except Exception:
+            traffic = None
+
+    views_total = n_views
+    mpix = views_total * W * H / 1e6
+    value = mpix / (ms_step * 1e-3)
+    iters = 1000.0 / ms_step
+
+    # ---------------- e2e: host (pinned) targets copied in and the loss read back every step
+    e2e = None
+    if not args.no_e2e:
+        host_t = torch.empty(targets.shape, dtype=torch.float32, pin_memory=True)
+        host_t.copy_(targets)
+        dev_t = torch.empty_like(targets)
+        loss_host = torch.empty(1, dtype=torch.float32, pin_memory=True)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(st)
+        for k in range(args.steps):
+            dev_t.copy_(host_t, non_blocking=True)
+            targets_saved = targets
+            targets = dev_t
+            step(total_steps + k if total_steps + k < loss_buf.numel() else 0)
+            targets = targets_saved
+            loss_host.copy_(loss_buf[(total_steps + k) % loss_buf.numel():][:1], non_blocking=True)
+            st.synchronize()
+        e1.record(st)
+        barrier()
+        e2e_ms = e0.elapsed_time(e1)
+        t = torch.tensor([e2e_ms], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_step = float(t.item()) / args.steps
+        e2e = {"value": round(mpix / (e2e_step * 1e-3), 3), "unit": "Mpixel/s",
+               "h2d_bytes_per_step": int(host_t.numel() * 4 * world), "d2h_bytes_per_step": 4 * world,
+               "ms_per_step": round(e2e_step, 3)}
+
+    launches = args.steps * (n_local * launches_per_view(n, rend.frames[0].c.tiles_x * rend.frames[0].c.tiles_y) + 1)
+
+    out = {
+        "metric": "fwd+bwd Mpixel/s (C5 training step: 8 views, fwd+bwd+allreduce+Adam)",
+        "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded scenegen, BASELINE configs[4] shape; random-init features)",
+        "iters_per_s": round(iters, 3),
+        "config": {"workload": "C5: 1M octahedra, SH deg 3, 8 views 1600x1060, training step (views sharded)",
+                   "n_primitives": n, "kind": "octahedron", "sh_degree": 3, "global_batch_views": views_total,
+                   "views_per_gpu": n_local, "width": W, "height": H, "parallelism": f"dp{world} (views)",
+                   "l2": "inputs larger than L2: features+grads+Adam state = %.2f GB touched per step"
+                         % (ds.flat.numel() * 4 * 5 / 1e9),
+                   "tile_list_entries_per_view": E, "iterated_pairs_per_px": round(I_tot / (n_local * W * H), 2),
+                   "intersected_pairs_per_px": round(X_tot / (n_local * W * H), 2),
+                   "frustum_primitives_per_view": frustum, "capacity": caps},
+        "stages_ms_per_view": {k: round(v, 4) for k, v in stage_ms.items()},
+        "roofline": {"kernel": "k_raster_bwd" if dom == "rbwd" else "k_raster_fwd", "bound": "alu",
+                     "achieved": round(achieved, 3), "peak": round(peak, 3),
+                     "unit": "T FP32 lane-instr/s (peak = 148 SM x 128 lanes x 1965 MHz, B200_PROFILING unit counts)",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "ops_per_launch": int(ops_per_launch)},
+        "e2e": e2e, "gpu_launches": launches, "wall_s_timed": round(wall, 3),
+        "context": PAPER_FPS_CONTEXT,
+    }
+    clk = clocks.summary()
+    out["clocks"] = clk
+    if clk.get("sm_mhz"):
+        out["roofline"]["frac_at_measured_clock"] = round(achieved / (148 * 128 * clk["sm_mhz"] * 1e6 / 1e12), 4)
+    return out, (scene, cams, my_views)
+
+
+# ------------------------------------------------------------------------------ oracle (CPU) legs
+
+def oracle_sample(scene, cam, rows, seed=0):
+    """Oracle fwd+bwd of the pixel band rows[0]:rows[1] of one view; returns (seconds, pixels)."""
+    import oracle
+    from paper_2501_16312_b200 import scenegen
+    W, H = cam["width"], cam["height"]
+    y0, y1 = rows
+    pix = (np.arange(y0, y1)[:, None] * W + np.arange(W)[None, :]).reshape(-1).astype(np.int32)
+    gx = (W + 15) // 16
+    mask = np.zeros(gx * ((H + 15) // 16), np.uint8)
+    for ty in range(y0 // 16, (y1 - 1) // 16 + 1):
+        mask[ty * gx:(ty + 1) * gx] = 1
+    G = scenegen.upstream_grad(W, H, seed=seed)[0]
+    osc = oracle.Scene(scene["kind"], scene["pos"], scene["rot"], scene["dist"], scene["opacity"], scene["sh"],
+                       scene["sh_degree"])
+    t = time.perf_counter()
+    oracle.forward_backward(osc, cam, G, pix=pix, tile_mask=mask)
+    return time.perf_counter() - t, len(pix)
+
+
+def cpu_baseline(scene, cams, budget_s=15.0):
+    import oracle
+    oracle.build()
+    H = cams[0]["height"]
+    secs, npx = oracle_sample(scene, cams[0], (512, 528))          # one tile row to size the sample
+    rows = int(min(H - 512, max(16, 16 * round((budget_s / max(secs, 1e-3)) * 16 / 16 / 1.0))))
+    rows = max(16, min(rows, 256))
+    secs, npx = oracle_sample(scene, cams[0], (512 - rows // 2, 512 - rows // 2 + rows))
+    return {"value": round(npx / secs / 1e6, 6), "unit": "Mpixel/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"fwd+bwd of rows {512 - rows // 2}..{512 - rows // 2 + rows} ({npx} px) of view 0 of the C5 "
+                      f"workload incl. preprocess of all 1M primitives and binning of the band; {secs:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle as it stands, on a bounded sample per step (rank 0 only)."""
+    if rank != 0:
+        return None
+    from paper_2501_16312_b200 import scenegen
+    import oracle
+    oracle.build()
+    scene, cams = scenegen.make_scene(WORKLOAD, seed=args.seed, n=args.n)
+    band = 16
+    for s in range(args.warmup):
+        oracle_sample(scene, cams[s % len(cams)], (512, 512 + band))
+    tot_s, tot_px = 0.0, 0
+    for s in range(args.steps):
+        secs, npx = oracle_sample(scene, cams[s % len(cams)], (512, 512 + band))
+        tot_s += secs
+        tot_px += npx
+    value = tot_px / tot_s / 1e6
+    return {"impl": "reference", "metric": "fwd+bwd Mpixel/s (C5 training step: 8 views, fwd+bwd+allreduce+Adam)",
+            "value": round(value, 6), "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1000 * tot_s / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C5: 1M octahedra, SH deg 3, 8 views 1600x1060, training step (views sharded)",
+                       "sample_per_step": f"{band} rows x 1600 px of one view (fwd+bwd), views round-robin"},
+            "cpu_baseline": {"value": round(value, 6), "unit": "Mpixel/s", "cores": os.cpu_count(),
+                             "kind": "oracle", "sample": f"{band}-row band per step, {args.steps} steps"},
+            "e2e": {"value": round(value, 6), "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out))
+        return
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out, ctx = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            scene, cams, _ = ctx
+            out["cpu_baseline"] = cpu_baseline(scene, cams)
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -139,7 +139,8 @@ lp_status lp_frame_init(lp_frame *frame, void *workspace, size_t bytes, int32_t 
 /* a1-a3: per primitive, for each view v:
  * vertices from features, view transform, EWA ray space, 2D filter, bbox -> tile rect,
  * depth key, raster record (slab / plane form), sigma (Eq. 1) and SH colour.
- * Also resets the frame's counters.  frames[v].n must equal prims->n. */
+ * Also resets the frame's counters and its backward scratch (rgrad).  frames[v].n must equal
+ * prims->n. */
 lp_status lp_preprocess(const lp_prims *prims, const lp_camera *cams, int32_t n_views,
                         const lp_raster_cfg *cfg, lp_frame *frames, void *stream);
 
@@ -168,6 +169,14 @@ lp_status lp_render_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_
                         const lp_raster_cfg *cfg, lp_frame *frames, const float *dL_dimage,
                         const lp_grads *grads, void *stream);
 
+/* The two halves of lp_render_bwd, exported separately so callers can time / overlap them:
+ * lp_raster_bwd  (a10-a11): reverse replay -> += rgrad moments (rgrad is zeroed by lp_preprocess).
+ * lp_preprocess_bwd (a12): rgrad moments -> world features (+= into grads). */
+lp_status lp_raster_bwd(const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg, lp_frame *frames,
+                        const float *dL_dimage, void *stream);
+lp_status lp_preprocess_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_views,
+                            const lp_raster_cfg *cfg, lp_frame *frames, const lp_grads *grads, void *stream);
+
 /* Copy the frame's counters to host (synchronises the stream). */
 lp_status lp_frame_counters(const lp_frame *frame, uint32_t *host_counters /* [LP_NUM_COUNTERS] words */,
                             void *stream);
@@ -179,9 +188,10 @@ lp_status lp_l1_grad(const float *image, const float *target, float *dL_dimage, 
 
 /* C5: one fused Adam step over a flat fp32 parameter buffer with per-group learning
  * rates; elements outside every group are left unchanged.  step >= 1 (bias correction). */
-lp_status lp_adam_step(float *param, const float *grad, float *m, float *v,
+lp_status lp_adam_step(float *param, float *grad, float *m, float *v,
                        const lp_adam_group *groups, int32_t n_groups, float beta1, float beta2,
-                       float eps, int32_t step, void *stream);
+                       float eps, int32_t step, int32_t zero_grad /* 1: grad = 0 after use */,
+                       void *stream);
 
 #ifdef __cplusplus
 }

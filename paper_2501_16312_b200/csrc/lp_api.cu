@@ -160,6 +160,8 @@ lp_status lp_preprocess(const lp_prims *prims, const lp_camera *cams, int32_t n_
     lp_frame &F = frames[v];
     F.sorted_tile = F.sorted_val = nullptr;
     cudaMemsetAsync(F.counters, 0, 4 * LP_NUM_COUNTERS, st);
+    // the backward's raster-moment scratch is consumed once per preprocess
+    cudaMemsetAsync(F.rgrad, 0, 4 * (size_t)F.rgrad_words * (F.n > 0 ? F.n : 1), st);
     launch_preprocess(*prims, cams[v], cfg->aa_kernel, F, st);
   }
   return last_error();
@@ -240,11 +242,37 @@ lp_status lp_render_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_
   size_t off = 0;
   for (int v = 0; v < n_views; ++v) {
     const lp_frame &F = frames[v];
-    cudaMemsetAsync(F.rgrad, 0, 4 * (size_t)F.rgrad_words * (F.n > 0 ? F.n : 1), st);
     launch_raster_bwd(F, *cfg, dL_dimage + off, st);
     launch_preprocess_bwd(*prims, cams[v], cfg->aa_kernel, F, *grads, st);
     off += (size_t)3 * cams[v].width * cams[v].height;
   }
+  return last_error();
+}
+
+lp_status lp_raster_bwd(const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg, lp_frame *frames,
+                        const float *dL_dimage, void *stream) {
+  if (!cams || !cfg || !frames || !dL_dimage || n_views < 0) return LP_ERR_ARG;
+  for (int v = 0; v < n_views; ++v)
+    if (!valid_cam(cams[v]) || !frame_matches(frames[v], cams[v]) || !frames[v].sorted_val) return LP_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  size_t off = 0;
+  for (int v = 0; v < n_views; ++v) {
+    const lp_frame &F = frames[v];
+    launch_raster_bwd(F, *cfg, dL_dimage + off, st);
+    off += (size_t)3 * cams[v].width * cams[v].height;
+  }
+  return last_error();
+}
+
+lp_status lp_preprocess_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg,
+                            lp_frame *frames, const lp_grads *grads, void *stream) {
+  if (check_prims(prims) != LP_OK || !cams || !cfg || !frames || !grads || n_views < 0) return LP_ERR_ARG;
+  for (int v = 0; v < n_views; ++v) {
+    if (!valid_cam(cams[v]) || !frame_matches(frames[v], cams[v]) || !frames[v].sorted_val) return LP_ERR_ARG;
+    if (frames[v].kind != prims->kind || frames[v].n != prims->n) return LP_ERR_ARG;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int v = 0; v < n_views; ++v) launch_preprocess_bwd(*prims, cams[v], cfg->aa_kernel, frames[v], *grads, st);
   return last_error();
 }
 
@@ -263,12 +291,14 @@ lp_status lp_l1_grad(const float *image, const float *target, float *dL_dimage, 
   return last_error();
 }
 
-lp_status lp_adam_step(float *param, const float *grad, float *m, float *v, const lp_adam_group *groups,
-                       int32_t n_groups, float beta1, float beta2, float eps, int32_t step, void *stream) {
+lp_status lp_adam_step(float *param, float *grad, float *m, float *v, const lp_adam_group *groups,
+                       int32_t n_groups, float beta1, float beta2, float eps, int32_t step, int32_t zero_grad,
+                       void *stream) {
   if (!param || !grad || !m || !v || (n_groups > 0 && !groups) || n_groups < 0 || step < 1) return LP_ERR_ARG;
   for (int g = 0; g < n_groups; ++g)
     if (groups[g].begin < 0 || groups[g].end < groups[g].begin) return LP_ERR_ARG;
-  launch_adam(param, grad, m, v, groups, n_groups, beta1, beta2, eps, step, static_cast<cudaStream_t>(stream));
+  launch_adam(param, grad, m, v, groups, n_groups, beta1, beta2, eps, step, zero_grad != 0,
+              static_cast<cudaStream_t>(stream));
   return last_error();
 }
 

@@ -34,7 +34,7 @@ void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float 
 // C5 helpers (lp_train.cu)
 void launch_l1_grad(const float *img, const float *tgt, float *dL, float *loss, int64_t n, float scale,
                     cudaStream_t st);
-void launch_adam(float *p, const float *g, float *m, float *v, const lp_adam_group *groups, int ng, float b1,
-                 float b2, float eps, int step, cudaStream_t st);
+void launch_adam(float *p, float *g, float *m, float *v, const lp_adam_group *groups, int ng, float b1,
+                 float b2, float eps, int step, bool zero_grad, cudaStream_t st);
 
 }  // namespace lp

@@ -66,9 +66,9 @@ struct AdamGroups {
   int n;
 };
 
-__global__ void __launch_bounds__(256) k_adam(float *__restrict__ p, const float *__restrict__ g, float *__restrict__ m,
+__global__ void __launch_bounds__(256) k_adam(float *__restrict__ p, float *__restrict__ g, float *__restrict__ m,
                                               float *__restrict__ v, AdamGroups G, float b1, float b2, float eps,
-                                              float bc1, float bc2) {
+                                              float bc1, float bc2, bool zero_grad) {
   const int gi = blockIdx.y;
   const int64_t b = G.begin[gi], e = G.end[gi];
   const float lr = G.lr[gi];
@@ -80,11 +80,12 @@ __global__ void __launch_bounds__(256) k_adam(float *__restrict__ p, const float
     m[i] = mm;
     v[i] = vv;
     p[i] -= lr * (mm / bc1) / (sqrtf(vv / bc2) + eps);
+    if (zero_grad) g[i] = 0.f;
   }
 }
 
-void launch_adam(float *p, const float *g, float *m, float *v, const lp_adam_group *groups, int ng, float b1, float b2,
-                 float eps, int step, cudaStream_t st) {
+void launch_adam(float *p, float *g, float *m, float *v, const lp_adam_group *groups, int ng, float b1, float b2,
+                 float eps, int step, bool zero_grad, cudaStream_t st) {
   for (int base = 0; base < ng; base += 8) {
     AdamGroups G;
     G.n = ng - base < 8 ? ng - base : 8;
@@ -99,7 +100,7 @@ void launch_adam(float *p, const float *g, float *m, float *v, const lp_adam_gro
     const float bc1 = 1.f - powf(b1, (float)step), bc2 = 1.f - powf(b2, (float)step);
     int64_t want = (longest + 255) / 256;
     const int gx = (int)(want < 148 * 4 ? want : 148 * 4);
-    k_adam<<<dim3(gx, G.n), 256, 0, st>>>(p, g, m, v, G, b1, b2, eps, bc1, bc2);
+    k_adam<<<dim3(gx, G.n), 256, 0, st>>>(p, g, m, v, G, b1, b2, eps, bc1, bc2, zero_grad);
   }
 }
 

@@ -74,10 +74,14 @@ _sig = {
                                 _p, _p]),
     "lp_render_bwd": (C.c_int, [C.POINTER(lp_prims), C.POINTER(lp_camera), C.c_int32, C.POINTER(lp_raster_cfg),
                                 C.POINTER(lp_frame), _p, C.POINTER(lp_grads), _p]),
+    "lp_raster_bwd": (C.c_int, [C.POINTER(lp_camera), C.c_int32, C.POINTER(lp_raster_cfg), C.POINTER(lp_frame),
+                                _p, _p]),
+    "lp_preprocess_bwd": (C.c_int, [C.POINTER(lp_prims), C.POINTER(lp_camera), C.c_int32,
+                                    C.POINTER(lp_raster_cfg), C.POINTER(lp_frame), C.POINTER(lp_grads), _p]),
     "lp_frame_counters": (C.c_int, [C.POINTER(lp_frame), C.POINTER(C.c_uint32), _p]),
     "lp_l1_grad": (C.c_int, [_p, _p, _p, _p, C.c_int64, C.c_float, _p]),
     "lp_adam_step": (C.c_int, [_p, _p, _p, _p, C.POINTER(lp_adam_group), C.c_int32, C.c_float, C.c_float,
-                               C.c_float, C.c_int32, _p]),
+                               C.c_float, C.c_int32, C.c_int32, _p]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -147,6 +151,16 @@ def lp_render_bwd(prims, cams, cfg, frames, dL_dimage, grads, stream):
                                      C.byref(grads), _stream(stream)), "lp_render_bwd")
 
 
+def lp_raster_bwd(cams, cfg, frames, dL_dimage, stream):
+    return _check(_lib.lp_raster_bwd(cams, len(cams), C.byref(cfg), frames, _ptr(dL_dimage), _stream(stream)),
+                  "lp_raster_bwd")
+
+
+def lp_preprocess_bwd(prims, cams, cfg, frames, grads, stream):
+    return _check(_lib.lp_preprocess_bwd(C.byref(prims), cams, len(cams), C.byref(cfg), frames, C.byref(grads),
+                                         _stream(stream)), "lp_preprocess_bwd")
+
+
 def lp_frame_counters(frame, stream) -> np.ndarray:
     out = (C.c_uint32 * LP_NUM_COUNTERS)()
     _check(_lib.lp_frame_counters(C.byref(frame), out, _stream(stream)), "lp_frame_counters")
@@ -158,10 +172,11 @@ def lp_l1_grad(image, target, dL, loss_sum, scale, stream):
                                   C.c_float(scale), _stream(stream)), "lp_l1_grad")
 
 
-def lp_adam_step(param, grad, m, v, groups, beta1, beta2, eps, step, stream):
+def lp_adam_step(param, grad, m, v, groups, beta1, beta2, eps, step, stream, zero_grad=False):
     arr = (lp_adam_group * len(groups))(*[lp_adam_group(int(b), int(e), float(lr)) for b, e, lr in groups])
     return _check(_lib.lp_adam_step(_ptr(param), _ptr(grad), _ptr(m), _ptr(v), arr, len(groups), C.c_float(beta1),
-                                    C.c_float(beta2), C.c_float(eps), int(step), _stream(stream)), "lp_adam_step")
+                                    C.c_float(beta2), C.c_float(eps), int(step), 1 if zero_grad else 0,
+                                    _stream(stream)), "lp_adam_step")
 
 
 # ------------------------------------------------------------------ struct builders

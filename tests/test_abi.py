@@ -79,7 +79,7 @@ def test_arguments_validated_before_any_launch(L):
     assert lib.lp_bin_sort(cams, 1, frames, None, None) == L.LP_ERR_ARG          # frame not initialised
     assert lib.lp_render_fwd(cams, 1, C.byref(cfg), frames, None, None) == L.LP_ERR_ARG
     assert lib.lp_frame_init(C.byref(frames[0]), None, 0, 0, 1, 16, 16, 10, 0) == L.LP_ERR_ARG
-    assert lib.lp_adam_step(None, None, None, None, None, 0, 0.9, 0.999, 1e-15, 1, None) == L.LP_ERR_ARG
+    assert lib.lp_adam_step(None, None, None, None, None, 0, 0.9, 0.999, 1e-15, 1, 0, None) == L.LP_ERR_ARG
 
 
 def test_no_oracle_in_product_path():
