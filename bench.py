@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--profile-step", action="store_true",
+                    help="after warm-up run ONE step between cudaProfilerStart/Stop (ncu --profile-from-start off) and exit")
     return ap.parse_args()
 
 
@@ -226,6 +228,12 @@ def run_ours(args, rank, world, local_rank):
     for s in range(args.warmup):
         step(s)
     barrier()
+    if args.profile_step:
+        torch.cuda.profiler.start()
+        step(args.warmup)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        return None, None
     # overflow check after warm-up (async binning must not have truncated)
     for i in range(n_local):
         c = rend.counters(i)
@@ -267,21 +275,44 @@ def run_ours(args, rank, world, local_rank):
     stage_ms = {nm: statistics.mean(vals) for nm, vals in stage.items()}
     stage_ms["adam"] = statistics.mean(ar_adam)
 
-    # roofline of the dominant kernel (raster forward or backward; both FP32-pipe bound)
+    # rooflines of the single-kernel stages; the dominant one is reported as "roofline"
     kind = ds.kind
     I_tot, X_tot = sum(it), sum(hit)
-    dom = "rbwd" if stage_ms["rbwd"] >= stage_ms["fwd"] else "fwd"
-    ops_per_launch = fp32_ops(kind, I_tot / n_local, X_tot / n_local, backward=(dom == "rbwd"))
-    achieved = ops_per_launch / (stage_ms[dom] * 1e-3) / 1e12          # T lane-instr / s
-    sm_max = 1965.0
-    peak = 148 * 128 * sm_max * 1e6 / 1e12                              # FP32 issue: 148 SM x 128 lanes x clock
-    traffic = None
-    prof_path = os.path.join(ROOT, "profiles", "latest_traffic.json")
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    alu_peak = 148 * 128 * 1965.0 * 1e6 / 1e12                          # T FP32 lane-instr/s at max SM clock
+    K = ds.K
+    RG, RW = (20, 20) if kind == 0 else (22, 24)
+    ncoef = (ds.sh_degree + 1) ** 2
+    Fb = 4 * (3 + 4 + K + 1 + 3 * ncoef)                                # feature bytes per primitive
+    vis = statistics.mean([int(s[L.LP_CNT_VISIBLE]) for s in stats])
+    traffic_db = {}
+    prof_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof_path):
         try:
-            traffic = json.load(open(prof_path)).get("k_raster_bwd" if dom == "rbwd" else "k_raster_fwd")
+            traffic_db = json.load(open(prof_path))
         except Exception:
-            traffic = None
+            traffic_db = {}
+    work = {
+        "fwd": ("k_raster_fwd", "alu", fp32_ops(kind, I_tot / n_local, X_tot / n_local, backward=False)),
+        "rbwd": ("k_raster_bwd", "alu", fp32_ops(kind, I_tot / n_local, X_tot / n_local, backward=True)),
+        "pbwd": ("k_preprocess_bwd", "hbm", 4 * n + vis * (4 * RG + 3 * Fb)),
+        "pre": ("k_preprocess", "hbm", n * (Fb + 24) + vis * 4 * RW),
+        "adam": ("k_adam", "hbm", 32 * ds.flat.numel()),
+    }
+    rooflines = {}
+    for key, (kname, bound, amount) in work.items():
+        sec = stage_ms[key] * 1e-3
+        if bound == "alu":
+            ach, pk, unit = amount / sec / 1e12, alu_peak, "T FP32 lane-instr/s"
+        else:
+            ach, pk, unit = amount / sec / 1e9, hbm_peak, "GB/s"
+        tr = traffic_db.get(kname)
+        rooflines[key] = {"kernel": kname, "bound": bound, "achieved": round(ach, 3), "peak": round(pk, 3),
+                          "unit": unit, "frac": round(ach / pk, 4), "ms": round(stage_ms[key], 4),
+                          "traffic": tr, "algorithmic_per_launch": int(amount)}
+    dom = max(work, key=lambda k: stage_ms[k])
 
     views_total = n_views
     mpix = views_total * W * H / 1e6
@@ -335,18 +366,14 @@ def run_ours(args, rank, world, local_rank):
                    "intersected_pairs_per_px": round(X_tot / (n_local * W * H), 2),
                    "frustum_primitives_per_view": frustum, "capacity": caps},
         "stages_ms_per_view": {k: round(v, 4) for k, v in stage_ms.items()},
-        "roofline": {"kernel": "k_raster_bwd" if dom == "rbwd" else "k_raster_fwd", "bound": "alu",
-                     "achieved": round(achieved, 3), "peak": round(peak, 3),
-                     "unit": "T FP32 lane-instr/s (peak = 148 SM x 128 lanes x 1965 MHz, B200_PROFILING unit counts)",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "ops_per_launch": int(ops_per_launch)},
+        "roofline": dict(rooflines[dom], peak_source="measured HBM copy (MEASURED_PEAKS.json)" if
+                         work[dom][1] == "hbm" else "148 SM x 128 FP32 lanes x 1965 MHz (B200_PROFILING unit counts)"),
+        "rooflines": rooflines,
         "e2e": e2e, "gpu_launches": launches, "wall_s_timed": round(wall, 3),
         "context": PAPER_FPS_CONTEXT,
     }
     clk = clocks.summary()
     out["clocks"] = clk
-    if clk.get("sm_mhz"):
-        out["roofline"]["frac_at_measured_clock"] = round(achieved / (148 * 128 * clk["sm_mhz"] * 1e6 / 1e12), 4)
     return out, (scene, cams, my_views)
 
 
@@ -428,6 +455,8 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out, ctx = run_ours(args, rank, world, local_rank)
+    if out is None:
+        return
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             scene, cams, _ = ctx

@@ -199,10 +199,10 @@ lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, 
       }
     }
     // 3. emission in depth order
-    launch_emit(Fv, n, st);
+    const int64_t nmax = E_host >= 0 ? E_host : F.capacity;
+    launch_emit(Fv, n, nmax, st);
     // 4. stable sort by tile id
     const int tiles = F.tiles_x * F.tiles_y;
-    const int64_t nmax = E_host >= 0 ? E_host : F.capacity;
     const uint32_t *ndev = E_host >= 0 ? nullptr : F.counters + LP_CNT_ENTRIES;
     const int tflip = radix_sort_pairs(F.tile_key, F.tile_key_alt, F.entry_val, F.entry_val_alt, nmax, ndev,
                                        bits_for(tiles), F.sort_hist, st);

@@ -157,21 +157,23 @@ __device__ __forceinline__ void canonical_geometry(const lp_prims &P, int i, con
 #pragma unroll
   for (int ax = 0; ax < 2; ++ax) {
     if (KIND == OCTA) {
+      // first argmax of |o_j| (value tracked in a register: no dynamic array indexing)
       int jm = 0;
+      float am = fabsf(g.off[0][ax]), v = g.off[0][ax];
 #pragma unroll
       for (int j = 1; j < 3; ++j)
-        if (fabsf(g.off[j][ax]) > fabsf(g.off[jm][ax])) jm = j;
-      const float v = g.off[jm][ax];
+        if (fabsf(g.off[j][ax]) > am) { am = fabsf(g.off[j][ax]); v = g.off[j][ax]; jm = j; }
       const float nv = fa(v, v >= 0.f ? h : -h);
 #pragma unroll
       for (int j = 0; j < 3; ++j)
         if (j == jm) g.off[j][ax] = nv;
     } else {
       int kmin = 0, kmax = 0;
+      float vmin = g.off[0][ax], vmax = g.off[0][ax];
 #pragma unroll
       for (int k = 1; k < 4; ++k) {
-        if (g.off[k][ax] < g.off[kmin][ax]) kmin = k;
-        if (g.off[k][ax] > g.off[kmax][ax]) kmax = k;
+        if (g.off[k][ax] < vmin) { vmin = g.off[k][ax]; kmin = k; }
+        if (g.off[k][ax] > vmax) { vmax = g.off[k][ax]; kmax = k; }
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k)
@@ -229,10 +231,15 @@ __device__ __forceinline__ void canonical_geometry(const lp_prims &P, int i, con
 // For the vertical pixel ray x = (r, c_z + t):  t in [L_s - h_s, L_s + h_s] with
 // L_s = b_s dx + g_s dy,  b = -row.x/row.z,  g = -row.y/row.z,  h = 1/|row.z|,  row = s^T G.
 // entry = max_s (L_s - h_s), exit = min_s (L_s + h_s)   (equals MTIA's i2 - i1).
-__device__ __constant__ static const signed char kSlabSign[4][3] = {{1, 1, 1}, {1, 1, -1}, {1, -1, 1}, {-1, 1, 1}};
-
-// Tetrahedron faces, outward for the S:102 basis (DESIGN.md conventions).
-__device__ __constant__ static const unsigned char kTetraFace[4][3] = {{1, 3, 2}, {0, 2, 3}, {0, 3, 1}, {0, 1, 2}};
+// Compile-time tables (functions of unrolled loop constants fold to immediates: no local memory).
+__host__ __device__ __forceinline__ constexpr int slab_sign(int s, int a) {   // (1,1,1) (1,1,-1) (1,-1,1) (-1,1,1)
+  return (s == 0) ? 1 : (s == 1 ? (a == 2 ? -1 : 1) : (s == 2 ? (a == 1 ? -1 : 1) : (a == 0 ? -1 : 1)));
+}
+// Tetrahedron faces (1,3,2) (0,2,3) (0,3,1) (0,1,2), outward for the S:102 basis (DESIGN.md conventions).
+__host__ __device__ __forceinline__ constexpr int tetra_face(int f, int c) {
+  return f == 0 ? (c == 0 ? 1 : (c == 1 ? 3 : 2))
+                : (f == 1 ? (c == 0 ? 0 : (c == 1 ? 2 : 3)) : (f == 2 ? (c == 0 ? 0 : (c == 1 ? 3 : 1)) : c));
+}
 
 __device__ __forceinline__ void inverse3(const double M[3][3], double G[3][3], double &det) {
   const double a00 = M[1][1] * M[2][2] - M[1][2] * M[2][1];
@@ -276,9 +283,19 @@ __device__ __forceinline__ void octa_slabs(const float off[4][3], SlabRows &S) {
   for (int s = 0; s < 4; ++s) {
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      S.r[s][c] = kSlabSign[s][0] * G[0][c] + kSlabSign[s][1] * G[1][c] + kSlabSign[s][2] * G[2][c];
+      S.r[s][c] = slab_sign(s, 0) * G[0][c] + slab_sign(s, 1) * G[1][c] + slab_sign(s, 2) * G[2][c];
     S.r[s][2] = clamp_away(S.r[s][2], fmax(fabs(S.r[s][0]), fabs(S.r[s][1])));
   }
+}
+
+// a[i] for a runtime index via unrolled selects (keeps small arrays in registers)
+template <typename T, int N>
+__device__ __forceinline__ T sel(const T (&a)[N], int i) {
+  T r = a[0];
+#pragma unroll
+  for (int k = 1; k < N; ++k)
+    if (i == k) r = a[k];
+  return r;
 }
 
 struct TetraPlanes {  // plane of each face: z = A + B dx + C dy relative to the centre
@@ -294,11 +311,11 @@ __device__ __forceinline__ void tetra_planes(const float off[4][3], TetraPlanes 
   for (int k = 0; k < 4; ++k)
 #pragma unroll
     for (int a = 0; a < 3; ++a) v[k][a] = (double)off[k][a];
-  int nf = 0, nb = 0, fr[4], bk[4];
+  int front = 0;
   T.ok = true;
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
-    const double *pa = v[kTetraFace[f][0]], *pb = v[kTetraFace[f][1]], *pc = v[kTetraFace[f][2]];
+    const double *pa = v[tetra_face(f, 0)], *pb = v[tetra_face(f, 1)], *pc = v[tetra_face(f, 2)];
     const double e1[3] = {pb[0] - pa[0], pb[1] - pa[1], pb[2] - pa[2]};
     const double e2[3] = {pc[0] - pa[0], pc[1] - pa[1], pc[2] - pa[2]};
     double nx = e1[1] * e2[2] - e1[2] * e2[1];
@@ -310,13 +327,25 @@ __device__ __forceinline__ void tetra_planes(const float off[4][3], TetraPlanes 
     T.B[f] = -nx / nz;
     T.C[f] = -ny / nz;
     T.A[f] = pa[2] - T.B[f] * pa[0] - T.C[f] * pa[1];
-    if (nz < 0.0) fr[nf++] = f; else bk[nb++] = f;   // outward normal towards the camera = entry face
+    if (nz < 0.0) front |= 1 << f;   // outward normal towards the camera = entry face
   }
-  if (nf == 0 || nb == 0) { T.ok = false; nf = nf ? nf : 1; nb = nb ? nb : 1; fr[0] = fr[0]; }
+  const int nf = __popc(front), nb = 4 - nf;
+  if (nf == 0 || nb == 0) T.ok = false;
+  // slot s (0..2) = the min(s, nf-1)-th front face; slot 3+s = the min(s, nb-1)-th back face
 #pragma unroll
   for (int s = 0; s < 3; ++s) {
-    T.slot_face[s] = (nf > 0) ? fr[s < nf ? s : nf - 1] : 0;
-    T.slot_face[3 + s] = (nb > 0) ? bk[s < nb ? s : nb - 1] : 0;
+    int sf = 0, sb = 0;
+    const int rf = s < nf ? s : nf - 1, rb = s < nb ? s : nb - 1;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const bool isf = (front >> f) & 1;
+      const int rank_f = __popc(front & ((1 << f) - 1));
+      const int rank_b = f - rank_f;
+      if (isf && rank_f == rf) sf = f;
+      if (!isf && rank_b == rb) sb = f;
+    }
+    T.slot_face[s] = sf;
+    T.slot_face[3 + s] = sb;
   }
 }
 

@@ -24,7 +24,7 @@ size_t scan_tmp_words(int64_t max_items);
 int radix_sort_pairs(uint32_t *keys, uint32_t *keys_alt, uint32_t *vals, uint32_t *vals_alt, int64_t n_max,
                      const uint32_t *n_dev, int bits, uint32_t *hist, cudaStream_t st);
 void launch_scan_tiles(const lp_frame &F, int n, cudaStream_t st);   // offsets + E -> counters
-void launch_emit(const lp_frame &F, int n, cudaStream_t st);
+void launch_emit(const lp_frame &F, int n, int64_t max_entries, cudaStream_t st);
 void launch_ranges(const lp_frame &F, const uint32_t *sorted_tile, int tiles, cudaStream_t st);
 
 // K3 / K4 (lp_raster.cu)

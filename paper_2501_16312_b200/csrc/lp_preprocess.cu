@@ -33,7 +33,9 @@ __device__ __forceinline__ void sh_colour_fp32(const lp_prims &P, int i, const l
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
     float acc = 0.5f;
-    for (int k = 0; k < ncoef; ++k) acc += P.sh[((size_t)k * 3 + ch) * P.n + i] * Y[k];
+#pragma unroll
+    for (int k = 0; k < 16; ++k)   // static indices keep Y[] in registers
+      if (k < ncoef) acc += P.sh[((size_t)k * 3 + ch) * P.n + i] * Y[k];
     raw[ch] = acc;
   }
 }
@@ -114,9 +116,9 @@ __global__ void __launch_bounds__(256) k_preprocess(lp_prims P, lp_camera cam, f
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       const int f = T.slot_face[s];
-      rec[2 + 3 * s] = T.ok ? (float)T.A[f] : (s < 3 ? 1.f : -1.f);   // empty: entry 1 > exit -1
-      rec[3 + 3 * s] = T.ok ? (float)T.B[f] : 0.f;
-      rec[4 + 3 * s] = T.ok ? (float)T.C[f] : 0.f;
+      rec[2 + 3 * s] = T.ok ? (float)sel(T.A, f) : (s < 3 ? 1.f : -1.f);   // empty: entry 1 > exit -1
+      rec[3 + 3 * s] = T.ok ? (float)sel(T.B, f) : 0.f;
+      rec[4 + 3 * s] = T.ok ? (float)sel(T.C, f) : 0.f;
     }
     rec[REC_TETRA_SIGMA] = sigma;
     rec[REC_TETRA_RGB + 0] = rgb[0];
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(256) k_preprocess(lp_prims P, lp_camera cam, f
 // K5: raster moments -> ray-space geometry -> world features
 // =============================================================================================
 template <int KIND>
-__global__ void __launch_bounds__(128) k_preprocess_bwd(lp_prims P, lp_camera cam, float kappa, lp_frame F,
+__global__ void __launch_bounds__(128, 4) k_preprocess_bwd(lp_prims P, lp_camera cam, float kappa, lp_frame F,
                                                         lp_grads Gs) {
   constexpr int K = Kind<KIND>::K, RG = Kind<KIND>::RG;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(lp_prims P, lp_camera ca
       const double drz = db * rx / rz2 + dg * ry / rz2 - dhh * (rz > 0 ? 1.0 : -1.0) / rz2;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        const double sa = kSlabSign[s][a];
+        const double sa = slab_sign(s, a);
         gG[a][0] += sa * drx;
         gG[a][1] += sa * dry;
         gG[a][2] += sa * drz;
@@ -208,12 +210,26 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(lp_prims P, lp_camera ca
     for (int k = 0; k < 4; ++k)
 #pragma unroll
       for (int a = 0; a < 3; ++a) v[k][a] = (double)g.off[k][a];
+    // slot moments -> per-face plane gradients (a face may fill several slots)
+    double fA[4] = {0, 0, 0, 0}, fB[4] = {0, 0, 0, 0}, fC[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
-      const double dA = m[3 * s], dB = m[3 * s + 1], dC = m[3 * s + 2];
+      const int sf = T.slot_face[s];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+        if (f == sf) {
+          fA[f] += m[3 * s];
+          fB[f] += m[3 * s + 1];
+          fC[f] += m[3 * s + 2];
+        }
+    }
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const double dA = fA[f], dB = fB[f], dC = fC[f];
       if (dA == 0.0 && dB == 0.0 && dC == 0.0) continue;
-      const int f = T.slot_face[s];
-      const int ia = kTetraFace[f][0], ib = kTetraFace[f][1], ic = kTetraFace[f][2];
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int ia = tetra_face(f, 0), ib = tetra_face(f, 1), ic = tetra_face(f, 2);
       const double B = T.B[f], C = T.C[f];
       gcr[0] -= B * dA;
       gcr[1] -= C * dA;
@@ -242,30 +258,31 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(lp_prims P, lp_camera ca
   if (Gs.mean2d_abs) Gs.mean2d_abs[i] += (float)sqrt(gcr[0] * gcr[0] + gcr[1] * gcr[1]);
 
   // ---- the 2D filter adds constants (fixed extreme index): identity.
+  using CT = float;   // the chain below is well conditioned: fp32 (the M^-1 / plane part above is fp64)
   // ---- o_j = J W (dh_j R b_j); c_ray = phi(p), p = W c + t  (fp64 chain)
-  double q[4] = {qf[0], qf[1], qf[2], qf[3]};
-  const double nq = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-  const double w = q[0] / nq, x = q[1] / nq, y = q[2] / nq, z = q[3] / nq;
-  const double R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+  CT q[4] = {qf[0], qf[1], qf[2], qf[3]};
+  const CT nq = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  const CT w = q[0] / nq, x = q[1] / nq, y = q[2] / nq, z = q[3] / nq;
+  const CT R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
                           {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
                           {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
-  double Wm[3][3];
+  CT Wm[3][3];
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) Wm[r][cc] = cam.W[3 * r + cc];
-  double p[3];
+  CT p[3];
 #pragma unroll
-  for (int r = 0; r < 3; ++r) p[r] = Wm[r][0] * cf[0] + Wm[r][1] * cf[1] + Wm[r][2] * cf[2] + (double)cam.t[r];
-  const double l = sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
-  const double fx = cam.fx, fy = cam.fy, pz = p[2], pz2 = pz * pz, pz3 = pz2 * pz;
-  const double J[3][3] = {{fx / pz, 0, -fx * p[0] / pz2}, {0, fy / pz, -fy * p[1] / pz2}, {p[0] / l, p[1] / l, p[2] / l}};
-  double gJ[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, gR[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-  double gdh[4] = {0, 0, 0, 0};
-  const double kk = 0.57735026918962576451;
+  for (int r = 0; r < 3; ++r) p[r] = Wm[r][0] * cf[0] + Wm[r][1] * cf[1] + Wm[r][2] * cf[2] + (CT)cam.t[r];
+  const CT l = sqrtf(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+  const CT fx = cam.fx, fy = cam.fy, pz = p[2], pz2 = pz * pz, pz3 = pz2 * pz;
+  const CT J[3][3] = {{fx / pz, 0, -fx * p[0] / pz2}, {0, fy / pz, -fy * p[1] / pz2}, {p[0] / l, p[1] / l, p[2] / l}};
+  CT gJ[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, gR[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  CT gdh[4] = {0, 0, 0, 0};
+  const CT kk = 0.57735026918962576451f;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    double bj[3];
+    CT bj[3];
     if (KIND == OCTA) {
       bj[0] = j == 0; bj[1] = j == 1; bj[2] = j == 2;
     } else {
@@ -273,11 +290,11 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(lp_prims P, lp_camera ca
       bj[1] = (j == 0 || j == 2) ? kk : -kk;
       bj[2] = (j == 0 || j == 3) ? kk : -kk;
     }
-    double Rb[3], ow[3], oc[3], goc[3], gow[3];
+    CT Rb[3], ow[3], oc[3], goc[3], gow[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) Rb[r] = R[r][0] * bj[0] + R[r][1] * bj[1] + R[r][2] * bj[2];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) ow[r] = (double)dhf[j] * Rb[r];
+    for (int r = 0; r < 3; ++r) ow[r] = (CT)dhf[j] * Rb[r];
 #pragma unroll
     for (int r = 0; r < 3; ++r) oc[r] = Wm[r][0] * ow[0] + Wm[r][1] * ow[1] + Wm[r][2] * ow[2];
 #pragma unroll
@@ -292,22 +309,22 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(lp_prims P, lp_camera ca
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int cc = 0; cc < 3; ++cc) gR[r][cc] += (double)dhf[j] * gow[r] * bj[cc];
+      for (int cc = 0; cc < 3; ++cc) gR[r][cc] += (CT)dhf[j] * gow[r] * bj[cc];
   }
-  double gp[3];
+  CT gp[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) gp[a] = J[0][a] * gcr[0] + J[1][a] * gcr[1];   // c_ray.z gets no gradient
   gp[2] += gJ[0][0] * (-fx / pz2);
   gp[0] += gJ[0][2] * (-fx / pz2);
-  gp[2] += gJ[0][2] * (2.0 * fx * p[0] / pz3);
+  gp[2] += gJ[0][2] * (2.0f * fx * p[0] / pz3);
   gp[2] += gJ[1][1] * (-fy / pz2);
   gp[1] += gJ[1][2] * (-fy / pz2);
-  gp[2] += gJ[1][2] * (2.0 * fy * p[1] / pz3);
+  gp[2] += gJ[1][2] * (2.0f * fy * p[1] / pz3);
 #pragma unroll
   for (int k = 0; k < 3; ++k)
 #pragma unroll
-    for (int mm = 0; mm < 3; ++mm) gp[mm] += gJ[2][k] * (((k == mm) ? 1.0 : 0.0) - p[k] * p[mm] / (l * l)) / l;
-  double gc[3];
+    for (int mm = 0; mm < 3; ++mm) gp[mm] += gJ[2][k] * (((k == mm) ? 1.0f : 0.0f) - p[k] * p[mm] / (l * l)) / l;
+  CT gc[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) gc[a] = Wm[0][a] * gp[0] + Wm[1][a] * gp[1] + Wm[2][a] * gp[2];
 
@@ -315,74 +332,98 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(lp_prims P, lp_camera ca
   if (Gs.dist) {
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      double gd = gdh[j];
-      if (P.filter3d) gd *= (double)P.dist[j * n + i] / (double)dhf[j];
+      CT gd = gdh[j];
+      if (P.filter3d) gd *= (CT)P.dist[j * n + i] / (CT)dhf[j];
       Gs.dist[(size_t)j * n + i] += (float)gd;
     }
   }
   // ---- rotation: R(q_hat) -> q_hat -> q
   if (Gs.rot) {
-    const double dR[4][3][3] = {
+    const CT dR[4][3][3] = {
         {{0, -2 * z, 2 * y}, {2 * z, 0, -2 * x}, {-2 * y, 2 * x, 0}},
         {{0, 2 * y, 2 * z}, {2 * y, -4 * x, -2 * w}, {2 * z, 2 * w, -4 * x}},
         {{-4 * y, 2 * x, 2 * w}, {2 * x, 0, 2 * z}, {-2 * w, 2 * z, -4 * y}},
         {{-4 * z, -2 * w, 2 * x}, {2 * w, -4 * z, 2 * y}, {2 * x, 2 * y, 0}}};
-    double gq[4] = {0, 0, 0, 0};
+    CT gq[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int cc = 0; cc < 3; ++cc) gq[a] += gR[r][cc] * dR[a][r][cc];
-    const double qh[4] = {w, x, y, z};
-    const double dot = qh[0] * gq[0] + qh[1] * gq[1] + qh[2] * gq[2] + qh[3] * gq[3];
+    const CT qh[4] = {w, x, y, z};
+    const CT dot = qh[0] * gq[0] + qh[1] * gq[1] + qh[2] * gq[2] + qh[3] * gq[3];
 #pragma unroll
     for (int a = 0; a < 4; ++a) Gs.rot[(size_t)a * n + i] += (float)((gq[a] - qh[a] * dot) / nq);
   }
   // ---- opacity: Eq. 1 with the denominator frozen, alpha = sigmoid(logit)
   if (Gs.opacity) {
-    const double alpha = 1.0 / (1.0 + exp(-(double)P.opacity[i]));
-    double md = dhf[0];
+    const CT alpha = 1.0f / (1.0f + expf(-(CT)P.opacity[i]));
+    CT md = dhf[0];
 #pragma unroll
-    for (int a = 1; a < K; ++a) md = fmin(md, (double)dhf[a]);
-    const double dsda = 0.99 / ((1.0 - 0.99 * alpha) * 2.0 * md);
-    Gs.opacity[i] += (float)(dsig * dsda * alpha * (1.0 - alpha));
+    for (int a = 1; a < K; ++a) md = fminf(md, (CT)dhf[a]);
+    const CT dsda = 0.99f / ((1.0f - 0.99f * alpha) * 2.0f * md);
+    Gs.opacity[i] += (float)(dsig * dsda * alpha * (1.0f - alpha));
   }
-  // ---- SH coefficients and the view-direction term of the centre
-  {
-    const double cp[3] = {-(Wm[0][0] * cam.t[0] + Wm[1][0] * cam.t[1] + Wm[2][0] * cam.t[2]),
-                          -(Wm[0][1] * cam.t[0] + Wm[1][1] * cam.t[1] + Wm[2][1] * cam.t[2]),
-                          -(Wm[0][2] * cam.t[0] + Wm[1][2] * cam.t[1] + Wm[2][2] * cam.t[2])};
-    double v[3] = {cf[0] - cp[0], cf[1] - cp[1], cf[2] - cp[2]};
-    const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
-    const double dir[3] = {v[0] / nv, v[1] / nv, v[2] / nv};
-    double Y[16];
-    sh_basis<double>(P.sh_degree, dir[0], dir[1], dir[2], Y);
-    const int ncoef = (P.sh_degree + 1) * (P.sh_degree + 1);
-    double wsum[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) wsum[k] = 0.0;
-    float raw[3];
-    sh_colour_fp32(P, i, cam, cf, raw);   // the forward's exact fp32 value decides the clamp
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      if (raw[ch] < 0.f) continue;
-      const double gr = drgb[ch];
-      for (int k = 0; k < ncoef; ++k) {
-        if (Gs.sh) Gs.sh[((size_t)k * 3 + ch) * n + i] += (float)(Y[k] * gr);
-        wsum[k] += gr * (double)P.sh[((size_t)k * 3 + ch) * n + i];
-      }
-    }
-    double gdir[3];
-    sh_basis_grad_dot<double>(P.sh_degree, dir[0], dir[1], dir[2], wsum, gdir);
-    const double dd = dir[0] * gdir[0] + dir[1] * gdir[1] + dir[2] * gdir[2];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) gc[a] += (gdir[a] - dir[a] * dd) / nv;
-  }
+  // (SH coefficients and the view-direction term of the centre: k_sh_bwd)
   if (Gs.pos) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += (float)gc[a];
   }
+}
+
+// =============================================================================================
+// K5b: SH colour backward ("impact of the position on ... view-dependent color").
+// A separate streaming kernel: ~40 registers, so enough warps are in flight to hide the
+// 2 x (deg+1)^2 x 3 scattered loads and (deg+1)^2 x 3 stores per primitive.
+// =============================================================================================
+template <int DEG>
+__global__ void __launch_bounds__(256, 2) k_sh_bwd(lp_prims P, lp_camera cam, lp_frame F, lp_grads Gs) {
+  constexpr int NC = (DEG + 1) * (DEG + 1);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = P.n;
+  if (i >= n || F.tiles_touched[i] == 0) return;
+  const int RG = F.rgrad_words;
+  float gr[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) gr[ch] = F.rgrad[(size_t)(RG - 3 + ch) * n + i];
+  if (gr[0] == 0.f && gr[1] == 0.f && gr[2] == 0.f) return;
+  const float *__restrict__ sh = P.sh;
+  float *__restrict__ gsh = Gs.sh;
+  const float c[3] = {P.pos[i], P.pos[n + i], P.pos[2 * n + i]};
+  float raw[3];
+  sh_colour_fp32(P, i, cam, c, raw);   // the forward's exact fp32 colour decides the clamp
+  const float cpx = -(cam.W[0] * cam.t[0] + cam.W[3] * cam.t[1] + cam.W[6] * cam.t[2]);
+  const float cpy = -(cam.W[1] * cam.t[0] + cam.W[4] * cam.t[1] + cam.W[7] * cam.t[2]);
+  const float cpz = -(cam.W[2] * cam.t[0] + cam.W[5] * cam.t[1] + cam.W[8] * cam.t[2]);
+  const float v[3] = {c[0] - cpx, c[1] - cpy, c[2] - cpz};
+  const float nv = sqrtf(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  const float dir[3] = {v[0] / nv, v[1] / nv, v[2] / nv};
+  float Y[16], wsum[16];
+  sh_basis<float>(DEG, dir[0], dir[1], dir[2], Y);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) wsum[k] = 0.f;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    if (raw[ch] < 0.f) continue;
+    float s[NC], g[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) s[k] = sh[((size_t)k * 3 + ch) * n + i];
+    if (gsh) {
+#pragma unroll
+      for (int k = 0; k < NC; ++k) g[k] = gsh[((size_t)k * 3 + ch) * n + i];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) gsh[((size_t)k * 3 + ch) * n + i] = fmaf(Y[k], gr[ch], g[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) wsum[k] = fmaf(gr[ch], s[k], wsum[k]);
+  }
+  if (DEG == 0 || !Gs.pos) return;
+  float gdir[3];
+  sh_basis_grad_dot<float>(DEG, dir[0], dir[1], dir[2], wsum, gdir);
+  const float dd = dir[0] * gdir[0] + dir[1] * gdir[1] + dir[2] * gdir[2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += (gdir[a] - dir[a] * dd) / nv;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -399,6 +440,14 @@ void launch_preprocess_bwd(const lp_prims &P, const lp_camera &cam, float kappa,
   const int grid = (P.n + 127) / 128;
   if (P.kind == LP_OCTAHEDRON) k_preprocess_bwd<LP_OCTAHEDRON><<<grid, 128, 0, st>>>(P, cam, kappa, F, G);
   else k_preprocess_bwd<LP_TETRAHEDRON><<<grid, 128, 0, st>>>(P, cam, kappa, F, G);
+  if (!G.sh && !G.pos) return;
+  const int g2 = (P.n + 255) / 256;
+  switch (P.sh_degree) {
+    case 0: k_sh_bwd<0><<<g2, 256, 0, st>>>(P, cam, F, G); break;
+    case 1: k_sh_bwd<1><<<g2, 256, 0, st>>>(P, cam, F, G); break;
+    case 2: k_sh_bwd<2><<<g2, 256, 0, st>>>(P, cam, F, G); break;
+    default: k_sh_bwd<3><<<g2, 256, 0, st>>>(P, cam, F, G); break;
+  }
 }
 
 }  // namespace lp

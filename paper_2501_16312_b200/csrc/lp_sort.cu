@@ -270,51 +270,71 @@ void launch_scan_tiles(const lp_frame &F, int n, cudaStream_t st) {
 
 // ---------------------------------------------------------------------------------------------
 // emission (a5): entries of sorted primitive j at [offsets[j], offsets[j] + tiles_touched)
+//
+// Load-balanced over OUTPUT entries: a CTA owns EMIT_TILE consecutive entries, finds the
+// depth-sorted primitives that produce them (binary search in the scan), stages their offsets,
+// ids and rects in shared memory and writes its entries coalesced.  (A thread or warp per
+// primitive is badly imbalanced: the nearest primitives -- adjacent in depth order -- are the
+// largest and cover thousands of tiles each.)
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ order, const uint32_t *__restrict__ tt,
-                                              const uint32_t *__restrict__ offsets, const ushort4 *__restrict__ rect,
-                                              int n, int tiles_x, int64_t capacity, uint32_t *__restrict__ tile_key,
-                                              uint32_t *__restrict__ entry_val) {
-  const int lane = threadIdx.x & 31;
-  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31;
-  const int j = j0 + lane;
-  uint32_t my_i = 0, my_tt = 0, my_off = 0;
-  ushort4 my_r = make_ushort4(0, 0, 0, 0);
-  if (j < n) {
-    my_i = order[j];
-    my_tt = tt[my_i];
-    if (my_tt) {
-      my_off = offsets[j];
-      my_r = rect[my_i];
-    }
+constexpr int EMIT_TILE = 2048;
+
+__device__ __forceinline__ int last_leq(const uint32_t *__restrict__ a, int n, uint32_t x) {   // max j: a[j] <= x
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a[mid] <= x) lo = mid; else hi = mid - 1;
   }
-  unsigned todo = __ballot_sync(0xffffffffu, my_tt != 0);
-  while (todo) {
-    const int src = __ffs(todo) - 1;
-    todo &= todo - 1;
-    const uint32_t i = __shfl_sync(0xffffffffu, my_i, src);
-    const uint32_t cntt = __shfl_sync(0xffffffffu, my_tt, src);
-    const uint32_t off = __shfl_sync(0xffffffffu, my_off, src);
-    const uint32_t tx0 = __shfl_sync(0xffffffffu, (uint32_t)my_r.x, src);
-    const uint32_t ty0 = __shfl_sync(0xffffffffu, (uint32_t)my_r.y, src);
-    const uint32_t tx1 = __shfl_sync(0xffffffffu, (uint32_t)my_r.z, src);
-    const uint32_t rw = tx1 - tx0 + 1;
-    for (uint32_t k = lane; k < cntt; k += 32) {
-      const uint32_t ty = ty0 + k / rw, tx = tx0 + k % rw;
-      const int64_t pos = (int64_t)off + k;
-      if (pos < capacity) {
-        tile_key[pos] = ty * (uint32_t)tiles_x + tx;
-        entry_val[pos] = i;
-      }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ order, const uint32_t *__restrict__ offsets,
+                                              const ushort4 *__restrict__ rect, int n, int tiles_x, int64_t capacity,
+                                              const uint32_t *__restrict__ E_dev, uint32_t *__restrict__ tile_key,
+                                              uint32_t *__restrict__ entry_val) {
+  __shared__ uint32_t s_off[EMIT_TILE];
+  __shared__ uint32_t s_id[EMIT_TILE];
+  __shared__ ushort4 s_rect[EMIT_TILE];
+  __shared__ int s_j0, s_cnt;
+  const int64_t E = item_count(E_dev, capacity);
+  const int64_t e0 = (int64_t)blockIdx.x * EMIT_TILE;
+  if (e0 >= E) return;
+  const int64_t e1 = e0 + EMIT_TILE < E ? e0 + EMIT_TILE : E;
+  if (threadIdx.x == 0) {
+    const int j0 = last_leq(offsets, n, (uint32_t)e0);
+    const int j1 = last_leq(offsets, n, (uint32_t)(e1 - 1));
+    s_j0 = j0;
+    s_cnt = j1 - j0 + 1;   // every primitive in the range owns >= 1 entry, so s_cnt <= EMIT_TILE
+  }
+  __syncthreads();
+  const int j0 = s_j0, cnt = s_cnt;
+  for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+    const uint32_t i = order[j0 + q];
+    s_off[q] = offsets[j0 + q];
+    s_id[q] = i;
+    s_rect[q] = rect[i];
+  }
+  __syncthreads();
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    int lo = 0, hi = cnt - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_off[mid] <= (uint32_t)e) lo = mid; else hi = mid - 1;
     }
+    const uint32_t k = (uint32_t)e - s_off[lo];
+    const ushort4 r = s_rect[lo];
+    const uint32_t rw = (uint32_t)r.z - r.x + 1;
+    const uint32_t ty = r.y + k / rw, tx = r.x + k % rw;
+    tile_key[e] = ty * (uint32_t)tiles_x + tx;
+    entry_val[e] = s_id[lo];
   }
 }
 
-void launch_emit(const lp_frame &F, int n, cudaStream_t st) {
-  if (n == 0) return;
-  k_emit<<<(n + 255) / 256, 256, 0, st>>>(F.prim_order, F.tiles_touched, F.offsets,
-                                          reinterpret_cast<const ushort4 *>(F.rect), n, F.tiles_x, F.capacity,
-                                          F.tile_key, F.entry_val);
+void launch_emit(const lp_frame &F, int n, int64_t max_entries, cudaStream_t st) {
+  if (n == 0 || max_entries <= 0) return;
+  const int64_t grid = (max_entries + EMIT_TILE - 1) / EMIT_TILE;
+  k_emit<<<(unsigned)grid, 256, 0, st>>>(F.prim_order, F.offsets, reinterpret_cast<const ushort4 *>(F.rect), n,
+                                         F.tiles_x, F.capacity, F.counters + LP_CNT_ENTRIES, F.tile_key, F.entry_val);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -73,13 +73,43 @@ __global__ void __launch_bounds__(256) k_adam(float *__restrict__ p, float *__re
   const int64_t b = G.begin[gi], e = G.end[gi];
   const float lr = G.lr[gi];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += stride) {
-    const float gg = g[i];
-    const float mm = fmaf(b1, m[i], (1.f - b1) * gg);
-    const float vv = fmaf(b2, v[i], (1.f - b2) * gg * gg);
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  auto upd = [&](float pp, float gg, float &mm, float &vv) {
+    mm = fmaf(b1, mm, (1.f - b1) * gg);
+    vv = fmaf(b2, vv, (1.f - b2) * gg * gg);
+    return pp - lr * (mm / bc1) / (sqrtf(vv / bc2) + eps);
+  };
+  // float4 body over the 16-byte aligned part of [b, e), scalar head / tail
+  const int64_t b4 = (b + 3) & ~int64_t(3), e4 = e & ~int64_t(3);
+  if (b4 < e4) {
+    float4 *p4 = reinterpret_cast<float4 *>(p + b4), *g4 = reinterpret_cast<float4 *>(g + b4);
+    float4 *m4 = reinterpret_cast<float4 *>(m + b4), *v4 = reinterpret_cast<float4 *>(v + b4);
+    const int64_t n4 = (e4 - b4) / 4;
+    for (int64_t i = tid; i < n4; i += stride) {
+      float4 pp = p4[i], gg = g4[i], mm = m4[i], vv = v4[i];
+      pp.x = upd(pp.x, gg.x, mm.x, vv.x);
+      pp.y = upd(pp.y, gg.y, mm.y, vv.y);
+      pp.z = upd(pp.z, gg.z, mm.z, vv.z);
+      pp.w = upd(pp.w, gg.w, mm.w, vv.w);
+      p4[i] = pp;
+      m4[i] = mm;
+      v4[i] = vv;
+      if (zero_grad) g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  const int64_t head_end = b4 < e ? b4 : e;
+  for (int64_t i = b + tid; i < head_end; i += stride) {
+    float mm = m[i], vv = v[i];
+    p[i] = upd(p[i], g[i], mm, vv);
     m[i] = mm;
     v[i] = vv;
-    p[i] -= lr * (mm / bc1) / (sqrtf(vv / bc2) + eps);
+    if (zero_grad) g[i] = 0.f;
+  }
+  for (int64_t i = (e4 > b ? (e4 > head_end ? e4 : head_end) : e) + tid; i < e; i += stride) {
+    float mm = m[i], vv = v[i];
+    p[i] = upd(p[i], g[i], mm, vv);
+    m[i] = mm;
+    v[i] = vv;
     if (zero_grad) g[i] = 0.f;
   }
 }
@@ -98,8 +128,8 @@ void launch_adam(float *p, float *g, float *m, float *v, const lp_adam_group *gr
     }
     for (int k = G.n; k < 8; ++k) { G.begin[k] = G.end[k] = 0; G.lr[k] = 0.f; }
     const float bc1 = 1.f - powf(b1, (float)step), bc2 = 1.f - powf(b2, (float)step);
-    int64_t want = (longest + 255) / 256;
-    const int gx = (int)(want < 148 * 4 ? want : 148 * 4);
+    const int64_t want = (longest / 4 + 255) / 256 + 1;
+    const int gx = (int)(want < 148 * 8 ? want : 148 * 8);
     k_adam<<<dim3(gx, G.n), 256, 0, st>>>(p, g, m, v, G, b1, b2, eps, bc1, bc2, zero_grad);
   }
 }

@@ -38,7 +38,7 @@ if __name__ == "__main__":
     ap.add_argument("--views", type=int, default=1)
     ap.add_argument("--sweep", action="store_true")
     a = ap.parse_args()
-    grid = [(s, m) for s in (0.25, 0.35, 0.5, 0.7, 1.0) for m in (-1.0, 0.0, 1.0)] if a.sweep else [(0.5, 0.0)]
+    grid = [(s, m) for s in (0.12, 0.15, 0.18, 0.22) for m in (-3.0, -2.0, -1.5, -1.0)] if a.sweep else [(0.5, 0.0)]
     for s, m in grid:
         t = time.time()
         print(json.dumps({"cfg": a.cfg, "size_scale": s, "opacity_mu": m, "views": stats(a.cfg, s, m, views=a.views),
