@@ -108,14 +108,17 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------------ work model
 
-def fp32_ops(kind, iterated, intersected, backward):
-    """Algorithmic FP32-pipe lane instructions: octahedron chord 26 per iterated pair,
-    tetrahedron 20; opacity + compositing 11 per intersected pair (forward); the backward replays the
-    chord (+6 argmax selects) and spends 61 per intersected pair (blend + moments)."""
-    chord = 26 if kind == 0 else 20
+def fp32_ops(kind, iterated, inbox, intersected, backward):
+    """Algorithmic FP32-pipe lane instructions: every iterated (pixel, entry) pair
+    costs the bbox reject (2 FADD + 2 FSETP|abs + vote ~ 6); a pair inside the bbox costs the chord
+    (octahedron 4 x (FMUL FFMA 2 FADD 2 FMNMX) - 2 + 2 FADD = 24, tetrahedron 6 x 2 FFMA + 4 FMNMX
+    + 3 = 19); an intersected pair costs opacity + compositing (11).  The backward replays the same
+    and adds the argmax tracking (+6 per in-bbox pair) and 61 per intersected pair (blend backward
+    + slab/plane moments)."""
+    chord = 24 if kind == 0 else 19
     if not backward:
-        return chord * iterated + 11 * intersected
-    return (chord + 6) * iterated + 61 * intersected
+        return 6 * iterated + chord * inbox + 11 * intersected
+    return 6 * iterated + (chord + 6) * inbox + 61 * intersected
 
 
 def launches_per_view(n, tiles):
@@ -164,6 +167,7 @@ def run_ours(args, rank, world, local_rank):
     E = [int(s[L.LP_CNT_ENTRIES]) for s in stats]
     it = [int(s[8]) | (int(s[9]) << 32) for s in stats]
     hit = [int(s[10]) | (int(s[11]) << 32) for s in stats]
+    box = [int(s[12]) | (int(s[13]) << 32) for s in stats]
     frustum = [int(s[L.LP_CNT_FRUSTUM]) for s in stats]
 
     # the timed renderer: async binning (no host sync), capacity sized from the counters pass
@@ -277,7 +281,7 @@ def run_ours(args, rank, world, local_rank):
 
     # rooflines of the single-kernel stages; the dominant one is reported as "roofline"
     kind = ds.kind
-    I_tot, X_tot = sum(it), sum(hit)
+    I_tot, X_tot, B_tot = sum(it), sum(hit), sum(box)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -295,8 +299,8 @@ def run_ours(args, rank, world, local_rank):
         except Exception:
             traffic_db = {}
     work = {
-        "fwd": ("k_raster_fwd", "alu", fp32_ops(kind, I_tot / n_local, X_tot / n_local, backward=False)),
-        "rbwd": ("k_raster_bwd", "alu", fp32_ops(kind, I_tot / n_local, X_tot / n_local, backward=True)),
+        "fwd": ("k_raster_fwd", "alu", fp32_ops(kind, I_tot / n_local, B_tot / n_local, X_tot / n_local, False)),
+        "rbwd": ("k_raster_bwd", "alu", fp32_ops(kind, I_tot / n_local, B_tot / n_local, X_tot / n_local, True)),
         "pbwd": ("k_preprocess_bwd", "hbm", 4 * n + vis * (4 * RG + 3 * Fb)),
         "pre": ("k_preprocess", "hbm", n * (Fb + 24) + vis * 4 * RW),
         "adam": ("k_adam", "hbm", 32 * ds.flat.numel()),
@@ -364,6 +368,7 @@ def run_ours(args, rank, world, local_rank):
                          % (ds.flat.numel() * 4 * 5 / 1e9),
                    "tile_list_entries_per_view": E, "iterated_pairs_per_px": round(I_tot / (n_local * W * H), 2),
                    "intersected_pairs_per_px": round(X_tot / (n_local * W * H), 2),
+                   "in_bbox_pairs_per_px": round(B_tot / (n_local * W * H), 2),
                    "frustum_primitives_per_view": frustum, "capacity": caps},
         "stages_ms_per_view": {k: round(v, 4) for k, v in stage_ms.items()},
         "roofline": dict(rooflines[dom], peak_source="measured HBM copy (MEASURED_PEAKS.json)" if

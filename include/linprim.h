@@ -79,7 +79,7 @@ typedef struct {
 typedef struct {
   int32_t kind, n, width, height, tiles_x, tiles_y;
   int64_t capacity;           /* maximum tile-list entries */
-  int32_t record_words;       /* floats per raster record (20 octa, 24 tetra) */
+  int32_t record_words;       /* floats per raster record (20 octa, 28 tetra) */
   int32_t rgrad_words;        /* floats per primitive in rgrad (20 octa, 22 tetra) */
   uint32_t *tiles_touched;    /* [n] */
   uint16_t *rect;             /* [n][4] tile rect tx0, ty0, tx1, ty1 (inclusive), zeros if none */
@@ -110,6 +110,7 @@ enum {
   LP_CNT_VISIBLE = 4,         /* primitives with tiles_touched > 0 */
   LP_CNT_ITERATED = 8,        /* words 8-9: u64 (pixel, entry) pairs evaluated by the forward (count_stats) */
   LP_CNT_INTERSECTED = 10,    /* words 10-11: u64 pairs with chord > 0 (count_stats) */
+  LP_CNT_INBOX = 12,          /* words 12-13: u64 pairs inside the primitive's screen bbox (count_stats) */
   LP_NUM_COUNTERS = 16
 };
 

@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include "../../include/linprim.h"
+#include "lp_device.cuh"
 #include "lp_kernels.h"
 
 namespace {
@@ -14,7 +15,7 @@ using namespace lp;
 constexpr size_t ALIGN = 256;
 inline size_t up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
-inline int record_words(int kind) { return kind == LP_OCTAHEDRON ? 20 : 24; }
+inline int record_words(int kind) { return kind == LP_OCTAHEDRON ? Kind<LP_OCTAHEDRON>::RW : Kind<LP_TETRAHEDRON>::RW; }
 inline int rgrad_words(int kind) { return kind == LP_OCTAHEDRON ? 20 : 22; }
 inline int offsets_k(int kind) { return kind == LP_OCTAHEDRON ? 3 : 4; }
 

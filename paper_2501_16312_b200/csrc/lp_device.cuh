@@ -21,20 +21,24 @@ constexpr int OCTA = LP_OCTAHEDRON;
 constexpr int TETRA = LP_TETRAHEDRON;
 
 template <int KIND> struct Kind;
+// Raster records (fp32, 16-byte aligned, gathered per tile-list entry).  The first float4 is
+// always the screen bounding box as (centre x, centre y, half width, half height): a pixel
+// outside it cannot intersect the primitive (convexity), so the raster rejects the pair with
+// ~6 instructions before the slab / plane evaluation.
+//   octahedron (20 words): bx=cx by=cy hx hy | (b g h) x 4 slabs | sigma r g b
+//   tetrahedron (28 words): bx by hx hy | cx cy | (A B C) x 6 slots | sigma r g b
 template <> struct Kind<LP_OCTAHEDRON> {
   static constexpr int K = 3;          // offset vectors (vertices are c +- o_j)
-  static constexpr int RW = 20;        // record words: cx cy (b g h)x4 sigma rgb pad2
+  static constexpr int RW = 20;        // record words
   static constexpr int RG = 20;        // raster-gradient words: (Mb Mg Mc Mh)x4 dsigma drgb
+  static constexpr int CX = 0, SLAB = 4, SIGMA = 16, RGB = 17;
 };
 template <> struct Kind<LP_TETRAHEDRON> {
   static constexpr int K = 4;          // vertices c + o_k
-  static constexpr int RW = 24;        // cx cy (A B C)x6 slots sigma rgb
+  static constexpr int RW = 28;        // record words
   static constexpr int RG = 22;        // (MA MB MC)x6 slots dsigma drgb
+  static constexpr int CX = 4, SLAB = 6, SIGMA = 24, RGB = 25;
 };
-
-// record word offsets
-constexpr int REC_OCTA_SIGMA = 14, REC_OCTA_RGB = 15;
-constexpr int REC_TETRA_SIGMA = 20, REC_TETRA_RGB = 21;
 
 __device__ __forceinline__ float fm(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float fa(float a, float b) { return __fadd_rn(a, b); }
@@ -352,16 +356,17 @@ __device__ __forceinline__ void tetra_planes(const float off[4][3], TetraPlanes 
 // ---------------------------------------------------------------------------------------------
 // chord evaluation (a8).  TRACK: also return the entry / exit slab (octa) or slot (tetra).
 // ---------------------------------------------------------------------------------------------
+// dx, dy: pixel centre minus the ray-space centre c_r (record word CX, CX+1), fs()-computed.
 template <bool TRACK>
-__device__ __forceinline__ float octa_chord(const float *rec, float px, float py, int &se, int &sx) {
-  const float dx = fs(px, rec[0]), dy = fs(py, rec[1]);
-  float L = __fmaf_rn(rec[2], dx, fm(rec[3], dy));
-  float en = fs(L, rec[4]), ex = fa(L, rec[4]);
+__device__ __forceinline__ float octa_chord(const float *rec, float dx, float dy, int &se, int &sx) {
+  constexpr int B = Kind<LP_OCTAHEDRON>::SLAB;
+  float L = __fmaf_rn(rec[B], dx, fm(rec[B + 1], dy));
+  float en = fs(L, rec[B + 2]), ex = fa(L, rec[B + 2]);
   if (TRACK) { se = 0; sx = 0; }
 #pragma unroll
   for (int s = 1; s < 4; ++s) {
-    L = __fmaf_rn(rec[2 + 3 * s], dx, fm(rec[3 + 3 * s], dy));
-    const float a = fs(L, rec[4 + 3 * s]), b = fa(L, rec[4 + 3 * s]);
+    L = __fmaf_rn(rec[B + 3 * s], dx, fm(rec[B + 1 + 3 * s], dy));
+    const float a = fs(L, rec[B + 2 + 3 * s]), b = fa(L, rec[B + 2 + 3 * s]);
     if (TRACK) {
       if (a > en) se = s;
       if (b < ex) sx = s;
@@ -373,11 +378,11 @@ __device__ __forceinline__ float octa_chord(const float *rec, float px, float py
 }
 
 template <bool TRACK>
-__device__ __forceinline__ float tetra_chord(const float *rec, float px, float py, int &se, int &sx) {
-  const float dx = fs(px, rec[0]), dy = fs(py, rec[1]);
+__device__ __forceinline__ float tetra_chord(const float *rec, float dx, float dy, int &se, int &sx) {
+  constexpr int B = Kind<LP_TETRAHEDRON>::SLAB;
   float z[6];
 #pragma unroll
-  for (int s = 0; s < 6; ++s) z[s] = __fmaf_rn(rec[4 + 3 * s], dy, __fmaf_rn(rec[3 + 3 * s], dx, rec[2 + 3 * s]));
+  for (int s = 0; s < 6; ++s) z[s] = __fmaf_rn(rec[B + 2 + 3 * s], dy, __fmaf_rn(rec[B + 1 + 3 * s], dx, rec[B + 3 * s]));
   float en = z[0], ex = z[3];
   if (TRACK) { se = 0; sx = 3; }
 #pragma unroll
@@ -390,6 +395,18 @@ __device__ __forceinline__ float tetra_chord(const float *rec, float px, float p
     ex = fminf(ex, z[3 + s]);
   }
   return fs(ex, en);
+}
+
+template <int KIND, bool TRACK>
+__device__ __forceinline__ float chord(const float *rec, float dx, float dy, int &se, int &sx) {
+  if (KIND == LP_OCTAHEDRON) return octa_chord<TRACK>(rec, dx, dy, se, sx);
+  return tetra_chord<TRACK>(rec, dx, dy, se, sx);
+}
+
+// slack of the bbox reject test: a pair rejected by it has chord <= 0 (up to fp32 rounding of
+// the bbox itself, covered by the slack)
+__device__ __forceinline__ bool in_bbox(const float4 &bb, float px, float py) {
+  return fabsf(px - bb.x) <= bb.z && fabsf(py - bb.y) <= bb.w;
 }
 
 // opacity transmittance factor E = exp(-sigma chord); identical in forward and backward.

@@ -92,39 +92,51 @@ __global__ void __launch_bounds__(256) k_preprocess(lp_prims P, lp_camera cam, f
   for (int ch = 0; ch < 3; ++ch) rgb[ch] = fmaxf(rgb[ch], 0.f);
 
   // ---- raster record
+  using KD = Kind<KIND>;
   float rec[RW];
-  rec[0] = g.crx;
-  rec[1] = g.cry;
+  // screen bbox of the (filtered) vertices, with a small slack (record word 0..3)
+  float xlo = g.off[0][0], xhi = g.off[0][0], ylo = g.off[0][1], yhi = g.off[0][1];
+#pragma unroll
+  for (int j = 1; j < K; ++j) {
+    xlo = fminf(xlo, g.off[j][0]); xhi = fmaxf(xhi, g.off[j][0]);
+    ylo = fminf(ylo, g.off[j][1]); yhi = fmaxf(yhi, g.off[j][1]);
+  }
+  if (KIND == OCTA) {   // vertices c +- o_j: symmetric about c
+    xhi = fmaxf(-xlo, xhi); xlo = -xhi;
+    yhi = fmaxf(-ylo, yhi); ylo = -yhi;
+  }
+  const float hx = 0.5f * (xhi - xlo), hy = 0.5f * (yhi - ylo);
+  rec[0] = g.crx + 0.5f * (xlo + xhi);
+  rec[1] = g.cry + 0.5f * (ylo + yhi);
+  rec[2] = hx * 1.0001f + 1e-3f;
+  rec[3] = hy * 1.0001f + 1e-3f;
+  rec[KD::CX] = g.crx;
+  rec[KD::CX + 1] = g.cry;
   if (KIND == OCTA) {
     SlabRows S;
     octa_slabs(g.off, S);
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const double rz = S.r[s][2];
-      rec[2 + 3 * s] = S.ok ? (float)(-S.r[s][0] / rz) : 0.f;
-      rec[3 + 3 * s] = S.ok ? (float)(-S.r[s][1] / rz) : 0.f;
-      rec[4 + 3 * s] = S.ok ? (float)(1.0 / fabs(rz)) : -1.f;   // h = -1: never intersected
+      rec[KD::SLAB + 3 * s] = S.ok ? (float)(-S.r[s][0] / rz) : 0.f;
+      rec[KD::SLAB + 1 + 3 * s] = S.ok ? (float)(-S.r[s][1] / rz) : 0.f;
+      rec[KD::SLAB + 2 + 3 * s] = S.ok ? (float)(1.0 / fabs(rz)) : -1.f;   // h = -1: never intersected
     }
-    rec[REC_OCTA_SIGMA] = sigma;
-    rec[REC_OCTA_RGB + 0] = rgb[0];
-    rec[REC_OCTA_RGB + 1] = rgb[1];
-    rec[REC_OCTA_RGB + 2] = rgb[2];
-    rec[18] = rec[19] = 0.f;
   } else {
     TetraPlanes T;
     tetra_planes(g.off, T);
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       const int f = T.slot_face[s];
-      rec[2 + 3 * s] = T.ok ? (float)sel(T.A, f) : (s < 3 ? 1.f : -1.f);   // empty: entry 1 > exit -1
-      rec[3 + 3 * s] = T.ok ? (float)sel(T.B, f) : 0.f;
-      rec[4 + 3 * s] = T.ok ? (float)sel(T.C, f) : 0.f;
+      rec[KD::SLAB + 3 * s] = T.ok ? (float)sel(T.A, f) : (s < 3 ? 1.f : -1.f);   // empty: entry 1 > exit -1
+      rec[KD::SLAB + 1 + 3 * s] = T.ok ? (float)sel(T.B, f) : 0.f;
+      rec[KD::SLAB + 2 + 3 * s] = T.ok ? (float)sel(T.C, f) : 0.f;
     }
-    rec[REC_TETRA_SIGMA] = sigma;
-    rec[REC_TETRA_RGB + 0] = rgb[0];
-    rec[REC_TETRA_RGB + 1] = rgb[1];
-    rec[REC_TETRA_RGB + 2] = rgb[2];
   }
+  rec[KD::SIGMA] = sigma;
+  rec[KD::RGB + 0] = rgb[0];
+  rec[KD::RGB + 1] = rgb[1];
+  rec[KD::RGB + 2] = rgb[2];
   float4 *dst = reinterpret_cast<float4 *>(F.record + (size_t)i * RW);
 #pragma unroll
   for (int w = 0; w < RW / 4; ++w) dst[w] = make_float4(rec[4 * w], rec[4 * w + 1], rec[4 * w + 2], rec[4 * w + 3]);

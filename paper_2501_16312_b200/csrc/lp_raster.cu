@@ -35,33 +35,26 @@ __device__ __forceinline__ void pixel_of(int tid, int k, int &x, int &y) {
   }
 }
 
-template <int KIND>
-__device__ __forceinline__ float chord_of(const float *rec, float px, float py, int &se, int &sx) {
-  if (KIND == OCTA) return octa_chord<false>(rec, px, py, se, sx);
-  return tetra_chord<false>(rec, px, py, se, sx);
-}
-
 // =============================================================================================
 // K3 forward
 // =============================================================================================
 template <int KIND, int NT>
 __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg, float *__restrict__ image) {
-  constexpr int RW = Kind<KIND>::RW, RW4 = RW / 4, PPT = 256 / NT;
-  constexpr int SIG = KIND == OCTA ? REC_OCTA_SIGMA : REC_TETRA_SIGMA;
-  constexpr int RGB = KIND == OCTA ? REC_OCTA_RGB : REC_TETRA_RGB;
+  using KD = Kind<KIND>;
+  constexpr int RW = KD::RW, RW4 = RW / 4, PPT = 256 / NT;
   __shared__ float4 s_rec[NT * RW4];
-  __shared__ unsigned long long s_stat[2];
+  __shared__ unsigned long long s_stat[3];
 
   const int tile = blockIdx.x;
   const int tx = tile % F.tiles_x, ty = tile / F.tiles_x;
   const uint32_t start = F.ranges[2 * tile], end = F.ranges[2 * tile + 1];
   const int W = F.width, H = F.height;
-  if (threadIdx.x < 2) s_stat[threadIdx.x] = 0ull;
+  if (threadIdx.x < 3) s_stat[threadIdx.x] = 0ull;
 
   float fx[PPT], fy[PPT], T[PPT], C[PPT][3];
   uint32_t nproc[PPT];
   bool done[PPT], inside[PPT];
-  uint32_t nhit = 0;
+  uint32_t nhit = 0, nbox = 0;
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     int x, y;
@@ -93,19 +86,29 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
     if (__all_sync(0xffffffffu, mine)) continue;
     const int cnt = (int)min((uint32_t)NT, end - b);
     for (int j = 0; j < cnt; ++j) {
+      // bbox reject (convexity: outside the vertex bbox the chord is 0), warp-uniform skip
+      const float4 bb = s_rec[j * RW4];
+      bool test[PPT], any = false;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        test[k] = !done[k] && in_bbox(bb, fx[k], fy[k]);
+        any = any || test[k];
+      }
+      if (!__any_sync(0xffffffffu, any)) continue;
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        if (done[k]) continue;
+        if (!test[k]) continue;
+        ++nbox;
         int se, sx;
-        const float ch = chord_of<KIND>(rec, fx[k], fy[k], se, sx);
+        const float ch = chord<KIND, false>(rec, fs(fx[k], rec[KD::CX]), fs(fy[k], rec[KD::CX + 1]), se, sx);
         if (ch > 0.f) {
-          const float E = transmit(rec[SIG], ch);
+          const float E = transmit(rec[KD::SIGMA], ch);
           const float o = 1.f - E;
           const float wgt = T[k] * o;
-          C[k][0] = fmaf(wgt, rec[RGB + 0], C[k][0]);
-          C[k][1] = fmaf(wgt, rec[RGB + 1], C[k][1]);
-          C[k][2] = fmaf(wgt, rec[RGB + 2], C[k][2]);
+          C[k][0] = fmaf(wgt, rec[KD::RGB + 0], C[k][0]);
+          C[k][1] = fmaf(wgt, rec[KD::RGB + 1], C[k][1]);
+          C[k][2] = fmaf(wgt, rec[KD::RGB + 2], C[k][2]);
           T[k] = T[k] * E;
           ++nhit;
           if (T[k] < cfg.t_stop) {       // include-then-stop (reading 9)
@@ -136,16 +139,19 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
     for (int o = 16; o > 0; o >>= 1) {
       it += __shfl_xor_sync(0xffffffffu, it, o);
       nhit += __shfl_xor_sync(0xffffffffu, nhit, o);
+      nbox += __shfl_xor_sync(0xffffffffu, nbox, o);
     }
     __syncthreads();
     if ((threadIdx.x & 31) == 0) {
       atomicAdd(&s_stat[0], it);
       atomicAdd(&s_stat[1], (unsigned long long)nhit);
+      atomicAdd(&s_stat[2], (unsigned long long)nbox);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       atomicAdd(reinterpret_cast<unsigned long long *>(F.counters + LP_CNT_ITERATED), s_stat[0]);
       atomicAdd(reinterpret_cast<unsigned long long *>(F.counters + LP_CNT_INTERSECTED), s_stat[1]);
+      atomicAdd(reinterpret_cast<unsigned long long *>(F.counters + LP_CNT_INBOX), s_stat[2]);
     }
   }
 }
@@ -199,9 +205,8 @@ __device__ __forceinline__ float warp_transpose_reduce(const float (&a)[N], int 
 // =============================================================================================
 template <int KIND, int NT>
 __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg, const float *__restrict__ dL) {
-  constexpr int RW = Kind<KIND>::RW, RW4 = RW / 4, PPT = 256 / NT, RG = Kind<KIND>::RG;
-  constexpr int SIG = KIND == OCTA ? REC_OCTA_SIGMA : REC_TETRA_SIGMA;
-  constexpr int RGB = KIND == OCTA ? REC_OCTA_RGB : REC_TETRA_RGB;
+  using KD = Kind<KIND>;
+  constexpr int RW = KD::RW, RW4 = RW / 4, PPT = 256 / NT, RG = KD::RG;
   __shared__ float4 s_rec[NT * RW4];
   __shared__ uint32_t s_id[NT];
   __shared__ uint32_t s_last;
@@ -259,6 +264,15 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
 
     for (int j = (int)(bend - bstart) - 1; j >= 0; --j) {
       const uint32_t ej = bstart + (uint32_t)j;
+      // the forward's bbox reject, replayed exactly (same test, same inputs)
+      const float4 bb = s_rec[j * RW4];
+      bool test[PPT], any = false;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        test[k] = ej < last[k] && in_bbox(bb, fx[k], fy[k]);
+        any = any || test[k];
+      }
+      if (!__any_sync(0xffffffffu, any)) continue;
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
       float acc[RG];
 #pragma unroll
@@ -266,13 +280,13 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
       bool hit = false;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        if (ej >= last[k]) continue;
+        if (!test[k]) continue;
         int se, sx;
-        const float ch = KIND == OCTA ? octa_chord<true>(rec, fx[k], fy[k], se, sx)
-                                      : tetra_chord<true>(rec, fx[k], fy[k], se, sx);
+        const float dx = fs(fx[k], rec[KD::CX]), dy = fs(fy[k], rec[KD::CX + 1]);
+        const float ch = chord<KIND, true>(rec, dx, dy, se, sx);
         if (!(ch > 0.f)) continue;
         hit = true;
-        const float sig = rec[SIG];
+        const float sig = rec[KD::SIGMA];
         const float E = transmit(sig, ch);
         const float o = 1.f - E;
         const float Tk = T[k] / E;                       // transmittance in front of this entry
@@ -280,15 +294,14 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           acc[RG - 3 + c] = fmaf(Tk * o, G[k][c], acc[RG - 3 + c]);   // dL/drgb
-          dLdo = fmaf(rec[RGB + c] - S[k][c], G[k][c], dLdo);
-          S[k][c] = fmaf(o, rec[RGB + c], E * S[k][c]);               // colour behind the previous entry
+          dLdo = fmaf(rec[KD::RGB + c] - S[k][c], G[k][c], dLdo);
+          S[k][c] = fmaf(o, rec[KD::RGB + c], E * S[k][c]);           // colour behind the previous entry
         }
         dLdo *= Tk;
         T[k] = Tk;
         const float gE = E * dLdo;
         acc[RG - 4] = fmaf(ch, gE, acc[RG - 4]);          // dL/dsigma = chord E dL/do
         const float g = sig * gE;                          // dL/d exit = g, dL/d entry = -g
-        const float dx = fx[k] - rec[0], dy = fy[k] - rec[1];
         if (KIND == OCTA) {
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
