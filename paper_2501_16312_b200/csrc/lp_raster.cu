@@ -13,6 +13,7 @@
 // and one RED.F32 per moment per (warp, primitive) into rgrad[moment][n].
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "lp_device.cuh"
 #include "lp_kernels.h"
@@ -33,6 +34,24 @@ __device__ __forceinline__ void pixel_of(int tid, int k, int &x, int &y) {
     x = (w & 1) * 8 + (lane & 7);
     y = (w >> 1) * 4 + (lane >> 3);
   }
+}
+
+// the warp's pixel-centre rectangle (absolute pixel coordinates + 0.5), for the warp-uniform reject
+template <int NT>
+__device__ __forceinline__ void warp_rect(int w, int tx, int ty, float &x0, float &x1, float &y0, float &y1) {
+  int ox, oy, wx, wy;
+  if (NT == 128) { ox = (w & 1) * 8; oy = (w >> 1) * 8; wx = 8; wy = 8; }
+  else if (NT == 64) { ox = 0; oy = w * 8; wx = 16; wy = 8; }
+  else { ox = (w & 1) * 8; oy = (w >> 1) * 4; wx = 8; wy = 4; }
+  x0 = (float)(tx * LP_TILE + ox) + 0.5f;
+  x1 = x0 + (float)(wx - 1);
+  y0 = (float)(ty * LP_TILE + oy) + 0.5f;
+  y1 = y0 + (float)(wy - 1);
+}
+
+// does the primitive's screen bbox reach any pixel centre of the warp? (warp-uniform)
+__device__ __forceinline__ bool rect_hits_bbox(const float4 &bb, float x0, float x1, float y0, float y1) {
+  return bb.x - bb.z <= x1 && bb.x + bb.z >= x0 && bb.y - bb.w <= y1 && bb.y + bb.w >= y0;
 }
 
 // =============================================================================================
@@ -69,6 +88,8 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
     done[k] = !inside[k];
     nproc[k] = end - start;
   }
+  float wx0, wx1, wy0, wy1;
+  warp_rect<NT>(threadIdx.x >> 5, tx, ty, wx0, wx1, wy0, wy1);
 
   for (uint32_t b = start; b < end; b += NT) {
     bool mine = true;
@@ -86,20 +107,14 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
     if (__all_sync(0xffffffffu, mine)) continue;
     const int cnt = (int)min((uint32_t)NT, end - b);
     for (int j = 0; j < cnt; ++j) {
-      // bbox reject (convexity: outside the vertex bbox the chord is 0), warp-uniform skip
+      // bbox reject (convexity: outside the vertex bbox the chord is <= 0): warp-uniform
       const float4 bb = s_rec[j * RW4];
-      bool test[PPT], any = false;
-#pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        test[k] = !done[k] && in_bbox(bb, fx[k], fy[k]);
-        any = any || test[k];
-      }
-      if (!__any_sync(0xffffffffu, any)) continue;
+      if (!rect_hits_bbox(bb, wx0, wx1, wy0, wy1)) continue;
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        if (!test[k]) continue;
-        ++nbox;
+        if (done[k]) continue;
+        if (cfg.count_stats) nbox += in_bbox(bb, fx[k], fy[k]) ? 1u : 0u;
         int se, sx;
         const float ch = chord<KIND, false>(rec, fs(fx[k], rec[KD::CX]), fs(fy[k], rec[KD::CX + 1]), se, sx);
         if (ch > 0.f) {
@@ -244,6 +259,8 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
   }
   __syncthreads();
   const uint32_t lmax = s_last;
+  float wx0, wx1, wy0, wy1;
+  warp_rect<NT>(threadIdx.x >> 5, tx, ty, wx0, wx1, wy0, wy1);
 
   for (uint32_t bend = lmax; bend > start; bend = (bend - start > NT) ? bend - NT : start) {
     const uint32_t bstart = (bend - start > NT) ? bend - NT : start;
@@ -264,15 +281,10 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
 
     for (int j = (int)(bend - bstart) - 1; j >= 0; --j) {
       const uint32_t ej = bstart + (uint32_t)j;
-      // the forward's bbox reject, replayed exactly (same test, same inputs)
+      // warp-uniform bbox reject: pixels outside the bbox have chord <= 0, so the set of hit
+      // pairs is the forward's regardless of either kernel's warp footprint
       const float4 bb = s_rec[j * RW4];
-      bool test[PPT], any = false;
-#pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        test[k] = ej < last[k] && in_bbox(bb, fx[k], fy[k]);
-        any = any || test[k];
-      }
-      if (!__any_sync(0xffffffffu, any)) continue;
+      if (!rect_hits_bbox(bb, wx0, wx1, wy0, wy1)) continue;
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
       float acc[RG];
 #pragma unroll
@@ -280,7 +292,7 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
       bool hit = false;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        if (!test[k]) continue;
+        if (ej >= last[k]) continue;
         int se, sx;
         const float dx = fs(fx[k], rec[KD::CX]), dy = fs(fy[k], rec[KD::CX + 1]);
         const float ch = chord<KIND, true>(rec, dx, dy, se, sx);
@@ -289,7 +301,7 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
         const float sig = rec[KD::SIGMA];
         const float E = transmit(sig, ch);
         const float o = 1.f - E;
-        const float Tk = T[k] / E;                       // transmittance in front of this entry
+        const float Tk = __fdividef(T[k], E);             // transmittance in front of this entry
         float dLdo = 0.f;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -333,19 +345,37 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
 }
 
 // ---------------------------------------------------------------------------------------------
-constexpr int FWD_NT = 128;
-constexpr int BWD_NT = 128;
+// CTA size = 256 / pixels-per-thread.  Tuning knobs LP_FWD_NT / LP_BWD_NT (64 or 128) exist for
+// measurement only; the defaults are the measured best.
+static int nt_from_env(const char *name, int dflt) {
+  const char *s = getenv(name);
+  if (!s) return dflt;
+  const int v = atoi(s);
+  return (v == 64 || v == 128) ? v : dflt;
+}
 
 void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image, cudaStream_t st) {
+  static const int nt = nt_from_env("LP_FWD_NT", 128);
   const int tiles = F.tiles_x * F.tiles_y;
-  if (F.kind == LP_OCTAHEDRON) k_raster_fwd<LP_OCTAHEDRON, FWD_NT><<<tiles, FWD_NT, 0, st>>>(F, cfg, image);
-  else k_raster_fwd<LP_TETRAHEDRON, FWD_NT><<<tiles, FWD_NT, 0, st>>>(F, cfg, image);
+  if (nt == 64) {
+    if (F.kind == LP_OCTAHEDRON) k_raster_fwd<LP_OCTAHEDRON, 64><<<tiles, 64, 0, st>>>(F, cfg, image);
+    else k_raster_fwd<LP_TETRAHEDRON, 64><<<tiles, 64, 0, st>>>(F, cfg, image);
+  } else {
+    if (F.kind == LP_OCTAHEDRON) k_raster_fwd<LP_OCTAHEDRON, 128><<<tiles, 128, 0, st>>>(F, cfg, image);
+    else k_raster_fwd<LP_TETRAHEDRON, 128><<<tiles, 128, 0, st>>>(F, cfg, image);
+  }
 }
 
 void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL, cudaStream_t st) {
+  static const int nt = nt_from_env("LP_BWD_NT", 64);
   const int tiles = F.tiles_x * F.tiles_y;
-  if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, BWD_NT><<<tiles, BWD_NT, 0, st>>>(F, cfg, dL);
-  else k_raster_bwd<LP_TETRAHEDRON, BWD_NT><<<tiles, BWD_NT, 0, st>>>(F, cfg, dL);
+  if (nt == 64) {
+    if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, 64><<<tiles, 64, 0, st>>>(F, cfg, dL);
+    else k_raster_bwd<LP_TETRAHEDRON, 64><<<tiles, 64, 0, st>>>(F, cfg, dL);
+  } else {
+    if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, 128><<<tiles, 128, 0, st>>>(F, cfg, dL);
+    else k_raster_bwd<LP_TETRAHEDRON, 128><<<tiles, 128, 0, st>>>(F, cfg, dL);
+  }
 }
 
 }  // namespace lp
