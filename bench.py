@@ -189,7 +189,9 @@ def run_ours(args, rank, world, local_rank):
               (off["sh"][0], off["sh"][0] + 3 * n, 2.5e-3), (off["sh"][0] + 3 * n, off["sh"][1], 1.25e-4)]
     scale = 1.0 / (3.0 * W * H * n_views)
     cams_c = rend.cams
-    ev_names = ["pre", "sort", "fwd", "l1", "rbwd", "pbwd"]
+    ev_names = ["pre", "sort", "fwd", "l1", "rbwd"]           # per view
+    fa_all = render.frames_array(rend.frames)
+    ca_all = rend._cams(list(range(n_local)))
 
     def step(si, events=None):
         for i in range(n_local):
@@ -212,17 +214,19 @@ def run_ours(args, rank, world, local_rank):
             L.lp_raster_bwd(ca, rend.cfg, fa, dL[i], st)
             if events is not None:
                 events[i][5].record(st)
-            L.lp_preprocess_bwd(ds.prims, ca, rend.cfg, fa, ds.grads, st)
-            if events is not None:
-                events[i][6].record(st)
             render._store_back([rend.frames[i]], fa)
+            fa_all[i] = rend.frames[i].c
+        # preprocess backward fused over this rank's views (feature + SH gradients written once)
+        L.lp_preprocess_bwd(ds.prims, ca_all, rend.cfg, fa_all, ds.grads, st)
+        if events is not None:
+            events[n_local][0].record(st)
         if world > 1:
             dist.all_reduce(ds.grad)
         if events is not None:
-            events[n_local][0].record(st)
+            events[n_local][1].record(st)
         L.lp_adam_step(ds.flat, ds.grad, m, v, groups, 0.9, 0.999, 1e-15, si + 1, st, zero_grad=True)
         if events is not None:
-            events[n_local][1].record(st)
+            events[n_local][2].record(st)
 
     def barrier():
         if world > 1:
@@ -245,8 +249,8 @@ def run_ours(args, rank, world, local_rank):
 
     vis = [s for s in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if s.strip().isdigit()]
     clocks = ClockSampler(int(vis[local_rank]) if local_rank < len(vis) else local_rank)
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(n_local)] + [
-        [torch.cuda.Event(enable_timing=True) for _ in range(2)]] for _ in range(args.steps)]
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(n_local)] + [
+        [torch.cuda.Event(enable_timing=True) for _ in range(3)]] for _ in range(args.steps)]
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     clocks.start()
@@ -269,15 +273,19 @@ def run_ours(args, rank, world, local_rank):
 
     # per-stage averages (ms per view-call) from the timed region's events
     stage = {nm: [] for nm in ev_names}
-    ar_adam = []
+    pb, ar, ad = [], [], []
     for k in range(args.steps):
         for i in range(n_local):
             e = evs[k][i]
             for j, nm in enumerate(ev_names):
                 stage[nm].append(e[j].elapsed_time(e[j + 1]))
-        ar_adam.append(evs[k][n_local][0].elapsed_time(evs[k][n_local][1]))
+        pb.append(evs[k][n_local - 1][5].elapsed_time(evs[k][n_local][0]))
+        ar.append(evs[k][n_local][0].elapsed_time(evs[k][n_local][1]))
+        ad.append(evs[k][n_local][1].elapsed_time(evs[k][n_local][2]))
     stage_ms = {nm: statistics.mean(vals) for nm, vals in stage.items()}
-    stage_ms["adam"] = statistics.mean(ar_adam)
+    stage_ms["pbwd_all_views"] = statistics.mean(pb)
+    stage_ms["allreduce"] = statistics.mean(ar)
+    stage_ms["adam"] = statistics.mean(ad)
 
     # rooflines of the single-kernel stages; the dominant one is reported as "roofline"
     kind = ds.kind
@@ -301,7 +309,9 @@ def run_ours(args, rank, world, local_rank):
     work = {
         "fwd": ("k_raster_fwd", "alu", fp32_ops(kind, I_tot / n_local, B_tot / n_local, X_tot / n_local, False)),
         "rbwd": ("k_raster_bwd", "alu", fp32_ops(kind, I_tot / n_local, B_tot / n_local, X_tot / n_local, True)),
-        "pbwd": ("k_preprocess_bwd", "hbm", 4 * n + vis * (4 * RG + 3 * Fb)),
+        # fused over the rank's views: tiles_touched + rgrad per view, features read and feature
+        # gradients read-modified-written once per call
+        "pbwd_all_views": ("k_preprocess_bwd+k_sh_bwd", "hbm", 4 * n * n_local + vis * n_local * 4 * RG + n * 3 * Fb),
         "pre": ("k_preprocess", "hbm", n * (Fb + 24) + vis * 4 * RW),
         "adam": ("k_adam", "hbm", 32 * ds.flat.numel()),
     }

@@ -242,11 +242,10 @@ lp_status lp_render_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   size_t off = 0;
   for (int v = 0; v < n_views; ++v) {
-    const lp_frame &F = frames[v];
-    launch_raster_bwd(F, *cfg, dL_dimage + off, st);
-    launch_preprocess_bwd(*prims, cams[v], cfg->aa_kernel, F, *grads, st);
+    launch_raster_bwd(frames[v], *cfg, dL_dimage + off, st);
     off += (size_t)3 * cams[v].width * cams[v].height;
   }
+  launch_preprocess_bwd(*prims, cams, cfg->aa_kernel, frames, n_views, *grads, st);
   return last_error();
 }
 
@@ -273,7 +272,7 @@ lp_status lp_preprocess_bwd(const lp_prims *prims, const lp_camera *cams, int32_
     if (frames[v].kind != prims->kind || frames[v].n != prims->n) return LP_ERR_ARG;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  for (int v = 0; v < n_views; ++v) launch_preprocess_bwd(*prims, cams[v], cfg->aa_kernel, frames[v], *grads, st);
+  launch_preprocess_bwd(*prims, cams, cfg->aa_kernel, frames, n_views, *grads, st);
   return last_error();
 }
 

@@ -144,23 +144,33 @@ __global__ void __launch_bounds__(256) k_preprocess(lp_prims P, lp_camera cam, f
 
 // =============================================================================================
 // K5: raster moments -> ray-space geometry -> world features
+// One thread per primitive, looping over up to LP_MAXV views (the frames of one call): the
+// feature gradients are accumulated in registers and written once per call, and a primitive
+// invisible in one view usually has work in another (better SIMT utilisation).
 // =============================================================================================
+constexpr int LP_MAXV = 8;
+struct ViewPack {
+  lp_camera cam[LP_MAXV];
+  const float *rgrad[LP_MAXV];
+  const uint32_t *tt[LP_MAXV];
+  int nv;
+};
+
+// one view's contribution; false if the view has no raster gradient for primitive i
 template <int KIND>
-__global__ void __launch_bounds__(128, 4) k_preprocess_bwd(lp_prims P, lp_camera cam, float kappa, lp_frame F,
-                                                        lp_grads Gs) {
+__device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_camera &cam, float kappa, int i,
+                                                  const float *__restrict__ rgrad, float gpos[3], float grot[4],
+                                                  float gdist[4], float &gop, float &m2d) {
   constexpr int K = Kind<KIND>::K, RG = Kind<KIND>::RG;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P.n) return;
-  if (F.tiles_touched[i] == 0) return;
   const int n = P.n;
   float m[RG];
   bool any = false;
 #pragma unroll
   for (int a = 0; a < RG; ++a) {
-    m[a] = F.rgrad[(size_t)a * n + i];
+    m[a] = rgrad[(size_t)a * n + i];
     any |= (m[a] != 0.f);
   }
-  if (!any) return;
+  if (!any) return false;
 
   Geom g;
   float dhf[4], qf[4], cf[3];
@@ -267,7 +277,7 @@ __global__ void __launch_bounds__(128, 4) k_preprocess_bwd(lp_prims P, lp_camera
     dsig = m[18];
     drgb[0] = m[19]; drgb[1] = m[20]; drgb[2] = m[21];
   }
-  if (Gs.mean2d_abs) Gs.mean2d_abs[i] += (float)sqrt(gcr[0] * gcr[0] + gcr[1] * gcr[1]);
+  m2d += (float)sqrt(gcr[0] * gcr[0] + gcr[1] * gcr[1]);
 
   // ---- the 2D filter adds constants (fixed extreme index): identity.
   using CT = float;   // the chain below is well conditioned: fp32 (the M^-1 / plane part above is fp64)
@@ -341,16 +351,16 @@ __global__ void __launch_bounds__(128, 4) k_preprocess_bwd(lp_prims P, lp_camera
   for (int a = 0; a < 3; ++a) gc[a] = Wm[0][a] * gp[0] + Wm[1][a] * gp[1] + Wm[2][a] * gp[2];
 
   // ---- distances (through the optional 3D filter)
-  if (Gs.dist) {
+  {
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       CT gd = gdh[j];
       if (P.filter3d) gd *= (CT)P.dist[j * n + i] / (CT)dhf[j];
-      Gs.dist[(size_t)j * n + i] += (float)gd;
+      gdist[j] += (float)gd;
     }
   }
   // ---- rotation: R(q_hat) -> q_hat -> q
-  if (Gs.rot) {
+  {
     const CT dR[4][3][3] = {
         {{0, -2 * z, 2 * y}, {2 * z, 0, -2 * x}, {-2 * y, 2 * x, 0}},
         {{0, 2 * y, 2 * z}, {2 * y, -4 * x, -2 * w}, {2 * z, 2 * w, -4 * x}},
@@ -366,76 +376,138 @@ __global__ void __launch_bounds__(128, 4) k_preprocess_bwd(lp_prims P, lp_camera
     const CT qh[4] = {w, x, y, z};
     const CT dot = qh[0] * gq[0] + qh[1] * gq[1] + qh[2] * gq[2] + qh[3] * gq[3];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) Gs.rot[(size_t)a * n + i] += (float)((gq[a] - qh[a] * dot) / nq);
+    for (int a = 0; a < 4; ++a) grot[a] += (float)((gq[a] - qh[a] * dot) / nq);
   }
   // ---- opacity: Eq. 1 with the denominator frozen, alpha = sigmoid(logit)
-  if (Gs.opacity) {
+  {
     const CT alpha = 1.0f / (1.0f + expf(-(CT)P.opacity[i]));
     CT md = dhf[0];
 #pragma unroll
     for (int a = 1; a < K; ++a) md = fminf(md, (CT)dhf[a]);
     const CT dsda = 0.99f / ((1.0f - 0.99f * alpha) * 2.0f * md);
-    Gs.opacity[i] += (float)(dsig * dsda * alpha * (1.0f - alpha));
+    gop += (float)(dsig * dsda * alpha * (1.0f - alpha));
   }
   // (SH coefficients and the view-direction term of the centre: k_sh_bwd)
+#pragma unroll
+  for (int a = 0; a < 3; ++a) gpos[a] += (float)gc[a];
+  return true;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(128, 4) k_preprocess_bwd(lp_prims P, float kappa, ViewPack V, lp_grads Gs) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  float gpos[3] = {0.f, 0.f, 0.f}, grot[4] = {0.f, 0.f, 0.f, 0.f}, gdist[4] = {0.f, 0.f, 0.f, 0.f};
+  float gop = 0.f, m2d = 0.f;
+  bool any = false;
+  for (int v = 0; v < V.nv; ++v) {
+    if (V.tt[v][i] == 0) continue;
+    any |= view_feature_grad<KIND>(P, V.cam[v], kappa, i, V.rgrad[v], gpos, grot, gdist, gop, m2d);
+  }
+  if (!any) return;
+  constexpr int K = Kind<KIND>::K;
+  const int n = P.n;
   if (Gs.pos) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += (float)gc[a];
+    for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += gpos[a];
   }
+  if (Gs.rot) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) Gs.rot[(size_t)a * n + i] += grot[a];
+  }
+  if (Gs.dist) {
+#pragma unroll
+    for (int a = 0; a < K; ++a) Gs.dist[(size_t)a * n + i] += gdist[a];
+  }
+  if (Gs.opacity) Gs.opacity[i] += gop;
+  if (Gs.mean2d_abs) Gs.mean2d_abs[i] += m2d;
 }
 
 // =============================================================================================
-// K5b: SH colour backward ("impact of the position on ... view-dependent color").
-// A separate streaming kernel: ~40 registers, so enough warps are in flight to hide the
-// 2 x (deg+1)^2 x 3 scattered loads and (deg+1)^2 x 3 stores per primitive.
+// K5b: SH colour backward ("impact of the position on ... view-dependent color"),
+// fused over the views of one call: the (deg+1)^2 x 3 coefficients are read once and their
+// gradients read-modified-written once per call instead of once per view.
 // =============================================================================================
 template <int DEG>
-__global__ void __launch_bounds__(256, 2) k_sh_bwd(lp_prims P, lp_camera cam, lp_frame F, lp_grads Gs) {
+__global__ void __launch_bounds__(256, 2) k_sh_bwd(lp_prims P, ViewPack V, int rg_words, lp_grads Gs) {
   constexpr int NC = (DEG + 1) * (DEG + 1);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = P.n;
-  if (i >= n || F.tiles_touched[i] == 0) return;
-  const int RG = F.rgrad_words;
-  float gr[3];
-#pragma unroll
-  for (int ch = 0; ch < 3; ++ch) gr[ch] = F.rgrad[(size_t)(RG - 3 + ch) * n + i];
-  if (gr[0] == 0.f && gr[1] == 0.f && gr[2] == 0.f) return;
+  if (i >= n) return;
+  // which views have a colour gradient for this primitive (bit v)
+  unsigned act = 0;
+  for (int v = 0; v < V.nv; ++v) {
+    if (V.tt[v][i] == 0) continue;
+    const float *rg = V.rgrad[v] + (size_t)(rg_words - 3) * n + i;
+    if (rg[0] != 0.f || rg[n] != 0.f || rg[2 * n] != 0.f) act |= 1u << v;
+  }
+  if (!act) return;
   const float *__restrict__ sh = P.sh;
   float *__restrict__ gsh = Gs.sh;
   const float c[3] = {P.pos[i], P.pos[n + i], P.pos[2 * n + i]};
-  float raw[3];
-  sh_colour_fp32(P, i, cam, c, raw);   // the forward's exact fp32 colour decides the clamp
-  const float cpx = -(cam.W[0] * cam.t[0] + cam.W[3] * cam.t[1] + cam.W[6] * cam.t[2]);
-  const float cpy = -(cam.W[1] * cam.t[0] + cam.W[4] * cam.t[1] + cam.W[7] * cam.t[2]);
-  const float cpz = -(cam.W[2] * cam.t[0] + cam.W[5] * cam.t[1] + cam.W[8] * cam.t[2]);
-  const float v[3] = {c[0] - cpx, c[1] - cpy, c[2] - cpz};
-  const float nv = sqrtf(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
-  const float dir[3] = {v[0] / nv, v[1] / nv, v[2] / nv};
-  float Y[16], wsum[16];
-  sh_basis<float>(DEG, dir[0], dir[1], dir[2], Y);
+  float gpos[3] = {0.f, 0.f, 0.f};
+  float acc[3][NC];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) wsum[k] = 0.f;
+  for (int ch = 0; ch < 3; ++ch)
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    if (raw[ch] < 0.f) continue;
-    float s[NC], g[NC];
+    for (int k = 0; k < NC; ++k) acc[ch][k] = 0.f;
+  unsigned touched = 0;   // bit ch: some view's unclamped colour gradient on channel ch
+  for (unsigned m = act; m; m &= m - 1) {
+    const int v = __ffs(m) - 1;
+    const lp_camera &cam = V.cam[v];
+    float gr[3];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) s[k] = sh[((size_t)k * 3 + ch) * n + i];
-    if (gsh) {
+    for (int ch = 0; ch < 3; ++ch) gr[ch] = V.rgrad[v][(size_t)(rg_words - 3 + ch) * n + i];
+    float raw[3];
+    sh_colour_fp32(P, i, cam, c, raw);   // the forward's exact fp32 colour decides the clamp
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+      if (raw[ch] < 0.f) gr[ch] = 0.f;
+    const float cpx = -(cam.W[0] * cam.t[0] + cam.W[3] * cam.t[1] + cam.W[6] * cam.t[2]);
+    const float cpy = -(cam.W[1] * cam.t[0] + cam.W[4] * cam.t[1] + cam.W[7] * cam.t[2]);
+    const float cpz = -(cam.W[2] * cam.t[0] + cam.W[5] * cam.t[1] + cam.W[8] * cam.t[2]);
+    const float d[3] = {c[0] - cpx, c[1] - cpy, c[2] - cpz};
+    const float nv = sqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    const float dir[3] = {d[0] / nv, d[1] / nv, d[2] / nv};
+    float Y[16];
+    sh_basis<float>(DEG, dir[0], dir[1], dir[2], Y);
+    float wk[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) wk[k] = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      if (gr[ch] == 0.f) continue;
+      touched |= 1u << ch;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        acc[ch][k] = fmaf(Y[k], gr[ch], acc[ch][k]);
+        wk[k] = fmaf(gr[ch], sh[((size_t)k * 3 + ch) * n + i], wk[k]);
+      }
+    }
+    if (DEG > 0 && Gs.pos) {
+      // direction term: d/d dir of sum_k sh_k Y_k, through dir = (c - campos)/|c - campos|
+      float gdir[3];
+      sh_basis_grad_dot<float>(DEG, dir[0], dir[1], dir[2], wk, gdir);
+      const float dd = dir[0] * gdir[0] + dir[1] * gdir[1] + dir[2] * gdir[2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) gpos[a] += (gdir[a] - dir[a] * dd) / nv;
+    }
+  }
+  if (gsh) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      if (!((touched >> ch) & 1u)) continue;
+      float g[NC];
 #pragma unroll
       for (int k = 0; k < NC; ++k) g[k] = gsh[((size_t)k * 3 + ch) * n + i];
 #pragma unroll
-      for (int k = 0; k < NC; ++k) gsh[((size_t)k * 3 + ch) * n + i] = fmaf(Y[k], gr[ch], g[k]);
+      for (int k = 0; k < NC; ++k) gsh[((size_t)k * 3 + ch) * n + i] = g[k] + acc[ch][k];
     }
-#pragma unroll
-    for (int k = 0; k < NC; ++k) wsum[k] = fmaf(gr[ch], s[k], wsum[k]);
   }
-  if (DEG == 0 || !Gs.pos) return;
-  float gdir[3];
-  sh_basis_grad_dot<float>(DEG, dir[0], dir[1], dir[2], wsum, gdir);
-  const float dd = dir[0] * gdir[0] + dir[1] * gdir[1] + dir[2] * gdir[2];
+  if (DEG > 0 && Gs.pos) {
 #pragma unroll
-  for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += (gdir[a] - dir[a] * dd) / nv;
+    for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += gpos[a];
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -446,19 +518,30 @@ void launch_preprocess(const lp_prims &P, const lp_camera &cam, float kappa, con
   else k_preprocess<LP_TETRAHEDRON><<<grid, 256, 0, st>>>(P, cam, kappa, F);
 }
 
-void launch_preprocess_bwd(const lp_prims &P, const lp_camera &cam, float kappa, const lp_frame &F,
+void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
                            const lp_grads &G, cudaStream_t st) {
-  if (P.n == 0) return;
-  const int grid = (P.n + 127) / 128;
-  if (P.kind == LP_OCTAHEDRON) k_preprocess_bwd<LP_OCTAHEDRON><<<grid, 128, 0, st>>>(P, cam, kappa, F, G);
-  else k_preprocess_bwd<LP_TETRAHEDRON><<<grid, 128, 0, st>>>(P, cam, kappa, F, G);
-  if (!G.sh && !G.pos) return;
-  const int g2 = (P.n + 255) / 256;
-  switch (P.sh_degree) {
-    case 0: k_sh_bwd<0><<<g2, 256, 0, st>>>(P, cam, F, G); break;
-    case 1: k_sh_bwd<1><<<g2, 256, 0, st>>>(P, cam, F, G); break;
-    case 2: k_sh_bwd<2><<<g2, 256, 0, st>>>(P, cam, F, G); break;
-    default: k_sh_bwd<3><<<g2, 256, 0, st>>>(P, cam, F, G); break;
+  if (P.n == 0 || n_views <= 0) return;
+  for (int v0 = 0; v0 < n_views; v0 += LP_MAXV) {
+    ViewPack V;
+    V.nv = n_views - v0 < LP_MAXV ? n_views - v0 : LP_MAXV;
+    for (int v = 0; v < LP_MAXV; ++v) {
+      const int s = v0 + (v < V.nv ? v : 0);
+      V.cam[v] = cams[s];
+      V.rgrad[v] = frames[s].rgrad;
+      V.tt[v] = frames[s].tiles_touched;
+    }
+    const int grid = (P.n + 127) / 128;
+    if (P.kind == LP_OCTAHEDRON) k_preprocess_bwd<LP_OCTAHEDRON><<<grid, 128, 0, st>>>(P, kappa, V, G);
+    else k_preprocess_bwd<LP_TETRAHEDRON><<<grid, 128, 0, st>>>(P, kappa, V, G);
+    if (!G.sh && !G.pos) continue;
+    const int g2 = (P.n + 255) / 256;
+    const int rg = frames[v0].rgrad_words;
+    switch (P.sh_degree) {
+      case 0: k_sh_bwd<0><<<g2, 256, 0, st>>>(P, V, rg, G); break;
+      case 1: k_sh_bwd<1><<<g2, 256, 0, st>>>(P, V, rg, G); break;
+      case 2: k_sh_bwd<2><<<g2, 256, 0, st>>>(P, V, rg, G); break;
+      default: k_sh_bwd<3><<<g2, 256, 0, st>>>(P, V, rg, G); break;
+    }
   }
 }
 

@@ -110,11 +110,18 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
       // bbox reject (convexity: outside the vertex bbox the chord is <= 0): warp-uniform
       const float4 bb = s_rec[j * RW4];
       if (!rect_hits_bbox(bb, wx0, wx1, wy0, wy1)) continue;
+      bool test[PPT], any = false;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        test[k] = !done[k] && in_bbox(bb, fx[k], fy[k]);
+        any = any || test[k];
+      }
+      if (!__any_sync(0xffffffffu, any)) continue;
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        if (done[k]) continue;
-        if (cfg.count_stats) nbox += in_bbox(bb, fx[k], fy[k]) ? 1u : 0u;
+        if (!test[k]) continue;
+        ++nbox;
         int se, sx;
         const float ch = chord<KIND, false>(rec, fs(fx[k], rec[KD::CX]), fs(fy[k], rec[KD::CX + 1]), se, sx);
         if (ch > 0.f) {
@@ -285,6 +292,13 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
       // pairs is the forward's regardless of either kernel's warp footprint
       const float4 bb = s_rec[j * RW4];
       if (!rect_hits_bbox(bb, wx0, wx1, wy0, wy1)) continue;
+      bool test[PPT], any = false;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        test[k] = ej < last[k] && in_bbox(bb, fx[k], fy[k]);
+        any = any || test[k];
+      }
+      if (!__any_sync(0xffffffffu, any)) continue;
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
       float acc[RG];
 #pragma unroll
@@ -292,7 +306,7 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
       bool hit = false;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        if (ej >= last[k]) continue;
+        if (!test[k]) continue;
         int se, sx;
         const float dx = fs(fx[k], rec[KD::CX]), dy = fs(fy[k], rec[KD::CX + 1]);
         const float ch = chord<KIND, true>(rec, dx, dy, se, sx);
@@ -367,7 +381,7 @@ void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image
 }
 
 void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL, cudaStream_t st) {
-  static const int nt = nt_from_env("LP_BWD_NT", 64);
+  static const int nt = nt_from_env("LP_BWD_NT", 128);
   const int tiles = F.tiles_x * F.tiles_y;
   if (nt == 64) {
     if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, 64><<<tiles, 64, 0, st>>>(F, cfg, dL);

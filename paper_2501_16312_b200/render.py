@@ -179,9 +179,10 @@ class Renderer:
         views = list(range(len(self.frames))) if views is None else list(views)
         st = self.stream()
         dL_dimage = dL_dimage.contiguous()
-        for i, v in enumerate(views):
-            fa = frames_array([self.frames[v]])
-            L.lp_render_bwd(self.scene.prims, self._cams([v]), self.cfg, fa, dL_dimage[i], self.scene.grads, st)
+        # one call for all views: the raster backward runs per view, the preprocess backward is
+        # fused over the views (feature / SH gradients read-modified-written once)
+        fa = frames_array([self.frames[v] for v in views])
+        L.lp_render_bwd(self.scene.prims, self._cams(views), self.cfg, fa, dL_dimage, self.scene.grads, st)
 
     def counters(self, v=0):
         return L.lp_frame_counters(self.frames[v].c, self.stream())
