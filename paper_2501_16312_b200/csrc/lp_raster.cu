@@ -49,9 +49,29 @@ __device__ __forceinline__ void warp_rect(int w, int tx, int ty, float &x0, floa
   y1 = y0 + (float)(wy - 1);
 }
 
-// does the primitive's screen bbox reach any pixel centre of the warp? (warp-uniform)
+// does the primitive's screen bbox reach the warp's pixel-centre rectangle?
 __device__ __forceinline__ bool rect_hits_bbox(const float4 &bb, float x0, float x1, float y0, float y1) {
   return bb.x - bb.z <= x1 && bb.x + bb.z >= x0 && bb.y - bb.w <= y1 && bb.y + bb.w >= y0;
+}
+
+// Build the warp's ordered sub-list of batch records [0, cnt) whose bbox reaches its rectangle.
+// Lane l tests records l, l+32, ...; returns the list length (warp-uniform).
+template <int NT, int RW4>
+__device__ __forceinline__ int warp_sublist(const float4 *s_rec, int cnt, float x0, float x1, float y0, float y1,
+                                            unsigned char *list) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int n = 0;
+#pragma unroll
+  for (int r = 0; r < NT; r += 32) {
+    const int j = r + lane;
+    const bool ov = j < cnt && rect_hits_bbox(s_rec[j * RW4], x0, x1, y0, y1);
+    const unsigned m = __ballot_sync(0xffffffffu, ov);
+    if (ov) list[n + __popc(m & lt)] = (unsigned char)j;
+    n += __popc(m);
+  }
+  __syncwarp();
+  return n;
 }
 
 // =============================================================================================
@@ -62,6 +82,7 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
   using KD = Kind<KIND>;
   constexpr int RW = KD::RW, RW4 = RW / 4, PPT = 256 / NT;
   __shared__ float4 s_rec[NT * RW4];
+  __shared__ unsigned char s_list[NT / 32][NT];
   __shared__ unsigned long long s_stat[3];
 
   const int tile = blockIdx.x;
@@ -106,10 +127,12 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
     __syncthreads();
     if (__all_sync(0xffffffffu, mine)) continue;
     const int cnt = (int)min((uint32_t)NT, end - b);
-    for (int j = 0; j < cnt; ++j) {
-      // bbox reject (convexity: outside the vertex bbox the chord is <= 0): warp-uniform
+    // per-warp sub-list: the batch records whose bbox reaches the warp's pixels, in list order
+    // (each lane tests NT/32 records; convexity: outside the vertex bbox the chord is <= 0)
+    const int nl = warp_sublist<NT, RW4>(s_rec, cnt, wx0, wx1, wy0, wy1, s_list[threadIdx.x >> 5]);
+    for (int q = 0; q < nl; ++q) {
+      const int j = s_list[threadIdx.x >> 5][q];
       const float4 bb = s_rec[j * RW4];
-      if (!rect_hits_bbox(bb, wx0, wx1, wy0, wy1)) continue;
       bool test[PPT], any = false;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
@@ -229,7 +252,11 @@ template <int KIND, int NT>
 __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg, const float *__restrict__ dL) {
   using KD = Kind<KIND>;
   constexpr int RW = KD::RW, RW4 = RW / 4, PPT = 256 / NT, RG = KD::RG;
+  constexpr int RGP = RG == 20 ? 20 : 28;      // padded row: 16-byte stores, conflict-free (RGP/4 odd)
+  constexpr int SMEM_RED_MAX = 16;             // <= 16 hit lanes: shared-memory column sums beat the shuffles
   __shared__ float4 s_rec[NT * RW4];
+  __shared__ unsigned char s_list[NT / 32][NT];
+  __shared__ __align__(16) float s_red[NT / 32][32][RGP];
   __shared__ uint32_t s_id[NT];
   __shared__ uint32_t s_last;
 
@@ -285,13 +312,14 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
 #pragma unroll
     for (int k = 0; k < PPT; ++k) act = act || (last[k] > bstart);
     if (!__any_sync(0xffffffffu, act)) continue;
+    const int w = threadIdx.x >> 5;
+    const int nl = warp_sublist<NT, RW4>(s_rec, (int)(bend - bstart), wx0, wx1, wy0, wy1, s_list[w]);
 
-    for (int j = (int)(bend - bstart) - 1; j >= 0; --j) {
+    for (int q = nl - 1; q >= 0; --q) {
+      const int j = s_list[w][q];
       const uint32_t ej = bstart + (uint32_t)j;
-      // warp-uniform bbox reject: pixels outside the bbox have chord <= 0, so the set of hit
-      // pairs is the forward's regardless of either kernel's warp footprint
+      // bbox reject per pixel: pixels outside the bbox have chord <= 0 (the forward's hit set)
       const float4 bb = s_rec[j * RW4];
-      if (!rect_hits_bbox(bb, wx0, wx1, wy0, wy1)) continue;
       bool test[PPT], any = false;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
@@ -300,9 +328,9 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
       }
       if (!__any_sync(0xffffffffu, any)) continue;
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
-      float acc[RG];
+      float acc[RGP];
 #pragma unroll
-      for (int a = 0; a < RG; ++a) acc[a] = 0.f;
+      for (int a = 0; a < RGP; ++a) acc[a] = 0.f;
       bool hit = false;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
@@ -348,11 +376,32 @@ __global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg
           }
         }
       }
-      if (__any_sync(0xffffffffu, hit)) {
+      // per-(warp, primitive) reduction of the <= 22 moments, one RED.F32 per moment
+      const unsigned hm = __ballot_sync(0xffffffffu, hit);
+      if (!hm) continue;
+      const uint32_t id = s_id[j];
+      if (__popc(hm) <= SMEM_RED_MAX) {
+        // few hit lanes: stage their moments in shared memory, lane m sums column m
+        float4 *row = reinterpret_cast<float4 *>(&s_red[w][lane][0]);
+        if (hit) {
+#pragma unroll
+          for (int a = 0; a < RGP / 4; ++a) row[a] = make_float4(acc[4 * a], acc[4 * a + 1], acc[4 * a + 2], acc[4 * a + 3]);
+        }
+        __syncwarp();
+        if (lane < RG) {
+          float sum = 0.f;
+          for (unsigned m = hm; m; m &= m - 1) sum += s_red[w][__ffs(m) - 1][lane];
+          if (sum != 0.f) atomicAdd(F.rgrad + (size_t)lane * F.n + id, sum);
+        }
+        __syncwarp();
+      } else {
         int idx;
         bool valid;
-        const float val = warp_transpose_reduce<RG>(acc, lane, idx, valid);
-        if (valid && val != 0.f) atomicAdd(F.rgrad + (size_t)idx * F.n + s_id[j], val);
+        float acc_r[RG];
+#pragma unroll
+        for (int a = 0; a < RG; ++a) acc_r[a] = acc[a];
+        const float val = warp_transpose_reduce<RG>(acc_r, lane, idx, valid);
+        if (valid && val != 0.f) atomicAdd(F.rgrad + (size_t)idx * F.n + id, val);
       }
     }
   }
