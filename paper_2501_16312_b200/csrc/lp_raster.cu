@@ -414,31 +414,35 @@ static int nt_from_env(const char *name, int dflt) {
   const char *s = getenv(name);
   if (!s) return dflt;
   const int v = atoi(s);
-  return (v == 64 || v == 128) ? v : dflt;
+  return (v == 64 || v == 128 || v == 256) ? v : dflt;
+}
+
+template <int NT>
+static void fwd_nt(const lp_frame &F, const lp_raster_cfg &cfg, float *image, cudaStream_t st) {
+  const int tiles = F.tiles_x * F.tiles_y;
+  if (F.kind == LP_OCTAHEDRON) k_raster_fwd<LP_OCTAHEDRON, NT><<<tiles, NT, 0, st>>>(F, cfg, image);
+  else k_raster_fwd<LP_TETRAHEDRON, NT><<<tiles, NT, 0, st>>>(F, cfg, image);
+}
+
+template <int NT>
+static void bwd_nt(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL, cudaStream_t st) {
+  const int tiles = F.tiles_x * F.tiles_y;
+  if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, NT><<<tiles, NT, 0, st>>>(F, cfg, dL);
+  else k_raster_bwd<LP_TETRAHEDRON, (NT > 128 ? 128 : NT)><<<tiles, (NT > 128 ? 128 : NT), 0, st>>>(F, cfg, dL);
 }
 
 void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image, cudaStream_t st) {
   static const int nt = nt_from_env("LP_FWD_NT", 128);
-  const int tiles = F.tiles_x * F.tiles_y;
-  if (nt == 64) {
-    if (F.kind == LP_OCTAHEDRON) k_raster_fwd<LP_OCTAHEDRON, 64><<<tiles, 64, 0, st>>>(F, cfg, image);
-    else k_raster_fwd<LP_TETRAHEDRON, 64><<<tiles, 64, 0, st>>>(F, cfg, image);
-  } else {
-    if (F.kind == LP_OCTAHEDRON) k_raster_fwd<LP_OCTAHEDRON, 128><<<tiles, 128, 0, st>>>(F, cfg, image);
-    else k_raster_fwd<LP_TETRAHEDRON, 128><<<tiles, 128, 0, st>>>(F, cfg, image);
-  }
+  if (nt == 64) fwd_nt<64>(F, cfg, image, st);
+  else if (nt == 256) fwd_nt<256>(F, cfg, image, st);
+  else fwd_nt<128>(F, cfg, image, st);
 }
 
 void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL, cudaStream_t st) {
   static const int nt = nt_from_env("LP_BWD_NT", 128);
-  const int tiles = F.tiles_x * F.tiles_y;
-  if (nt == 64) {
-    if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, 64><<<tiles, 64, 0, st>>>(F, cfg, dL);
-    else k_raster_bwd<LP_TETRAHEDRON, 64><<<tiles, 64, 0, st>>>(F, cfg, dL);
-  } else {
-    if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, 128><<<tiles, 128, 0, st>>>(F, cfg, dL);
-    else k_raster_bwd<LP_TETRAHEDRON, 128><<<tiles, 128, 0, st>>>(F, cfg, dL);
-  }
+  if (nt == 64) bwd_nt<64>(F, cfg, dL, st);
+  else if (nt == 256) bwd_nt<256>(F, cfg, dL, st);
+  else bwd_nt<128>(F, cfg, dL, st);
 }
 
 }  // namespace lp
