@@ -193,14 +193,15 @@ __device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_ca
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const double rx = S.r[s][0], ry = S.r[s][1], rz = S.r[s][2];
-      const double b = -rx / rz, gg = -ry / rz;
+      const double irz = 1.0 / rz;                       // one fp64 division per slab
+      const double b = -rx * irz, gg = -ry * irz;
       const double db = m[4 * s + 0], dg = m[4 * s + 1], mc = m[4 * s + 2], dhh = m[4 * s + 3];
       // L_s = b dx + g dy with dx = px - c.x: d/dc.x = -b (summed weights M_c)
       gcr[0] -= b * mc;
       gcr[1] -= gg * mc;
-      const double rz2 = rz * rz;
-      const double drx = -db / rz, dry = -dg / rz;
-      const double drz = db * rx / rz2 + dg * ry / rz2 - dhh * (rz > 0 ? 1.0 : -1.0) / rz2;
+      // b = -rx/rz, g = -ry/rz, h = 1/|rz|
+      const double drx = -db * irz, dry = -dg * irz;
+      const double drz = ((db * rx + dg * ry) - dhh * (rz > 0 ? 1.0 : -1.0)) * irz * irz;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const double sa = slab_sign(s, a);
@@ -393,120 +394,148 @@ __device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_ca
   return true;
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(128, 4) k_preprocess_bwd(lp_prims P, float kappa, ViewPack V, lp_grads Gs) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P.n) return;
-  float gpos[3] = {0.f, 0.f, 0.f}, grot[4] = {0.f, 0.f, 0.f, 0.f}, gdist[4] = {0.f, 0.f, 0.f, 0.f};
-  float gop = 0.f, m2d = 0.f;
-  bool any = false;
-  for (int v = 0; v < V.nv; ++v) {
-    if (V.tt[v][i] == 0) continue;
-    any |= view_feature_grad<KIND>(P, V.cam[v], kappa, i, V.rgrad[v], gpos, grot, gdist, gop, m2d);
-  }
-  if (!any) return;
-  constexpr int K = Kind<KIND>::K;
+// SH part of one (primitive, view) item: colour gradient -> SH coefficients (accumulated into the
+// primitive's shared-memory row, layout [k*3 + ch] like the global SoA) and the view-direction
+// term of the centre ("impact of the position on ... view-dependent color").
+template <int DEG>
+__device__ __forceinline__ void sh_view_grad(const lp_prims &P, const lp_camera &cam, int i,
+                                             const float *__restrict__ rgrad, int rg_words, float *sh_row,
+                                             float gpos[3]) {
+  constexpr int NC = (DEG + 1) * (DEG + 1);
   const int n = P.n;
+  const float c[3] = {P.pos[i], P.pos[n + i], P.pos[2 * n + i]};
+  float gr[3], raw[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) gr[ch] = rgrad[(size_t)(rg_words - 3 + ch) * n + i];
+  sh_colour_fp32(P, i, cam, c, raw);   // the forward's exact fp32 colour decides the clamp
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch)
+    if (raw[ch] < 0.f) gr[ch] = 0.f;
+  if (gr[0] == 0.f && gr[1] == 0.f && gr[2] == 0.f) return;
+  const float cpx = -(cam.W[0] * cam.t[0] + cam.W[3] * cam.t[1] + cam.W[6] * cam.t[2]);
+  const float cpy = -(cam.W[1] * cam.t[0] + cam.W[4] * cam.t[1] + cam.W[7] * cam.t[2]);
+  const float cpz = -(cam.W[2] * cam.t[0] + cam.W[5] * cam.t[1] + cam.W[8] * cam.t[2]);
+  const float d[3] = {c[0] - cpx, c[1] - cpy, c[2] - cpz};
+  const float nv = sqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+  const float dir[3] = {d[0] / nv, d[1] / nv, d[2] / nv};
+  float Y[16], wk[16];
+  sh_basis<float>(DEG, dir[0], dir[1], dir[2], Y);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) wk[k] = 0.f;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    if (gr[ch] == 0.f) continue;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      atomicAdd(sh_row + k * 3 + ch, Y[k] * gr[ch]);
+      wk[k] = fmaf(gr[ch], P.sh[((size_t)k * 3 + ch) * n + i], wk[k]);
+    }
+  }
+  if (DEG > 0) {
+    float gdir[3];
+    sh_basis_grad_dot<float>(DEG, dir[0], dir[1], dir[2], wk, gdir);
+    const float dd = dir[0] * gdir[0] + dir[1] * gdir[1] + dir[2] * gdir[2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) gpos[a] += (gdir[a] - dir[a] * dd) / nv;
+  }
+}
+
+template <int KIND, int DEG>
+struct AccRow {   // per-primitive accumulator row in shared memory
+  static constexpr int K = Kind<KIND>::K, NC = (DEG + 1) * (DEG + 1);
+  static constexpr int POS = 0, ROT = 3, DIST = 7, OP = 7 + K, M2D = 8 + K, SH = 9 + K;
+  static constexpr int N = SH + 3 * NC;
+  static constexpr int STRIDE = N | 1;   // odd stride: lanes on different rows hit different banks
+};
+
+// K5, one launch for up to LP_MAXV views.  A warp owns 32 consecutive primitives; their active
+// (primitive, view) items -- raster gradient present -- are compacted into a warp-local list and
+// processed 32 at a time (dense SIMT lanes instead of a per-thread view loop at ~8/32 active
+// lanes), accumulating into shared-memory rows that are written back once per primitive.
+template <int KIND, int DEG>
+__global__ void __launch_bounds__(128, 4) k_preprocess_bwd(lp_prims P, float kappa, ViewPack V, int rg_words,
+                                                           lp_grads Gs) {
+  using AR = AccRow<KIND, DEG>;
+  constexpr int WARPS = 4;
+  __shared__ lp_camera s_cam[LP_MAXV];
+  __shared__ const float *s_rg[LP_MAXV];
+  __shared__ float s_acc[WARPS][32 * AR::STRIDE];
+  __shared__ unsigned char s_items[WARPS][32 * LP_MAXV];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < V.nv) {
+    s_cam[threadIdx.x] = V.cam[threadIdx.x];
+    s_rg[threadIdx.x] = V.rgrad[threadIdx.x];
+  }
+  float *acc = s_acc[w];
+  for (int a = lane; a < 32 * AR::STRIDE; a += 32) acc[a] = 0.f;
+  __syncthreads();
+  const int n = P.n;
+  const int base = (blockIdx.x * WARPS + w) * 32;
+  const int i = base + lane;
+  unsigned vm = 0;   // views with a raster gradient for this lane's primitive
+  if (i < n) {
+    for (int v = 0; v < V.nv; ++v) {
+      if (V.tt[v][i] == 0) continue;
+      const float *rg = V.rgrad[v] + (size_t)(rg_words - 4) * n + i;   // dsigma, drgb
+      if (rg[0] != 0.f || rg[n] != 0.f || rg[2 * n] != 0.f || rg[3 * n] != 0.f) vm |= 1u << v;
+    }
+  }
+  const int c = __popc(vm);
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0) return;
+  int slot = incl - c;
+  for (unsigned m = vm; m; m &= m - 1) s_items[w][slot++] = (unsigned char)((lane << 3) | (__ffs(m) - 1));
+  __syncwarp();
+  for (int r = 0; r < total; r += 32) {
+    const int it = r + lane;
+    if (it < total) {
+      const int item = s_items[w][it];
+      const int pl = item >> 3, v = item & 7;
+      const int ii = base + pl;
+      float *row = acc + pl * AR::STRIDE;
+      float gpos[3] = {0.f, 0.f, 0.f}, grot[4] = {0.f, 0.f, 0.f, 0.f}, gdist[4] = {0.f, 0.f, 0.f, 0.f};
+      float gop = 0.f, m2d = 0.f;
+      view_feature_grad<KIND>(P, s_cam[v], kappa, ii, s_rg[v], gpos, grot, gdist, gop, m2d);
+      if (Gs.sh || Gs.pos) sh_view_grad<DEG>(P, s_cam[v], ii, s_rg[v], rg_words, row + AR::SH, gpos);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) atomicAdd(row + AR::POS + a, gpos[a]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a) atomicAdd(row + AR::ROT + a, grot[a]);
+#pragma unroll
+      for (int a = 0; a < AR::K; ++a) atomicAdd(row + AR::DIST + a, gdist[a]);
+      atomicAdd(row + AR::OP, gop);
+      atomicAdd(row + AR::M2D, m2d);
+    }
+  }
+  __syncwarp();
+  if (!vm) return;
+  const float *row = acc + lane * AR::STRIDE;
   if (Gs.pos) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += gpos[a];
+    for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += row[AR::POS + a];
   }
   if (Gs.rot) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a) Gs.rot[(size_t)a * n + i] += grot[a];
+    for (int a = 0; a < 4; ++a) Gs.rot[(size_t)a * n + i] += row[AR::ROT + a];
   }
   if (Gs.dist) {
 #pragma unroll
-    for (int a = 0; a < K; ++a) Gs.dist[(size_t)a * n + i] += gdist[a];
+    for (int a = 0; a < AR::K; ++a) Gs.dist[(size_t)a * n + i] += row[AR::DIST + a];
   }
-  if (Gs.opacity) Gs.opacity[i] += gop;
-  if (Gs.mean2d_abs) Gs.mean2d_abs[i] += m2d;
-}
-
-// =============================================================================================
-// K5b: SH colour backward ("impact of the position on ... view-dependent color"),
-// fused over the views of one call: the (deg+1)^2 x 3 coefficients are read once and their
-// gradients read-modified-written once per call instead of once per view.
-// =============================================================================================
-template <int DEG>
-__global__ void __launch_bounds__(256, 2) k_sh_bwd(lp_prims P, ViewPack V, int rg_words, lp_grads Gs) {
-  constexpr int NC = (DEG + 1) * (DEG + 1);
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int n = P.n;
-  if (i >= n) return;
-  // which views have a colour gradient for this primitive (bit v)
-  unsigned act = 0;
-  for (int v = 0; v < V.nv; ++v) {
-    if (V.tt[v][i] == 0) continue;
-    const float *rg = V.rgrad[v] + (size_t)(rg_words - 3) * n + i;
-    if (rg[0] != 0.f || rg[n] != 0.f || rg[2 * n] != 0.f) act |= 1u << v;
-  }
-  if (!act) return;
-  const float *__restrict__ sh = P.sh;
-  float *__restrict__ gsh = Gs.sh;
-  const float c[3] = {P.pos[i], P.pos[n + i], P.pos[2 * n + i]};
-  float gpos[3] = {0.f, 0.f, 0.f};
-  float acc[3][NC];
+  if (Gs.opacity) Gs.opacity[i] += row[AR::OP];
+  if (Gs.mean2d_abs) Gs.mean2d_abs[i] += row[AR::M2D];
+  if (Gs.sh) {
+    float g[3 * AR::NC];
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch)
+    for (int q = 0; q < 3 * AR::NC; ++q) g[q] = Gs.sh[(size_t)q * n + i];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) acc[ch][k] = 0.f;
-  unsigned touched = 0;   // bit ch: some view's unclamped colour gradient on channel ch
-  for (unsigned m = act; m; m &= m - 1) {
-    const int v = __ffs(m) - 1;
-    const lp_camera &cam = V.cam[v];
-    float gr[3];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) gr[ch] = V.rgrad[v][(size_t)(rg_words - 3 + ch) * n + i];
-    float raw[3];
-    sh_colour_fp32(P, i, cam, c, raw);   // the forward's exact fp32 colour decides the clamp
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch)
-      if (raw[ch] < 0.f) gr[ch] = 0.f;
-    const float cpx = -(cam.W[0] * cam.t[0] + cam.W[3] * cam.t[1] + cam.W[6] * cam.t[2]);
-    const float cpy = -(cam.W[1] * cam.t[0] + cam.W[4] * cam.t[1] + cam.W[7] * cam.t[2]);
-    const float cpz = -(cam.W[2] * cam.t[0] + cam.W[5] * cam.t[1] + cam.W[8] * cam.t[2]);
-    const float d[3] = {c[0] - cpx, c[1] - cpy, c[2] - cpz};
-    const float nv = sqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-    const float dir[3] = {d[0] / nv, d[1] / nv, d[2] / nv};
-    float Y[16];
-    sh_basis<float>(DEG, dir[0], dir[1], dir[2], Y);
-    float wk[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) wk[k] = 0.f;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      if (gr[ch] == 0.f) continue;
-      touched |= 1u << ch;
-#pragma unroll
-      for (int k = 0; k < NC; ++k) {
-        acc[ch][k] = fmaf(Y[k], gr[ch], acc[ch][k]);
-        wk[k] = fmaf(gr[ch], sh[((size_t)k * 3 + ch) * n + i], wk[k]);
-      }
-    }
-    if (DEG > 0 && Gs.pos) {
-      // direction term: d/d dir of sum_k sh_k Y_k, through dir = (c - campos)/|c - campos|
-      float gdir[3];
-      sh_basis_grad_dot<float>(DEG, dir[0], dir[1], dir[2], wk, gdir);
-      const float dd = dir[0] * gdir[0] + dir[1] * gdir[1] + dir[2] * gdir[2];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) gpos[a] += (gdir[a] - dir[a] * dd) / nv;
-    }
-  }
-  if (gsh) {
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      if (!((touched >> ch) & 1u)) continue;
-      float g[NC];
-#pragma unroll
-      for (int k = 0; k < NC; ++k) g[k] = gsh[((size_t)k * 3 + ch) * n + i];
-#pragma unroll
-      for (int k = 0; k < NC; ++k) gsh[((size_t)k * 3 + ch) * n + i] = g[k] + acc[ch][k];
-    }
-  }
-  if (DEG > 0 && Gs.pos) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += gpos[a];
+    for (int q = 0; q < 3 * AR::NC; ++q) Gs.sh[(size_t)q * n + i] = g[q] + row[AR::SH + q];
   }
 }
 
@@ -516,6 +545,17 @@ void launch_preprocess(const lp_prims &P, const lp_camera &cam, float kappa, con
   const int grid = (P.n + 255) / 256;
   if (P.kind == LP_OCTAHEDRON) k_preprocess<LP_OCTAHEDRON><<<grid, 256, 0, st>>>(P, cam, kappa, F);
   else k_preprocess<LP_TETRAHEDRON><<<grid, 256, 0, st>>>(P, cam, kappa, F);
+}
+
+template <int KIND>
+static void bwd_deg(const lp_prims &P, float kappa, const ViewPack &V, int rg, const lp_grads &G, cudaStream_t st) {
+  const int grid = (P.n + 127) / 128;
+  switch (P.sh_degree) {
+    case 0: k_preprocess_bwd<KIND, 0><<<grid, 128, 0, st>>>(P, kappa, V, rg, G); break;
+    case 1: k_preprocess_bwd<KIND, 1><<<grid, 128, 0, st>>>(P, kappa, V, rg, G); break;
+    case 2: k_preprocess_bwd<KIND, 2><<<grid, 128, 0, st>>>(P, kappa, V, rg, G); break;
+    default: k_preprocess_bwd<KIND, 3><<<grid, 128, 0, st>>>(P, kappa, V, rg, G); break;
+  }
 }
 
 void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
@@ -530,18 +570,8 @@ void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa
       V.rgrad[v] = frames[s].rgrad;
       V.tt[v] = frames[s].tiles_touched;
     }
-    const int grid = (P.n + 127) / 128;
-    if (P.kind == LP_OCTAHEDRON) k_preprocess_bwd<LP_OCTAHEDRON><<<grid, 128, 0, st>>>(P, kappa, V, G);
-    else k_preprocess_bwd<LP_TETRAHEDRON><<<grid, 128, 0, st>>>(P, kappa, V, G);
-    if (!G.sh && !G.pos) continue;
-    const int g2 = (P.n + 255) / 256;
-    const int rg = frames[v0].rgrad_words;
-    switch (P.sh_degree) {
-      case 0: k_sh_bwd<0><<<g2, 256, 0, st>>>(P, V, rg, G); break;
-      case 1: k_sh_bwd<1><<<g2, 256, 0, st>>>(P, V, rg, G); break;
-      case 2: k_sh_bwd<2><<<g2, 256, 0, st>>>(P, V, rg, G); break;
-      default: k_sh_bwd<3><<<g2, 256, 0, st>>>(P, V, rg, G); break;
-    }
+    if (P.kind == LP_OCTAHEDRON) bwd_deg<LP_OCTAHEDRON>(P, kappa, V, frames[v0].rgrad_words, G, st);
+    else bwd_deg<LP_TETRAHEDRON>(P, kappa, V, frames[v0].rgrad_words, G, st);
   }
 }
 
