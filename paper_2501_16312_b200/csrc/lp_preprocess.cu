@@ -394,80 +394,74 @@ __device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_ca
   return true;
 }
 
-// SH part of one (primitive, view) item: colour gradient -> SH coefficients (accumulated into the
-// primitive's shared-memory row, layout [k*3 + ch] like the global SoA) and the view-direction
-// term of the centre ("impact of the position on ... view-dependent color").
+// SH inputs of one (primitive, view) item: the clamp-masked colour gradient gr and the view
+// direction dir (the SH coefficient gradient Y(dir) gr is expanded later by the primitive's
+// owner lane), plus the view-direction term of the centre gradient.
 template <int DEG>
-__device__ __forceinline__ void sh_view_grad(const lp_prims &P, const lp_camera &cam, int i,
-                                             const float *__restrict__ rgrad, int rg_words, float *sh_row,
-                                             float gpos[3]) {
+__device__ __forceinline__ void sh_view_inputs(const lp_prims &P, const lp_camera &cam, int i,
+                                               const float *__restrict__ rgrad, int rg_words, float gr[3],
+                                               float dir[3], float gpos[3]) {
   constexpr int NC = (DEG + 1) * (DEG + 1);
   const int n = P.n;
   const float c[3] = {P.pos[i], P.pos[n + i], P.pos[2 * n + i]};
-  float gr[3], raw[3];
+  float raw[3];
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) gr[ch] = rgrad[(size_t)(rg_words - 3 + ch) * n + i];
   sh_colour_fp32(P, i, cam, c, raw);   // the forward's exact fp32 colour decides the clamp
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch)
     if (raw[ch] < 0.f) gr[ch] = 0.f;
-  if (gr[0] == 0.f && gr[1] == 0.f && gr[2] == 0.f) return;
   const float cpx = -(cam.W[0] * cam.t[0] + cam.W[3] * cam.t[1] + cam.W[6] * cam.t[2]);
   const float cpy = -(cam.W[1] * cam.t[0] + cam.W[4] * cam.t[1] + cam.W[7] * cam.t[2]);
   const float cpz = -(cam.W[2] * cam.t[0] + cam.W[5] * cam.t[1] + cam.W[8] * cam.t[2]);
   const float d[3] = {c[0] - cpx, c[1] - cpy, c[2] - cpz};
   const float nv = sqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-  const float dir[3] = {d[0] / nv, d[1] / nv, d[2] / nv};
-  float Y[16], wk[16];
-  sh_basis<float>(DEG, dir[0], dir[1], dir[2], Y);
+  dir[0] = d[0] / nv;
+  dir[1] = d[1] / nv;
+  dir[2] = d[2] / nv;
+  if (DEG == 0 || (gr[0] == 0.f && gr[1] == 0.f && gr[2] == 0.f)) return;
+  float wk[16];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) wk[k] = 0.f;
+  for (int k = 0; k < 16; ++k) {
+    wk[k] = 0.f;
+    if (k < NC) {
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    if (gr[ch] == 0.f) continue;
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      atomicAdd(sh_row + k * 3 + ch, Y[k] * gr[ch]);
-      wk[k] = fmaf(gr[ch], P.sh[((size_t)k * 3 + ch) * n + i], wk[k]);
+      for (int ch = 0; ch < 3; ++ch) wk[k] = fmaf(gr[ch], P.sh[((size_t)k * 3 + ch) * n + i], wk[k]);
     }
   }
-  if (DEG > 0) {
-    float gdir[3];
-    sh_basis_grad_dot<float>(DEG, dir[0], dir[1], dir[2], wk, gdir);
-    const float dd = dir[0] * gdir[0] + dir[1] * gdir[1] + dir[2] * gdir[2];
+  float gdir[3];
+  sh_basis_grad_dot<float>(DEG, dir[0], dir[1], dir[2], wk, gdir);
+  const float dd = dir[0] * gdir[0] + dir[1] * gdir[1] + dir[2] * gdir[2];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) gpos[a] += (gdir[a] - dir[a] * dd) / nv;
-  }
+  for (int a = 0; a < 3; ++a) gpos[a] += (gdir[a] - dir[a] * dd) / nv;
 }
 
-template <int KIND, int DEG>
-struct AccRow {   // per-primitive accumulator row in shared memory
-  static constexpr int K = Kind<KIND>::K, NC = (DEG + 1) * (DEG + 1);
-  static constexpr int POS = 0, ROT = 3, DIST = 7, OP = 7 + K, M2D = 8 + K, SH = 9 + K;
-  static constexpr int N = SH + 3 * NC;
-  static constexpr int STRIDE = N | 1;   // odd stride: lanes on different rows hit different banks
+// per-item result record in shared memory
+struct ItemRes {
+  static constexpr int POS = 0, ROT = 3, DIST = 7, OP = 11, M2D = 12, GR = 13, DIR = 16;
+  static constexpr int N = 19;
 };
 
-// K5, one launch for up to LP_MAXV views.  A warp owns 32 consecutive primitives; their active
-// (primitive, view) items -- raster gradient present -- are compacted into a warp-local list and
-// processed 32 at a time (dense SIMT lanes instead of a per-thread view loop at ~8/32 active
-// lanes), accumulating into shared-memory rows that are written back once per primitive.
+// K5, one launch for up to LP_MAXV views.  A warp owns 32 consecutive primitives.  Phase A: their
+// active (primitive, view) items -- raster gradient present -- are compacted into a warp-local list
+// and evaluated 32 at a time (dense SIMT lanes; the per-view geometry chain is the expensive part),
+// each writing a 19-float result to shared memory.  Phase B: lane l owns primitive l, sums its
+// items (contiguous in the list), expands the SH gradient sum_v Y(dir_v) gr_v in registers, and
+// read-modify-writes every feature gradient once.  No shared-memory float atomics (sm_100 has
+// none: they compile to CAS loops).
 template <int KIND, int DEG>
-__global__ void __launch_bounds__(128, 4) k_preprocess_bwd(lp_prims P, float kappa, ViewPack V, int rg_words,
-                                                           lp_grads Gs) {
-  using AR = AccRow<KIND, DEG>;
-  constexpr int WARPS = 4;
+__global__ void __launch_bounds__(64) k_preprocess_bwd(lp_prims P, float kappa, ViewPack V, int rg_words,
+                                                       lp_grads Gs) {
+  constexpr int WARPS = 2, K = Kind<KIND>::K, NC = (DEG + 1) * (DEG + 1);
   __shared__ lp_camera s_cam[LP_MAXV];
   __shared__ const float *s_rg[LP_MAXV];
-  __shared__ float s_acc[WARPS][32 * AR::STRIDE];
+  __shared__ float s_res[WARPS][32 * LP_MAXV][ItemRes::N];
   __shared__ unsigned char s_items[WARPS][32 * LP_MAXV];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < V.nv) {
     s_cam[threadIdx.x] = V.cam[threadIdx.x];
     s_rg[threadIdx.x] = V.rgrad[threadIdx.x];
   }
-  float *acc = s_acc[w];
-  for (int a = lane; a < 32 * AR::STRIDE; a += 32) acc[a] = 0.f;
   __syncthreads();
   const int n = P.n;
   const int base = (blockIdx.x * WARPS + w) * 32;
@@ -489,53 +483,85 @@ __global__ void __launch_bounds__(128, 4) k_preprocess_bwd(lp_prims P, float kap
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
   if (total == 0) return;
-  int slot = incl - c;
-  for (unsigned m = vm; m; m &= m - 1) s_items[w][slot++] = (unsigned char)((lane << 3) | (__ffs(m) - 1));
+  const int first = incl - c;   // this lane's items are [first, first + c)
+  {
+    int slot = first;
+    for (unsigned m = vm; m; m &= m - 1) s_items[w][slot++] = (unsigned char)((lane << 3) | (__ffs(m) - 1));
+  }
   __syncwarp();
+  // ---- phase A: dense evaluation of the items
   for (int r = 0; r < total; r += 32) {
     const int it = r + lane;
     if (it < total) {
       const int item = s_items[w][it];
       const int pl = item >> 3, v = item & 7;
       const int ii = base + pl;
-      float *row = acc + pl * AR::STRIDE;
       float gpos[3] = {0.f, 0.f, 0.f}, grot[4] = {0.f, 0.f, 0.f, 0.f}, gdist[4] = {0.f, 0.f, 0.f, 0.f};
-      float gop = 0.f, m2d = 0.f;
+      float gop = 0.f, m2d = 0.f, gr[3] = {0.f, 0.f, 0.f}, dir[3] = {0.f, 0.f, 1.f};
       view_feature_grad<KIND>(P, s_cam[v], kappa, ii, s_rg[v], gpos, grot, gdist, gop, m2d);
-      if (Gs.sh || Gs.pos) sh_view_grad<DEG>(P, s_cam[v], ii, s_rg[v], rg_words, row + AR::SH, gpos);
+      if (Gs.sh || Gs.pos) sh_view_inputs<DEG>(P, s_cam[v], ii, s_rg[v], rg_words, gr, dir, gpos);
+      float *res = s_res[w][it];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) atomicAdd(row + AR::POS + a, gpos[a]);
+      for (int a = 0; a < 3; ++a) res[ItemRes::POS + a] = gpos[a];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) atomicAdd(row + AR::ROT + a, grot[a]);
+      for (int a = 0; a < 4; ++a) res[ItemRes::ROT + a] = grot[a];
 #pragma unroll
-      for (int a = 0; a < AR::K; ++a) atomicAdd(row + AR::DIST + a, gdist[a]);
-      atomicAdd(row + AR::OP, gop);
-      atomicAdd(row + AR::M2D, m2d);
+      for (int a = 0; a < 4; ++a) res[ItemRes::DIST + a] = gdist[a];
+      res[ItemRes::OP] = gop;
+      res[ItemRes::M2D] = m2d;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        res[ItemRes::GR + a] = gr[a];
+        res[ItemRes::DIR + a] = dir[a];
+      }
     }
   }
   __syncwarp();
   if (!vm) return;
-  const float *row = acc + lane * AR::STRIDE;
+  // ---- phase B: owner lane sums its items and writes its primitive's gradients once
+  float acc[ItemRes::M2D + 1];
+#pragma unroll
+  for (int a = 0; a <= ItemRes::M2D; ++a) acc[a] = 0.f;
+  float gs[3][NC];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+    for (int k = 0; k < NC; ++k) gs[ch][k] = 0.f;
+  for (int it = first; it < first + c; ++it) {
+    const float *res = s_res[w][it];
+#pragma unroll
+    for (int a = 0; a <= ItemRes::M2D; ++a) acc[a] += res[a];
+    const float gr[3] = {res[ItemRes::GR], res[ItemRes::GR + 1], res[ItemRes::GR + 2]};
+    if (gr[0] == 0.f && gr[1] == 0.f && gr[2] == 0.f) continue;
+    float Y[16];
+    sh_basis<float>(DEG, res[ItemRes::DIR], res[ItemRes::DIR + 1], res[ItemRes::DIR + 2], Y);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) gs[ch][k] = fmaf(Y[k], gr[ch], gs[ch][k]);
+  }
   if (Gs.pos) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += row[AR::POS + a];
+    for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += acc[ItemRes::POS + a];
   }
   if (Gs.rot) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a) Gs.rot[(size_t)a * n + i] += row[AR::ROT + a];
+    for (int a = 0; a < 4; ++a) Gs.rot[(size_t)a * n + i] += acc[ItemRes::ROT + a];
   }
   if (Gs.dist) {
 #pragma unroll
-    for (int a = 0; a < AR::K; ++a) Gs.dist[(size_t)a * n + i] += row[AR::DIST + a];
+    for (int a = 0; a < K; ++a) Gs.dist[(size_t)a * n + i] += acc[ItemRes::DIST + a];
   }
-  if (Gs.opacity) Gs.opacity[i] += row[AR::OP];
-  if (Gs.mean2d_abs) Gs.mean2d_abs[i] += row[AR::M2D];
+  if (Gs.opacity) Gs.opacity[i] += acc[ItemRes::OP];
+  if (Gs.mean2d_abs) Gs.mean2d_abs[i] += acc[ItemRes::M2D];
   if (Gs.sh) {
-    float g[3 * AR::NC];
 #pragma unroll
-    for (int q = 0; q < 3 * AR::NC; ++q) g[q] = Gs.sh[(size_t)q * n + i];
+    for (int k = 0; k < NC; ++k)
 #pragma unroll
-    for (int q = 0; q < 3 * AR::NC; ++q) Gs.sh[(size_t)q * n + i] = g[q] + row[AR::SH + q];
+      for (int ch = 0; ch < 3; ++ch) {
+        float *g = Gs.sh + ((size_t)k * 3 + ch) * n + i;
+        *g += gs[ch][k];
+      }
   }
 }
 
@@ -549,12 +575,12 @@ void launch_preprocess(const lp_prims &P, const lp_camera &cam, float kappa, con
 
 template <int KIND>
 static void bwd_deg(const lp_prims &P, float kappa, const ViewPack &V, int rg, const lp_grads &G, cudaStream_t st) {
-  const int grid = (P.n + 127) / 128;
+  const int grid = (P.n + 63) / 64;
   switch (P.sh_degree) {
-    case 0: k_preprocess_bwd<KIND, 0><<<grid, 128, 0, st>>>(P, kappa, V, rg, G); break;
-    case 1: k_preprocess_bwd<KIND, 1><<<grid, 128, 0, st>>>(P, kappa, V, rg, G); break;
-    case 2: k_preprocess_bwd<KIND, 2><<<grid, 128, 0, st>>>(P, kappa, V, rg, G); break;
-    default: k_preprocess_bwd<KIND, 3><<<grid, 128, 0, st>>>(P, kappa, V, rg, G); break;
+    case 0: k_preprocess_bwd<KIND, 0><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
+    case 1: k_preprocess_bwd<KIND, 1><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
+    case 2: k_preprocess_bwd<KIND, 2><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
+    default: k_preprocess_bwd<KIND, 3><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
   }
 }
 
