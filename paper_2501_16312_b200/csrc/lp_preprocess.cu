@@ -468,11 +468,23 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd(lp_prims P, float kappa, 
   const int i = base + lane;
   unsigned vm = 0;   // views with a raster gradient for this lane's primitive
   if (i < n) {
-    for (int v = 0; v < V.nv; ++v) {
-      if (V.tt[v][i] == 0) continue;
-      const float *rg = V.rgrad[v] + (size_t)(rg_words - 4) * n + i;   // dsigma, drgb
-      if (rg[0] != 0.f || rg[n] != 0.f || rg[2 * n] != 0.f || rg[3 * n] != 0.f) vm |= 1u << v;
+    // independent loads for all views first (a dependent chain per view would serialise latency)
+    unsigned vis = 0;
+#pragma unroll
+    for (int v = 0; v < LP_MAXV; ++v)
+      if (v < V.nv && V.tt[v][i] != 0) vis |= 1u << v;
+    float probe[LP_MAXV];
+#pragma unroll
+    for (int v = 0; v < LP_MAXV; ++v) {
+      probe[v] = 0.f;
+      if ((vis >> v) & 1u) {
+        const float *rg = V.rgrad[v] + (size_t)(rg_words - 4) * n + i;   // dsigma, drgb
+        probe[v] = fabsf(rg[0]) + fabsf(rg[n]) + fabsf(rg[2 * n]) + fabsf(rg[3 * n]);
+      }
     }
+#pragma unroll
+    for (int v = 0; v < LP_MAXV; ++v)
+      if (probe[v] != 0.f) vm |= 1u << v;
   }
   const int c = __popc(vm);
   int incl = c;
@@ -555,13 +567,14 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd(lp_prims P, float kappa, 
   if (Gs.opacity) Gs.opacity[i] += acc[ItemRes::OP];
   if (Gs.mean2d_abs) Gs.mean2d_abs[i] += acc[ItemRes::M2D];
   if (Gs.sh) {
+    // all loads first, then the stores (the compiler cannot reorder loads past stores that may alias)
+    float old[3 * NC];
+#pragma unroll
+    for (int q = 0; q < 3 * NC; ++q) old[q] = Gs.sh[(size_t)q * n + i];
 #pragma unroll
     for (int k = 0; k < NC; ++k)
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        float *g = Gs.sh + ((size_t)k * 3 + ch) * n + i;
-        *g += gs[ch][k];
-      }
+      for (int ch = 0; ch < 3; ++ch) Gs.sh[((size_t)k * 3 + ch) * n + i] = old[k * 3 + ch] + gs[ch][k];
   }
 }
 
