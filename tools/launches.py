@@ -18,7 +18,7 @@ def load(path):
         if d["Metric Name"] != "gpu__time_duration.sum":
             continue
         k = d["Kernel Name"].split("(")[0].replace("void ", "")[:48]
-        v = float(d["Metric Value"]) * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(d["Metric Unit"], 1.0)
+        v = float(d["Metric Value"].replace(",", "")) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(d["Metric Unit"], 1.0)
         agg.setdefault(k, [0, 0.0])
         agg[k][0] += 1
         agg[k][1] += v
