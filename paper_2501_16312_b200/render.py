@@ -13,11 +13,7 @@ import numpy as np
 import torch
 
 from . import linprim as L
-
-
-def section_sizes(kind, n, sh_degree):
-    K = 3 if kind == L.LP_OCTAHEDRON else 4
-    return [("pos", 3 * n), ("rot", 4 * n), ("dist", K * n), ("opacity", n), ("sh", (sh_degree + 1) ** 2 * 3 * n)]
+from .train import section_sizes
 
 
 class DeviceScene:

@@ -1,0 +1,50 @@
+"""Host-side logic of the C5 multi-view training step (row a13): view sharding, the flat gradient
+layout, the single gradient allreduce and the paper's per-group learning rates.
+
+The device work of a step is liblinprim (preprocess / bin_sort / render_fwd / l1 / raster_bwd per
+local view, one fused preprocess_bwd, one Adam); this module only decides WHICH views a rank
+renders and HOW the per-rank gradients are combined, so it is testable on CPU with gloo
+(tests/test_multigpu_gloo.py).
+"""
+from __future__ import annotations
+
+
+def section_sizes(kind, n, sh_degree):
+    """Sections of the flat feature / gradient buffer (same SoA layout as lp_prims)."""
+    K = 3 if kind == 0 else 4
+    return [("pos", 3 * n), ("rot", 4 * n), ("dist", K * n), ("opacity", n), ("sh", (sh_degree + 1) ** 2 * 3 * n)]
+
+
+def shard_views(n_views: int, rank: int, world: int) -> list:
+    """views[r::N] on rank r: strong scaling of a fixed global batch (north_star: 8 views, 1/2/4/8 GPUs)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return list(range(rank, n_views, world))
+
+
+def flat_offsets(kind: int, n: int, sh_degree: int) -> dict:
+    """[begin, end) of each feature section in the flat buffer [pos | rot | dist | opacity | sh]."""
+    out, o = {}, 0
+    for name, size in section_sizes(kind, n, sh_degree):
+        out[name] = (o, o + size)
+        o += size
+    return out
+
+
+def lr_groups(offsets: dict, n: int, extent: float = 4.0) -> list:
+    """Adam groups (begin, end, lr): colour (SH DC) 2.5e-3, SH rest 1.25e-4, opacity 2.5e-2,
+    rotation 1e-3, distance 2.6^-1 1e-4 x extent; position 1.6e-4 x extent (3DGS)."""
+    return [(offsets["pos"][0], offsets["pos"][1], 1.6e-4 * extent),
+            (offsets["rot"][0], offsets["rot"][1], 1e-3),
+            (offsets["dist"][0], offsets["dist"][1], 1e-4 / 2.6 * extent),
+            (offsets["opacity"][0], offsets["opacity"][1], 2.5e-2),
+            (offsets["sh"][0], offsets["sh"][0] + 3 * n, 2.5e-3),
+            (offsets["sh"][0] + 3 * n, offsets["sh"][1], 1.25e-4)]
+
+
+def allreduce_gradients(flat_grad, world: int):
+    """The step's single exchange: SUM-allreduce of the flat fp32 gradient (NCCL on GPUs, gloo in tests)."""
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(flat_grad, op=dist.ReduceOp.SUM)
+    return flat_grad
