@@ -135,14 +135,14 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2501_16312_b200 import linprim as L
-    from paper_2501_16312_b200 import render, scenegen
+    from paper_2501_16312_b200 import render, scenegen, train
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     scene, cams = scenegen.make_scene(WORKLOAD, seed=args.seed, n=args.n)
     n_views = len(cams)
     W, H = cams[0]["width"], cams[0]["height"]
-    my_views = list(range(rank, n_views, world))
+    my_views = train.shard_views(n_views, rank, world)
     ds = render.DeviceScene(scene, device=dev)
 
     # synthetic targets: the same scene with jittered centres, rendered once at setup
@@ -181,12 +181,8 @@ def run_ours(args, rank, world, local_rank):
     m = torch.zeros_like(ds.flat)
     v = torch.zeros_like(ds.flat)
     # paper's learning rates; position 1.6e-4 x extent (3DGS), distances 2.6^-1 1e-4 x extent
-    extent = 4.0
-    off = ds.offsets
     n = ds.n
-    groups = [(off["pos"][0], off["pos"][1], 1.6e-4 * extent), (off["rot"][0], off["rot"][1], 1e-3),
-              (off["dist"][0], off["dist"][1], 1e-4 / 2.6 * extent), (off["opacity"][0], off["opacity"][1], 2.5e-2),
-              (off["sh"][0], off["sh"][0] + 3 * n, 2.5e-3), (off["sh"][0] + 3 * n, off["sh"][1], 1.25e-4)]
+    groups = train.lr_groups(ds.offsets, n, extent=4.0)
     scale = 1.0 / (3.0 * W * H * n_views)
     cams_c = rend.cams
     ev_names = ["pre", "sort", "fwd", "l1", "rbwd"]           # per view
@@ -221,7 +217,7 @@ def run_ours(args, rank, world, local_rank):
         if events is not None:
             events[n_local][0].record(st)
         if world > 1:
-            dist.all_reduce(ds.grad)
+            train.allreduce_gradients(ds.grad, world)
         if events is not None:
             events[n_local][1].record(st)
         L.lp_adam_step(ds.flat, ds.grad, m, v, groups, 0.9, 0.999, 1e-15, si + 1, st, zero_grad=True)

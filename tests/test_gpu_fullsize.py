@@ -1,0 +1,108 @@
+"""Full-size parity on BASELINE.json configs[1..4] (C2 100k tetra 1280x720, C3 1M octa 1600x1060,
+C4 3M tetra 1957x1091, C5 view 0 of the 8-view ring) in the launch configuration bench.py times.
+
+The oracle preprocesses and bins ALL primitives (bit-exact per-primitive outputs), orders the lists
+of a sample of tiles, and renders + backpropagates the pixels of those tiles; the GPU runs the whole
+frame with dL/dC non-zero only on the sampled tiles, so every per-primitive gradient is comparable.
+Global properties (E, range partition, key order) are checked on the full GPU list."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2501_16312_b200 import scenegen
+from tests import parity as PT
+from tests.helpers import oscene
+
+pytestmark = pytest.mark.gpu
+
+K_OF = {0: 3, 1: 4}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2501_16312_b200 import _build
+    _build.build()
+
+
+def _sample_tiles(gx, gy, k, seed):
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(gx * gy, size=min(k, gx * gy), replace=False))
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
+def test_fullsize_sampled_parity(cfg):
+    import torch
+    scene, cams = scenegen.make_scene(cfg, seed=0)
+    cam = cams[0]
+    W, H = cam["width"], cam["height"]
+    n = scene["pos"].shape[1]
+    K = K_OF[scene["kind"]]
+    gx, gy = (W + 15) // 16, (H + 15) // 16
+    tiles = _sample_tiles(gx, gy, 24, seed=len(cfg) + n % 97)
+    mask_t = np.zeros(gx * gy, np.uint8)
+    mask_t[tiles] = 1
+    # pixels of the sampled tiles
+    pix = []
+    for t in tiles:
+        ty, tx = divmod(int(t), gx)
+        ys = np.arange(ty * 16, min(ty * 16 + 16, H))
+        xs = np.arange(tx * 16, min(tx * 16 + 16, W))
+        pix.append((ys[:, None] * W + xs[None, :]).reshape(-1))
+    pix = np.concatenate(pix).astype(np.int32)
+
+    osc = oscene(scene)
+    pre = oracle.preprocess(osc, cam, kappa=0.1, mode=0)
+    keys, vals, ranges = oracle.bin_tiles(pre, W, H, tile_mask=mask_t)
+    f0 = oracle.render(osc, cam, pre, vals, ranges, pix=pix)
+    stop_mask = np.zeros((H, W), bool)
+    stop_mask.reshape(-1)[pix] = f0.m_stop.reshape(-1)[pix] < PT.STOP_MARGIN
+    G = np.zeros((3, H, W), np.float32)
+    Gs = scenegen.upstream_grad(W, H, seed=1)[0]
+    sel = np.zeros(H * W, bool)
+    sel[pix] = True
+    sel &= ~stop_mask.reshape(-1)
+    G.reshape(3, -1)[:, sel] = Gs.reshape(3, -1)[:, sel]
+
+    ds, r, img = PT.gpu_run(scene, [cam], G=G)
+    got = PT.frame_arrays(r, 0, n, K)
+    # ---- per-primitive outputs, all primitives, bit-exact
+    assert np.array_equal(got["tiles_touched"], pre.tiles_touched)
+    assert np.array_equal(got["rect"], pre.rect)
+    assert np.array_equal(got["depth_key"], pre.depth_key)
+    assert np.array_equal(got["canon"].view(np.uint32), pre.canon.view(np.uint32))
+    # ---- global list properties
+    E = got["E"]
+    assert E == int(pre.tiles_touched.astype(np.int64).sum())
+    st = got["sorted_tile"].astype(np.int64)
+    assert np.all(np.diff(st) >= 0)
+    k64 = (st.astype(np.uint64) << np.uint64(32)) | got["depth_key"][got["sorted_val"]].astype(np.uint64)
+    same = st[1:] == st[:-1]
+    assert np.all(k64[1:][same] >= k64[:-1][same])
+    tie = same & (k64[1:] == k64[:-1])
+    assert np.all(got["sorted_val"][1:][tie] > got["sorted_val"][:-1][tie])
+    rg = got["ranges"].astype(np.int64)
+    nz = rg[rg[:, 1] > rg[:, 0]]
+    assert nz[0, 0] == 0 and nz[-1, 1] == E and np.all(nz[1:, 0] == nz[:-1, 1])
+    # ---- sampled tiles: bit-exact lists
+    for t in tiles:
+        a, b = rg[t]
+        oa, ob = ranges[t]
+        assert np.array_equal(got["sorted_val"][a:b], vals[oa:ob]), f"tile {t}"
+    # ---- image on the sampled pixels
+    im = img[0].cpu().numpy().reshape(3, -1)[:, pix]
+    ref = f0.image.reshape(3, -1)[:, pix]
+    ok = ~stop_mask.reshape(-1)[pix]
+    assert np.abs(im - ref)[:, ok].max() <= PT.IMG_TOL
+    assert np.array_equal(got["n_proc"].reshape(-1)[pix][ok], f0.n_proc.reshape(-1)[pix][ok])
+    # ---- gradients (dL/dC non-zero only on the sampled pixels)
+    fb = oracle.render(osc, cam, pre, vals, ranges, pix=pix, dL_dimage=G)
+    g = oracle.preprocess_bwd(osc, cam, pre, fb)
+    flagged = fb.face_margin < PT.FACE_MARGIN
+    gd = ds.grad_dict()
+    for name, refg, fl in (("pos", g.pos, flagged), ("rot", g.rot, flagged), ("dist", g.dist, flagged),
+                           ("opacity", g.opacity, None), ("sh", g.sh, None)):
+        ok_g, worst, rep = PT.grad_close(name, gd[name].cpu().numpy().reshape(refg.shape), refg, fl)
+        assert ok_g, rep
+    torch.cuda.empty_cache()
