@@ -100,7 +100,16 @@ typedef struct {
   uint32_t *n_proc;           /* [H][W] tile-list entries processed per pixel (from the tile's start) */
   float    *rgrad;            /* [rgrad_words][n] raster-gradient scratch of the backward */
   float    *canon;            /* [n][2 + 3K] canonical fp32 cr_x, cr_y, offsets (debug; NULL unless requested) */
+  int32_t  *tile_diff;        /* [(tiles_y+1)][(tiles_x+1)] 2-D difference counts of the tile rects (bucket sort) */
+  uint32_t *tile_cursor;      /* [tiles] bucket fill cursors (bucket sort) */
+  int32_t   sort_method;      /* LP_SORT_BUCKET (default set by lp_frame_init) or LP_SORT_RADIX; caller may change */
 } lp_frame;
+
+/* lp_bin_sort methods; both produce the identical (tile, depth, id) order. */
+enum {
+  LP_SORT_BUCKET = 0,         /* 2-D difference histogram of the rects -> per-tile buckets -> per-tile bitonic sort */
+  LP_SORT_RADIX = 1           /* depth sort of the primitives -> emission in depth order -> stable radix sort by tile */
+};
 
 enum {
   LP_CNT_ENTRIES = 0,         /* E, tile-list length */

@@ -22,7 +22,7 @@ inline int offsets_k(int kind) { return kind == LP_OCTAHEDRON ? 3 : 4; }
 struct Layout {
   size_t tiles_touched, rect, depth_key, record, prim_key, prim_key_alt, prim_order, prim_order_alt, offsets, tile_key,
       tile_key_alt, entry_val, entry_val_alt, ranges, sort_hist, scan_tmp, counters, T_final, n_proc, rgrad, canon,
-      total;
+      tile_diff, tile_cursor, total;
 };
 
 Layout layout(int kind, int64_t n, int w, int h, int64_t cap, int canon) {
@@ -53,6 +53,9 @@ Layout layout(int kind, int64_t n, int w, int h, int64_t cap, int canon) {
   L.n_proc = take(4 * hw);
   L.rgrad = take(4 * (size_t)rgrad_words(kind) * nn);
   L.canon = canon ? take(4 * (size_t)(2 + 3 * offsets_k(kind)) * nn) : 0;
+  const int64_t gx = (w + LP_TILE - 1) / LP_TILE, gy = (h + LP_TILE - 1) / LP_TILE;
+  L.tile_diff = take(4 * (gx + 1) * (gy + 1));
+  L.tile_cursor = take(4 * tiles);
   L.total = o;
   return L;
 }
@@ -145,6 +148,9 @@ lp_status lp_frame_init(lp_frame *F, void *workspace, size_t bytes, int32_t kind
   F->n_proc = reinterpret_cast<uint32_t *>(b + L.n_proc);
   F->rgrad = reinterpret_cast<float *>(b + L.rgrad);
   F->canon = with_canon ? reinterpret_cast<float *>(b + L.canon) : nullptr;
+  F->tile_diff = reinterpret_cast<int32_t *>(b + L.tile_diff);
+  F->tile_cursor = reinterpret_cast<uint32_t *>(b + L.tile_cursor);
+  F->sort_method = LP_SORT_BUCKET;
   return LP_OK;
 }
 
@@ -163,6 +169,7 @@ lp_status lp_preprocess(const lp_prims *prims, const lp_camera *cams, int32_t n_
     cudaMemsetAsync(F.counters, 0, 4 * LP_NUM_COUNTERS, st);
     // the backward's raster-moment scratch is consumed once per preprocess
     cudaMemsetAsync(F.rgrad, 0, 4 * (size_t)F.rgrad_words * (F.n > 0 ? F.n : 1), st);
+    cudaMemsetAsync(F.tile_diff, 0, 4 * (size_t)(F.tiles_x + 1) * (F.tiles_y + 1), st);
     launch_preprocess(*prims, cams[v], cfg->aa_kernel, F, st);
   }
   return last_error();
@@ -177,6 +184,26 @@ lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, 
   for (int v = 0; v < n_views; ++v) {
     lp_frame &F = frames[v];
     const int n = F.n;
+    if (F.sort_method == LP_SORT_BUCKET) {
+      // counts (2-D prefix of the rect difference grid K1 filled) -> ranges, cursors, E
+      launch_tile_counts(F, st);
+      if (n_entries) {
+        uint32_t e32 = 0;
+        cudaMemcpyAsync(&e32, F.counters + LP_CNT_ENTRIES, 4, cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) return LP_ERR_CUDA;
+        n_entries[v] = e32;
+        if ((int64_t)e32 > F.capacity) {
+          status = LP_ERR_CAPACITY;
+          continue;
+        }
+      }
+      launch_bucket(F, st);
+      launch_tile_sort(F, st);
+      F.sorted_tile = F.tile_key;
+      F.sorted_val = F.entry_val;
+      continue;
+    }
+    // LP_SORT_RADIX
     // 1. depth sort of the primitives (stable: ties keep ascending id, reading 11)
     const int flip = radix_sort_pairs(F.prim_key, F.prim_key_alt, F.prim_order, F.prim_order_alt, n, nullptr, 32,
                                       F.sort_hist, st);

@@ -77,6 +77,14 @@ __global__ void __launch_bounds__(256) k_preprocess(lp_prims P, lp_camera cam, f
       for (int a = 0; a < 3; ++a) cn[2 + 3 * j + a] = ok ? g.off[j][a] : 0.f;
   }
   if (g.tiles == 0) return;   // only visible primitives need a record
+  {
+    // tile rect into the 2-D difference grid of the bucket sort (4 atomics instead of tiles_touched)
+    const int cols = F.tiles_x + 1;
+    atomicAdd(F.tile_diff + g.rect[1] * cols + g.rect[0], 1);
+    atomicAdd(F.tile_diff + g.rect[1] * cols + g.rect[2] + 1, -1);
+    atomicAdd(F.tile_diff + (g.rect[3] + 1) * cols + g.rect[0], -1);
+    atomicAdd(F.tile_diff + (g.rect[3] + 1) * cols + g.rect[2] + 1, 1);
+  }
 
   // ---- density, Eq. 1: sigma = -log(1 - 0.99 alpha) / (2 min dhat)
   const float alpha = 1.f / (1.f + expf(-P.opacity[i]));

@@ -358,3 +358,209 @@ void launch_ranges(const lp_frame &F, const uint32_t *sorted_tile, int tiles, cu
 }
 
 }  // namespace lp
+
+// =============================================================================================
+// LP_SORT_BUCKET: (tile, depth, id) order without a global sort.
+//   K1 adds each visible primitive's tile rect to a 2-D difference grid (4 atomics);
+//   k_tile_counts: 2-D prefix -> per-tile counts -> exclusive scan -> ranges, cursors, E;
+//   k_bucket: every primitive appends (depth key, id) to the buckets of its tiles (cursor atomics;
+//             order inside a bucket is arbitrary);
+//   k_tile_sort: one CTA per tile sorts its bucket by the 64-bit (depth key << 32 | id) in shared
+//             memory (bitonic network, ascending-only variant so +inf padding never moves), or in
+//             place in global memory for a bucket larger than the shared-memory capacity.
+// The result is the same total order as the radix path and the oracle.
+// =============================================================================================
+namespace lp {
+
+constexpr int TS_THREADS = 256;
+constexpr int TS_CAP = 4096;      // entries sorted in shared memory (32 KB of u64)
+
+__global__ void __launch_bounds__(1024) k_tile_counts(int32_t *__restrict__ diff, int gx, int gy,
+                                                      uint32_t *__restrict__ ranges, uint32_t *__restrict__ cursor,
+                                                      uint32_t *__restrict__ counters, int64_t capacity) {
+  extern __shared__ int32_t s_grid[];   // (gy+1) x (gx+1)
+  __shared__ uint32_t s_warp[32];
+  const int cols = gx + 1, rows = gy + 1, cells = cols * rows;
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) s_grid[c] = diff[c];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // inclusive prefix along x, one warp per row (32-wide chunks with carry)
+  for (int r = warp; r < rows; r += nw) {
+    int carry = 0;
+    for (int c0 = 0; c0 < cols; c0 += 32) {
+      const int c = c0 + lane;
+      int v = c < cols ? s_grid[r * cols + c] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (c < cols) s_grid[r * cols + c] = v + carry;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  // inclusive prefix along y, one warp per column
+  for (int c = warp; c < cols; c += nw) {
+    int carry = 0;
+    for (int r0 = 0; r0 < rows; r0 += 32) {
+      const int r = r0 + lane;
+      int v = r < rows ? s_grid[r * cols + c] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (r < rows) s_grid[r * cols + c] = v + carry;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  // exclusive scan of the per-tile counts in row-major tile order
+  const int tiles = gx * gy;
+  uint32_t base = 0;
+  for (int t0 = 0; t0 < tiles; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    const uint32_t cnt = t < tiles ? (uint32_t)s_grid[(t / gx) * cols + (t % gx)] : 0u;
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan(cnt, s_warp, total);
+    if (t < tiles) {
+      const uint32_t off = base + ex;
+      ranges[2 * (size_t)t] = off;
+      ranges[2 * (size_t)t + 1] = off + cnt;
+      cursor[t] = off;
+    }
+    base += total;
+  }
+  if (threadIdx.x == 0) {
+    counters[LP_CNT_ENTRIES] = base;
+    counters[LP_CNT_OVERFLOW] = (int64_t)base > capacity ? 1u : 0u;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bucket(const uint32_t *__restrict__ tt, const ushort4 *__restrict__ rect,
+                                                const uint32_t *__restrict__ depth_key, int n, int tiles_x,
+                                                int64_t capacity, uint32_t *__restrict__ cursor,
+                                                uint32_t *__restrict__ bkey, uint32_t *__restrict__ bval) {
+  const int lane = threadIdx.x & 31;
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t my_tt = 0, my_key = 0;
+  ushort4 my_r = make_ushort4(0, 0, 0, 0);
+  if (i0 < n) {
+    my_tt = tt[i0];
+    if (my_tt) {
+      my_r = rect[i0];
+      my_key = depth_key[i0];
+    }
+  }
+  unsigned todo = __ballot_sync(0xffffffffu, my_tt != 0);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const uint32_t i = (uint32_t)((i0 & ~31) + src);
+    const uint32_t cnt = __shfl_sync(0xffffffffu, my_tt, src);
+    const uint32_t key = __shfl_sync(0xffffffffu, my_key, src);
+    const uint32_t tx0 = __shfl_sync(0xffffffffu, (uint32_t)my_r.x, src);
+    const uint32_t ty0 = __shfl_sync(0xffffffffu, (uint32_t)my_r.y, src);
+    const uint32_t tx1 = __shfl_sync(0xffffffffu, (uint32_t)my_r.z, src);
+    const uint32_t rw = tx1 - tx0 + 1;
+    for (uint32_t k = lane; k < cnt; k += 32) {
+      const uint32_t t = (ty0 + k / rw) * (uint32_t)tiles_x + tx0 + k % rw;
+      const uint32_t pos = atomicAdd(cursor + t, 1u);
+      if ((int64_t)pos < capacity) {
+        bkey[pos] = key;
+        bval[pos] = i;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned long long composite(uint32_t key, uint32_t id) {
+  return ((unsigned long long)key << 32) | id;
+}
+
+__global__ void __launch_bounds__(TS_THREADS) k_tile_sort(const uint32_t *__restrict__ ranges, int64_t capacity,
+                                                          uint32_t *__restrict__ bkey, uint32_t *__restrict__ bval,
+                                                          uint32_t *__restrict__ out_tile,
+                                                          uint32_t *__restrict__ out_val) {
+  __shared__ unsigned long long s_k[TS_CAP];
+  const int t = blockIdx.x;
+  int64_t off = ranges[2 * (size_t)t], end = ranges[2 * (size_t)t + 1];
+  if (end > capacity) end = capacity;
+  if (off >= end) return;
+  const int L = (int)(end - off);
+  int P = 1;
+  while (P < L) P <<= 1;
+  if (P <= TS_CAP) {
+    for (int i = threadIdx.x; i < P; i += TS_THREADS)
+      s_k[i] = i < L ? composite(bkey[off + i], bval[off + i]) : ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k - 1; j > 0; j = (j == k - 1) ? (k >> 2) : (j >> 1)) {
+        for (int i = threadIdx.x; i < P; i += TS_THREADS) {
+          const int p = i ^ j;
+          if (p > i) {
+            const unsigned long long a = s_k[i], b = s_k[p];
+            if (a > b) { s_k[i] = b; s_k[p] = a; }
+          }
+        }
+        __syncthreads();
+        if (k == 2) break;
+      }
+    }
+    for (int i = threadIdx.x; i < L; i += TS_THREADS) {
+      out_val[off + i] = (uint32_t)s_k[i];
+      out_tile[off + i] = (uint32_t)t;
+    }
+    return;
+  }
+  // oversize bucket: the same network in place in global memory; partners beyond L are +inf
+  uint32_t *K = bkey + off, *V = bval + off;
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k - 1; j > 0; j = (j == k - 1) ? (k >> 2) : (j >> 1)) {
+      for (int i = threadIdx.x; i < L; i += TS_THREADS) {
+        const int p = i ^ j;
+        if (p > i && p < L) {
+          const unsigned long long a = composite(K[i], V[i]), b = composite(K[p], V[p]);
+          if (a > b) {
+            K[i] = (uint32_t)(b >> 32); V[i] = (uint32_t)b;
+            K[p] = (uint32_t)(a >> 32); V[p] = (uint32_t)a;
+          }
+        }
+      }
+      __syncthreads();
+      if (k == 2) break;
+    }
+  }
+  for (int i = threadIdx.x; i < L; i += TS_THREADS) {
+    out_val[off + i] = V[i];
+    out_tile[off + i] = (uint32_t)t;
+  }
+}
+
+void launch_tile_counts(const lp_frame &F, cudaStream_t st) {
+  const size_t smem = 4 * (size_t)(F.tiles_x + 1) * (F.tiles_y + 1);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tile_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  k_tile_counts<<<1, 1024, smem, st>>>(F.tile_diff, F.tiles_x, F.tiles_y, F.ranges, F.tile_cursor, F.counters,
+                                       F.capacity);
+}
+
+void launch_bucket(const lp_frame &F, cudaStream_t st) {
+  if (F.n == 0) return;
+  k_bucket<<<(F.n + 255) / 256, 256, 0, st>>>(F.tiles_touched, reinterpret_cast<const ushort4 *>(F.rect), F.depth_key,
+                                              F.n, F.tiles_x, F.capacity, F.tile_cursor, F.tile_key_alt,
+                                              F.entry_val_alt);
+}
+
+void launch_tile_sort(const lp_frame &F, cudaStream_t st) {
+  const int tiles = F.tiles_x * F.tiles_y;
+  if (tiles == 0) return;
+  k_tile_sort<<<tiles, TS_THREADS, 0, st>>>(F.ranges, F.capacity, F.tile_key_alt, F.entry_val_alt, F.tile_key,
+                                            F.entry_val);
+}
+
+}  // namespace lp

@@ -22,7 +22,8 @@ LP_OK, LP_ERR_ARG, LP_ERR_CAPACITY, LP_ERR_CUDA, LP_ERR_UNSUPPORTED = range(5)
 LP_OCTAHEDRON, LP_TETRAHEDRON = 0, 1
 LP_TILE = 16
 LP_CNT_ENTRIES, LP_CNT_OVERFLOW, LP_CNT_INVALID, LP_CNT_FRUSTUM, LP_CNT_VISIBLE = 0, 1, 2, 3, 4
-LP_CNT_ITERATED, LP_CNT_INTERSECTED, LP_NUM_COUNTERS = 8, 10, 16
+LP_CNT_ITERATED, LP_CNT_INTERSECTED, LP_CNT_INBOX, LP_NUM_COUNTERS = 8, 10, 12, 16
+LP_SORT_BUCKET, LP_SORT_RADIX = 0, 1
 
 _p = C.c_void_p
 
@@ -50,7 +51,8 @@ class lp_frame(C.Structure):
         [(f, _p) for f in ("tiles_touched", "rect", "depth_key", "record", "prim_key", "prim_key_alt",
                            "prim_order", "prim_order_alt", "offsets", "tile_key", "tile_key_alt", "entry_val",
                            "entry_val_alt", "sorted_tile", "sorted_val", "ranges", "sort_hist", "scan_tmp",
-                           "counters", "T_final", "n_proc", "rgrad", "canon")]
+                           "counters", "T_final", "n_proc", "rgrad", "canon", "tile_diff", "tile_cursor")] + \
+        [("sort_method", C.c_int32)]
 
 
 class lp_adam_group(C.Structure):

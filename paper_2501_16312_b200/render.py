@@ -108,8 +108,9 @@ class Renderer:
     """Forward / backward of the LinPrim tile rasterizer over a list of views (C-ABI calls only)."""
 
     def __init__(self, scene: DeviceScene, cams, aa_kernel=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), capacity=None,
-                 with_canon=False, count_stats=False, sync_capacity=True):
+                 with_canon=False, count_stats=False, sync_capacity=True, sort_method=None):
         self.scene = scene
+        self.sort_method = L.LP_SORT_BUCKET if sort_method is None else int(sort_method)
         self.cam_dicts = list(cams)
         self.cams = L.cameras(self.cam_dicts)
         self.cfg = L.raster_cfg(aa_kernel, t_stop, bg, count_stats)
@@ -119,8 +120,14 @@ class Renderer:
         self.frames = []
         for c in self.cam_dicts:
             cap = capacity or estimate_capacity(scene.n, c["width"], c["height"])
-            self.frames.append(Frame(scene.kind, scene.n, c["width"], c["height"], cap, dev, with_canon))
+            self.frames.append(self._new_frame(c, cap))
         self.sizes = [3 * c["width"] * c["height"] for c in self.cam_dicts]
+
+    def _new_frame(self, cam, capacity):
+        f = Frame(self.scene.kind, self.scene.n, cam["width"], cam["height"], capacity, self.scene.flat.device,
+                  self.with_canon)
+        f.c.sort_method = self.sort_method
+        return f
 
     def stream(self):
         return torch.cuda.current_stream(self.scene.flat.device)
@@ -144,9 +151,7 @@ class Renderer:
                     status = L.lp_bin_sort(cams, fa, st, ne)
                     _store_back([self.frames[v]], fa)
                     if status == L.LP_ERR_CAPACITY:
-                        c = self.cam_dicts[v]
-                        self.frames[v] = Frame(self.scene.kind, self.scene.n, c["width"], c["height"],
-                                               int(ne[0] * 1.25) + 1024, self.scene.flat.device, self.with_canon)
+                        self.frames[v] = self._new_frame(self.cam_dicts[v], int(ne[0] * 1.25) + 1024)
                         continue
                 else:
                     L.lp_bin_sort(cams, fa, st, None)
