@@ -540,10 +540,9 @@ __global__ void __launch_bounds__(TS_THREADS) k_tile_sort(const uint32_t *__rest
 
 void launch_tile_counts(const lp_frame &F, cudaStream_t st) {
   const size_t smem = 4 * (size_t)(F.tiles_x + 1) * (F.tiles_y + 1);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_tile_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
+  if (smem > 48 * 1024) {   // grids above ~12k tiles (e.g. > 4K x 3K pixels) need the opt-in carve-out
+    if (cudaFuncSetAttribute(k_tile_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return;   // the launch below is skipped; lp_bin_sort reports the recorded CUDA error
   }
   k_tile_counts<<<1, 1024, smem, st>>>(F.tile_diff, F.tiles_x, F.tiles_y, F.ranges, F.tile_cursor, F.counters,
                                        F.capacity);
