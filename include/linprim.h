@@ -102,7 +102,8 @@ typedef struct {
   float    *canon;            /* [n][2 + 3K] canonical fp32 cr_x, cr_y, offsets (debug; NULL unless requested) */
   int32_t  *tile_diff;        /* [(tiles_y+1)][(tiles_x+1)] 2-D difference counts of the tile rects (bucket sort) */
   uint32_t *tile_cursor;      /* [tiles] bucket fill cursors (bucket sort) */
-  int32_t   sort_method;      /* LP_SORT_BUCKET (default set by lp_frame_init) or LP_SORT_RADIX; caller may change */
+  int32_t   sort_method;      /* LP_SORT_RADIX (default set by lp_frame_init) or LP_SORT_BUCKET; caller may change
+                                 before lp_preprocess (K1 fills the bucket method's rect grid only when selected) */
 } lp_frame;
 
 /* lp_bin_sort methods; both produce the identical (tile, depth, id) order. */

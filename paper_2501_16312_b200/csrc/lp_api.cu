@@ -150,7 +150,7 @@ lp_status lp_frame_init(lp_frame *F, void *workspace, size_t bytes, int32_t kind
   F->canon = with_canon ? reinterpret_cast<float *>(b + L.canon) : nullptr;
   F->tile_diff = reinterpret_cast<int32_t *>(b + L.tile_diff);
   F->tile_cursor = reinterpret_cast<uint32_t *>(b + L.tile_cursor);
-  F->sort_method = LP_SORT_BUCKET;
+  F->sort_method = LP_SORT_RADIX;   // measured faster on C5
   return LP_OK;
 }
 

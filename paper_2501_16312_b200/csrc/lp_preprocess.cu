@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) k_preprocess(lp_prims P, lp_camera cam, f
       for (int a = 0; a < 3; ++a) cn[2 + 3 * j + a] = ok ? g.off[j][a] : 0.f;
   }
   if (g.tiles == 0) return;   // only visible primitives need a record
-  {
+  if (F.sort_method == LP_SORT_BUCKET) {
     // tile rect into the 2-D difference grid of the bucket sort (4 atomics instead of tiles_touched)
     const int cols = F.tiles_x + 1;
     atomicAdd(F.tile_diff + g.rect[1] * cols + g.rect[0], 1);

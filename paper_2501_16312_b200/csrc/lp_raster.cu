@@ -74,6 +74,13 @@ __device__ __forceinline__ int warp_sublist(const float4 *s_rec, int cnt, float 
   return n;
 }
 
+// resident CTAs per SM the backward asks the register allocator for (LP_BWD_BLOCKS overrides at
+// build time): 8 x 128 threads caps it at 64 registers
+#ifndef LP_BWD_BLOCKS
+#define LP_BWD_BLOCKS 8
+#endif
+#define BWD_MIN_BLOCKS(nt) ((nt) == 128 ? LP_BWD_BLOCKS : 1)
+
 // =============================================================================================
 // K3 forward
 // =============================================================================================
@@ -249,7 +256,8 @@ __device__ __forceinline__ float warp_transpose_reduce(const float (&a)[N], int 
 // K4 backward
 // =============================================================================================
 template <int KIND, int NT>
-__global__ void __launch_bounds__(NT) k_raster_bwd(lp_frame F, lp_raster_cfg cfg, const float *__restrict__ dL) {
+__global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(NT)) k_raster_bwd(lp_frame F, lp_raster_cfg cfg,
+                                                                      const float *__restrict__ dL) {
   using KD = Kind<KIND>;
   constexpr int RW = KD::RW, RW4 = RW / 4, PPT = 256 / NT, RG = KD::RG;
   constexpr int RGP = RG == 20 ? 20 : 28;      // padded row: 16-byte stores, conflict-free (RGP/4 odd)

@@ -110,7 +110,7 @@ class Renderer:
     def __init__(self, scene: DeviceScene, cams, aa_kernel=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), capacity=None,
                  with_canon=False, count_stats=False, sync_capacity=True, sort_method=None):
         self.scene = scene
-        self.sort_method = L.LP_SORT_BUCKET if sort_method is None else int(sort_method)
+        self.sort_method = L.LP_SORT_RADIX if sort_method is None else int(sort_method)
         self.cam_dicts = list(cams)
         self.cams = L.cameras(self.cam_dicts)
         self.cfg = L.raster_cfg(aa_kernel, t_stop, bg, count_stats)
