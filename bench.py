@@ -3,8 +3,8 @@
 
 Workload (BASELINE.json configs[4], the config its metric "fwd+bwd Mpixel/s and train iters/s at
 1/2/4/8 B200" is quoted on): 1M octahedra, SH degree 3, a batch of 8 views at 1600x1060, one
-training step = for each local view: lp_preprocess -> lp_bin_sort -> lp_render_fwd -> lp_l1_grad
--> lp_raster_bwd -> lp_preprocess_bwd; then (N > 1) one NCCL allreduce of the flat gradient; then
+training step = one lp_preprocess over all local views; for each local view lp_bin_sort ->
+lp_render_fwd -> lp_l1_grad -> lp_raster_bwd; one lp_preprocess_bwd over all local views; then (N > 1) one NCCL allreduce of the flat gradient; then
 one fused Adam (lp_adam_step, also zeroing the gradient).  Views are sharded views[r::N] over
 ranks (strong scaling, fixed global batch of 8).
 
@@ -125,7 +125,7 @@ def launches_per_view(n, tiles):
     bits = max(1, math.ceil(math.log2(tiles)))
     tile_passes = math.ceil(bits / 8)
     sort_prims = 4 * 3
-    return 1 + sort_prims + 3 + 1 + 3 * tile_passes + 1 + 1 + 1 + 1   # K1 | depth sort | scan | emit | tile sort | ranges | fwd | l1 | raster bwd
+    return sort_prims + 3 + 1 + 3 * tile_passes + 1 + 1 + 1 + 1   # depth sort | scan | emit | tile sort | ranges | fwd | l1 | raster bwd
 
 
 # ------------------------------------------------------------------------------ our implementation
@@ -185,44 +185,51 @@ def run_ours(args, rank, world, local_rank):
     groups = train.lr_groups(ds.offsets, n, extent=4.0)
     scale = 1.0 / (3.0 * W * H * n_views)
     cams_c = rend.cams
-    ev_names = ["pre", "sort", "fwd", "l1", "rbwd"]           # per view
+    ev_names = ["sort", "fwd", "l1", "rbwd"]           # per view
     fa_all = render.frames_array(rend.frames)
     ca_all = rend._cams(list(range(n_local)))
 
     def step(si, events=None):
+        S = events[n_local] if events is not None else None
+        # preprocess of all local views in one launch (each primitive's features read once)
+        if S is not None:
+            S[0].record(st)
+        for i in range(n_local):
+            fa_all[i] = rend.frames[i].c
+        L.lp_preprocess(ds.prims, ca_all, rend.cfg, fa_all, st)
+        render._store_back(rend.frames, fa_all)
+        if S is not None:
+            S[1].record(st)
         for i in range(n_local):
             ca = rend._cams([i])
             fa = render.frames_array([rend.frames[i]])
             if events is not None:
                 events[i][0].record(st)
-            L.lp_preprocess(ds.prims, ca, rend.cfg, fa, st)
-            if events is not None:
-                events[i][1].record(st)
             L.lp_bin_sort(ca, fa, st, None)
             if events is not None:
-                events[i][2].record(st)
+                events[i][1].record(st)
             L.lp_render_fwd(ca, rend.cfg, fa, img[i], st)
             if events is not None:
-                events[i][3].record(st)
+                events[i][2].record(st)
             L.lp_l1_grad(img[i], targets[i], dL[i], loss_buf[si:si + 1], scale, st)
             if events is not None:
-                events[i][4].record(st)
+                events[i][3].record(st)
             L.lp_raster_bwd(ca, rend.cfg, fa, dL[i], st)
             if events is not None:
-                events[i][5].record(st)
+                events[i][4].record(st)
             render._store_back([rend.frames[i]], fa)
             fa_all[i] = rend.frames[i].c
         # preprocess backward fused over this rank's views (feature + SH gradients written once)
         L.lp_preprocess_bwd(ds.prims, ca_all, rend.cfg, fa_all, ds.grads, st)
-        if events is not None:
-            events[n_local][0].record(st)
+        if S is not None:
+            S[2].record(st)
         if world > 1:
             train.allreduce_gradients(ds.grad, world)
-        if events is not None:
-            events[n_local][1].record(st)
+        if S is not None:
+            S[3].record(st)
         L.lp_adam_step(ds.flat, ds.grad, m, v, groups, 0.9, 0.999, 1e-15, si + 1, st, zero_grad=True)
-        if events is not None:
-            events[n_local][2].record(st)
+        if S is not None:
+            S[4].record(st)
 
     def barrier():
         if world > 1:
@@ -245,8 +252,8 @@ def run_ours(args, rank, world, local_rank):
 
     vis = [s for s in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if s.strip().isdigit()]
     clocks = ClockSampler(int(vis[local_rank]) if local_rank < len(vis) else local_rank)
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(n_local)] + [
-        [torch.cuda.Event(enable_timing=True) for _ in range(3)]] for _ in range(args.steps)]
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(n_local)] + [
+        [torch.cuda.Event(enable_timing=True) for _ in range(5)]] for _ in range(args.steps)]
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     clocks.start()
@@ -269,16 +276,19 @@ def run_ours(args, rank, world, local_rank):
 
     # per-stage averages (ms per view-call) from the timed region's events
     stage = {nm: [] for nm in ev_names}
-    pb, ar, ad = [], [], []
+    pre, pb, ar, ad = [], [], [], []
     for k in range(args.steps):
         for i in range(n_local):
             e = evs[k][i]
             for j, nm in enumerate(ev_names):
                 stage[nm].append(e[j].elapsed_time(e[j + 1]))
-        pb.append(evs[k][n_local - 1][5].elapsed_time(evs[k][n_local][0]))
-        ar.append(evs[k][n_local][0].elapsed_time(evs[k][n_local][1]))
-        ad.append(evs[k][n_local][1].elapsed_time(evs[k][n_local][2]))
+        S = evs[k][n_local]
+        pre.append(S[0].elapsed_time(S[1]))
+        pb.append(evs[k][n_local - 1][4].elapsed_time(S[2]))
+        ar.append(S[2].elapsed_time(S[3]))
+        ad.append(S[3].elapsed_time(S[4]))
     stage_ms = {nm: statistics.mean(vals) for nm, vals in stage.items()}
+    stage_ms["pre_all_views"] = statistics.mean(pre)
     stage_ms["pbwd_all_views"] = statistics.mean(pb)
     stage_ms["allreduce"] = statistics.mean(ar)
     stage_ms["adam"] = statistics.mean(ad)
@@ -308,7 +318,7 @@ def run_ours(args, rank, world, local_rank):
         # fused over the rank's views: tiles_touched + rgrad per view, features read and feature
         # gradients read-modified-written once per call
         "pbwd_all_views": ("k_preprocess_bwd+k_sh_bwd", "hbm", 4 * n * n_local + vis * n_local * 4 * RG + n * 3 * Fb),
-        "pre": ("k_preprocess", "hbm", n * (Fb + 24) + vis * 4 * RW),
+        "pre_all_views": ("k_preprocess", "hbm", n * Fb + n_local * (n * 24 + vis * 4 * RW)),
         "adam": ("k_adam", "hbm", 32 * ds.flat.numel()),
     }
     rooflines = {}
@@ -322,7 +332,7 @@ def run_ours(args, rank, world, local_rank):
         rooflines[key] = {"kernel": kname, "bound": bound, "achieved": round(ach, 3), "peak": round(pk, 3),
                           "unit": unit, "frac": round(ach / pk, 4), "ms": round(stage_ms[key], 4),
                           "traffic": tr, "algorithmic_per_launch": int(amount)}
-    per_step = {k: stage_ms[k] * (1 if k in ("pbwd_all_views", "adam") else n_local) for k in work}
+    per_step = {k: stage_ms[k] * (1 if k in ("pbwd_all_views", "pre_all_views", "adam") else n_local) for k in work}
     dom = max(work, key=lambda k: per_step[k])        # the kernel with the largest share of the step
     for k in rooflines:
         rooflines[k]["ms_per_step"] = round(per_step[k], 4)
@@ -363,7 +373,7 @@ def run_ours(args, rank, world, local_rank):
                "ms_per_step": round(e2e_step, 3)}
 
     # + one fused preprocess backward and one Adam per step
-    launches = args.steps * (n_local * launches_per_view(n, rend.frames[0].c.tiles_x * rend.frames[0].c.tiles_y) + 2)
+    launches = args.steps * (n_local * launches_per_view(n, rend.frames[0].c.tiles_x * rend.frames[0].c.tiles_y) + 3)  # + K1, K5, Adam
 
     out = {
         "metric": "fwd+bwd Mpixel/s (C5 training step: 8 views, fwd+bwd+allreduce+Adam)",

@@ -169,9 +169,11 @@ lp_status lp_preprocess(const lp_prims *prims, const lp_camera *cams, int32_t n_
     cudaMemsetAsync(F.counters, 0, 4 * LP_NUM_COUNTERS, st);
     // the backward's raster-moment scratch is consumed once per preprocess
     cudaMemsetAsync(F.rgrad, 0, 4 * (size_t)F.rgrad_words * (F.n > 0 ? F.n : 1), st);
-    cudaMemsetAsync(F.tile_diff, 0, 4 * (size_t)(F.tiles_x + 1) * (F.tiles_y + 1), st);
-    launch_preprocess(*prims, cams[v], cfg->aa_kernel, F, st);
+    if (F.sort_method == LP_SORT_BUCKET)
+      cudaMemsetAsync(F.tile_diff, 0, 4 * (size_t)(F.tiles_x + 1) * (F.tiles_y + 1), st);
   }
+  // one launch per 8 views: each primitive's features are read once for all of them
+  launch_preprocess(*prims, cams, cfg->aa_kernel, frames, n_views, st);
   return last_error();
 }
 

@@ -8,7 +8,8 @@
 namespace lp {
 
 // K1 / K5 (lp_preprocess.cu)
-void launch_preprocess(const lp_prims &P, const lp_camera &cam, float kappa, const lp_frame &F, cudaStream_t st);
+void launch_preprocess(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
+                       cudaStream_t st);
 // fused over the views of one call (chunks of 8): feature / SH gradients written once per chunk
 void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
                            const lp_grads &G, cudaStream_t st);

@@ -43,10 +43,31 @@ __device__ __forceinline__ void sh_colour_fp32(const lp_prims &P, int i, const l
 // =============================================================================================
 // K1: features -> canonical geometry -> record, sigma (Eq. 1), SH colour
 // =============================================================================================
+// views preprocessed by one launch (features are read from HBM once, then L1/L2 for the others)
+constexpr int LP_PRE_MAXV = 8;
+struct PreViews {
+  lp_camera cam[LP_PRE_MAXV];
+  lp_frame frame[LP_PRE_MAXV];
+  int nv;
+};
+
 template <int KIND>
-__global__ void __launch_bounds__(256) k_preprocess(lp_prims P, lp_camera cam, float kappa, lp_frame F) {
+__device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_camera &cam, float kappa,
+                                                const lp_frame &F, int i);
+
+template <int KIND>
+__global__ void __launch_bounds__(256) k_preprocess(lp_prims P, float kappa, PreViews V) {
+  // view-interleaved grid: the nv consecutive blocks of one primitive range run the nv views, so
+  // the primitive features come from HBM once and from L2 for the other views
+  const int v = blockIdx.x % V.nv;
+  const int i = (blockIdx.x / V.nv) * blockDim.x + threadIdx.x;
+  preprocess_view<KIND>(P, V.cam[v], kappa, V.frame[v], i);
+}
+
+template <int KIND>
+__device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_camera &cam, float kappa,
+                                                const lp_frame &F, int i) {
   constexpr int K = Kind<KIND>::K, RW = Kind<KIND>::RW;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool inb = i < P.n;
   Geom g;
   float dh[4], q[4], c[3];
@@ -587,11 +608,21 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd(lp_prims P, float kappa, 
 }
 
 // ---------------------------------------------------------------------------------------------
-void launch_preprocess(const lp_prims &P, const lp_camera &cam, float kappa, const lp_frame &F, cudaStream_t st) {
-  if (P.n == 0) return;
+void launch_preprocess(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
+                       cudaStream_t st) {
+  if (P.n == 0 || n_views <= 0) return;
   const int grid = (P.n + 255) / 256;
-  if (P.kind == LP_OCTAHEDRON) k_preprocess<LP_OCTAHEDRON><<<grid, 256, 0, st>>>(P, cam, kappa, F);
-  else k_preprocess<LP_TETRAHEDRON><<<grid, 256, 0, st>>>(P, cam, kappa, F);
+  for (int v0 = 0; v0 < n_views; v0 += LP_PRE_MAXV) {
+    PreViews V;
+    V.nv = n_views - v0 < LP_PRE_MAXV ? n_views - v0 : LP_PRE_MAXV;
+    for (int v = 0; v < LP_PRE_MAXV; ++v) {
+      const int s = v0 + (v < V.nv ? v : 0);
+      V.cam[v] = cams[s];
+      V.frame[v] = frames[s];
+    }
+    if (P.kind == LP_OCTAHEDRON) k_preprocess<LP_OCTAHEDRON><<<grid * V.nv, 256, 0, st>>>(P, kappa, V);
+    else k_preprocess<LP_TETRAHEDRON><<<grid * V.nv, 256, 0, st>>>(P, kappa, V);
+  }
 }
 
 template <int KIND>

@@ -84,7 +84,7 @@ __device__ __forceinline__ int warp_sublist(const float4 *s_rec, int cnt, float 
 // =============================================================================================
 // K3 forward
 // =============================================================================================
-template <int KIND, int NT>
+template <int KIND, int NT, bool STATS>
 __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg, float *__restrict__ image) {
   using KD = Kind<KIND>;
   constexpr int RW = KD::RW, RW4 = RW / 4, PPT = 256 / NT;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         if (!test[k]) continue;
-        ++nbox;
+        if (STATS) ++nbox;
         int se, sx;
         const float ch = chord<KIND, false>(rec, fs(fx[k], rec[KD::CX]), fs(fy[k], rec[KD::CX + 1]), se, sx);
         if (ch > 0.f) {
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
           C[k][1] = fmaf(wgt, rec[KD::RGB + 1], C[k][1]);
           C[k][2] = fmaf(wgt, rec[KD::RGB + 2], C[k][2]);
           T[k] = T[k] * E;
-          ++nhit;
+          if (STATS) ++nhit;
           if (T[k] < cfg.t_stop) {       // include-then-stop (reading 9)
             done[k] = true;
             nproc[k] = b + (uint32_t)j - start + 1;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
     F.n_proc[p] = nproc[k];
     it += nproc[k];
   }
-  if (cfg.count_stats) {
+  if (STATS) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       it += __shfl_xor_sync(0xffffffffu, it, o);
@@ -397,8 +397,12 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(NT)) k_raster_bwd(lp_frame 
         }
         __syncwarp();
         if (lane < RG) {
-          float sum = 0.f;
-          for (unsigned m = hm; m; m &= m - 1) sum += s_red[w][__ffs(m) - 1][lane];
+          // independent predicated loads (no serial ffs/LDS chain), 4 partial sums
+          float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int l = 0; l < 32; ++l)
+            if ((hm >> l) & 1u) s4[l & 3] += s_red[w][l][lane];
+          const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
           if (sum != 0.f) atomicAdd(F.rgrad + (size_t)lane * F.n + id, sum);
         }
         __syncwarp();
@@ -428,8 +432,13 @@ static int nt_from_env(const char *name, int dflt) {
 template <int NT>
 static void fwd_nt(const lp_frame &F, const lp_raster_cfg &cfg, float *image, cudaStream_t st) {
   const int tiles = F.tiles_x * F.tiles_y;
-  if (F.kind == LP_OCTAHEDRON) k_raster_fwd<LP_OCTAHEDRON, NT><<<tiles, NT, 0, st>>>(F, cfg, image);
-  else k_raster_fwd<LP_TETRAHEDRON, NT><<<tiles, NT, 0, st>>>(F, cfg, image);
+  if (cfg.count_stats) {
+    if (F.kind == LP_OCTAHEDRON) k_raster_fwd<LP_OCTAHEDRON, NT, true><<<tiles, NT, 0, st>>>(F, cfg, image);
+    else k_raster_fwd<LP_TETRAHEDRON, NT, true><<<tiles, NT, 0, st>>>(F, cfg, image);
+  } else {
+    if (F.kind == LP_OCTAHEDRON) k_raster_fwd<LP_OCTAHEDRON, NT, false><<<tiles, NT, 0, st>>>(F, cfg, image);
+    else k_raster_fwd<LP_TETRAHEDRON, NT, false><<<tiles, NT, 0, st>>>(F, cfg, image);
+  }
 }
 
 template <int NT>
