@@ -31,7 +31,8 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
         nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-        cmd = [nvcc] + NVCC_FLAGS + ["-o", LIB + ".tmp"] + sources()
+        extra = os.environ.get("LP_EXTRA_NVCC_FLAGS", "").split()   # measurement variants only
+        cmd = [nvcc] + NVCC_FLAGS + extra + ["-o", LIB + ".tmp"] + sources()
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

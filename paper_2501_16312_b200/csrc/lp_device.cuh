@@ -409,11 +409,24 @@ __device__ __forceinline__ bool in_bbox(const float4 &bb, float px, float py) {
   return fabsf(px - bb.x) <= bb.z && fabsf(py - bb.y) <= bb.w;
 }
 
+// MUFU approximations without the denormal range fix-ups (arguments and results stay normal here)
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // opacity transmittance factor E = exp(-sigma chord); identical in forward and backward.
 // sigma*chord is capped at 80 so E stays a normal fp32 (>= 1.8e-35) and the backward can divide
-// by it; the cap changes o by < 1e-34.
+// by it (T / E = T * rcp_ftz(E)); the cap changes o by < 1e-34.  Same value as __expf (which is
+// ex2.approx of x log2 e) minus its denormal-result handling, never needed above 2^-116.
 __device__ __forceinline__ float transmit(float sigma, float chord) {
-  return __expf(-fminf(fm(sigma, chord), 80.f));
+  return ex2_ftz(fm(-fminf(fm(sigma, chord), 80.f), 1.44269504f));
 }
 
 }  // namespace lp

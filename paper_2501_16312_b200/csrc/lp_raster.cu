@@ -9,8 +9,8 @@
 //
 // Backward: the same lists in reverse.  Per (pixel, entry) with chord > 0 it recovers T_k = T/E,
 // runs the blend backward and the chord backward (App. E, in slab/plane
-// moment form), accumulates <= 22 moments per thread, then a warp transpose-reduce (24 SHFL)
-// and one RED.F32 per moment per (warp, primitive) into rgrad[moment][n].
+// moment form), accumulates <= 22 moments per thread, then a shared-memory column sum over the
+// hit lanes and one RED.F32 per moment per (warp, primitive) into rgrad[moment][n].
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -79,7 +79,26 @@ __device__ __forceinline__ int warp_sublist(const float4 *s_rec, int cnt, float 
 #ifndef LP_BWD_BLOCKS
 #define LP_BWD_BLOCKS 8
 #endif
-#define BWD_MIN_BLOCKS(nt) ((nt) == 128 ? LP_BWD_BLOCKS : 1)
+// (tetrahedra: 29.7 KB of shared memory per CTA fits 7 per SM, so ask for 7)
+#define BWD_MIN_BLOCKS(kind, nt) ((nt) == 128 ? ((kind) == LP_OCTAHEDRON ? LP_BWD_BLOCKS : 7) : 1)
+
+#ifdef LP_BWD_STATS
+// measurement build only (-DLP_BWD_STATS): warp-level event counts of the backward
+// [0] sublist records, [1] records with a lane in bbox, [2] records with a hit lane, [3] sum of hit lanes,
+// [5] in-bbox lane tests
+__device__ unsigned long long g_bwd_stats[8];
+extern "C" int lp_debug_bwd_stats(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, g_bwd_stats, sizeof(g_bwd_stats));
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_bwd_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#define BWD_STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_bwd_stats[i], (unsigned long long)(v)); } while (0)
+#else
+#define BWD_STAT(i, v) do { } while (0)
+#endif
 
 // =============================================================================================
 // K3 forward
@@ -209,59 +228,14 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
 }
 
 // =============================================================================================
-// warp transpose-reduce: every lane holds N partials; afterwards lane l holds the warp sum of
-// partial idx(l) (valid when `valid`).  5 steps, sum_l ceil(N_l / 2) shuffles.
-// =============================================================================================
-template <int N, int OFF>
-__device__ __forceinline__ void tr_step(const float (&in)[N], float (&out)[(N + 1) / 2], bool upper) {
-  constexpr int H = (N + 1) / 2;
-#pragma unroll
-  for (int i = 0; i < H; ++i) {
-    const float lo = in[i];
-    const float hi = (i + H < N) ? in[i + H] : 0.f;
-    const float send = upper ? lo : hi;
-    const float keep = upper ? hi : lo;
-    out[i] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);
-  }
-}
-
-template <int N>
-__device__ __forceinline__ float warp_transpose_reduce(const float (&a)[N], int lane, int &idx, bool &valid) {
-  constexpr int N1 = (N + 1) / 2, N2 = (N1 + 1) / 2, N3 = (N2 + 1) / 2, N4 = (N3 + 1) / 2;
-  float b1[N1], b2[N2], b3[N3], b4[N4], b5[(N4 + 1) / 2];
-  tr_step<N, 16>(a, b1, lane & 16);
-  tr_step<N1, 8>(b1, b2, lane & 8);
-  tr_step<N2, 4>(b2, b3, lane & 4);
-  tr_step<N3, 2>(b3, b4, lane & 2);
-  tr_step<N4, 1>(b4, b5, lane & 1);
-  // which partial did this lane end up with?
-  const int Ns[5] = {N, N1, N2, N3, N4};
-  int base = 0, size = N;
-#pragma unroll
-  for (int s = 0; s < 5; ++s) {
-    const int Hs = (Ns[s] + 1) / 2;
-    if (lane & (16 >> s)) {
-      base += Hs;
-      size -= Hs;
-    } else {
-      size = size < Hs ? size : Hs;
-    }
-  }
-  idx = base;
-  valid = size >= 1;
-  return b5[0];
-}
-
-// =============================================================================================
 // K4 backward
 // =============================================================================================
 template <int KIND, int NT>
-__global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(NT)) k_raster_bwd(lp_frame F, lp_raster_cfg cfg,
+__global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_frame F, lp_raster_cfg cfg,
                                                                       const float *__restrict__ dL) {
   using KD = Kind<KIND>;
   constexpr int RW = KD::RW, RW4 = RW / 4, PPT = 256 / NT, RG = KD::RG;
   constexpr int RGP = RG == 20 ? 20 : 28;      // padded row: 16-byte stores, conflict-free (RGP/4 odd)
-  constexpr int SMEM_RED_MAX = 16;             // <= 16 hit lanes: shared-memory column sums beat the shuffles
   __shared__ float4 s_rec[NT * RW4];
   __shared__ unsigned char s_list[NT / 32][NT];
   __shared__ __align__(16) float s_red[NT / 32][32][RGP];
@@ -322,6 +296,7 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(NT)) k_raster_bwd(lp_frame 
     if (!__any_sync(0xffffffffu, act)) continue;
     const int w = threadIdx.x >> 5;
     const int nl = warp_sublist<NT, RW4>(s_rec, (int)(bend - bstart), wx0, wx1, wy0, wy1, s_list[w]);
+    BWD_STAT(0, nl);
 
     for (int q = nl - 1; q >= 0; --q) {
       const int j = s_list[w][q];
@@ -335,6 +310,14 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(NT)) k_raster_bwd(lp_frame 
         any = any || test[k];
       }
       if (!__any_sync(0xffffffffu, any)) continue;
+      BWD_STAT(1, 1);
+#ifdef LP_BWD_STATS
+      {
+        unsigned nb = 0;
+        for (int k = 0; k < PPT; ++k) nb += __popc(__ballot_sync(0xffffffffu, test[k]));
+        BWD_STAT(5, nb);
+      }
+#endif
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
       float acc[RGP];
 #pragma unroll
@@ -351,7 +334,7 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(NT)) k_raster_bwd(lp_frame 
         const float sig = rec[KD::SIGMA];
         const float E = transmit(sig, ch);
         const float o = 1.f - E;
-        const float Tk = __fdividef(T[k], E);             // transmittance in front of this entry
+        const float Tk = T[k] * rcp_ftz(E);               // transmittance in front of this entry
         float dLdo = 0.f;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -384,37 +367,38 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(NT)) k_raster_bwd(lp_frame 
           }
         }
       }
-      // per-(warp, primitive) reduction of the <= 22 moments, one RED.F32 per moment
+      // per-(warp, primitive) reduction of the <= 22 moments, one RED.F32 per moment: the hit
+      // lanes stage their moments in compacted shared-memory rows, lane m < RG sums column m
+      // over the h rows (2 instructions per row, 4 independent partial sums)
       const unsigned hm = __ballot_sync(0xffffffffu, hit);
       if (!hm) continue;
+      BWD_STAT(2, 1);
+      BWD_STAT(3, __popc(hm));
       const uint32_t id = s_id[j];
-      if (__popc(hm) <= SMEM_RED_MAX) {
-        // few hit lanes: stage their moments in shared memory, lane m sums column m
-        float4 *row = reinterpret_cast<float4 *>(&s_red[w][lane][0]);
-        if (hit) {
+      const int h = __popc(hm);
+      if (hit) {
+        float4 *row = reinterpret_cast<float4 *>(&s_red[w][__popc(hm & ((1u << lane) - 1u))][0]);
 #pragma unroll
-          for (int a = 0; a < RGP / 4; ++a) row[a] = make_float4(acc[4 * a], acc[4 * a + 1], acc[4 * a + 2], acc[4 * a + 3]);
-        }
-        __syncwarp();
-        if (lane < RG) {
-          // independent predicated loads (no serial ffs/LDS chain), 4 partial sums
-          float s4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int l = 0; l < 32; ++l)
-            if ((hm >> l) & 1u) s4[l & 3] += s_red[w][l][lane];
-          const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-          if (sum != 0.f) atomicAdd(F.rgrad + (size_t)lane * F.n + id, sum);
-        }
-        __syncwarp();
-      } else {
-        int idx;
-        bool valid;
-        float acc_r[RG];
-#pragma unroll
-        for (int a = 0; a < RG; ++a) acc_r[a] = acc[a];
-        const float val = warp_transpose_reduce<RG>(acc_r, lane, idx, valid);
-        if (valid && val != 0.f) atomicAdd(F.rgrad + (size_t)idx * F.n + id, val);
+        for (int a = 0; a < RGP / 4; ++a) row[a] = make_float4(acc[4 * a], acc[4 * a + 1], acc[4 * a + 2], acc[4 * a + 3]);
       }
+      __syncwarp();
+      if (lane < RG) {
+        const float *col = &s_red[w][0][lane];
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        int q = 0;
+        for (; q + 4 <= h; q += 4) {
+          s0 += col[(q + 0) * RGP];
+          s1 += col[(q + 1) * RGP];
+          s2 += col[(q + 2) * RGP];
+          s3 += col[(q + 3) * RGP];
+        }
+        if (q + 0 < h) s0 += col[(q + 0) * RGP];
+        if (q + 1 < h) s1 += col[(q + 1) * RGP];
+        if (q + 2 < h) s2 += col[(q + 2) * RGP];
+        const float sum = (s0 + s1) + (s2 + s3);
+        if (sum != 0.f) atomicAdd(F.rgrad + (size_t)lane * F.n + id, sum);
+      }
+      __syncwarp();
     }
   }
 }
