@@ -4,8 +4,9 @@
 Workload (BASELINE.json configs[4], the config its metric "fwd+bwd Mpixel/s and train iters/s at
 1/2/4/8 B200" is quoted on): 1M octahedra, SH degree 3, a batch of 8 views at 1600x1060, one
 training step = one lp_preprocess over all local views; for each local view lp_bin_sort ->
-lp_render_fwd -> lp_l1_grad -> lp_raster_bwd; one lp_preprocess_bwd over all local views; then (N > 1) one NCCL allreduce of the flat gradient; then
-one fused Adam (lp_adam_step, also zeroing the gradient).  Views are sharded views[r::N] over
+lp_render_fwd -> lp_l1_grad -> lp_raster_bwd (views spread over --streams CUDA streams); one
+lp_preprocess_bwd over all local views; then (N > 1) one NCCL allreduce of the flat gradient;
+then one fused Adam (lp_adam_step, also zeroing the gradient).  Views are sharded views[r::N] over
 ranks (strong scaling, fixed global batch of 8).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -45,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--streams", type=int, default=2, help="CUDA streams the views of a step are spread over")
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop (ncu --profile-from-start off) and exit")
     return ap.parse_args()
@@ -188,48 +190,61 @@ def run_ours(args, rank, world, local_rank):
     ev_names = ["sort", "fwd", "l1", "rbwd"]           # per view
     fa_all = render.frames_array(rend.frames)
     ca_all = rend._cams(list(range(n_local)))
+    fa_view = [render.frames_array([rend.frames[i]]) for i in range(n_local)]
+    ca_view = [rend._cams([i]) for i in range(n_local)]
+    # views run round-robin on `--streams` CUDA streams so one view's sort kernels overlap another
+    # view's raster (views are independent between the fused preprocess and preprocess backward)
+    n_str = max(1, min(args.streams, n_local))
+    streams = [st] + [torch.cuda.Stream(dev) for _ in range(n_str - 1)]
+    fork = torch.cuda.Event()
+    joins = [torch.cuda.Event() for _ in streams[1:]]
 
-    def step(si, events=None):
+    def rec(evl, j, stream):
+        if evl is not None:
+            evl[j].record(stream)
+
+    def step(si, events=None, tgt=None, serial=False):
+        tg = targets if tgt is None else tgt
         S = events[n_local] if events is not None else None
         # preprocess of all local views in one launch (each primitive's features read once)
-        if S is not None:
-            S[0].record(st)
+        rec(S, 0, st)
         for i in range(n_local):
-            fa_all[i] = rend.frames[i].c
+            fa_all[i] = fa_view[i][0]
         L.lp_preprocess(ds.prims, ca_all, rend.cfg, fa_all, st)
-        render._store_back(rend.frames, fa_all)
-        if S is not None:
-            S[1].record(st)
         for i in range(n_local):
-            ca = rend._cams([i])
-            fa = render.frames_array([rend.frames[i]])
-            if events is not None:
-                events[i][0].record(st)
-            L.lp_bin_sort(ca, fa, st, None)
-            if events is not None:
-                events[i][1].record(st)
-            L.lp_render_fwd(ca, rend.cfg, fa, img[i], st)
-            if events is not None:
-                events[i][2].record(st)
-            L.lp_l1_grad(img[i], targets[i], dL[i], loss_buf[si:si + 1], scale, st)
-            if events is not None:
-                events[i][3].record(st)
-            L.lp_raster_bwd(ca, rend.cfg, fa, dL[i], st)
-            if events is not None:
-                events[i][4].record(st)
-            render._store_back([rend.frames[i]], fa)
-            fa_all[i] = rend.frames[i].c
+            fa_view[i][0] = fa_all[i]
+        rec(S, 1, st)
+        strs = [st] if serial else streams
+        if len(strs) > 1:
+            fork.record(st)
+            for s_ in strs[1:]:
+                s_.wait_event(fork)
+        for i in range(n_local):
+            sx = strs[i % len(strs)]
+            ca, fa = ca_view[i], fa_view[i]
+            ev = events[i] if events is not None else None
+            rec(ev, 0, sx)
+            L.lp_bin_sort(ca, fa, sx, None)
+            rec(ev, 1, sx)
+            L.lp_render_fwd(ca, rend.cfg, fa, img[i], sx)
+            rec(ev, 2, sx)
+            L.lp_l1_grad(img[i], tg[i], dL[i], loss_buf[si:si + 1], scale, sx)
+            rec(ev, 3, sx)
+            L.lp_raster_bwd(ca, rend.cfg, fa, dL[i], sx)
+            rec(ev, 4, sx)
+            fa_all[i] = fa[0]
+        if len(strs) > 1:
+            for j, s_ in enumerate(strs[1:]):
+                joins[j].record(s_)
+                st.wait_event(joins[j])
         # preprocess backward fused over this rank's views (feature + SH gradients written once)
         L.lp_preprocess_bwd(ds.prims, ca_all, rend.cfg, fa_all, ds.grads, st)
-        if S is not None:
-            S[2].record(st)
+        rec(S, 2, st)
         if world > 1:
             train.allreduce_gradients(ds.grad, world)
-        if S is not None:
-            S[3].record(st)
+        rec(S, 3, st)
         L.lp_adam_step(ds.flat, ds.grad, m, v, groups, 0.9, 0.999, 1e-15, si + 1, st, zero_grad=True)
-        if S is not None:
-            S[4].record(st)
+        rec(S, 4, st)
 
     def barrier():
         if world > 1:
@@ -262,7 +277,7 @@ def run_ours(args, rank, world, local_rank):
     wall0 = time.perf_counter()
     t0.record(st)
     for k in range(args.steps):
-        step(args.warmup + k, evs[k])
+        step(args.warmup + k)
     t1.record(st)
     barrier()
     wall = time.perf_counter() - wall0
@@ -274,7 +289,12 @@ def run_ours(args, rank, world, local_rank):
     ms_max = float(ms_t.item())
     ms_step = ms_max / args.steps
 
-    # per-stage averages (ms per view-call) from the timed region's events
+    # per-stage averages (ms per view-call): an attribution region of the same K steps run with the
+    # views serialised on one stream and CUDA events around every stage
+    barrier()
+    for k in range(args.steps):
+        step(args.warmup + k, evs[k], serial=True)
+    barrier()
     stage = {nm: [] for nm in ev_names}
     pre, pb, ar, ad = [], [], [], []
     for k in range(args.steps):
@@ -292,6 +312,7 @@ def run_ours(args, rank, world, local_rank):
     stage_ms["pbwd_all_views"] = statistics.mean(pb)
     stage_ms["allreduce"] = statistics.mean(ar)
     stage_ms["adam"] = statistics.mean(ad)
+    serial_step_ms = statistics.mean(evs[k][n_local][0].elapsed_time(evs[k][n_local][4]) for k in range(args.steps))
 
     # rooflines of the single-kernel stages; the dominant one is reported as "roofline"
     kind = ds.kind
@@ -301,7 +322,7 @@ def run_ours(args, rank, world, local_rank):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     alu_peak = 148 * 128 * 1965.0 * 1e6 / 1e12                          # T FP32 lane-instr/s at max SM clock
     K = ds.K
-    RG, RW = (20, 20) if kind == 0 else (22, 24)
+    RG, RW = (20, 20) if kind == 0 else (22, 28)
     ncoef = (ds.sh_degree + 1) ** 2
     Fb = 4 * (3 + 4 + K + 1 + 3 * ncoef)                                # feature bytes per primitive
     vis = statistics.mean([int(s[L.LP_CNT_VISIBLE]) for s in stats])
@@ -345,32 +366,56 @@ def run_ours(args, rank, world, local_rank):
     # ---------------- e2e: host (pinned) targets copied in and the loss read back every step
     e2e = None
     if not args.no_e2e:
+        # every step: H2D of that step's targets from pinned memory (prefetched one step ahead on a
+        # copy stream into a double buffer) and a D2H read of that step's loss (pinned ring; the host
+        # waits for step k's loss while step k+1 is already queued)
         host_t = torch.empty(targets.shape, dtype=torch.float32, pin_memory=True)
         host_t.copy_(targets)
-        dev_t = torch.empty_like(targets)
-        loss_host = torch.empty(1, dtype=torch.float32, pin_memory=True)
+        dev_t = [torch.empty_like(targets), torch.empty_like(targets)]
+        cp = torch.cuda.Stream(dev)
+        copied = [torch.cuda.Event(), torch.cuda.Event()]
+        freed = [torch.cuda.Event(), torch.cuda.Event()]
+        loss_host = torch.zeros(args.steps, dtype=torch.float32, pin_memory=True)
+        read = [torch.cuda.Event() for _ in range(args.steps)]
+        base = total_steps
+        loss_buf.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         barrier()
         e0.record(st)
+        cp.wait_stream(st)
+        with torch.cuda.stream(cp):
+            dev_t[0].copy_(host_t, non_blocking=True)
+        copied[0].record(cp)
+        losses = []
         for k in range(args.steps):
-            dev_t.copy_(host_t, non_blocking=True)
-            targets_saved = targets
-            targets = dev_t
-            step(total_steps + k if total_steps + k < loss_buf.numel() else 0)
-            targets = targets_saved
-            loss_host.copy_(loss_buf[(total_steps + k) % loss_buf.numel():][:1], non_blocking=True)
-            st.synchronize()
+            b = k & 1
+            if k + 1 < args.steps:
+                cp.wait_event(freed[1 - b]) if k >= 1 else None
+                with torch.cuda.stream(cp):
+                    dev_t[1 - b].copy_(host_t, non_blocking=True)
+                copied[1 - b].record(cp)
+            st.wait_event(copied[b])
+            step(base + k, tgt=dev_t[b])
+            freed[b].record(st)
+            loss_host[k:k + 1].copy_(loss_buf[base + k:base + k + 1], non_blocking=True)
+            read[k].record(st)
+            if k >= 1:
+                read[k - 1].synchronize()
+                losses.append(float(loss_host[k - 1]))
         e1.record(st)
+        read[args.steps - 1].synchronize()
+        losses.append(float(loss_host[args.steps - 1]))
         barrier()
         e2e_ms = e0.elapsed_time(e1)
         t = torch.tensor([e2e_ms], device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_step = float(t.item()) / args.steps
+        assert all(math.isfinite(x) for x in losses)
         e2e = {"value": round(mpix / (e2e_step * 1e-3), 3), "unit": "Mpixel/s",
                "h2d_bytes_per_step": int(host_t.numel() * 4 * world), "d2h_bytes_per_step": 4 * world,
-               "ms_per_step": round(e2e_step, 3)}
+               "ms_per_step": round(e2e_step, 3), "loss_last": losses[-1]}
 
     # + one fused preprocess backward and one Adam per step
     launches = args.steps * (n_local * launches_per_view(n, rend.frames[0].c.tiles_x * rend.frames[0].c.tiles_y) + 3)  # + K1, K5, Adam
@@ -390,7 +435,9 @@ def run_ours(args, rank, world, local_rank):
                    "intersected_pairs_per_px": round(X_tot / (n_local * W * H), 2),
                    "in_bbox_pairs_per_px": round(B_tot / (n_local * W * H), 2),
                    "frustum_primitives_per_view": frustum, "capacity": caps},
+        "streams": n_str,
         "stages_ms_per_view": {k: round(v, 4) for k, v in stage_ms.items()},
+        "serial_step_ms": round(serial_step_ms, 3),
         "roofline": dict(rooflines[dom], peak_source="measured HBM copy (MEASURED_PEAKS.json)" if
                          work[dom][1] == "hbm" else "148 SM x 128 FP32 lanes x 1965 MHz (B200_PROFILING unit counts)"),
         "rooflines": rooflines,
