@@ -185,6 +185,9 @@ class RenderOut:
     dsigma: np.ndarray = None
     drgb: np.ndarray = None
     face_margin: np.ndarray = None
+    depth: np.ndarray = None       # depth mode: entry distance at cumulative opacity > 0.5, else 0
+    m_depth: np.ndarray = None     # min |ln(T_after / 0.5)| over the pixel's hits
+    alpha: np.ndarray = None       # alpha mode: 1 - T_final
 
 
 def render(scene: Scene, cam, pre: Pre, vals, ranges, bg=(0.0, 0.0, 0.0), t_stop=1e-3,
@@ -199,7 +202,8 @@ def render(scene: Scene, cam, pre: Pre, vals, ranges, bg=(0.0, 0.0, 0.0), t_stop
     cfg.brute = 1 if brute else 0
     out = RenderOut(image=np.zeros((3, H, W), np.float64), T_final=np.zeros((H, W), np.float64),
                     n_proc=np.zeros((H, W), np.int32), m_stop=np.full((H, W), np.inf),
-                    m_face=np.full((H, W), np.inf), counters=np.zeros(2, np.int64))
+                    m_face=np.full((H, W), np.inf), counters=np.zeros(2, np.int64),
+                    depth=np.zeros((H, W), np.float64), m_depth=np.full((H, W), np.inf))
     pix_a = None if pix is None else np.ascontiguousarray(pix, np.int32)
     npix = 0 if pix_a is None else pix_a.shape[0]
     g = None
@@ -219,8 +223,10 @@ def render(scene: Scene, cam, pre: Pre, vals, ranges, bg=(0.0, 0.0, 0.0), t_stop
                           C.c_void_p(_ptr(out.m_face)), C.c_void_p(_ptr(g)),
                           C.c_void_p(_ptr(out.dv)), C.c_void_p(_ptr(out.dsigma)),
                           C.c_void_p(_ptr(out.drgb)), C.c_void_p(_ptr(out.face_margin)),
-                          C.c_void_p(_ptr(out.counters)))
+                          C.c_void_p(_ptr(out.counters)), C.c_void_p(_ptr(out.depth)),
+                          C.c_void_p(_ptr(out.m_depth)))
     assert rc == 0
+    out.alpha = 1.0 - out.T_final
     return out
 
 

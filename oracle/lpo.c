@@ -365,7 +365,8 @@ typedef struct {
 
 static void primitive_hit(int kind, const double *geo, double rx, double ry, double *chord,
                           int *f_in, double *u_in, double *v_in, double *d_in,
-                          int *f_out, double *u_out, double *v_out, double *d_out, int *nhits)
+                          int *f_out, double *u_out, double *v_out, double *d_out, int *nhits,
+                          double *entry)
 {
   double V[6][3];
   vertices(kind, geo, V);
@@ -384,6 +385,7 @@ static void primitive_hit(int kind, const double *geo, double rx, double ry, dou
   *nhits = cnt;
   /* reading 4: chord = max - min over all hits if >= 2 hits, else 0 */
   *chord = cnt >= 2 ? hi - lo : 0.0;
+  *entry = lo;   /* i1, the entry depth */
 }
 
 static void add_face_grad(int kind, const double *geo, int f, double u, double v, double d,
@@ -425,7 +427,7 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
                const lpo_render_cfg *cfg, const int32_t *pix, int64_t npix,
                double *image, double *T_final, int32_t *n_proc, double *m_stop, double *m_face,
                const float *dL_dimage, double *dv, double *dsigma, double *drgb,
-               double *face_margin, int64_t *counters)
+               double *face_margin, int64_t *counters, double *depth, double *m_depth)
 {
   const int W = cam->width, H = cam->height, gx = (W + LPO_TILE - 1) / LPO_TILE;
   const int kind = s->kind, K = noffs(kind), G = 3 + 3 * K, NV = nverts(kind);
@@ -463,7 +465,8 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
         list = sorted_vals + ranges[2 * t];
         cnt = ranges[2 * t + 1] - ranges[2 * t];
       }
-      double T = 1.0, C[3] = {0, 0, 0}, ms = DBL_MAX, mf = DBL_MAX;
+      double T = 1.0, C[3] = {0, 0, 0}, ms = DBL_MAX, mf = DBL_MAX, dep = 0.0, md = DBL_MAX;
+      int dep_set = 0;
       int64_t nh = 0, np = 0;
       for (int64_t e = 0; e < cnt; ++e) {
         int i = (int)list[e];
@@ -471,8 +474,9 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
         const double *geo = pre->geom + (size_t)i * G;
         double chord, u_in = 0, v_in = 0, d_in = 1, u_out = 0, v_out = 0, d_out = 1;
         int f_in = 0, f_out = 0, nhit;
+        double i1;
         primitive_hit(kind, geo, rx, ry, &chord, &f_in, &u_in, &v_in, &d_in, &f_out, &u_out,
-                      &v_out, &d_out, &nhit);
+                      &v_out, &d_out, &nhit, &i1);
         if (!(chord > 0.0)) continue;
         /* opacity from the chord, App. E */
         double sig = pre->sigma[i];
@@ -489,6 +493,12 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
         /* front-to-back compositing */
         for (int ch = 0; ch < 3; ++ch) C[ch] += T * o * pre->rgb[(size_t)i * 3 + ch];
         T *= E;
+        /* depth mode: first primitive after which cumulative opacity 1 - T > 0.5 */
+        {
+          double m = fabs(log(T / 0.5));
+          if (m < md) md = m;
+          if (!dep_set && 1.0 - T > 0.5) { dep = i1; dep_set = 1; }
+        }
         if (cfg->t_stop > 0.0f) {
           double m = fabs(log(T / (double)cfg->t_stop));
           if (m < ms) ms = m;
@@ -503,6 +513,8 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
       if (n_proc) n_proc[p] = (int32_t)np;
       if (m_stop) m_stop[p] = ms;
       if (m_face) m_face[p] = mf;
+      if (depth) depth[p] = dep;
+      if (m_depth) m_depth[p] = md;
 
       if (dL_dimage) {
         /* blend backward: S = colour behind k incl. background */

@@ -93,13 +93,19 @@ typedef struct {
  * Backward (dL_dimage != NULL): accumulates (+=) into
  *   dv[n][V][3] (ray-space vertex gradients, V = 6 octa / 4 tetra), dsigma[n], drgb[n][3];
  *   face_margin[n] receives min barycentric over the primitive's hit faces (min-accumulate).
- * counters[2] (+=): iterated pairs, intersected pairs.  Returns 0 or -1. */
+ * counters[2] (+=): iterated pairs, intersected pairs.
+ * Depth mode (App. B "distance to the first primitive along the viewing ray where
+ * cumulative opacity exceeds 0.5"): depth[H][W] = entry distance i1 (ray-space z of the entry
+ * hit, whose scale is the camera distance |p|) of the first composited primitive after which
+ * 1 - T > 0.5, else 0 (the invalid marker, reading 24); m_depth[H][W] = min over the pixel's
+ * hits of |ln(T_after / 0.5)| (how far the 0.5 decision is from flipping).  Either may be NULL.
+ * Returns 0 or -1. */
 int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
                const uint32_t *sorted_vals, const int64_t *ranges,
                const lpo_render_cfg *cfg, const int32_t *pix, int64_t npix,
                double *image, double *T_final, int32_t *n_proc, double *m_stop, double *m_face,
                const float *dL_dimage, double *dv, double *dsigma, double *drgb,
-               double *face_margin, int64_t *counters);
+               double *face_margin, int64_t *counters, double *depth, double *m_depth);
 
 /* Chain ray-space gradients to the world features (+= into SoA fp64 gradients with the
  * same layout as the features).  Primitives with flag != 0 receive nothing. */
