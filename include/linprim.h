@@ -171,6 +171,15 @@ lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, 
 lp_status lp_render_fwd(const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg,
                         lp_frame *frames, float *image, void *stream);
 
+/* lp_render_fwd plus the depth and alpha render modes, from the same pass:
+ * depth (App. B): per pixel the entry distance i1 (ray-space, i.e. camera distance
+ *   |p| of the centre plus the entry offset along the ray) of the FIRST composited primitive
+ *   after which the cumulative opacity 1 - T exceeds 0.5; 0 where it never does (#24).
+ * alpha: 1 - T_final.
+ * depth, alpha: device [n_views][H][W] fp32 or NULL (each independently). */
+lp_status lp_render_fwd_aux(const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg,
+                            lp_frame *frames, float *image, float *depth, float *alpha, void *stream);
+
 /* a10-a12 (App. E): reverse replay of each tile list, blend backward,
  * chord -> entry/exit -> slab/plane moments reduced per (warp, primitive) -> rgrad, then the
  * preprocess backward to world features (+= into grads).  Requires the frames filled by

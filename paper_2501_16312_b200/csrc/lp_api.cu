@@ -247,18 +247,25 @@ lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, 
   return status != LP_OK ? status : e;
 }
 
-lp_status lp_render_fwd(const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg, lp_frame *frames,
-                        float *image, void *stream) {
+lp_status lp_render_fwd_aux(const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg, lp_frame *frames,
+                            float *image, float *depth, float *alpha, void *stream) {
   if (!cams || !cfg || !frames || !image || n_views < 0) return LP_ERR_ARG;
   for (int v = 0; v < n_views; ++v)
     if (!valid_cam(cams[v]) || !frame_matches(frames[v], cams[v]) || !frames[v].sorted_val) return LP_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   size_t off = 0;
   for (int v = 0; v < n_views; ++v) {
-    launch_raster_fwd(frames[v], *cfg, image + off, st);
-    off += (size_t)3 * cams[v].width * cams[v].height;
+    const size_t hw = (size_t)cams[v].width * cams[v].height;
+    launch_raster_fwd(frames[v], *cfg, image + 3 * off, depth ? depth + off : nullptr, alpha ? alpha + off : nullptr,
+                      st);
+    off += hw;
   }
   return last_error();
+}
+
+lp_status lp_render_fwd(const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg, lp_frame *frames,
+                        float *image, void *stream) {
+  return lp_render_fwd_aux(cams, n_views, cfg, frames, image, nullptr, nullptr, stream);
 }
 
 lp_status lp_render_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg,

@@ -403,6 +403,27 @@ __device__ __forceinline__ float chord(const float *rec, float dx, float dy, int
   return tetra_chord<TRACK>(rec, dx, dy, se, sx);
 }
 
+// entry offset max_s(entry_s) along the ray relative to the ray-space centre depth l (depth mode,
+// P:840-841): the same slab / plane values as chord(), so entry + l is the entry distance i1.
+template <int KIND>
+__device__ __forceinline__ float entry_offset(const float *rec, float dx, float dy) {
+  if (KIND == LP_OCTAHEDRON) {
+    constexpr int B = Kind<LP_OCTAHEDRON>::SLAB;
+    float en = fs(__fmaf_rn(rec[B], dx, fm(rec[B + 1], dy)), rec[B + 2]);
+#pragma unroll
+    for (int s = 1; s < 4; ++s)
+      en = fmaxf(en, fs(__fmaf_rn(rec[B + 3 * s], dx, fm(rec[B + 1 + 3 * s], dy)), rec[B + 2 + 3 * s]));
+    return en;
+  } else {
+    constexpr int B = Kind<LP_TETRAHEDRON>::SLAB;
+    float en = -3.402823466e38f;
+#pragma unroll
+    for (int s = 0; s < 3; ++s)
+      en = fmaxf(en, __fmaf_rn(rec[B + 2 + 3 * s], dy, __fmaf_rn(rec[B + 1 + 3 * s], dx, rec[B + 3 * s])));
+    return en;
+  }
+}
+
 // slack of the bbox reject test: a pair rejected by it has chord <= 0 (up to fp32 rounding of
 // the bbox itself, covered by the slack)
 __device__ __forceinline__ bool in_bbox(const float4 &bb, float px, float py) {

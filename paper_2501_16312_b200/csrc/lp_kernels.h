@@ -34,7 +34,9 @@ void launch_bucket(const lp_frame &F, cudaStream_t st);
 void launch_tile_sort(const lp_frame &F, cudaStream_t st);
 
 // K3 / K4 (lp_raster.cu)
-void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image, cudaStream_t st);
+// depth / alpha: optional [H][W] outputs (depth mode P:840-841, alpha = 1 - T_final), may be null
+void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image, float *depth, float *alpha,
+                       cudaStream_t st);
 void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL_dimage, cudaStream_t st);
 
 // C5 helpers (lp_train.cu)

@@ -103,8 +103,12 @@ extern "C" int lp_debug_bwd_stats(unsigned long long *out, int reset) {
 // =============================================================================================
 // K3 forward
 // =============================================================================================
-template <int KIND, int NT, bool STATS>
-__global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg, float *__restrict__ image) {
+// AUX: also the depth (entry distance of the first primitive after which the cumulative
+// opacity 1 - T exceeds 0.5, 0 if never; reading 24) and alpha (1 - T_final) images,
+// either pointer may be null.
+template <int KIND, int NT, bool STATS, bool AUX>
+__global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg, float *__restrict__ image,
+                                                   float *__restrict__ depth, float *__restrict__ alpha) {
   using KD = Kind<KIND>;
   constexpr int RW = KD::RW, RW4 = RW / 4, PPT = 256 / NT;
   __shared__ float4 s_rec[NT * RW4];
@@ -117,9 +121,9 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
   const int W = F.width, H = F.height;
   if (threadIdx.x < 3) s_stat[threadIdx.x] = 0ull;
 
-  float fx[PPT], fy[PPT], T[PPT], C[PPT][3];
+  float fx[PPT], fy[PPT], T[PPT], C[PPT][3], dep[PPT];
   uint32_t nproc[PPT];
-  bool done[PPT], inside[PPT];
+  bool done[PPT], inside[PPT], dset[PPT];
   uint32_t nhit = 0, nbox = 0;
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
@@ -134,6 +138,8 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
     C[k][0] = C[k][1] = C[k][2] = 0.f;
     done[k] = !inside[k];
     nproc[k] = end - start;
+    dep[k] = 0.f;
+    dset[k] = false;
   }
   float wx0, wx1, wy0, wy1;
   warp_rect<NT>(threadIdx.x >> 5, tx, ty, wx0, wx1, wy0, wy1);
@@ -172,7 +178,8 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
         if (!test[k]) continue;
         if (STATS) ++nbox;
         int se, sx;
-        const float ch = chord<KIND, false>(rec, fs(fx[k], rec[KD::CX]), fs(fy[k], rec[KD::CX + 1]), se, sx);
+        const float dx = fs(fx[k], rec[KD::CX]), dy = fs(fy[k], rec[KD::CX + 1]);
+        const float ch = chord<KIND, false>(rec, dx, dy, se, sx);
         if (ch > 0.f) {
           const float E = transmit(rec[KD::SIGMA], ch);
           const float o = 1.f - E;
@@ -181,6 +188,11 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
           C[k][1] = fmaf(wgt, rec[KD::RGB + 1], C[k][1]);
           C[k][2] = fmaf(wgt, rec[KD::RGB + 2], C[k][2]);
           T[k] = T[k] * E;
+          if (AUX && !dset[k] && T[k] < 0.5f) {      // cumulative opacity 1 - T > 0.5 (once per pixel)
+            dset[k] = true;
+            const uint32_t id = F.sorted_val[b + (uint32_t)j];
+            dep[k] = fa(__uint_as_float(F.depth_key[id]), entry_offset<KIND>(rec, dx, dy));
+          }
           if (STATS) ++nhit;
           if (T[k] < cfg.t_stop) {       // include-then-stop (reading 9)
             done[k] = true;
@@ -203,6 +215,10 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
     image[2 * HW + p] = fmaf(T[k], cfg.bg[2], C[k][2]);
     F.T_final[p] = T[k];
     F.n_proc[p] = nproc[k];
+    if (AUX) {
+      if (depth) depth[p] = dep[k];
+      if (alpha) alpha[p] = 1.f - T[k];
+    }
     it += nproc[k];
   }
   if (STATS) {
@@ -413,15 +429,25 @@ static int nt_from_env(const char *name, int dflt) {
   return (v == 64 || v == 128 || v == 256) ? v : dflt;
 }
 
-template <int NT>
-static void fwd_nt(const lp_frame &F, const lp_raster_cfg &cfg, float *image, cudaStream_t st) {
+template <int NT, bool STATS, bool AUX>
+static void fwd_k(const lp_frame &F, const lp_raster_cfg &cfg, float *image, float *depth, float *alpha,
+                  cudaStream_t st) {
   const int tiles = F.tiles_x * F.tiles_y;
+  if (F.kind == LP_OCTAHEDRON)
+    k_raster_fwd<LP_OCTAHEDRON, NT, STATS, AUX><<<tiles, NT, 0, st>>>(F, cfg, image, depth, alpha);
+  else k_raster_fwd<LP_TETRAHEDRON, NT, STATS, AUX><<<tiles, NT, 0, st>>>(F, cfg, image, depth, alpha);
+}
+
+template <int NT>
+static void fwd_nt(const lp_frame &F, const lp_raster_cfg &cfg, float *image, float *depth, float *alpha,
+                   cudaStream_t st) {
+  const bool aux = depth || alpha;
   if (cfg.count_stats) {
-    if (F.kind == LP_OCTAHEDRON) k_raster_fwd<LP_OCTAHEDRON, NT, true><<<tiles, NT, 0, st>>>(F, cfg, image);
-    else k_raster_fwd<LP_TETRAHEDRON, NT, true><<<tiles, NT, 0, st>>>(F, cfg, image);
+    if (aux) fwd_k<NT, true, true>(F, cfg, image, depth, alpha, st);
+    else fwd_k<NT, true, false>(F, cfg, image, depth, alpha, st);
   } else {
-    if (F.kind == LP_OCTAHEDRON) k_raster_fwd<LP_OCTAHEDRON, NT, false><<<tiles, NT, 0, st>>>(F, cfg, image);
-    else k_raster_fwd<LP_TETRAHEDRON, NT, false><<<tiles, NT, 0, st>>>(F, cfg, image);
+    if (aux) fwd_k<NT, false, true>(F, cfg, image, depth, alpha, st);
+    else fwd_k<NT, false, false>(F, cfg, image, depth, alpha, st);
   }
 }
 
@@ -432,11 +458,12 @@ static void bwd_nt(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL,
   else k_raster_bwd<LP_TETRAHEDRON, (NT > 128 ? 128 : NT)><<<tiles, (NT > 128 ? 128 : NT), 0, st>>>(F, cfg, dL);
 }
 
-void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image, cudaStream_t st) {
+void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image, float *depth, float *alpha,
+                       cudaStream_t st) {
   static const int nt = nt_from_env("LP_FWD_NT", 128);
-  if (nt == 64) fwd_nt<64>(F, cfg, image, st);
-  else if (nt == 256) fwd_nt<256>(F, cfg, image, st);
-  else fwd_nt<128>(F, cfg, image, st);
+  if (nt == 64) fwd_nt<64>(F, cfg, image, depth, alpha, st);
+  else if (nt == 256) fwd_nt<256>(F, cfg, image, depth, alpha, st);
+  else fwd_nt<128>(F, cfg, image, depth, alpha, st);
 }
 
 void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL, cudaStream_t st) {

@@ -74,6 +74,8 @@ _sig = {
     "lp_bin_sort": (C.c_int, [C.POINTER(lp_camera), C.c_int32, C.POINTER(lp_frame), C.POINTER(C.c_int64), _p]),
     "lp_render_fwd": (C.c_int, [C.POINTER(lp_camera), C.c_int32, C.POINTER(lp_raster_cfg), C.POINTER(lp_frame),
                                 _p, _p]),
+    "lp_render_fwd_aux": (C.c_int, [C.POINTER(lp_camera), C.c_int32, C.POINTER(lp_raster_cfg),
+                                    C.POINTER(lp_frame), _p, _p, _p, _p]),
     "lp_render_bwd": (C.c_int, [C.POINTER(lp_prims), C.POINTER(lp_camera), C.c_int32, C.POINTER(lp_raster_cfg),
                                 C.POINTER(lp_frame), _p, C.POINTER(lp_grads), _p]),
     "lp_raster_bwd": (C.c_int, [C.POINTER(lp_camera), C.c_int32, C.POINTER(lp_raster_cfg), C.POINTER(lp_frame),
@@ -146,6 +148,11 @@ def lp_bin_sort(cams, frames, stream, n_entries=None):
 def lp_render_fwd(cams, cfg, frames, image, stream):
     return _check(_lib.lp_render_fwd(cams, len(cams), C.byref(cfg), frames, _ptr(image), _stream(stream)),
                   "lp_render_fwd")
+
+
+def lp_render_fwd_aux(cams, cfg, frames, image, depth, alpha, stream):
+    return _check(_lib.lp_render_fwd_aux(cams, len(cams), C.byref(cfg), frames, _ptr(image), _ptr(depth),
+                                         _ptr(alpha), _stream(stream)), "lp_render_fwd_aux")
 
 
 def lp_render_bwd(prims, cams, cfg, frames, dL_dimage, grads, stream):

@@ -158,22 +158,34 @@ class Renderer:
                     _store_back([self.frames[v]], fa)
                 break
 
-    def render_views(self, image, views=None):
+    def render_views(self, image, views=None, depth=None, alpha=None):
+        """Forward raster of the views into image[i] (and depth[i] / alpha[i] when given, the
+        depth / alpha render modes, lp_render_fwd_aux)."""
         views = list(range(len(self.frames))) if views is None else list(views)
         st = self.stream()
         for i, v in enumerate(views):
             fa = frames_array([self.frames[v]])
-            L.lp_render_fwd(self._cams([v]), self.cfg, fa, image[i], st)
+            if depth is None and alpha is None:
+                L.lp_render_fwd(self._cams([v]), self.cfg, fa, image[i], st)
+            else:
+                L.lp_render_fwd_aux(self._cams([v]), self.cfg, fa, image[i],
+                                    None if depth is None else depth[i], None if alpha is None else alpha[i], st)
             _store_back([self.frames[v]], fa)
 
-    def forward(self, views=None, image=None):
+    def forward(self, views=None, image=None, depth=False, alpha=False):
+        """Render the views; returns image [V,3,H,W], or (image, depth [V,H,W] | None, alpha [V,H,W] | None)
+        when depth or alpha is requested."""
         views = list(range(len(self.frames))) if views is None else list(views)
+        c = self.cam_dicts[views[0]]
+        dev = self.scene.flat.device
         if image is None:
-            c = self.cam_dicts[views[0]]
-            image = torch.empty((len(views), 3, c["height"], c["width"]), dtype=torch.float32,
-                                device=self.scene.flat.device)
+            image = torch.empty((len(views), 3, c["height"], c["width"]), dtype=torch.float32, device=dev)
+        dmap = torch.empty((len(views), c["height"], c["width"]), dtype=torch.float32, device=dev) if depth else None
+        amap = torch.empty((len(views), c["height"], c["width"]), dtype=torch.float32, device=dev) if alpha else None
         self.preprocess_and_sort(views)
-        self.render_views(image, views)
+        self.render_views(image, views, depth=dmap, alpha=amap)
+        if depth or alpha:
+            return image, dmap, amap
         return image
 
     def backward(self, dL_dimage, views=None):
