@@ -4,7 +4,8 @@
 Workload (BASELINE.json configs[4], the config its metric "fwd+bwd Mpixel/s and train iters/s at
 1/2/4/8 B200" is quoted on): 1M octahedra, SH degree 3, a batch of 8 views at 1600x1060, one
 training step = one lp_preprocess over all local views; for each local view lp_bin_sort ->
-lp_render_fwd -> lp_l1_grad -> lp_raster_bwd (views spread over --streams CUDA streams); one
+lp_render_fwd -> lp_loss_grad (3DGS L1 + SSIM; --loss l1 for L1 only) -> lp_raster_bwd (views
+spread over --streams CUDA streams); one
 lp_preprocess_bwd over all local views; then (N > 1) one NCCL allreduce of the flat gradient;
 then one fused Adam (lp_adam_step, also zeroing the gradient).  Views are sharded views[r::N] over
 ranks (strong scaling, fixed global batch of 8).
@@ -46,6 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--loss", default="l1ssim", choices=["l1ssim", "l1"],
+                    help="training loss: 3DGS (1-0.2) L1 + 0.2 (1-SSIM) (P:212) or L1 only")
     ap.add_argument("--streams", type=int, default=2, help="CUDA streams the views of a step are spread over")
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop (ncu --profile-from-start off) and exit")
@@ -187,7 +190,7 @@ def run_ours(args, rank, world, local_rank):
     groups = train.lr_groups(ds.offsets, n, extent=4.0)
     scale = 1.0 / (3.0 * W * H * n_views)
     cams_c = rend.cams
-    ev_names = ["sort", "fwd", "l1", "rbwd"]           # per view
+    ev_names = ["sort", "fwd", "loss", "rbwd"]         # per view
     fa_all = render.frames_array(rend.frames)
     ca_all = rend._cams(list(range(n_local)))
     fa_view = [render.frames_array([rend.frames[i]]) for i in range(n_local)]
@@ -228,7 +231,10 @@ def run_ours(args, rank, world, local_rank):
             rec(ev, 1, sx)
             L.lp_render_fwd(ca, rend.cfg, fa, img[i], sx)
             rec(ev, 2, sx)
-            L.lp_l1_grad(img[i], tg[i], dL[i], loss_buf[si:si + 1], scale, sx)
+            if args.loss == "l1":
+                L.lp_l1_grad(img[i], tg[i], dL[i], loss_buf[si:si + 1], scale, sx)
+            else:
+                L.lp_loss_grad(img[i], tg[i], dL[i], loss_buf[si:si + 1], 0.2, scale, sx)
             rec(ev, 3, sx)
             L.lp_raster_bwd(ca, rend.cfg, fa, dL[i], sx)
             rec(ev, 4, sx)
@@ -341,6 +347,9 @@ def run_ours(args, rank, world, local_rank):
         "pbwd_all_views": ("k_preprocess_bwd+k_sh_bwd", "hbm", 4 * n * n_local + vis * n_local * 4 * RG + n * 3 * Fb),
         "pre_all_views": ("k_preprocess", "hbm", n * Fb + n_local * (n * 24 + vis * 4 * RW)),
         "adam": ("k_adam", "hbm", 32 * ds.flat.numel()),
+        # separable 11-tap window: 5 products x 2 directions x 11 + 3 G maps x 2 x 11 FMA + ~30 for
+        # S and the G maps per pixel-channel; L1 only: 12 B per pixel-channel
+        "loss": ("k_loss_ssim", "alu", 206 * 3 * W * H) if args.loss == "l1ssim" else ("k_l1_grad", "hbm", 12 * 3 * W * H),
     }
     rooflines = {}
     for key, (kname, bound, amount) in work.items():
@@ -427,6 +436,7 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "f32", "data": "synthetic (seeded scenegen, BASELINE configs[4] shape; random-init features)",
         "iters_per_s": round(iters, 3),
         "config": {"workload": "C5: 1M octahedra, SH deg 3, 8 views 1600x1060, training step (views sharded)",
+                   "loss": "3DGS 0.8 L1 + 0.2 (1 - SSIM)" if args.loss == "l1ssim" else "L1",
                    "n_primitives": n, "kind": "octahedron", "sh_degree": 3, "global_batch_views": views_total,
                    "views_per_gpu": n_local, "width": W, "height": H, "parallelism": f"dp{world} (views)",
                    "l2": "inputs larger than L2: features+grads+Adam state = %.2f GB touched per step"

@@ -206,6 +206,18 @@ lp_status lp_frame_counters(const lp_frame *frame, uint32_t *host_counters /* [L
 lp_status lp_l1_grad(const float *image, const float *target, float *dL_dimage, float *loss_sum,
                      int64_t n, float scale, void *stream);
 
+/* f1 (#25): the 3DGS loss L = (1 - lambda) L1 + lambda (1 - SSIM) of
+ * n_planes fp32 image planes [n_planes][height][width] (n_views * 3 channels, CHW per view) and its
+ * gradient, in one kernel.  SSIM: 11 x 11 Gaussian window (sigma 1.5) with zero padding,
+ * C1 = 0.01^2, C2 = 0.03^2.
+ * dL_dimage = scale * [(1 - lambda) sign(x - y) - lambda dSumS/dx] (written, not accumulated);
+ * loss_sum[0] += scale * sum_p [(1 - lambda)|x_p - y_p| + lambda (1 - S_p)] (device float).
+ * scale = 1 / (3 H W n_views) makes both the mean over views of the per-view losses.
+ * lambda = 0 reduces to lp_l1_grad. */
+lp_status lp_loss_grad(const float *image, const float *target, float *dL_dimage, float *loss_sum,
+                       int32_t n_planes, int32_t height, int32_t width, float lambda, float scale,
+                       void *stream);
+
 /* C5: one fused Adam step over a flat fp32 parameter buffer with per-group learning
  * rates; elements outside every group are left unchanged.  step >= 1 (bias correction). */
 lp_status lp_adam_step(float *param, float *grad, float *m, float *v,

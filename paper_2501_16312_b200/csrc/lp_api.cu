@@ -327,6 +327,16 @@ lp_status lp_l1_grad(const float *image, const float *target, float *dL_dimage, 
   return last_error();
 }
 
+lp_status lp_loss_grad(const float *image, const float *target, float *dL_dimage, float *loss_sum, int32_t n_planes,
+                       int32_t height, int32_t width, float lambda, float scale, void *stream) {
+  if (!image || !target || !dL_dimage || !loss_sum || n_planes < 0 || height < 0 || width < 0 || n_planes > 65535 ||
+      !(lambda >= 0.f && lambda <= 1.f))
+    return LP_ERR_ARG;
+  launch_loss_ssim(image, target, dL_dimage, loss_sum, n_planes, height, width, lambda, scale,
+                   static_cast<cudaStream_t>(stream));
+  return last_error();
+}
+
 lp_status lp_adam_step(float *param, float *grad, float *m, float *v, const lp_adam_group *groups,
                        int32_t n_groups, float beta1, float beta2, float eps, int32_t step, int32_t zero_grad,
                        void *stream) {

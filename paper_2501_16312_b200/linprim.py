@@ -84,6 +84,7 @@ _sig = {
                                     C.POINTER(lp_raster_cfg), C.POINTER(lp_frame), C.POINTER(lp_grads), _p]),
     "lp_frame_counters": (C.c_int, [C.POINTER(lp_frame), C.POINTER(C.c_uint32), _p]),
     "lp_l1_grad": (C.c_int, [_p, _p, _p, _p, C.c_int64, C.c_float, _p]),
+    "lp_loss_grad": (C.c_int, [_p, _p, _p, _p, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_float, _p]),
     "lp_adam_step": (C.c_int, [_p, _p, _p, _p, C.POINTER(lp_adam_group), C.c_int32, C.c_float, C.c_float,
                                C.c_float, C.c_int32, C.c_int32, _p]),
 }
@@ -179,6 +180,14 @@ def lp_frame_counters(frame, stream) -> np.ndarray:
 def lp_l1_grad(image, target, dL, loss_sum, scale, stream):
     return _check(_lib.lp_l1_grad(_ptr(image), _ptr(target), _ptr(dL), _ptr(loss_sum), image.numel(),
                                   C.c_float(scale), _stream(stream)), "lp_l1_grad")
+
+
+def lp_loss_grad(image, target, dL, loss_sum, lam, scale, stream):
+    """image / target / dL: contiguous [..., H, W] fp32 tensors (all leading dims are planes)."""
+    H, W = image.shape[-2], image.shape[-1]
+    planes = image.numel() // (H * W) if H * W else 0
+    return _check(_lib.lp_loss_grad(_ptr(image), _ptr(target), _ptr(dL), _ptr(loss_sum), planes, H, W,
+                                    C.c_float(lam), C.c_float(scale), _stream(stream)), "lp_loss_grad")
 
 
 def lp_adam_step(param, grad, m, v, groups, beta1, beta2, eps, step, stream, zero_grad=False):

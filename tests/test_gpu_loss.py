@@ -1,0 +1,77 @@
+"""GPU parity of the fused L1 + SSIM loss kernel (lp_loss_grad) against oracle/loss.py.
+
+Tolerances: loss within 1e-5 relative; gradient |err| <= 1e-3 |g| + 1e-5 max|g| (north_star's
+gradient bar), on sizes spanning several 32 x 32 tiles with ragged edges.
+"""
+import numpy as np
+import pytest
+
+from oracle import loss as OL
+from tests import parity as PT
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    assert torch.cuda.is_available(), "gpu tests need CUDA"
+    from paper_2501_16312_b200 import _build
+    _build.build()
+    torch.cuda.set_device(0)
+
+
+def images(V, H, W, seed):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(0, 1, (V, 3, H, W)).astype(np.float32)
+    # structured target: smooth blobs + noise so SSIM is far from 0 and 1
+    yy, xx = np.mgrid[0:H, 0:W]
+    y = 0.5 + 0.4 * np.sin(xx / 7.0)[None, None] * np.cos(yy / 5.0)[None, None] + rng.normal(0, 0.05, x.shape)
+    y = np.clip(0.6 * y + 0.4 * x, 0, 1).astype(np.float32)
+    return x, y
+
+
+def run(x, y, lam):
+    import torch
+
+    from paper_2501_16312_b200 import linprim as L
+    X = torch.as_tensor(x, device="cuda")
+    Y = torch.as_tensor(y, device="cuda")
+    D = torch.empty_like(X)
+    loss = torch.zeros(1, device="cuda")
+    V, C, H, W = x.shape
+    L.lp_loss_grad(X, Y, D, loss, lam, 1.0 / (C * H * W * V), torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    return float(loss.item()), D.cpu().numpy()
+
+
+@pytest.mark.parametrize("V,H,W,seed", [(1, 32, 32, 0), (1, 45, 70, 1), (2, 96, 128, 2), (1, 100, 33, 3),
+                                         (1, 7, 5, 4)])
+@pytest.mark.parametrize("lam", [0.2, 1.0])
+def test_loss_and_grad_vs_oracle(V, H, W, seed, lam):
+    x, y = images(V, H, W, seed)
+    L_ref, G_ref = OL.batch_loss_and_grad(x.astype(np.float64), y.astype(np.float64), lam)
+    L_got, G_got = run(x, y, lam)
+    assert abs(L_got - L_ref) <= 1e-5 * abs(L_ref), (L_got, L_ref)
+    ok, worst, rep = PT.grad_close("dL/dimage", G_got, G_ref)
+    assert ok, rep
+
+
+def test_lambda_zero_matches_l1_kernel():
+    import torch
+
+    from paper_2501_16312_b200 import linprim as L
+    x, y = images(2, 50, 61, 7)
+    _, G = run(x, y, 0.0)
+    X, Y = torch.as_tensor(x, device="cuda"), torch.as_tensor(y, device="cuda")
+    D = torch.empty_like(X)
+    loss = torch.zeros(1, device="cuda")
+    L.lp_l1_grad(X, Y, D, loss, 1.0 / x.size, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    assert np.array_equal(G, D.cpu().numpy())
+
+
+def test_identical_images_zero_loss():
+    x, _ = images(1, 40, 40, 3)
+    L_got, G = run(x, x, 0.2)
+    assert abs(L_got) < 1e-6 and np.abs(G).max() < 1e-9
