@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include "lp_kernels.h"
+#include "lp_x2.cuh"
 
 namespace lp {
 
@@ -34,17 +35,26 @@ struct Win {
 };
 
 struct LossSmem {
-  float x[RI][RI + 1];
-  float y[RI][RI + 1];
+  float2 xy[RI][RI + 1];             // (x, y) pairs of the input region
   union {
-    float h[5][RI][RA];              // stage 2: horizontal sums of x, y, xx, yy, xy
-    float h2[3][RA][TS];             // stage 4: horizontal sums of the G maps
+    struct {
+      float2 h01[RI][RA];            // stage 2: horizontal sums of (x, y)
+      float2 h23[RI][RA];            //          (xx, yy)
+      float h4[RI][RA];              //          xy
+    } a;
+    struct {
+      float2 h01[RA][TS];            // stage 4: horizontal sums of (G_m, G_xy)
+      float h2[RA][TS];              //          G_xx
+    } b;
   } u;
-  float gm[3][RA][RA + 1];           // G_m, G_xy, G_xx
+  float2 g01[RA][RA + 1];            // (G_m, G_xy)
+  float g2[RA][RA + 1];              // G_xx
   float red[LT / 32];
 };
 }  // namespace
 
+// The window sums run on (x, y) and (xx, yy) as FFMA2 pairs (one instruction for two maps) and
+// on xy as a scalar FFMA; pass 2 pairs (G_m, G_xy) and runs G_xx scalar.
 __global__ void __launch_bounds__(LT, 2) k_loss_ssim(const float *__restrict__ img, const float *__restrict__ tgt,
                                                      float *__restrict__ dL, float *__restrict__ loss_sum, int H,
                                                      int W, int tiles_x, float lam, float scale, Win win) {
@@ -57,7 +67,7 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim(const float *__restrict__ i
   const float *X = img + plane, *Y = tgt + plane;
   float *D = dL + plane;
 
-  // ---- stage 1: x, y on the 52 x 52 input region (zero outside the image); warp w loads rows
+  // ---- stage 1: (x, y) on the 52 x 52 input region (zero outside the image); warp w loads rows
   // w, w + 12, ..., lanes the columns; all loads issued before the shared-memory stores
   {
     const int lane = tid & 31, warp = tid >> 5;
@@ -82,10 +92,7 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim(const float *__restrict__ i
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = lane + 32 * h;
-        if (r < RI && c < RI) {
-          S.x[r][c] = ax[q][h];
-          S.y[r][c] = ay[q][h];
-        }
+        if (r < RI && c < RI) S.xy[r][c] = make_float2(ax[q][h], ay[q][h]);
       }
     }
   }
@@ -96,28 +103,34 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim(const float *__restrict__ i
     constexpr int CH = 6, NCH = RA / CH;   // 7 chunks per row
     for (int it = tid; it < RI * NCH; it += LT) {
       const int r = it / NCH, c0 = (it % NCH) * CH;
-      float acc[5][CH];
+      float2 a01[CH], a23[CH];
+      float a4[CH];
 #pragma unroll
-      for (int m = 0; m < 5; ++m)
-#pragma unroll
-        for (int j = 0; j < CH; ++j) acc[m][j] = 0.f;
+      for (int j = 0; j < CH; ++j) {
+        a01[j] = a23[j] = make_float2(0.f, 0.f);
+        a4[j] = 0.f;
+      }
 #pragma unroll
       for (int k = 0; k < CH + TAPS - 1; ++k) {
-        const float a = S.x[r][c0 + k], b = S.y[r][c0 + k];
-        const float v[5] = {a, b, a * a, b * b, a * b};
+        const float2 v01 = S.xy[r][c0 + k];
+        const float2 v23 = fmul2(v01, v01);
+        const float v4 = v01.x * v01.y;
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const int t = k - j;
           if (t >= 0 && t < TAPS) {
-#pragma unroll
-            for (int m = 0; m < 5; ++m) acc[m][j] = fmaf(win.g[t], v[m], acc[m][j]);
+            a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+            a23[j] = ffma2(bc(win.g[t]), v23, a23[j]);
+            a4[j] = fmaf(win.g[t], v4, a4[j]);
           }
         }
       }
 #pragma unroll
-      for (int m = 0; m < 5; ++m)
-#pragma unroll
-        for (int j = 0; j < CH; ++j) S.u.h[m][r][c0 + j] = acc[m][j];
+      for (int j = 0; j < CH; ++j) {
+        S.u.a.h01[r][c0 + j] = a01[j];
+        S.u.a.h23[r][c0 + j] = a23[j];
+        S.u.a.h4[r][c0 + j] = a4[j];
+      }
     }
   }
   __syncthreads();
@@ -128,22 +141,24 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim(const float *__restrict__ i
     constexpr int CH = 6, NCH = RA / CH;   // 7 row chunks per column
     for (int it = tid; it < RA * NCH; it += LT) {
       const int c = it % RA, r0 = (it / RA) * CH;
-      float acc[5][CH];
+      float2 a01[CH], a23[CH];
+      float a4[CH];
 #pragma unroll
-      for (int m = 0; m < 5; ++m)
-#pragma unroll
-        for (int j = 0; j < CH; ++j) acc[m][j] = 0.f;
+      for (int j = 0; j < CH; ++j) {
+        a01[j] = a23[j] = make_float2(0.f, 0.f);
+        a4[j] = 0.f;
+      }
 #pragma unroll
       for (int k = 0; k < CH + TAPS - 1; ++k) {
-        float v[5];
-#pragma unroll
-        for (int m = 0; m < 5; ++m) v[m] = S.u.h[m][r0 + k][c];
+        const float2 v01 = S.u.a.h01[r0 + k][c], v23 = S.u.a.h23[r0 + k][c];
+        const float v4 = S.u.a.h4[r0 + k][c];
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const int t = k - j;
           if (t >= 0 && t < TAPS) {
-#pragma unroll
-            for (int m = 0; m < 5; ++m) acc[m][j] = fmaf(win.g[t], v[m], acc[m][j]);
+            a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+            a23[j] = ffma2(bc(win.g[t]), v23, a23[j]);
+            a4[j] = fmaf(win.g[t], v4, a4[j]);
           }
         }
       }
@@ -153,8 +168,8 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim(const float *__restrict__ i
         const int gy = ty0 - RAD + r, gx = tx0 - RAD + c;
         float gmv = 0.f, gxy = 0.f, gxx = 0.f;
         if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
-          const float mx = acc[0][j], my = acc[1][j];
-          const float vx = acc[2][j] - mx * mx, vy = acc[3][j] - my * my, cxy = acc[4][j] - mx * my;
+          const float mx = a01[j].x, my = a01[j].y;
+          const float vx = a23[j].x - mx * mx, vy = a23[j].y - my * my, cxy = a4[j] - mx * my;
           const float A1 = 2.f * mx * my + C1, A2 = 2.f * cxy + C2;
           const float B1 = mx * mx + my * my + C1, B2 = vx + vy + C2;
           const float iB1 = __fdividef(1.f, B1), iB2 = __fdividef(1.f, B2);   // B1, B2 >= C1, C2 > 0
@@ -164,9 +179,8 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim(const float *__restrict__ i
           gxx = -ssim * iB2;
           if (r >= RAD && r < RAD + TS && c >= RAD && c < RAD + TS) lsum += lam * (1.f - ssim);
         }
-        S.gm[0][r][c] = gmv;
-        S.gm[1][r][c] = gxy;
-        S.gm[2][r][c] = gxx;
+        S.g01[r][c] = make_float2(gmv, gxy);
+        S.g2[r][c] = gxx;
       }
     }
   }
@@ -177,29 +191,31 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim(const float *__restrict__ i
     constexpr int CH = 4, NCH = TS / CH;   // 8
     for (int it = tid; it < RA * NCH; it += LT) {
       const int r = it / NCH, c0 = (it % NCH) * CH;
-      float acc[3][CH];
+      float2 a01[CH];
+      float a2[CH];
 #pragma unroll
-      for (int m = 0; m < 3; ++m)
-#pragma unroll
-        for (int j = 0; j < CH; ++j) acc[m][j] = 0.f;
+      for (int j = 0; j < CH; ++j) {
+        a01[j] = make_float2(0.f, 0.f);
+        a2[j] = 0.f;
+      }
 #pragma unroll
       for (int k = 0; k < CH + TAPS - 1; ++k) {
-        float v[3];
-#pragma unroll
-        for (int m = 0; m < 3; ++m) v[m] = S.gm[m][r][c0 + k];
+        const float2 v01 = S.g01[r][c0 + k];
+        const float v2 = S.g2[r][c0 + k];
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const int t = k - j;
           if (t >= 0 && t < TAPS) {
-#pragma unroll
-            for (int m = 0; m < 3; ++m) acc[m][j] = fmaf(win.g[t], v[m], acc[m][j]);
+            a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+            a2[j] = fmaf(win.g[t], v2, a2[j]);
           }
         }
       }
 #pragma unroll
-      for (int m = 0; m < 3; ++m)
-#pragma unroll
-        for (int j = 0; j < CH; ++j) S.u.h2[m][r][c0 + j] = acc[m][j];
+      for (int j = 0; j < CH; ++j) {
+        S.u.b.h01[r][c0 + j] = a01[j];
+        S.u.b.h2[r][c0 + j] = a2[j];
+      }
     }
   }
   __syncthreads();
@@ -209,22 +225,23 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim(const float *__restrict__ i
     constexpr int CH = 4, NCH = TS / CH;   // 8
     for (int it = tid; it < TS * NCH; it += LT) {
       const int c = it % TS, r0 = (it / TS) * CH;
-      float acc[3][CH];
+      float2 a01[CH];
+      float a2[CH];
 #pragma unroll
-      for (int m = 0; m < 3; ++m)
-#pragma unroll
-        for (int j = 0; j < CH; ++j) acc[m][j] = 0.f;
+      for (int j = 0; j < CH; ++j) {
+        a01[j] = make_float2(0.f, 0.f);
+        a2[j] = 0.f;
+      }
 #pragma unroll
       for (int k = 0; k < CH + TAPS - 1; ++k) {
-        float v[3];
-#pragma unroll
-        for (int m = 0; m < 3; ++m) v[m] = S.u.h2[m][r0 + k][c];
+        const float2 v01 = S.u.b.h01[r0 + k][c];
+        const float v2 = S.u.b.h2[r0 + k][c];
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const int t = k - j;
           if (t >= 0 && t < TAPS) {
-#pragma unroll
-            for (int m = 0; m < 3; ++m) acc[m][j] = fmaf(win.g[t], v[m], acc[m][j]);
+            a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+            a2[j] = fmaf(win.g[t], v2, a2[j]);
           }
         }
       }
@@ -232,10 +249,10 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim(const float *__restrict__ i
       for (int j = 0; j < CH; ++j) {
         const int gy = ty0 + r0 + j, gx = tx0 + c;
         if (gy < H && gx < W) {
-          const float x = S.x[r0 + j + 2 * RAD][c + 2 * RAD], y = S.y[r0 + j + 2 * RAD][c + 2 * RAD];
-          const float d = x - y;
+          const float2 p = S.xy[r0 + j + 2 * RAD][c + 2 * RAD];
+          const float d = p.x - p.y;
           const float sg = (float)((d > 0.f) - (d < 0.f));
-          const float dS = acc[0][j] + y * acc[1][j] + 2.f * x * acc[2][j];
+          const float dS = a01[j].x + p.y * a01[j].y + 2.f * p.x * a2[j];
           D[(size_t)gy * W + gx] = scale * ((1.f - lam) * sg - lam * dS);
           lsum += (1.f - lam) * fabsf(d);
         }
