@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include "../../include/linprim.h"
+#include "lp_x2.cuh"
 
 namespace lp {
 
@@ -357,15 +358,18 @@ __device__ __forceinline__ void tetra_planes(const float off[4][3], TetraPlanes 
 // chord evaluation (a8).  TRACK: also return the entry / exit slab (octa) or slot (tetra).
 // ---------------------------------------------------------------------------------------------
 // dx, dy: pixel centre minus the ray-space centre c_r (record word CX, CX+1), fs()-computed.
+// Slab value L_s = fma(g_s, dy, b_s dx), plane depth z_s = fma(C_s, dy, fma(B_s, dx, A_s)): the
+// dx part first, so the two pixels of a thread (same column, PPT 2) share it and the paired
+// forward (chord2 below, FFMA2 / FADD2 lanes) is bitwise this scalar evaluation.
 template <bool TRACK>
 __device__ __forceinline__ float octa_chord(const float *rec, float dx, float dy, int &se, int &sx) {
   constexpr int B = Kind<LP_OCTAHEDRON>::SLAB;
-  float L = __fmaf_rn(rec[B], dx, fm(rec[B + 1], dy));
+  float L = __fmaf_rn(rec[B + 1], dy, fm(rec[B], dx));
   float en = fs(L, rec[B + 2]), ex = fa(L, rec[B + 2]);
   if (TRACK) { se = 0; sx = 0; }
 #pragma unroll
   for (int s = 1; s < 4; ++s) {
-    L = __fmaf_rn(rec[B + 3 * s], dx, fm(rec[B + 1 + 3 * s], dy));
+    L = __fmaf_rn(rec[B + 1 + 3 * s], dy, fm(rec[B + 3 * s], dx));
     const float a = fs(L, rec[B + 2 + 3 * s]), b = fa(L, rec[B + 2 + 3 * s]);
     if (TRACK) {
       if (a > en) se = s;
@@ -403,25 +407,45 @@ __device__ __forceinline__ float chord(const float *rec, float dx, float dy, int
   return tetra_chord<TRACK>(rec, dx, dy, se, sx);
 }
 
-// entry offset max_s(entry_s) along the ray relative to the ray-space centre depth l (depth mode,
-// P:840-841): the same slab / plane values as chord(), so entry + l is the entry distance i1.
+// Paired chord of the thread's two pixels (same dx, dy2 = their two dy): lane k is bitwise
+// chord<KIND, false>(rec, dx, dy2[k]); en2 receives the entry offsets (depth mode).
 template <int KIND>
-__device__ __forceinline__ float entry_offset(const float *rec, float dx, float dy) {
+__device__ __forceinline__ float2 chord2(const float *rec, float dx, float2 dy2, float2 &en2) {
+  float2 en, ex;
   if (KIND == LP_OCTAHEDRON) {
     constexpr int B = Kind<LP_OCTAHEDRON>::SLAB;
-    float en = fs(__fmaf_rn(rec[B], dx, fm(rec[B + 1], dy)), rec[B + 2]);
 #pragma unroll
-    for (int s = 1; s < 4; ++s)
-      en = fmaxf(en, fs(__fmaf_rn(rec[B + 3 * s], dx, fm(rec[B + 1 + 3 * s], dy)), rec[B + 2 + 3 * s]));
-    return en;
+    for (int s = 0; s < 4; ++s) {
+      const float2 L = ffma2(bc(rec[B + 1 + 3 * s]), dy2, bc(fm(rec[B + 3 * s], dx)));
+      const float2 a = fsub2(L, bc(rec[B + 2 + 3 * s])), b = fadd2(L, bc(rec[B + 2 + 3 * s]));
+      if (s == 0) {
+        en = a;
+        ex = b;
+      } else {
+        en.x = fmaxf(en.x, a.x);
+        en.y = fmaxf(en.y, a.y);
+        ex.x = fminf(ex.x, b.x);
+        ex.y = fminf(ex.y, b.y);
+      }
+    }
   } else {
     constexpr int B = Kind<LP_TETRAHEDRON>::SLAB;
-    float en = -3.402823466e38f;
 #pragma unroll
-    for (int s = 0; s < 3; ++s)
-      en = fmaxf(en, __fmaf_rn(rec[B + 2 + 3 * s], dy, __fmaf_rn(rec[B + 1 + 3 * s], dx, rec[B + 3 * s])));
-    return en;
+    for (int s = 0; s < 6; ++s) {
+      const float2 z = ffma2(bc(rec[B + 2 + 3 * s]), dy2, bc(__fmaf_rn(rec[B + 1 + 3 * s], dx, rec[B + 3 * s])));
+      if (s == 0) en = z;
+      else if (s == 3) ex = z;
+      else if (s < 3) {
+        en.x = fmaxf(en.x, z.x);
+        en.y = fmaxf(en.y, z.y);
+      } else {
+        ex.x = fminf(ex.x, z.x);
+        ex.y = fminf(ex.y, z.y);
+      }
+    }
   }
+  en2 = en;
+  return fsub2(ex, en);
 }
 
 // slack of the bbox reject test: a pair rejected by it has chord <= 0 (up to fp32 rounding of

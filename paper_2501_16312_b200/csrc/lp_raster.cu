@@ -106,11 +106,16 @@ extern "C" int lp_debug_bwd_stats(unsigned long long *out, int reset) {
 // AUX: also the depth (entry distance of the first primitive after which the cumulative
 // opacity 1 - T exceeds 0.5, 0 if never; reading 24) and alpha (1 - T_final) images,
 // either pointer may be null.
-template <int KIND, int NT, bool STATS, bool AUX>
-__global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg, float *__restrict__ image,
-                                                   float *__restrict__ depth, float *__restrict__ alpha) {
+//
+// 128 threads, 2 pixels per thread: pixel k = 0 / 1 of a thread are (x, y) and (x, y + 4), so they
+// share dx and the bbox x test, and their chords are ONE paired evaluation (chord2: FFMA2 / FADD2
+// lanes, bitwise the scalar chord the backward replays).
+template <int KIND, bool STATS, bool AUX>
+__global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_raster_cfg cfg, float *__restrict__ image,
+                                                    float *__restrict__ depth, float *__restrict__ alpha) {
+  constexpr int NT = 128, PPT = 2;
   using KD = Kind<KIND>;
-  constexpr int RW = KD::RW, RW4 = RW / 4, PPT = 256 / NT;
+  constexpr int RW = KD::RW, RW4 = RW / 4;
   __shared__ float4 s_rec[NT * RW4];
   __shared__ unsigned char s_list[NT / 32][NT];
   __shared__ unsigned long long s_stat[3];
@@ -121,10 +126,11 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
   const int W = F.width, H = F.height;
   if (threadIdx.x < 3) s_stat[threadIdx.x] = 0ull;
 
-  float fx[PPT], fy[PPT], T[PPT], C[PPT][3], dep[PPT];
+  float fy[PPT], T[PPT], C[PPT][3], dep[PPT];
   uint32_t nproc[PPT];
   bool done[PPT], inside[PPT], dset[PPT];
   uint32_t nhit = 0, nbox = 0;
+  float fx;
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     int x, y;
@@ -132,7 +138,7 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
     x += tx * LP_TILE;
     y += ty * LP_TILE;
     inside[k] = x < W && y < H;
-    fx[k] = (float)x + 0.5f;
+    fx = (float)x + 0.5f;
     fy[k] = (float)y + 0.5f;
     T[k] = 1.f;
     C[k][0] = C[k][1] = C[k][2] = 0.f;
@@ -145,10 +151,7 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
   warp_rect<NT>(threadIdx.x >> 5, tx, ty, wx0, wx1, wy0, wy1);
 
   for (uint32_t b = start; b < end; b += NT) {
-    bool mine = true;
-#pragma unroll
-    for (int k = 0; k < PPT; ++k) mine = mine && done[k];
-    if (__syncthreads_and(mine)) break;   // also protects s_rec from the previous batch
+    if (__syncthreads_and(done[0] && done[1])) break;   // also protects s_rec from the previous batch
     const uint32_t e = b + threadIdx.x;
     if (e < end) {
       const uint32_t v = F.sorted_val[e];
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
       for (int w = 0; w < RW4; ++w) s_rec[threadIdx.x * RW4 + w] = __ldg(src + w);
     }
     __syncthreads();
-    if (__all_sync(0xffffffffu, mine)) continue;
+    if (__all_sync(0xffffffffu, done[0] && done[1])) continue;
     const int cnt = (int)min((uint32_t)NT, end - b);
     // per-warp sub-list: the batch records whose bbox reaches the warp's pixels, in list order
     // (each lane tests NT/32 records; convexity: outside the vertex bbox the chord is <= 0)
@@ -165,23 +168,26 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
     for (int q = 0; q < nl; ++q) {
       const int j = s_list[threadIdx.x >> 5][q];
       const float4 bb = s_rec[j * RW4];
-      bool test[PPT], any = false;
+      const bool inx = fabsf(fx - bb.x) <= bb.z;
+      bool test[PPT];
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        test[k] = !done[k] && in_bbox(bb, fx[k], fy[k]);
-        any = any || test[k];
-      }
+      for (int k = 0; k < PPT; ++k) test[k] = !done[k] && inx && fabsf(fy[k] - bb.y) <= bb.w;
+      const bool any = test[0] || test[1];
       if (!__any_sync(0xffffffffu, any)) continue;
+      if (!any) continue;
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
+      const float dx = fs(fx, rec[KD::CX]);
+      const float2 dy2 = fsub2(make_float2(fy[0], fy[1]), bc(rec[KD::CX + 1]));
+      float2 en2;
+      const float2 ch2 = chord2<KIND>(rec, dx, dy2, en2);
+      const float ch[PPT] = {ch2.x, ch2.y};
+      const float enk[PPT] = {en2.x, en2.y};
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         if (!test[k]) continue;
         if (STATS) ++nbox;
-        int se, sx;
-        const float dx = fs(fx[k], rec[KD::CX]), dy = fs(fy[k], rec[KD::CX + 1]);
-        const float ch = chord<KIND, false>(rec, dx, dy, se, sx);
-        if (ch > 0.f) {
-          const float E = transmit(rec[KD::SIGMA], ch);
+        if (ch[k] > 0.f) {
+          const float E = transmit(rec[KD::SIGMA], ch[k]);
           const float o = 1.f - E;
           const float wgt = T[k] * o;
           C[k][0] = fmaf(wgt, rec[KD::RGB + 0], C[k][0]);
@@ -191,7 +197,7 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
           if (AUX && !dset[k] && T[k] < 0.5f) {      // cumulative opacity 1 - T > 0.5 (once per pixel)
             dset[k] = true;
             const uint32_t id = F.sorted_val[b + (uint32_t)j];
-            dep[k] = fa(__uint_as_float(F.depth_key[id]), entry_offset<KIND>(rec, dx, dy));
+            dep[k] = fa(__uint_as_float(F.depth_key[id]), enk[k]);
           }
           if (STATS) ++nhit;
           if (T[k] < cfg.t_stop) {       // include-then-stop (reading 9)
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(NT) k_raster_fwd(lp_frame F, lp_raster_cfg cfg
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     if (!inside[k]) continue;
-    const int x = (int)fx[k], y = (int)fy[k];
+    const int x = (int)fx, y = (int)fy[k];
     const size_t p = (size_t)y * W + x;
     image[p] = fmaf(T[k], cfg.bg[0], C[k][0]);
     image[HW + p] = fmaf(T[k], cfg.bg[1], C[k][1]);
@@ -420,7 +426,7 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
 }
 
 // ---------------------------------------------------------------------------------------------
-// CTA size = 256 / pixels-per-thread.  Tuning knobs LP_FWD_NT / LP_BWD_NT (64 or 128) exist for
+// Backward CTA size = 256 / pixels-per-thread.  The tuning knob LP_BWD_NT (64 or 256) exists for
 // measurement only; the defaults are the measured best.
 static int nt_from_env(const char *name, int dflt) {
   const char *s = getenv(name);
@@ -429,26 +435,13 @@ static int nt_from_env(const char *name, int dflt) {
   return (v == 64 || v == 128 || v == 256) ? v : dflt;
 }
 
-template <int NT, bool STATS, bool AUX>
+template <bool STATS, bool AUX>
 static void fwd_k(const lp_frame &F, const lp_raster_cfg &cfg, float *image, float *depth, float *alpha,
                   cudaStream_t st) {
   const int tiles = F.tiles_x * F.tiles_y;
   if (F.kind == LP_OCTAHEDRON)
-    k_raster_fwd<LP_OCTAHEDRON, NT, STATS, AUX><<<tiles, NT, 0, st>>>(F, cfg, image, depth, alpha);
-  else k_raster_fwd<LP_TETRAHEDRON, NT, STATS, AUX><<<tiles, NT, 0, st>>>(F, cfg, image, depth, alpha);
-}
-
-template <int NT>
-static void fwd_nt(const lp_frame &F, const lp_raster_cfg &cfg, float *image, float *depth, float *alpha,
-                   cudaStream_t st) {
-  const bool aux = depth || alpha;
-  if (cfg.count_stats) {
-    if (aux) fwd_k<NT, true, true>(F, cfg, image, depth, alpha, st);
-    else fwd_k<NT, true, false>(F, cfg, image, depth, alpha, st);
-  } else {
-    if (aux) fwd_k<NT, false, true>(F, cfg, image, depth, alpha, st);
-    else fwd_k<NT, false, false>(F, cfg, image, depth, alpha, st);
-  }
+    k_raster_fwd<LP_OCTAHEDRON, STATS, AUX><<<tiles, 128, 0, st>>>(F, cfg, image, depth, alpha);
+  else k_raster_fwd<LP_TETRAHEDRON, STATS, AUX><<<tiles, 128, 0, st>>>(F, cfg, image, depth, alpha);
 }
 
 template <int NT>
@@ -460,10 +453,14 @@ static void bwd_nt(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL,
 
 void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image, float *depth, float *alpha,
                        cudaStream_t st) {
-  static const int nt = nt_from_env("LP_FWD_NT", 128);
-  if (nt == 64) fwd_nt<64>(F, cfg, image, depth, alpha, st);
-  else if (nt == 256) fwd_nt<256>(F, cfg, image, depth, alpha, st);
-  else fwd_nt<128>(F, cfg, image, depth, alpha, st);
+  const bool aux = depth || alpha;
+  if (cfg.count_stats) {
+    if (aux) fwd_k<true, true>(F, cfg, image, depth, alpha, st);
+    else fwd_k<true, false>(F, cfg, image, depth, alpha, st);
+  } else {
+    if (aux) fwd_k<false, true>(F, cfg, image, depth, alpha, st);
+    else fwd_k<false, false>(F, cfg, image, depth, alpha, st);
+  }
 }
 
 void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL, cudaStream_t st) {
