@@ -407,45 +407,76 @@ __device__ __forceinline__ float chord(const float *rec, float dx, float dy, int
   return tetra_chord<TRACK>(rec, dx, dy, se, sx);
 }
 
-// Paired chord of the thread's two pixels (same dx, dy2 = their two dy): lane k is bitwise
-// chord<KIND, false>(rec, dx, dy2[k]); en2 receives the entry offsets (depth mode).
+// Paired entry / exit values of the thread's two pixels (same dx, dy2 = their two dy): lane k of
+// en[s] / ex[s] is bitwise the scalar chord's value for slab s (octahedron: L - h, L + h) or for the
+// front / back plane slot s (tetrahedron: z_s, z_{3+s}).
+template <int KIND> struct Planes2 {
+  static constexpr int N = KIND == LP_OCTAHEDRON ? 4 : 3;
+  float2 en[N], ex[N];
+};
+
 template <int KIND>
-__device__ __forceinline__ float2 chord2(const float *rec, float dx, float2 dy2, float2 &en2) {
-  float2 en, ex;
+__device__ __forceinline__ void planes2(const float *rec, float dx, float2 dy2, Planes2<KIND> &P) {
   if (KIND == LP_OCTAHEDRON) {
     constexpr int B = Kind<LP_OCTAHEDRON>::SLAB;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const float2 L = ffma2(bc(rec[B + 1 + 3 * s]), dy2, bc(fm(rec[B + 3 * s], dx)));
-      const float2 a = fsub2(L, bc(rec[B + 2 + 3 * s])), b = fadd2(L, bc(rec[B + 2 + 3 * s]));
-      if (s == 0) {
-        en = a;
-        ex = b;
-      } else {
-        en.x = fmaxf(en.x, a.x);
-        en.y = fmaxf(en.y, a.y);
-        ex.x = fminf(ex.x, b.x);
-        ex.y = fminf(ex.y, b.y);
-      }
+      P.en[s] = fsub2(L, bc(rec[B + 2 + 3 * s]));
+      P.ex[s] = fadd2(L, bc(rec[B + 2 + 3 * s]));
     }
   } else {
     constexpr int B = Kind<LP_TETRAHEDRON>::SLAB;
 #pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      const float2 z = ffma2(bc(rec[B + 2 + 3 * s]), dy2, bc(__fmaf_rn(rec[B + 1 + 3 * s], dx, rec[B + 3 * s])));
-      if (s == 0) en = z;
-      else if (s == 3) ex = z;
-      else if (s < 3) {
-        en.x = fmaxf(en.x, z.x);
-        en.y = fmaxf(en.y, z.y);
-      } else {
-        ex.x = fminf(ex.x, z.x);
-        ex.y = fminf(ex.y, z.y);
-      }
+    for (int s = 0; s < 3; ++s) {
+      P.en[s] = ffma2(bc(rec[B + 2 + 3 * s]), dy2, bc(__fmaf_rn(rec[B + 1 + 3 * s], dx, rec[B + 3 * s])));
+      const int t = s + 3;
+      P.ex[s] = ffma2(bc(rec[B + 2 + 3 * t]), dy2, bc(__fmaf_rn(rec[B + 1 + 3 * t], dx, rec[B + 3 * t])));
     }
   }
-  en2 = en;
-  return fsub2(ex, en);
+}
+
+__device__ __forceinline__ float lane_k(float2 v, int k) { return k == 0 ? v.x : v.y; }
+
+// max entry / min exit per pixel (FMNMX3 chains); chord = exit - entry as one FADD2
+template <int KIND>
+__device__ __forceinline__ float2 chord2_of(const Planes2<KIND> &P, float2 &en2, float2 &ex2) {
+  constexpr int N = Planes2<KIND>::N;
+  en2 = P.en[0];
+  ex2 = P.ex[0];
+#pragma unroll
+  for (int s = 1; s < N; ++s) {
+    en2.x = fmaxf(en2.x, P.en[s].x);
+    en2.y = fmaxf(en2.y, P.en[s].y);
+    ex2.x = fminf(ex2.x, P.ex[s].x);
+    ex2.y = fminf(ex2.y, P.ex[s].y);
+  }
+  return fsub2(ex2, en2);
+}
+
+// Paired chord (forward): lane k is bitwise chord<KIND, false>(rec, dx, dy2[k]); en2 receives the
+// entry offsets (depth mode).
+template <int KIND>
+__device__ __forceinline__ float2 chord2(const float *rec, float dx, float2 dy2, float2 &en2) {
+  Planes2<KIND> P;
+  planes2<KIND>(rec, dx, dy2, P);
+  float2 ex2;
+  return chord2_of<KIND>(P, en2, ex2);
+}
+
+// Entry / exit slab (octa) or slot (tetra: exit slots 3..5) of pixel k: the FIRST index attaining
+// the max entry / min exit, the same choice chord<KIND, true> makes while scanning.
+template <int KIND>
+__device__ __forceinline__ void track_k(const Planes2<KIND> &P, int k, float en, float ex, int &se, int &sx) {
+  constexpr int N = Planes2<KIND>::N;
+  se = N - 1;
+  sx = N - 1;
+#pragma unroll
+  for (int s = N - 2; s >= 0; --s) {
+    if (lane_k(P.en[s], k) == en) se = s;
+    if (lane_k(P.ex[s], k) == ex) sx = s;
+  }
+  if (KIND == LP_TETRAHEDRON) sx += 3;
 }
 
 // slack of the bbox reject test: a pair rejected by it has chord <= 0 (up to fp32 rounding of

@@ -13,7 +13,6 @@
 // hit lanes and one RED.F32 per moment per (warp, primitive) into rgrad[moment][n].
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <stdlib.h>
 
 #include "lp_device.cuh"
 #include "lp_kernels.h"
@@ -75,12 +74,13 @@ __device__ __forceinline__ int warp_sublist(const float4 *s_rec, int cnt, float 
 }
 
 // resident CTAs per SM the backward asks the register allocator for (LP_BWD_BLOCKS overrides at
-// build time): 8 x 128 threads caps it at 64 registers
+// build time): 7 x 128 threads allows 72 registers (measured best; 6 -> 80 is spill-free but slower)
 #ifndef LP_BWD_BLOCKS
-#define LP_BWD_BLOCKS 8
+#define LP_BWD_BLOCKS 7
 #endif
-// (tetrahedra: 29.7 KB of shared memory per CTA fits 7 per SM, so ask for 7)
-#define BWD_MIN_BLOCKS(kind, nt) ((nt) == 128 ? ((kind) == LP_OCTAHEDRON ? LP_BWD_BLOCKS : 7) : 1)
+// (tetrahedra: 29.7 KB of shared memory per CTA fits at most 7 per SM)
+#define BWD_MIN_BLOCKS(kind, nt) \
+  ((nt) == 128 ? ((kind) == LP_OCTAHEDRON || LP_BWD_BLOCKS < 7 ? LP_BWD_BLOCKS : 7) : 1)
 
 #ifdef LP_BWD_STATS
 // measurement build only (-DLP_BWD_STATS): warp-level event counts of the backward
@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_raster_cfg cf
 template <int KIND, int NT>
 __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_frame F, lp_raster_cfg cfg,
                                                                       const float *__restrict__ dL) {
+  static_assert(NT == 128, "paired pixel evaluation assumes 2 pixels per thread");
   using KD = Kind<KIND>;
   constexpr int RW = KD::RW, RW4 = RW / 4, PPT = 256 / NT, RG = KD::RG;
   constexpr int RGP = RG == 20 ? 20 : 28;      // padded row: 16-byte stores, conflict-free (RGP/4 odd)
@@ -345,14 +346,23 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
 #pragma unroll
       for (int a = 0; a < RGP; ++a) acc[a] = 0.f;
       bool hit = false;
+      if (any) {
+      // both pixels' entry / exit values as one paired evaluation (bitwise the forward's chord2);
+      // the entry / exit slab is resolved only for pixels the primitive actually hits
+      const float dx = fs(fx[0], rec[KD::CX]);
+      const float2 dy2 = fsub2(make_float2(fy[0], fy[1]), bc(rec[KD::CX + 1]));
+      Planes2<KIND> P;
+      planes2<KIND>(rec, dx, dy2, P);
+      float2 en2, ex2;
+      const float2 ch2 = chord2_of<KIND>(P, en2, ex2);
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        if (!test[k]) continue;
-        int se, sx;
-        const float dx = fs(fx[k], rec[KD::CX]), dy = fs(fy[k], rec[KD::CX + 1]);
-        const float ch = chord<KIND, true>(rec, dx, dy, se, sx);
-        if (!(ch > 0.f)) continue;
+        const float ch = lane_k(ch2, k);
+        if (!test[k] || !(ch > 0.f)) continue;
         hit = true;
+        int se, sx;
+        track_k<KIND>(P, k, lane_k(en2, k), lane_k(ex2, k), se, sx);
+        const float dy = lane_k(dy2, k);
         const float sig = rec[KD::SIGMA];
         const float E = transmit(sig, ch);
         const float o = 1.f - E;
@@ -388,6 +398,7 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
             acc[3 * s + 2] = fmaf(ws, dy, acc[3 * s + 2]);
           }
         }
+      }
       }
       // per-(warp, primitive) reduction of the <= 22 moments, one RED.F32 per moment: the hit
       // lanes stage their moments in compacted shared-memory rows, lane m < RG sums column m
@@ -426,15 +437,6 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
 }
 
 // ---------------------------------------------------------------------------------------------
-// Backward CTA size = 256 / pixels-per-thread.  The tuning knob LP_BWD_NT (64 or 256) exists for
-// measurement only; the defaults are the measured best.
-static int nt_from_env(const char *name, int dflt) {
-  const char *s = getenv(name);
-  if (!s) return dflt;
-  const int v = atoi(s);
-  return (v == 64 || v == 128 || v == 256) ? v : dflt;
-}
-
 template <bool STATS, bool AUX>
 static void fwd_k(const lp_frame &F, const lp_raster_cfg &cfg, float *image, float *depth, float *alpha,
                   cudaStream_t st) {
@@ -442,13 +444,6 @@ static void fwd_k(const lp_frame &F, const lp_raster_cfg &cfg, float *image, flo
   if (F.kind == LP_OCTAHEDRON)
     k_raster_fwd<LP_OCTAHEDRON, STATS, AUX><<<tiles, 128, 0, st>>>(F, cfg, image, depth, alpha);
   else k_raster_fwd<LP_TETRAHEDRON, STATS, AUX><<<tiles, 128, 0, st>>>(F, cfg, image, depth, alpha);
-}
-
-template <int NT>
-static void bwd_nt(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL, cudaStream_t st) {
-  const int tiles = F.tiles_x * F.tiles_y;
-  if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, NT><<<tiles, NT, 0, st>>>(F, cfg, dL);
-  else k_raster_bwd<LP_TETRAHEDRON, (NT > 128 ? 128 : NT)><<<tiles, (NT > 128 ? 128 : NT), 0, st>>>(F, cfg, dL);
 }
 
 void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image, float *depth, float *alpha,
@@ -464,10 +459,9 @@ void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image
 }
 
 void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL, cudaStream_t st) {
-  static const int nt = nt_from_env("LP_BWD_NT", 128);
-  if (nt == 64) bwd_nt<64>(F, cfg, dL, st);
-  else if (nt == 256) bwd_nt<256>(F, cfg, dL, st);
-  else bwd_nt<128>(F, cfg, dL, st);
+  const int tiles = F.tiles_x * F.tiles_y;
+  if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, 128><<<tiles, 128, 0, st>>>(F, cfg, dL);
+  else k_raster_bwd<LP_TETRAHEDRON, 128><<<tiles, 128, 0, st>>>(F, cfg, dL);
 }
 
 }  // namespace lp
