@@ -133,7 +133,10 @@ typedef struct {
 /* Gradient sinks, device fp32, same layout as lp_prims; += semantics.  Any may be NULL. */
 typedef struct {
   float *pos, *rot, *dist, *opacity, *sh;
-  float *mean2d_abs;          /* [n] += |dL/d c_ray.xy| per view (densification statistic) or NULL */
+  float *mean2d_abs;          /* [n] += |dL/d c_ray.xy| per view, pixel units (densification statistic,
+                                 P:252-260, #26) or NULL */
+  float *vis_count;           /* [n] += number of the call's views with tiles_touched > 0 (the statistic's
+                                 denominator) or NULL */
 } lp_grads;
 
 int32_t     lp_abi_version(void);
@@ -205,6 +208,15 @@ lp_status lp_frame_counters(const lp_frame *frame, uint32_t *host_counters /* [L
  * (written, not accumulated) and loss_sum[0] += scale * sum |C - target| (device float). */
 lp_status lp_l1_grad(const float *image, const float *target, float *dL_dimage, float *loss_sum,
                      int64_t n, float scale, void *stream);
+
+/* f4 (#26): 3D smoothing filter size per primitive from the training
+ * cameras, s_3d = kappa * min over the cameras that see the centre (p_z > znear, projection inside
+ * [0, W] x [0, H]) of p_z / fx, or kappa |p| / fx of the nearest camera when none sees it.
+ * pos: device [3][n] world centres; cams_dev: DEVICE array of n_cams lp_camera (unlike the other
+ * entry points, so any number of training cameras fits); filter3d: device [n] fp32, written.
+ * Feed the result to lp_prims.filter3d (d -> sqrt(d^2 + s^2)). */
+lp_status lp_filter3d(const float *pos, int32_t n, const lp_camera *cams_dev, int32_t n_cams, float kappa,
+                      float *filter3d, void *stream);
 
 /* f1 (#25): the 3DGS loss L = (1 - lambda) L1 + lambda (1 - SSIM) of
  * n_planes fp32 image planes [n_planes][height][width] (n_views * 3 channels, CHW per view) and its

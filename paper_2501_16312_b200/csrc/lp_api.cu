@@ -327,6 +327,13 @@ lp_status lp_l1_grad(const float *image, const float *target, float *dL_dimage, 
   return last_error();
 }
 
+lp_status lp_filter3d(const float *pos, int32_t n, const lp_camera *cams_dev, int32_t n_cams, float kappa,
+                      float *filter3d, void *stream) {
+  if (n < 0 || n_cams < 1 || !cams_dev || !filter3d || (n > 0 && !pos) || !(kappa >= 0.f)) return LP_ERR_ARG;
+  launch_filter3d(pos, n, cams_dev, n_cams, kappa, filter3d, static_cast<cudaStream_t>(stream));
+  return last_error();
+}
+
 lp_status lp_loss_grad(const float *image, const float *target, float *dL_dimage, float *loss_sum, int32_t n_planes,
                        int32_t height, int32_t width, float lambda, float scale, void *stream) {
   if (!image || !target || !dL_dimage || !loss_sum || n_planes < 0 || height < 0 || width < 0 || n_planes > 65535 ||

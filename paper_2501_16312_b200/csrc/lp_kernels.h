@@ -42,6 +42,9 @@ void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float 
 // C5 helpers (lp_train.cu)
 void launch_l1_grad(const float *img, const float *tgt, float *dL, float *loss, int64_t n, float scale,
                     cudaStream_t st);
+// f4 (lp_train.cu): 3D smoothing filter size; cams in device memory
+void launch_filter3d(const float *pos, int n, const lp_camera *cams, int nc, float kappa, float *out,
+                     cudaStream_t st);
 // f1 (lp_loss.cu): fused L1 + SSIM loss and gradient over n_planes [H][W] planes
 void launch_loss_ssim(const float *img, const float *tgt, float *dL, float *loss_sum, int n_planes, int H, int W,
                       float lam, float scale, cudaStream_t st);

@@ -502,6 +502,7 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd(lp_prims P, float kappa, 
 #pragma unroll
     for (int v = 0; v < LP_MAXV; ++v)
       if (v < V.nv && V.tt[v][i] != 0) vis |= 1u << v;
+    if (Gs.vis_count && vis) Gs.vis_count[i] += (float)__popc(vis);   // densification denominator
     float probe[LP_MAXV];
 #pragma unroll
     for (int v = 0; v < LP_MAXV; ++v) {

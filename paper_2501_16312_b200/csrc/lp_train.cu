@@ -60,6 +60,52 @@ void launch_l1_grad(const float *img, const float *tgt, float *dL, float *loss, 
   k_l1_grad<<<grid, 256, 0, st>>>(img, tgt, dL, loss, n, scale);
 }
 
+// ---------------------------------------------------------------------------------------------
+// f4: 3D smoothing filter size from the training cameras (#26).
+// One thread per primitive; the cameras are staged through shared memory 64 at a time.
+__global__ void __launch_bounds__(256) k_filter3d(const float *__restrict__ pos, int n,
+                                                  const lp_camera *__restrict__ cams, int nc, float kappa,
+                                                  float *__restrict__ out) {
+  __shared__ lp_camera s_cam[64];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  float c[3] = {0.f, 0.f, 0.f};
+  if (i < n) {
+    c[0] = pos[i];
+    c[1] = pos[n + i];
+    c[2] = pos[2 * n + i];
+  }
+  float best = INFINITY, near_d = INFINITY, near_v = 0.f;
+  for (int c0 = 0; c0 < nc; c0 += 64) {
+    const int m = nc - c0 < 64 ? nc - c0 : 64;
+    __syncthreads();
+    if (threadIdx.x < m) s_cam[threadIdx.x] = cams[c0 + threadIdx.x];
+    __syncthreads();
+    for (int v = 0; v < m; ++v) {
+      const lp_camera &cam = s_cam[v];
+      float p[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+        p[r] = fmaf(cam.W[3 * r + 2], c[2], fmaf(cam.W[3 * r + 1], c[1], fmaf(cam.W[3 * r], c[0], cam.t[r])));
+      if (p[2] > cam.znear) {
+        const float u = fmaf(cam.fx, p[0] / p[2], cam.cx), w = fmaf(cam.fy, p[1] / p[2], cam.cy);
+        if (u >= 0.f && u <= (float)cam.width && w >= 0.f && w <= (float)cam.height) best = fminf(best, p[2] / cam.fx);
+      }
+      const float d = sqrtf(fmaf(p[0], p[0], fmaf(p[1], p[1], p[2] * p[2])));
+      if (d < near_d) {
+        near_d = d;
+        near_v = d / cam.fx;
+      }
+    }
+  }
+  if (i < n) out[i] = kappa * (best < INFINITY ? best : near_v);
+}
+
+void launch_filter3d(const float *pos, int n, const lp_camera *cams, int nc, float kappa, float *out,
+                     cudaStream_t st) {
+  if (n <= 0) return;
+  k_filter3d<<<(n + 255) / 256, 256, 0, st>>>(pos, n, cams, nc, kappa, out);
+}
+
 struct AdamGroups {
   int64_t begin[8], end[8];
   float lr[8];

@@ -60,7 +60,7 @@ class lp_adam_group(C.Structure):
 
 
 class lp_grads(C.Structure):
-    _fields_ = [(f, _p) for f in ("pos", "rot", "dist", "opacity", "sh", "mean2d_abs")]
+    _fields_ = [(f, _p) for f in ("pos", "rot", "dist", "opacity", "sh", "mean2d_abs", "vis_count")]
 
 
 _sig = {
@@ -84,6 +84,7 @@ _sig = {
                                     C.POINTER(lp_raster_cfg), C.POINTER(lp_frame), C.POINTER(lp_grads), _p]),
     "lp_frame_counters": (C.c_int, [C.POINTER(lp_frame), C.POINTER(C.c_uint32), _p]),
     "lp_l1_grad": (C.c_int, [_p, _p, _p, _p, C.c_int64, C.c_float, _p]),
+    "lp_filter3d": (C.c_int, [_p, C.c_int32, _p, C.c_int32, C.c_float, _p, _p]),
     "lp_loss_grad": (C.c_int, [_p, _p, _p, _p, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_float, _p]),
     "lp_adam_step": (C.c_int, [_p, _p, _p, _p, C.POINTER(lp_adam_group), C.c_int32, C.c_float, C.c_float,
                                C.c_float, C.c_int32, C.c_int32, _p]),
@@ -182,6 +183,12 @@ def lp_l1_grad(image, target, dL, loss_sum, scale, stream):
                                   C.c_float(scale), _stream(stream)), "lp_l1_grad")
 
 
+def lp_filter3d(pos, n, cams_dev, n_cams, kappa, out, stream):
+    """pos: device [3, n] fp32; cams_dev: device uint8 tensor holding n_cams lp_camera structs."""
+    return _check(_lib.lp_filter3d(_ptr(pos), int(n), _ptr(cams_dev), int(n_cams), C.c_float(kappa), _ptr(out),
+                                   _stream(stream)), "lp_filter3d")
+
+
 def lp_loss_grad(image, target, dL, loss_sum, lam, scale, stream):
     """image / target / dL: contiguous [..., H, W] fp32 tensors (all leading dims are planes)."""
     H, W = image.shape[-2], image.shape[-1]
@@ -232,9 +239,10 @@ def prims_struct(kind, n, sh_degree, pos, rot, dist, opacity, sh, filter3d=None)
     return p
 
 
-def grads_struct(pos=None, rot=None, dist=None, opacity=None, sh=None, mean2d_abs=None) -> lp_grads:
+def grads_struct(pos=None, rot=None, dist=None, opacity=None, sh=None, mean2d_abs=None,
+                 vis_count=None) -> lp_grads:
     g = lp_grads()
     for f, t in (("pos", pos), ("rot", rot), ("dist", dist), ("opacity", opacity), ("sh", sh),
-                 ("mean2d_abs", mean2d_abs)):
+                 ("mean2d_abs", mean2d_abs), ("vis_count", vis_count)):
         setattr(g, f, None if t is None else t.data_ptr())
     return g

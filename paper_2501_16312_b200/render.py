@@ -37,6 +37,7 @@ class DeviceScene:
             o += size
         self.filter3d = None if filter3d is None else torch.as_tensor(filter3d, dtype=torch.float32, device=device)
         self.mean2d = None
+        self.vis_count = None
         self._rebuild()
 
     def view(self, name, grad=False):
@@ -48,12 +49,25 @@ class DeviceScene:
         self.prims = L.prims_struct(self.kind, self.n, self.sh_degree, v["pos"], v["rot"], v["dist"], v["opacity"],
                                     v["sh"], self.filter3d)
         g = {k: self.view(k, grad=True) for k in self.offsets}
-        self.grads = L.grads_struct(g["pos"], g["rot"], g["dist"], g["opacity"], g["sh"],
-                                    None if self.mean2d is None else self.mean2d)
+        self.grads = L.grads_struct(g["pos"], g["rot"], g["dist"], g["opacity"], g["sh"], self.mean2d,
+                                    self.vis_count)
 
     def track_mean2d(self):
+        """Accumulate the densification statistics (lp_grads.mean2d_abs / vis_count) from now on."""
         self.mean2d = torch.zeros(self.n, dtype=torch.float32, device=self.flat.device)
+        self.vis_count = torch.zeros(self.n, dtype=torch.float32, device=self.flat.device)
         self._rebuild()
+
+    def set_filter3d(self, cams, kappa):
+        """s_3d from training cameras (lp_filter3d, f4) -> lp_prims.filter3d for the following calls."""
+        arr = L.cameras(cams)
+        raw = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(self.flat.device)
+        out = torch.empty(self.n, dtype=torch.float32, device=self.flat.device)
+        b, e = self.offsets["pos"]
+        L.lp_filter3d(self.flat[b:e], self.n, raw, len(cams), kappa, out, torch.cuda.current_stream(self.flat.device))
+        self.filter3d = out
+        self._rebuild()
+        return out
 
     def grad_dict(self):
         return {k: self.view(k, grad=True) for k in self.offsets}
