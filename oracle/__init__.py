@@ -70,7 +70,7 @@ class _Pre(C.Structure):
 
 
 class _RenderCfg(C.Structure):
-    _fields_ = [("bg", C.c_float * 3), ("t_stop", C.c_float), ("brute", C.c_int32)]
+    _fields_ = [("bg", C.c_float * 3), ("t_stop", C.c_float), ("brute", C.c_int32), ("exact", C.c_int32)]
 
 
 def _ptr(a):
@@ -134,8 +134,9 @@ class Pre:
         return p
 
 
-def preprocess(scene: Scene, cam, kappa=0.1, mode=0, den_override=None) -> Pre:
-    """Per-primitive geometry (mode 0 canonical fp32, 1 fp64), Eq. 1 sigma and SH colour."""
+def preprocess(scene: Scene, cam, kappa=0.1, mode=0, den_override=None, exact=False) -> Pre:
+    """Per-primitive geometry (mode 0 canonical fp32, 1 fp64), Eq. 1 sigma and SH colour.
+    exact: the "no ray space" variant (App. D): camera-space geometry, perspective bbox, no 2D filter."""
     n = scene.n
     K = 3 if scene.kind == OCTA else 4
     out = Pre(flag=np.zeros(n, np.int32), tiles_touched=np.zeros(n, np.uint32),
@@ -145,7 +146,7 @@ def preprocess(scene: Scene, cam, kappa=0.1, mode=0, den_override=None) -> Pre:
               rgb=np.zeros((n, 3), np.float64))
     den = None if den_override is None else np.ascontiguousarray(den_override, np.float64)
     s, c, p = scene.c(), camera(cam), out.c()
-    rc = lib().lpo_preprocess(C.byref(s), C.byref(c), C.c_float(kappa), C.c_int32(mode),
+    rc = lib().lpo_preprocess(C.byref(s), C.byref(c), C.c_float(kappa), C.c_int32(mode), C.c_int32(1 if exact else 0),
                               C.c_void_p(_ptr(den)), C.byref(p))
     assert rc == 0
     return out
@@ -191,7 +192,7 @@ class RenderOut:
 
 
 def render(scene: Scene, cam, pre: Pre, vals, ranges, bg=(0.0, 0.0, 0.0), t_stop=1e-3,
-           pix=None, dL_dimage=None, brute=False) -> RenderOut:
+           pix=None, dL_dimage=None, brute=False, exact=False) -> RenderOut:
     """MTIA rasterisation of the requested pixels (all when pix is None), optional backward."""
     W, H = int(cam["width"]), int(cam["height"])
     n = scene.n
@@ -200,6 +201,7 @@ def render(scene: Scene, cam, pre: Pre, vals, ranges, bg=(0.0, 0.0, 0.0), t_stop
     cfg.bg[:] = [float(b) for b in bg]
     cfg.t_stop = float(t_stop)
     cfg.brute = 1 if brute else 0
+    cfg.exact = 1 if exact else 0
     out = RenderOut(image=np.zeros((3, H, W), np.float64), T_final=np.zeros((H, W), np.float64),
                     n_proc=np.zeros((H, W), np.int32), m_stop=np.full((H, W), np.inf),
                     m_face=np.full((H, W), np.inf), counters=np.zeros(2, np.int64),
@@ -239,13 +241,14 @@ class Grads:
     sh: np.ndarray
 
 
-def preprocess_bwd(scene: Scene, cam, pre: Pre, r: RenderOut, den_override=None) -> Grads:
+def preprocess_bwd(scene: Scene, cam, pre: Pre, r: RenderOut, den_override=None, exact=False) -> Grads:
     n = scene.n
     g = Grads(pos=np.zeros((3, n)), rot=np.zeros((4, n)), dist=np.zeros(scene.dist.shape),
               opacity=np.zeros(n), sh=np.zeros(scene.sh.shape))
     den = None if den_override is None else np.ascontiguousarray(den_override, np.float64)
     s, c, p = scene.c(), camera(cam), pre.c()
-    rc = lib().lpo_preprocess_bwd(C.byref(s), C.byref(c), C.byref(p), C.c_void_p(_ptr(den)),
+    rc = lib().lpo_preprocess_bwd(C.byref(s), C.byref(c), C.byref(p), C.c_int32(1 if exact else 0),
+                                  C.c_void_p(_ptr(den)),
                                   C.c_void_p(_ptr(r.dv)), C.c_void_p(_ptr(r.dsigma)), C.c_void_p(_ptr(r.drgb)),
                                   C.c_void_p(_ptr(g.pos)), C.c_void_p(_ptr(g.rot)), C.c_void_p(_ptr(g.dist)),
                                   C.c_void_p(_ptr(g.opacity)), C.c_void_p(_ptr(g.sh)))
@@ -274,19 +277,19 @@ class Forward:
 
 
 def forward(scene, cam, kappa=0.1, mode=0, bg=(0, 0, 0), t_stop=1e-3, pix=None, den_override=None,
-            dL_dimage=None, tile_mask=None, brute=False) -> Forward:
-    pre = preprocess(scene, cam, kappa=kappa, mode=mode, den_override=den_override)
+            dL_dimage=None, tile_mask=None, brute=False, exact=False) -> Forward:
+    pre = preprocess(scene, cam, kappa=kappa, mode=mode, den_override=den_override, exact=exact)
     keys, vals, ranges = bin_tiles(pre, cam["width"], cam["height"], tile_mask=tile_mask)
     out = render(scene, cam, pre, vals, ranges, bg=bg, t_stop=t_stop, pix=pix, dL_dimage=dL_dimage,
-                 brute=brute)
+                 brute=brute, exact=exact)
     return Forward(pre, keys, vals, ranges, out)
 
 
 def forward_backward(scene, cam, dL_dimage, kappa=0.1, mode=0, bg=(0, 0, 0), t_stop=1e-3, pix=None,
-                     den_override=None, tile_mask=None):
+                     den_override=None, tile_mask=None, exact=False):
     f = forward(scene, cam, kappa=kappa, mode=mode, bg=bg, t_stop=t_stop, pix=pix,
-                den_override=den_override, dL_dimage=dL_dimage, tile_mask=tile_mask)
-    g = preprocess_bwd(scene, cam, f.pre, f.out, den_override=den_override)
+                den_override=den_override, dL_dimage=dL_dimage, tile_mask=tile_mask, exact=exact)
+    g = preprocess_bwd(scene, cam, f.pre, f.out, den_override=den_override, exact=exact)
     return f, g
 
 
@@ -307,3 +310,21 @@ def mtia_grad(A, B, C_, r, u, v, d):
                         C.c_double(r[0]), C.c_double(r[1]), C.c_double(u), C.c_double(v), C.c_double(d),
                         C.c_void_p(di.ctypes.data))
     return di
+
+
+def mtia3(A, B, C_, r):
+    """(hit, u, v, det, t) of the 3-D Moller-Trumbore test of the ray t r (origin 0), App. D mode."""
+    out = np.zeros(4)
+    A, B, C_, r = (np.ascontiguousarray(x, np.float64) for x in (A, B, C_, r))
+    hit = lib().lpo_mtia3(C.c_void_p(A.ctypes.data), C.c_void_p(B.ctypes.data), C.c_void_p(C_.ctypes.data),
+                          C.c_void_p(r.ctypes.data), C.c_void_p(out.ctypes.data))
+    return bool(hit), out[0], out[1], out[2], out[3]
+
+
+def mtia3_grad(A, B, C_, r):
+    """d t / d(A, B, C) [3][3] of the 3-D hit (zeros on a miss)."""
+    dt = np.zeros((3, 3))
+    A, B, C_, r = (np.ascontiguousarray(x, np.float64) for x in (A, B, C_, r))
+    lib().lpo_mtia3_grad(C.c_void_p(A.ctypes.data), C.c_void_p(B.ctypes.data), C.c_void_p(C_.ctypes.data),
+                         C.c_void_p(r.ctypes.data), C.c_void_p(dt.ctypes.data))
+    return dt

@@ -32,6 +32,7 @@
 #define REAL float
 #define GTYPE geom_f
 #define GFN geom_f32
+#define GFN_RECT geom_rect_f32
 #define RSQRT(x) sqrtf(x)
 #define RCEIL(x) ceilf(x)
 #define RFLOOR(x) floorf(x)
@@ -40,6 +41,7 @@
 #undef REAL
 #undef GTYPE
 #undef GFN
+#undef GFN_RECT
 #undef RSQRT
 #undef RCEIL
 #undef RFLOOR
@@ -48,6 +50,7 @@
 #define REAL double
 #define GTYPE geom_d
 #define GFN geom_f64
+#define GFN_RECT geom_rect_f64
 #define RSQRT(x) sqrt(x)
 #define RCEIL(x) ceil(x)
 #define RFLOOR(x) floor(x)
@@ -56,6 +59,7 @@
 #undef REAL
 #undef GTYPE
 #undef GFN
+#undef GFN_RECT
 #undef RSQRT
 #undef RCEIL
 #undef RFLOOR
@@ -140,7 +144,7 @@ static double min_dhat(const lpo_scene *s, int i)
   return m;
 }
 
-int lpo_preprocess(const lpo_scene *s, const lpo_camera *cam, float kappa, int32_t mode,
+int lpo_preprocess(const lpo_scene *s, const lpo_camera *cam, float kappa, int32_t mode, int32_t exact,
                    const double *den_override, lpo_pre *out)
 {
   if (!s || !cam || !out || (s->kind != LPO_OCTA && s->kind != LPO_TETRA)) return -1;
@@ -157,10 +161,10 @@ int lpo_preprocess(const lpo_scene *s, const lpo_camera *cam, float kappa, int32
     double geo[15];
     if (mode == 0) {
       geom_f g;
-      geom_f32(s, cam, i, kappa, &g);
+      geom_f32(s, cam, i, kappa, exact, &g);
       flag = g.flag; tt = g.tiles_touched; key = g.depth_key;
       memcpy(rect, g.rect, sizeof(rect));
-      geo[0] = g.cr_x; geo[1] = g.cr_y; geo[2] = g.l;
+      geo[0] = g.cr_x; geo[1] = g.cr_y; geo[2] = exact ? g.cz : g.l;
       for (int j = 0; j < K; ++j)
         for (int a = 0; a < 3; ++a) geo[3 + 3 * j + a] = g.off[j][a];
       if (out->canon) {
@@ -171,10 +175,10 @@ int lpo_preprocess(const lpo_scene *s, const lpo_camera *cam, float kappa, int32
       }
     } else {
       geom_d g;
-      geom_f64(s, cam, i, kappa, &g);
+      geom_f64(s, cam, i, kappa, exact, &g);
       flag = g.flag; tt = g.tiles_touched; key = g.depth_key;
       memcpy(rect, g.rect, sizeof(rect));
-      geo[0] = g.cr_x; geo[1] = g.cr_y; geo[2] = g.l;
+      geo[0] = g.cr_x; geo[1] = g.cr_y; geo[2] = exact ? g.cz : g.l;
       for (int j = 0; j < K; ++j)
         for (int a = 0; a < 3; ++a) geo[3 + 3 * j + a] = g.off[j][a];
       if (out->canon) memset(out->canon + (size_t)i * NC, 0, sizeof(float) * NC);
@@ -356,6 +360,49 @@ static void mtia_grad(const double A[3], const double B[3], const double C[3], d
   }
 }
 
+/* 3-D Moller-Trumbore (the "no ray space" variant, App. D): ray t r from the camera centre
+ * against triangle (A, B, C) in camera space.  Returns 1 on a hit with t > 0, barycentrics
+ * (u, v), determinant d = e1 . (r x e2) and the ray parameter t (the camera-space depth, r_z = 1). */
+static int mtia3(const double A[3], const double B[3], const double C[3], const double r[3],
+                 double *u, double *v, double *d, double *t)
+{
+  double e1[3] = {B[0] - A[0], B[1] - A[1], B[2] - A[2]};
+  double e2[3] = {C[0] - A[0], C[1] - A[1], C[2] - A[2]};
+  double P[3] = {r[1] * e2[2] - r[2] * e2[1], r[2] * e2[0] - r[0] * e2[2], r[0] * e2[1] - r[1] * e2[0]};
+  double det = e1[0] * P[0] + e1[1] * P[1] + e1[2] * P[2];
+  double scale = (fabs(e1[0]) + fabs(e1[1]) + fabs(e1[2])) * (fabs(e2[0]) + fabs(e2[1]) + fabs(e2[2]));
+  if (fabs(det) <= 1e-14 * scale) return 0;
+  double T[3] = {-A[0], -A[1], -A[2]};
+  double uu = (T[0] * P[0] + T[1] * P[1] + T[2] * P[2]) / det;
+  double Q[3] = {T[1] * e1[2] - T[2] * e1[1], T[2] * e1[0] - T[0] * e1[2], T[0] * e1[1] - T[1] * e1[0]};
+  double vv = (r[0] * Q[0] + r[1] * Q[1] + r[2] * Q[2]) / det;
+  if (uu < 0.0 || vv < 0.0 || uu + vv > 1.0) return 0;
+  double tt = (e2[0] * Q[0] + e2[1] * Q[1] + e2[2] * Q[2]) / det;
+  if (!(tt > 0.0)) return 0;
+  *u = uu; *v = vv; *d = det; *t = tt;
+  return 1;
+}
+
+/* d t / d(A, B, C) of the hit above, from t = (n . A)/(n . r), n = (B - A) x (C - A):
+ * with w = A - t r:  dt/dB = (e2 x w)/(n . r),  dt/dC = (w x e1)/(n . r),
+ *                    dt/dA = (n - e2 x w - w x e1)/(n . r). */
+static void mtia3_grad(const double A[3], const double B[3], const double C[3], const double r[3], double t,
+                       double dt[3][3])
+{
+  double e1[3] = {B[0] - A[0], B[1] - A[1], B[2] - A[2]};
+  double e2[3] = {C[0] - A[0], C[1] - A[1], C[2] - A[2]};
+  double n[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+  double D = n[0] * r[0] + n[1] * r[1] + n[2] * r[2];
+  double w[3] = {A[0] - t * r[0], A[1] - t * r[1], A[2] - t * r[2]};
+  double gB[3] = {e2[1] * w[2] - e2[2] * w[1], e2[2] * w[0] - e2[0] * w[2], e2[0] * w[1] - e2[1] * w[0]};
+  double gC[3] = {w[1] * e1[2] - w[2] * e1[1], w[2] * e1[0] - w[0] * e1[2], w[0] * e1[1] - w[1] * e1[0]};
+  for (int a = 0; a < 3; ++a) {
+    dt[1][a] = gB[a] / D;
+    dt[2][a] = gC[a] / D;
+    dt[0][a] = (n[a] - gB[a] - gC[a]) / D;
+  }
+}
+
 typedef struct {
   int32_t prim;
   double o, chord, E, T_before;
@@ -363,10 +410,12 @@ typedef struct {
   double u_in, v_in, d_in, u_out, v_out, d_out;
 } hit_rec;
 
+/* exact (App. D): r = perspective ray of the pixel, depths are ray parameters t, and the chord
+ * and entry are scaled by |r| to Euclidean lengths (r_z = 1). */
 static void primitive_hit(int kind, const double *geo, double rx, double ry, double *chord,
                           int *f_in, double *u_in, double *v_in, double *d_in,
                           int *f_out, double *u_out, double *v_out, double *d_out, int *nhits,
-                          double *entry)
+                          double *entry, int exact, const double r[3])
 {
   double V[6][3];
   vertices(kind, geo, V);
@@ -377,26 +426,37 @@ static void primitive_hit(int kind, const double *geo, double rx, double ry, dou
     int idx[3];
     face_indices(kind, f, idx);
     double u, v, d, dep;
-    if (!mtia(V[idx[0]], V[idx[1]], V[idx[2]], rx, ry, &u, &v, &d, &dep)) continue;
+    int hit = exact ? mtia3(V[idx[0]], V[idx[1]], V[idx[2]], r, &u, &v, &d, &dep)
+                    : mtia(V[idx[0]], V[idx[1]], V[idx[2]], rx, ry, &u, &v, &d, &dep);
+    if (!hit) continue;
     ++cnt;
     if (dep < lo) { lo = dep; *f_in = f; *u_in = u; *v_in = v; *d_in = d; }
     if (dep > hi) { hi = dep; *f_out = f; *u_out = u; *v_out = v; *d_out = d; }
   }
   *nhits = cnt;
   /* reading 4: chord = max - min over all hits if >= 2 hits, else 0 */
-  *chord = cnt >= 2 ? hi - lo : 0.0;
-  *entry = lo;   /* i1, the entry depth */
+  double rn = exact ? sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]) : 1.0;
+  *chord = cnt >= 2 ? (hi - lo) * rn : 0.0;
+  *entry = lo * rn;   /* i1, the entry depth (exact: Euclidean distance from the camera) */
+  if (exact) { *d_in = lo; *d_out = hi; }   /* exact mode keeps the hit parameters t for the backward */
 }
 
 static void add_face_grad(int kind, const double *geo, int f, double u, double v, double d,
-                          double rx, double ry, double dLdi, double *dvp)
+                          double rx, double ry, double dLdi, double *dvp, int exact, const double r[3])
 {
   double V[6][3];
   vertices(kind, geo, V);
   int idx[3];
   face_indices(kind, f, idx);
   double di[3][3];
-  mtia_grad(V[idx[0]], V[idx[1]], V[idx[2]], rx, ry, u, v, d, di);
+  if (exact) {
+    /* d is the hit parameter t here; chord = (t_out - t_in)|r| */
+    double rn = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+    mtia3_grad(V[idx[0]], V[idx[1]], V[idx[2]], r, d, di);
+    dLdi *= rn;
+  } else {
+    mtia_grad(V[idx[0]], V[idx[1]], V[idx[2]], rx, ry, u, v, d, di);
+  }
   for (int k = 0; k < 3; ++k)
     for (int a = 0; a < 3; ++a) {
       double val = dLdi * di[k][a];
@@ -457,6 +517,8 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
       int64_t p = pix ? pix[q] : q;
       int px = (int)(p % W), py = (int)(p / W);
       double rx = px + 0.5, ry = py + 0.5;
+      const double rv[3] = {(rx - (double)cam->cx) / (double)cam->fx, (ry - (double)cam->cy) / (double)cam->fy, 1.0};
+      const int exact = cfg->exact;
       const uint32_t *list;
       int64_t cnt;
       if (cfg->brute) { list = bl; cnt = nb; }
@@ -476,7 +538,7 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
         int f_in = 0, f_out = 0, nhit;
         double i1;
         primitive_hit(kind, geo, rx, ry, &chord, &f_in, &u_in, &v_in, &d_in, &f_out, &u_out,
-                      &v_out, &d_out, &nhit, &i1);
+                      &v_out, &d_out, &nhit, &i1, exact, rv);
         if (!(chord > 0.0)) continue;
         /* opacity from the chord, App. E */
         double sig = pre->sigma[i];
@@ -540,8 +602,8 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
           double g = sig * h->E * dLdo;     /* dL/d i2 = g, dL/d i1 = -g */
           const double *geo = pre->geom + (size_t)i * G;
           double *dvp = dv + (size_t)i * NV * 3;
-          add_face_grad(kind, geo, h->f_in, h->u_in, h->v_in, h->d_in, rx, ry, -g, dvp);
-          add_face_grad(kind, geo, h->f_out, h->u_out, h->v_out, h->d_out, rx, ry, g, dvp);
+          add_face_grad(kind, geo, h->f_in, h->u_in, h->v_in, h->d_in, rx, ry, -g, dvp, exact, rv);
+          add_face_grad(kind, geo, h->f_out, h->u_out, h->v_out, h->d_out, rx, ry, g, dvp, exact, rv);
           if (face_margin) {
             double m = bary_margin(h->u_in, h->v_in), m2 = bary_margin(h->u_out, h->v_out);
             if (m2 < m) m = m2;
@@ -561,7 +623,7 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
 /* ------------------------------------------------------------------ */
 /* preprocess backward, fp64          */
 /* ------------------------------------------------------------------ */
-int lpo_preprocess_bwd(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
+int lpo_preprocess_bwd(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre, int32_t exact,
                        const double *den_override, const double *dv, const double *dsigma,
                        const double *drgb, double *g_pos, double *g_rot, double *g_dist,
                        double *g_opacity, double *g_sh)
@@ -629,12 +691,12 @@ int lpo_preprocess_bwd(const lpo_scene *s, const lpo_camera *cam, const lpo_pre 
     }
     /* the 2D filter adds a constant (fixed index) -> identity */
 
-    /* o_j = J oc_j, oc_j = W ow_j */
+    /* o_j = J oc_j, oc_j = W ow_j  (exact mode: the vertices are p +- oc_j, no J) */
     double gJ[3][3] = {{0}}, gp[3] = {0, 0, 0}, gR[3][3] = {{0}}, gdh[4] = {0, 0, 0, 0};
     for (int j = 0; j < K; ++j) {
       double goc[3], gow[3];
       for (int a = 0; a < 3; ++a)
-        goc[a] = J[0][a] * go[j][0] + J[1][a] * go[j][1] + J[2][a] * go[j][2];
+        goc[a] = exact ? go[j][a] : J[0][a] * go[j][0] + J[1][a] * go[j][1] + J[2][a] * go[j][2];
       for (int r = 0; r < 3; ++r)
         for (int a = 0; a < 3; ++a) gJ[r][a] += go[j][r] * oc[j][a];
       for (int a = 0; a < 3; ++a)
@@ -646,10 +708,14 @@ int lpo_preprocess_bwd(const lpo_scene *s, const lpo_camera *cam, const lpo_pre 
       for (int r = 0; r < 3; ++r)
         for (int cc = 0; cc < 3; ++cc) gR[r][cc] += dh[j] * gow[r] * bvec[j][cc];
     }
-    /* centre: c_r = phi(p), d phi / dp = J */
-    for (int a = 0; a < 3; ++a) gp[a] += J[0][a] * gcr[0] + J[1][a] * gcr[1] + J[2][a] * gcr[2];
-    /* dJ/dp terms ("impact of the position on the ray space approximation") */
-    {
+    /* centre: c_r = phi(p), d phi / dp = J  (exact mode: the centre is p itself) */
+    if (exact) {
+      for (int a = 0; a < 3; ++a) gp[a] += gcr[a];
+    } else {
+      for (int a = 0; a < 3; ++a) gp[a] += J[0][a] * gcr[0] + J[1][a] * gcr[1] + J[2][a] * gcr[2];
+    }
+    /* dJ/dp terms ("impact of the position on the ray space approximation"); gJ = 0 in exact mode */
+    if (!exact) {
       double pz = p[2], pz2 = pz * pz, pz3 = pz2 * pz;
       gp[2] += gJ[0][0] * (-fx / pz2);
       gp[0] += gJ[0][2] * (-fx / pz2);
@@ -711,6 +777,20 @@ int lpo_preprocess_bwd(const lpo_scene *s, const lpo_camera *cam, const lpo_pre 
     for (int a = 0; a < 3; ++a) g_pos[(size_t)a * n + i] += gc[a];
   }
   return 0;
+}
+
+int lpo_mtia3(const double *A, const double *B, const double *C, const double *r, double *out)
+{
+  /* out = (u, v, det, t) */
+  return mtia3(A, B, C, r, &out[0], &out[1], &out[2], &out[3]);
+}
+
+void lpo_mtia3_grad(const double *A, const double *B, const double *C, const double *r, double *dt)
+{
+  double u, v, d, t, g[3][3];
+  if (!mtia3(A, B, C, r, &u, &v, &d, &t)) { memset(dt, 0, sizeof(g)); return; }
+  mtia3_grad(A, B, C, r, t, g);
+  memcpy(dt, g, sizeof(g));
 }
 
 /* ------------------------------------------------------------------ */

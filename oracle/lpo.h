@@ -58,7 +58,8 @@ typedef struct {
   uint32_t *tiles_touched; /* [n] */
   int32_t  *rect;          /* [n][4] tx0, ty0, tx1, ty1 (inclusive); zeros when tiles_touched == 0 */
   uint32_t *depth_key;     /* [n] bits of the fp32 ray-space depth l = |p| */
-  double   *geom;          /* [n][3 + 3K] c_r (x, y, l), then K post-filter ray-space offsets */
+  double   *geom;          /* [n][3 + 3K] c_r (x, y, l), then K post-filter ray-space offsets;
+                              exact mode: camera-space centre p, then K camera-space offsets */
   float    *canon;         /* [n][2 + 3K] fp32 cr_x, cr_y, offsets (mode 0 only; may be NULL) */
   double   *sigma;         /* [n] Eq. 1 */
   double   *sigma_den;     /* [n] 2 * min(dhat), the frozen denominator */
@@ -66,8 +67,11 @@ typedef struct {
 } lpo_pre;
 
 /* Preprocess every primitive.  mode 0 = canonical fp32 geometry, 1 = fp64 geometry.
+ * exact = 1: the "no ray space" variant (App. D): camera-space geometry, tile bbox
+ * from the perspective projections of the vertices (whole screen if a vertex has p_z <= 0),
+ * no 2D filter (kappa ignored); the depth key is still |p|.
  * den_override: NULL, or [n] frozen Eq. 1 denominators (finite-difference pins). */
-int lpo_preprocess(const lpo_scene *s, const lpo_camera *cam, float kappa, int32_t mode,
+int lpo_preprocess(const lpo_scene *s, const lpo_camera *cam, float kappa, int32_t mode, int32_t exact,
                    const double *den_override, lpo_pre *out);
 
 /* Bin visible primitives to tiles and order every tile's list by (depth key, id).
@@ -83,6 +87,9 @@ typedef struct {
   float bg[3];
   float t_stop;           /* stop once T < t_stop (include-then-stop), 0 disables */
   int32_t brute;          /* 1: ignore tiling, every valid primitive in (key, id) order */
+  int32_t exact;          /* 1: geometry from lpo_preprocess(exact = 1); per-pixel perspective rays
+                             r = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1) against the camera-space faces by
+                             3-D Moller-Trumbore, chord = (t_out - t_in) |r| (App. D) */
 } lpo_render_cfg;
 
 /* Render (and optionally backprop) a set of pixels.
@@ -108,11 +115,17 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
                double *face_margin, int64_t *counters, double *depth, double *m_depth);
 
 /* Chain ray-space gradients to the world features (+= into SoA fp64 gradients with the
- * same layout as the features).  Primitives with flag != 0 receive nothing. */
-int lpo_preprocess_bwd(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
+ * same layout as the features).  Primitives with flag != 0 receive nothing.
+ * exact = 1: dv are camera-space vertex gradients (render with cfg.exact = 1). */
+int lpo_preprocess_bwd(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre, int32_t exact,
                        const double *den_override, const double *dv, const double *dsigma,
                        const double *drgb, double *g_pos, double *g_rot, double *g_dist,
                        double *g_opacity, double *g_sh);
+
+/* exported for the pins only: 3-D Moller-Trumbore of the ray t r (origin 0) against triangle
+ * (A, B, C); out = (u, v, det, t); and d t / d(A, B, C) [3][3]. */
+int lpo_mtia3(const double *A, const double *B, const double *C, const double *r, double *out);
+void lpo_mtia3_grad(const double *A, const double *B, const double *C, const double *r, double *dt);
 
 #ifdef __cplusplus
 }
