@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 1
+#define LP_ABI_VERSION 2
 #define LP_TILE 16            /* 16 x 16 pixel tiles */
 
 typedef enum {
@@ -71,6 +71,10 @@ typedef struct {
   float t_stop;               /* stop once transmittance T < t_stop (1e-3), 0 disables */
   float bg[3];                /* background colour (reading 14) */
   int32_t count_stats;        /* 1: count iterated / intersected pairs into the frame counters */
+  int32_t exact;              /* 0: EWA ray space (the method); 1: the "no ray space" variant
+                                 (App. D, #27): per-pixel perspective rays against
+                                 the camera-space faces, perspective tile bbox, no 2D filter.  Must be the
+                                 same for every call on a frame. */
 } lp_raster_cfg;
 
 /* Per-view scratch carved from one caller-allocated device workspace by lp_frame_init.
@@ -79,7 +83,7 @@ typedef struct {
 typedef struct {
   int32_t kind, n, width, height, tiles_x, tiles_y;
   int64_t capacity;           /* maximum tile-list entries */
-  int32_t record_words;       /* floats per raster record (20 octa, 28 tetra) */
+  int32_t record_words;       /* record stride in floats (24 octa, 28 tetra) */
   int32_t rgrad_words;        /* floats per primitive in rgrad (20 octa, 22 tetra) */
   uint32_t *tiles_touched;    /* [n] */
   uint16_t *rect;             /* [n][4] tile rect tx0, ty0, tx1, ty1 (inclusive), zeros if none */

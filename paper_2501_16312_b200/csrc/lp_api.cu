@@ -15,7 +15,8 @@ using namespace lp;
 constexpr size_t ALIGN = 256;
 inline size_t up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
-inline int record_words(int kind) { return kind == LP_OCTAHEDRON ? Kind<LP_OCTAHEDRON>::RW : Kind<LP_TETRAHEDRON>::RW; }
+// record stride (words): room for both the ray-space and the exact-mode record
+inline int record_words(int kind) { return kind == LP_OCTAHEDRON ? Kind<LP_OCTAHEDRON>::RS : Kind<LP_TETRAHEDRON>::RS; }
 inline int rgrad_words(int kind) { return kind == LP_OCTAHEDRON ? 20 : 22; }
 inline int offsets_k(int kind) { return kind == LP_OCTAHEDRON ? 3 : 4; }
 
@@ -157,7 +158,7 @@ lp_status lp_frame_init(lp_frame *F, void *workspace, size_t bytes, int32_t kind
 lp_status lp_preprocess(const lp_prims *prims, const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg,
                         lp_frame *frames, void *stream) {
   if (check_prims(prims) != LP_OK || !cams || !cfg || !frames || n_views < 0) return LP_ERR_ARG;
-  if (!(cfg->aa_kernel >= 0.f)) return LP_ERR_ARG;
+  if (!(cfg->aa_kernel >= 0.f) || (cfg->exact != 0 && cfg->exact != 1)) return LP_ERR_ARG;
   for (int v = 0; v < n_views; ++v) {
     if (!valid_cam(cams[v]) || !frame_matches(frames[v], cams[v])) return LP_ERR_ARG;
     if (frames[v].kind != prims->kind || frames[v].n != prims->n) return LP_ERR_ARG;
@@ -173,7 +174,7 @@ lp_status lp_preprocess(const lp_prims *prims, const lp_camera *cams, int32_t n_
       cudaMemsetAsync(F.tile_diff, 0, 4 * (size_t)(F.tiles_x + 1) * (F.tiles_y + 1), st);
   }
   // one launch per 8 views: each primitive's features are read once for all of them
-  launch_preprocess(*prims, cams, cfg->aa_kernel, frames, n_views, st);
+  launch_preprocess(*prims, cams, cfg->aa_kernel, frames, n_views, cfg->exact != 0, st);
   return last_error();
 }
 
@@ -256,7 +257,7 @@ lp_status lp_render_fwd_aux(const lp_camera *cams, int32_t n_views, const lp_ras
   size_t off = 0;
   for (int v = 0; v < n_views; ++v) {
     const size_t hw = (size_t)cams[v].width * cams[v].height;
-    launch_raster_fwd(frames[v], *cfg, image + 3 * off, depth ? depth + off : nullptr, alpha ? alpha + off : nullptr,
+    launch_raster_fwd(frames[v], cams[v], *cfg, image + 3 * off, depth ? depth + off : nullptr, alpha ? alpha + off : nullptr,
                       st);
     off += hw;
   }
@@ -278,10 +279,10 @@ lp_status lp_render_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   size_t off = 0;
   for (int v = 0; v < n_views; ++v) {
-    launch_raster_bwd(frames[v], *cfg, dL_dimage + off, st);
+    launch_raster_bwd(frames[v], cams[v], *cfg, dL_dimage + off, st);
     off += (size_t)3 * cams[v].width * cams[v].height;
   }
-  launch_preprocess_bwd(*prims, cams, cfg->aa_kernel, frames, n_views, *grads, st);
+  launch_preprocess_bwd(*prims, cams, cfg->aa_kernel, frames, n_views, *grads, cfg->exact != 0, st);
   return last_error();
 }
 
@@ -294,7 +295,7 @@ lp_status lp_raster_bwd(const lp_camera *cams, int32_t n_views, const lp_raster_
   size_t off = 0;
   for (int v = 0; v < n_views; ++v) {
     const lp_frame &F = frames[v];
-    launch_raster_bwd(F, *cfg, dL_dimage + off, st);
+    launch_raster_bwd(F, cams[v], *cfg, dL_dimage + off, st);
     off += (size_t)3 * cams[v].width * cams[v].height;
   }
   return last_error();
@@ -308,7 +309,7 @@ lp_status lp_preprocess_bwd(const lp_prims *prims, const lp_camera *cams, int32_
     if (frames[v].kind != prims->kind || frames[v].n != prims->n) return LP_ERR_ARG;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  launch_preprocess_bwd(*prims, cams, cfg->aa_kernel, frames, n_views, *grads, st);
+  launch_preprocess_bwd(*prims, cams, cfg->aa_kernel, frames, n_views, *grads, cfg->exact != 0, st);
   return last_error();
 }
 

@@ -30,15 +30,36 @@ template <int KIND> struct Kind;
 //   tetrahedron (28 words): bx by hx hy | cx cy | (A B C) x 6 slots | sigma r g b
 template <> struct Kind<LP_OCTAHEDRON> {
   static constexpr int K = 3;          // offset vectors (vertices are c +- o_j)
-  static constexpr int RW = 20;        // record words
+  static constexpr int RW = 20;        // record words (ray space)
+  static constexpr int RS = 24;        // record stride in words (room for the exact-mode record)
   static constexpr int RG = 20;        // raster-gradient words: (Mb Mg Mc Mh)x4 dsigma drgb
   static constexpr int CX = 0, SLAB = 4, SIGMA = 16, RGB = 17;
 };
 template <> struct Kind<LP_TETRAHEDRON> {
   static constexpr int K = 4;          // vertices c + o_k
-  static constexpr int RW = 28;        // record words
+  static constexpr int RW = 28;        // record words (ray space)
+  static constexpr int RS = 28;        // record stride in words
   static constexpr int RG = 22;        // (MA MB MC)x6 slots dsigma drgb
   static constexpr int CX = 4, SLAB = 6, SIGMA = 24, RGB = 25;
+};
+
+// Exact-mode ("no ray space", App. D) records, camera space.  For the pixel ray q = t r,
+// r = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1), k = n . r, and with the centre p the planes are
+// evaluated relative to it: t = p_z + tau, tau = (c + n . d) / k, d = p - p_z r = (p_x - p_z r_x,
+// p_y - p_z r_y, 0) (small: no cancellation between two depths ~ p_z in the chord):
+//   octahedron (24 words): bbox(4) | 4 slabs x n_s(3) | p(3) | sigma | rgb | pad
+//     slab s = {q : |n_s . (q - p)| <= 1}, n_s = s^T M^-1 of the camera-space offsets: c = -+1
+//   tetrahedron (28 words): bbox(4) | 4 faces x (n_f, m'_f) | p(3) | sigma | rgb | pad
+//     face f = {q : n_f . (q - p) <= m'_f} (outward n_f, m'_f = n_f . oc_a): c = m'_f, entering
+//     when k < 0
+//   chord = (min exit - max entry) |r|, no intersection unless the entry is in front (t > 0).
+// The backward accumulates the plane moments relative to p (dL/dn = -sum dL/dt (q - p)/k).
+template <int KIND> struct ExactRec;
+template <> struct ExactRec<LP_OCTAHEDRON> {
+  static constexpr int W = 24, N = 4, P = 16, SIGMA = 19, RGB = 20;
+};
+template <> struct ExactRec<LP_TETRAHEDRON> {
+  static constexpr int W = 28, N = 4, P = 20, SIGMA = 23, RGB = 24;
 };
 
 __device__ __forceinline__ float fm(float a, float b) { return __fmul_rn(a, b); }
@@ -52,22 +73,29 @@ __device__ __forceinline__ float tetra_k() { return __uint_as_float(0x3F13CD3Au)
 
 struct Geom {
   int flag;                  // 0 in frustum, 1 invalid input, 2 culled by znear
-  float crx, cry, l;         // ray-space centre (l = |p|, the depth key source)
-  float off[4][3];           // post-filter ray-space offsets
+  float crx, cry, l;         // ray-space centre (l = |p|, the depth key source); exact: p_x, p_y
+  float cz;                  // exact mode: camera-space p_z
+  float blo[2], bhi[2];      // exact mode: screen bbox of the projected vertices
+  float off[4][3];           // post-filter ray-space offsets; exact mode: camera-space offsets
   uint32_t tiles;            // tiles_touched
   int rect[4];               // tx0 ty0 tx1 ty1
 };
 
 // Canonical fp32 geometry.  Also returns the fp32 inputs used downstream.
+// exact: the "no ray space" variant (App. D, reading 27): camera-space
+// offsets, tile bbox from the perspective projections of the vertices, no 2D filter.
+__device__ __forceinline__ void rect_from_bbox(const lp_camera &cam, const float lo_[2], const float hi_[2], Geom &g);
+
 template <int KIND>
 __device__ __forceinline__ void canonical_geometry(const lp_prims &P, int i, const lp_camera &cam, float kappa,
-                                                   Geom &g, float dh[4], float q_out[4], float c_out[3]) {
+                                                   Geom &g, float dh[4], float q_out[4], float c_out[3],
+                                                   bool exact = false) {
   constexpr int K = Kind<KIND>::K;
   const int n = P.n;
   g.flag = 0;
   g.tiles = 0;
   g.rect[0] = g.rect[1] = g.rect[2] = g.rect[3] = 0;
-  g.crx = g.cry = g.l = 0.f;
+  g.crx = g.cry = g.l = g.cz = 0.f;
   float c[3], q[4], d[4], op = P.opacity[i];
 #pragma unroll
   for (int a = 0; a < 3; ++a) c[a] = P.pos[a * n + i];
@@ -152,9 +180,52 @@ __device__ __forceinline__ void canonical_geometry(const lp_prims &P, int i, con
 #pragma unroll
     for (int r = 0; r < 3; ++r)
       oc[r] = fa(fa(fm(cam.W[3 * r + 0], ow[0]), fm(cam.W[3 * r + 1], ow[1])), fm(cam.W[3 * r + 2], ow[2]));
-    g.off[j][0] = fa(fm(J00, oc[0]), fm(J02, oc[2]));
-    g.off[j][1] = fa(fm(J11, oc[1]), fm(J12, oc[2]));
-    g.off[j][2] = fa(fa(fm(J20, oc[0]), fm(J21, oc[1])), fm(J22, oc[2]));
+    if (exact) {
+      g.off[j][0] = oc[0];
+      g.off[j][1] = oc[1];
+      g.off[j][2] = oc[2];
+    } else {
+      g.off[j][0] = fa(fm(J00, oc[0]), fm(J02, oc[2]));
+      g.off[j][1] = fa(fm(J11, oc[1]), fm(J12, oc[2]));
+      g.off[j][2] = fa(fa(fm(J20, oc[0]), fm(J21, oc[1])), fm(J22, oc[2]));
+    }
+  }
+  if (exact) {
+    // camera space; bbox of the perspective projections of the vertices (whole screen if a vertex
+    // is at or behind the camera plane)
+    g.crx = p[0];
+    g.cry = p[1];
+    g.cz = p[2];
+    constexpr int NV = KIND == OCTA ? 6 : 4;
+    float lo[2] = {0.f, 0.f}, hi[2] = {0.f, 0.f};
+    bool behind = false;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      float q[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const float o = KIND == OCTA ? g.off[v >> 1][r] : g.off[v][r];
+        q[r] = (KIND == OCTA && (v & 1)) ? fs(p[r], o) : fa(p[r], o);
+      }
+      behind = behind || !(q[2] > 0.f);
+      const float u = fa(fm(cam.fx, fdv(q[0], q[2])), cam.cx);
+      const float w = fa(fm(cam.fy, fdv(q[1], q[2])), cam.cy);
+      lo[0] = v == 0 ? u : fminf(lo[0], u);
+      hi[0] = v == 0 ? u : fmaxf(hi[0], u);
+      lo[1] = v == 0 ? w : fminf(lo[1], w);
+      hi[1] = v == 0 ? w : fmaxf(hi[1], w);
+    }
+    if (behind) {
+      lo[0] = lo[1] = -2.f;
+      hi[0] = (float)(cam.width + 2);
+      hi[1] = (float)(cam.height + 2);
+    }
+    g.blo[0] = lo[0];
+    g.blo[1] = lo[1];
+    g.bhi[0] = hi[0];
+    g.bhi[1] = hi[1];
+    rect_from_bbox(cam, lo, hi, g);
+    return;
   }
 
   // 2D anti-aliasing filter (readings 19-20)
@@ -190,18 +261,16 @@ __device__ __forceinline__ void canonical_geometry(const lp_prims &P, int i, con
   }
 
   // bbox -> pixel rect -> tile rect
-  const int dims[2] = {cam.width, cam.height};
   const float cr[2] = {g.crx, g.cry};
-  int pmin[2], pmax[2];
+  float lo[2], hi[2];
 #pragma unroll
   for (int ax = 0; ax < 2; ++ax) {
-    float lo, hi;
     if (KIND == OCTA) {
       float m = fabsf(g.off[0][ax]);
 #pragma unroll
       for (int j = 1; j < 3; ++j) m = fabsf(g.off[j][ax]) > m ? fabsf(g.off[j][ax]) : m;
-      lo = fs(cr[ax], m);
-      hi = fa(cr[ax], m);
+      lo[ax] = fs(cr[ax], m);
+      hi[ax] = fa(cr[ax], m);
     } else {
       float mn = g.off[0][ax], mx = g.off[0][ax];
 #pragma unroll
@@ -209,10 +278,20 @@ __device__ __forceinline__ void canonical_geometry(const lp_prims &P, int i, con
         mn = g.off[k][ax] < mn ? g.off[k][ax] : mn;
         mx = g.off[k][ax] > mx ? g.off[k][ax] : mx;
       }
-      lo = fa(cr[ax], mn);
-      hi = fa(cr[ax], mx);
+      lo[ax] = fa(cr[ax], mn);
+      hi[ax] = fa(cr[ax], mx);
     }
-    float a = fs(lo, 0.5f), b = fs(hi, 0.5f);
+  }
+  rect_from_bbox(cam, lo, hi, g);
+}
+
+// screen bbox -> clamped pixel rect -> tile rect; canonical fp32
+__device__ __forceinline__ void rect_from_bbox(const lp_camera &cam, const float lo_[2], const float hi_[2], Geom &g) {
+  const int dims[2] = {cam.width, cam.height};
+  int pmin[2], pmax[2];
+#pragma unroll
+  for (int ax = 0; ax < 2; ++ax) {
+    float a = fs(lo_[ax], 0.5f), b = fs(hi_[ax], 0.5f);
     const float top = (float)(dims[ax] + 2);
     a = a < -2.f ? -2.f : (a > top ? top : a);
     b = b < -2.f ? -2.f : (b > top ? top : b);
@@ -477,6 +556,94 @@ __device__ __forceinline__ void track_k(const Planes2<KIND> &P, int k, float en,
     if (lane_k(P.ex[s], k) == ex) sx = s;
   }
   if (KIND == LP_TETRAHEDRON) sx += 3;
+}
+
+// ---------------------------------------------------------------------------------------------
+// exact mode (App. D): paired per-plane entry / exit parameters of the thread's two pixels
+// (same r.x, ry2 = their two r.y); lane k of en[f] / ex[f] is this plane's entry / exit t.
+// ---------------------------------------------------------------------------------------------
+struct PlanesE2 {
+  float2 en[4], ex[4];
+};
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));   // rcp(+-0) = +-inf: a plane parallel to the ray
+  return y;
+}
+
+// plane normal of plane f in an exact record, and (tetra) its offset m_f
+template <int KIND>
+__device__ __forceinline__ const float *plane_n(const float *rec, int f) {
+  return KIND == LP_OCTAHEDRON ? rec + 4 + 3 * f : rec + 4 + 4 * f;
+}
+
+// per-pixel offsets of the centre from the pixel ray at depth p_z: d = p - p_z r (d_z = 0)
+template <int KIND>
+__device__ __forceinline__ void exact_d(const float *rec, float rx, float2 ry2, float &dx, float2 &dy2) {
+  using ER = ExactRec<KIND>;
+  const float px = rec[ER::P], py = rec[ER::P + 1], pz = rec[ER::P + 2];
+  dx = __fmaf_rn(-pz, rx, px);
+  dy2 = ffma2(bc(-pz), ry2, bc(py));
+}
+
+template <int KIND>
+__device__ __forceinline__ void planesE2(const float *rec, float rx, float2 ry2, PlanesE2 &P) {
+  float dx;
+  float2 dy2;
+  exact_d<KIND>(rec, rx, ry2, dx, dy2);
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const float *n = plane_n<KIND>(rec, f);
+    const float2 k = ffma2(bc(n[1]), ry2, bc(__fmaf_rn(n[0], rx, n[2])));
+    const float2 ik = make_float2(rcp_approx(k.x), rcp_approx(k.y));
+    const float2 L = ffma2(bc(n[1]), dy2, bc(fm(n[0], dx)));          // n . d
+    if (KIND == LP_OCTAHEDRON) {
+      const float2 ta = fmul2(fsub2(L, bc(1.f)), ik), tb = fmul2(fadd2(L, bc(1.f)), ik);
+      P.en[f] = make_float2(fminf(ta.x, tb.x), fminf(ta.y, tb.y));
+      P.ex[f] = make_float2(fmaxf(ta.x, tb.x), fmaxf(ta.y, tb.y));
+    } else {
+      const float2 t = fmul2(fadd2(L, bc(n[3])), ik);
+      P.en[f] = make_float2(k.x < 0.f ? t.x : -INFINITY, k.y < 0.f ? t.y : -INFINITY);
+      P.ex[f] = make_float2(k.x > 0.f ? t.x : INFINITY, k.y > 0.f ? t.y : INFINITY);
+    }
+  }
+}
+
+// 1/k of plane f for one pixel, bitwise the paired evaluation above
+template <int KIND>
+__device__ __forceinline__ float plane_ik(const float *rec, int f, float rx, float ry) {
+  const float *n = plane_n<KIND>(rec, f);
+  return rcp_approx(__fmaf_rn(n[1], ry, __fmaf_rn(n[0], rx, n[2])));
+}
+
+// chord in ray parameter, ex - en (negative when there is no intersection in front of the camera,
+// i.e. unless p_z + entry > 0); en2 / ex2 receive the entry / exit tau.  Euclidean chord = this |r|.
+__device__ __forceinline__ float2 chordE2_of(const PlanesE2 &P, float pz, float2 &en2, float2 &ex2) {
+  en2 = P.en[0];
+  ex2 = P.ex[0];
+#pragma unroll
+  for (int f = 1; f < 4; ++f) {
+    en2.x = fmaxf(en2.x, P.en[f].x);
+    en2.y = fmaxf(en2.y, P.en[f].y);
+    ex2.x = fminf(ex2.x, P.ex[f].x);
+    ex2.y = fminf(ex2.y, P.ex[f].y);
+  }
+  float2 ch = fsub2(ex2, en2);
+  if (!(fa(en2.x, pz) > 0.f)) ch.x = -1.f;   // entry behind the camera: the oracle's single-hit case (reading 27)
+  if (!(fa(en2.y, pz) > 0.f)) ch.y = -1.f;
+  return ch;
+}
+
+// first plane attaining the max entry / min exit of pixel k
+__device__ __forceinline__ void trackE_k(const PlanesE2 &P, int k, float en, float ex, int &se, int &sx) {
+  se = 3;
+  sx = 3;
+#pragma unroll
+  for (int f = 2; f >= 0; --f) {
+    if (lane_k(P.en[f], k) == en) se = f;
+    if (lane_k(P.ex[f], k) == ex) sx = f;
+  }
 }
 
 // slack of the bbox reject test: a pair rejected by it has chord <= 0 (up to fp32 rounding of

@@ -8,11 +8,12 @@
 namespace lp {
 
 // K1 / K5 (lp_preprocess.cu)
+// exact: the no-ray-space variant (App. D, reading 27)
 void launch_preprocess(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
-                       cudaStream_t st);
+                       bool exact, cudaStream_t st);
 // fused over the views of one call (chunks of 8): feature / SH gradients written once per chunk
 void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
-                           const lp_grads &G, cudaStream_t st);
+                           const lp_grads &G, bool exact, cudaStream_t st);
 
 // K2 (lp_sort.cu)
 constexpr int SORT_THREADS = 256;
@@ -35,9 +36,10 @@ void launch_tile_sort(const lp_frame &F, cudaStream_t st);
 
 // K3 / K4 (lp_raster.cu)
 // depth / alpha: optional [H][W] outputs (depth mode P:840-841, alpha = 1 - T_final), may be null
-void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image, float *depth, float *alpha,
+void launch_raster_fwd(const lp_frame &F, const lp_camera &cam, const lp_raster_cfg &cfg, float *image, float *depth,
+                       float *alpha, cudaStream_t st);
+void launch_raster_bwd(const lp_frame &F, const lp_camera &cam, const lp_raster_cfg &cfg, const float *dL_dimage,
                        cudaStream_t st);
-void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL_dimage, cudaStream_t st);
 
 // C5 helpers (lp_train.cu)
 void launch_l1_grad(const float *img, const float *tgt, float *dL, float *loss, int64_t n, float scale,

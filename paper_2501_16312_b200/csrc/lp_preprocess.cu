@@ -51,29 +51,86 @@ struct PreViews {
   int nv;
 };
 
-template <int KIND>
+template <int KIND, bool EXACT>
 __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_camera &cam, float kappa,
                                                 const lp_frame &F, int i);
 
-template <int KIND>
+template <int KIND, bool EXACT>
 __global__ void __launch_bounds__(256) k_preprocess(lp_prims P, float kappa, PreViews V) {
   // view-interleaved grid: the nv consecutive blocks of one primitive range run the nv views, so
   // the primitive features come from HBM once and from L2 for the other views
   const int v = blockIdx.x % V.nv;
   const int i = (blockIdx.x / V.nv) * blockDim.x + threadIdx.x;
-  preprocess_view<KIND>(P, V.cam[v], kappa, V.frame[v], i);
+  preprocess_view<KIND, EXACT>(P, V.cam[v], kappa, V.frame[v], i);
 }
 
+// exact-mode record planes (App. D, reading 27), fp64 from the canonical fp32 geometry
+// returns false for a degenerate primitive (the caller empties its bbox)
 template <int KIND>
+__device__ __forceinline__ bool exact_planes(const Geom &g, float *rec) {
+  using ER = ExactRec<KIND>;
+  const double p[3] = {(double)g.crx, (double)g.cry, (double)g.cz};
+  rec[ER::P] = g.crx;
+  rec[ER::P + 1] = g.cry;
+  rec[ER::P + 2] = g.cz;
+  if (KIND == OCTA) {
+    double M[3][3], G[3][3], det;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) M[a][j] = (double)g.off[j][a];
+    inverse3(M, G, det);
+    const bool ok = isfinite(det) && det != 0.0;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      float *n = rec + 4 + 3 * s;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        n[c] = ok ? (float)(slab_sign(s, 0) * G[0][c] + slab_sign(s, 1) * G[1][c] + slab_sign(s, 2) * G[2][c]) : 0.f;
+    }
+    return ok;
+  } else {
+    double v[4][3];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) v[k][a] = p[a] + (double)g.off[k][a];
+    bool ok = true;
+    double nn[4][3], mm[4];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const int ia = tetra_face(f, 0), ib = tetra_face(f, 1), ic = tetra_face(f, 2);
+      const double e1[3] = {v[ib][0] - v[ia][0], v[ib][1] - v[ia][1], v[ib][2] - v[ia][2]};
+      const double e2[3] = {v[ic][0] - v[ia][0], v[ic][1] - v[ia][1], v[ic][2] - v[ia][2]};
+      nn[f][0] = e1[1] * e2[2] - e1[2] * e2[1];
+      nn[f][1] = e1[2] * e2[0] - e1[0] * e2[2];
+      nn[f][2] = e1[0] * e2[1] - e1[1] * e2[0];
+      if (nn[f][0] == 0.0 && nn[f][1] == 0.0 && nn[f][2] == 0.0) ok = false;
+      // m'_f = n_f . oc_a: the plane offset relative to the centre
+      mm[f] = nn[f][0] * (double)g.off[ia][0] + nn[f][1] * (double)g.off[ia][1] + nn[f][2] * (double)g.off[ia][2];
+    }
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      float *pl = rec + 4 + 4 * f;
+      pl[0] = ok ? (float)nn[f][0] : 0.f;
+      pl[1] = ok ? (float)nn[f][1] : 0.f;
+      pl[2] = ok ? (float)nn[f][2] : 1.f;
+      pl[3] = ok ? (float)mm[f] : 0.f;
+    }
+    return ok;
+  }
+}
+
+template <int KIND, bool EXACT>
 __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_camera &cam, float kappa,
                                                 const lp_frame &F, int i) {
-  constexpr int K = Kind<KIND>::K, RW = Kind<KIND>::RW;
+  constexpr int K = Kind<KIND>::K, RW = Kind<KIND>::RW, RS = Kind<KIND>::RS;
   const bool inb = i < P.n;
   Geom g;
   float dh[4], q[4], c[3];
   g.flag = 1;
   g.tiles = 0;
-  if (inb) canonical_geometry<KIND>(P, i, cam, kappa, g, dh, q, c);
+  if (inb) canonical_geometry<KIND>(P, i, cam, kappa, g, dh, q, c, EXACT);
   warp_count(F.counters + LP_CNT_INVALID, inb && g.flag == 1);
   warp_count(F.counters + LP_CNT_FRUSTUM, inb && g.flag == 0);
   warp_count(F.counters + LP_CNT_VISIBLE, inb && g.tiles > 0);
@@ -122,6 +179,26 @@ __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_came
 
   // ---- raster record
   using KD = Kind<KIND>;
+  if (EXACT) {
+    using ER = ExactRec<KIND>;
+    float rec[ER::W];
+    const float hx = 0.5f * (g.bhi[0] - g.blo[0]), hy = 0.5f * (g.bhi[1] - g.blo[1]);
+    rec[0] = 0.5f * (g.blo[0] + g.bhi[0]);
+    rec[1] = 0.5f * (g.blo[1] + g.bhi[1]);
+    rec[2] = hx * 1.0001f + 1e-3f;
+    rec[3] = hy * 1.0001f + 1e-3f;
+    if (!exact_planes<KIND>(g, rec)) rec[2] = rec[3] = -1.f;   // degenerate: no pixel passes the bbox test
+    rec[ER::SIGMA] = sigma;
+    rec[ER::RGB + 0] = rgb[0];
+    rec[ER::RGB + 1] = rgb[1];
+    rec[ER::RGB + 2] = rgb[2];
+    rec[ER::W - 1] = 0.f;
+    float4 *dst = reinterpret_cast<float4 *>(F.record + (size_t)i * RS);
+#pragma unroll
+    for (int w = 0; w < ER::W / 4; ++w)
+      dst[w] = make_float4(rec[4 * w], rec[4 * w + 1], rec[4 * w + 2], rec[4 * w + 3]);
+    return;
+  }
   float rec[RW];
   // screen bbox of the (filtered) vertices, with a small slack (record word 0..3)
   float xlo = g.off[0][0], xhi = g.off[0][0], ylo = g.off[0][1], yhi = g.off[0][1];
@@ -166,7 +243,7 @@ __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_came
   rec[KD::RGB + 0] = rgb[0];
   rec[KD::RGB + 1] = rgb[1];
   rec[KD::RGB + 2] = rgb[2];
-  float4 *dst = reinterpret_cast<float4 *>(F.record + (size_t)i * RW);
+  float4 *dst = reinterpret_cast<float4 *>(F.record + (size_t)i * RS);
 #pragma unroll
   for (int w = 0; w < RW / 4; ++w) dst[w] = make_float4(rec[4 * w], rec[4 * w + 1], rec[4 * w + 2], rec[4 * w + 3]);
 }
@@ -185,8 +262,9 @@ struct ViewPack {
   int nv;
 };
 
-// one view's contribution; false if the view has no raster gradient for primitive i
-template <int KIND>
+// one view's contribution; false if the view has no raster gradient for primitive i.
+// EXACT: the no-ray-space moments (per plane: dL/dm, dL/dn) -> camera-space offsets and centre.
+template <int KIND, bool EXACT>
 __device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_camera &cam, float kappa, int i,
                                                   const float *__restrict__ rgrad, float gpos[3], float grot[4],
                                                   float gdist[4], float &gop, float &m2d) {
@@ -203,13 +281,84 @@ __device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_ca
 
   Geom g;
   float dhf[4], qf[4], cf[3];
-  canonical_geometry<KIND>(P, i, cam, kappa, g, dhf, qf, cf);
+  canonical_geometry<KIND>(P, i, cam, kappa, g, dhf, qf, cf, EXACT);
 
   // ---- raster moments -> d/d(ray-space offsets) and d/d(ray-space centre xy)
   double go[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   double gcr[2] = {0, 0};
+  double gpc[3] = {0, 0, 0};   // exact mode: d/d(camera-space centre p)
   double dsig, drgb[3];
-  if (KIND == OCTA) {
+  if (EXACT) {
+    // planes n . q = m (+-1 for slabs); moments per plane f: (dL/dm, dL/dn.x, dL/dn.y, dL/dn.z)
+    const double pc[3] = {(double)g.crx, (double)g.cry, (double)g.cz};
+    if (KIND == OCTA) {
+      double M[3][3], G[3][3], det;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) M[a][j] = (double)g.off[j][a];
+      inverse3(M, G, det);
+      double gG[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        double n3[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          n3[c] = slab_sign(s, 0) * G[0][c] + slab_sign(s, 1) * G[1][c] + slab_sign(s, 2) * G[2][c];
+        const double dm = m[4 * s];
+        // centred moments: dL/dn_s (plane moving with p) and dL/dp += dm n_s
+        const double dn[3] = {m[4 * s + 1], m[4 * s + 2], m[4 * s + 3]};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          gpc[a] += dm * n3[a];
+          const double sa = slab_sign(s, a);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) gG[a][c] += sa * dn[c];
+        }
+      }
+      double t1[3][3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) t1[a][b] = G[0][a] * gG[0][b] + G[1][a] * gG[1][b] + G[2][a] * gG[2][b];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) go[j][a] += -(t1[a][0] * G[j][0] + t1[a][1] * G[j][1] + t1[a][2] * G[j][2]);
+    } else {
+      // faces relative to the centre: n_f . (q - p) = m'_f, m'_f = n_f . oc_a, n_f = (oc_b - oc_a) x (oc_c - oc_a)
+      double v[4][3];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) v[k][a] = (double)g.off[k][a];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const double dm = m[4 * f];
+        const int ia = tetra_face(f, 0), ib = tetra_face(f, 1), ic = tetra_face(f, 2);
+        const double e1[3] = {v[ib][0] - v[ia][0], v[ib][1] - v[ia][1], v[ib][2] - v[ia][2]};
+        const double e2[3] = {v[ic][0] - v[ia][0], v[ic][1] - v[ia][1], v[ic][2] - v[ia][2]};
+        const double nf[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+        // centred moments: dL/dn_f at fixed m'_f, plus m'_f = n_f . oc_a
+        const double gn[3] = {m[4 * f + 1] + dm * v[ia][0], m[4 * f + 2] + dm * v[ia][1], m[4 * f + 3] + dm * v[ia][2]};
+        const double ge1[3] = {e2[1] * gn[2] - e2[2] * gn[1], e2[2] * gn[0] - e2[0] * gn[2], e2[0] * gn[1] - e2[1] * gn[0]};
+        const double ge2[3] = {gn[1] * e1[2] - gn[2] * e1[1], gn[2] * e1[0] - gn[0] * e1[2], gn[0] * e1[1] - gn[1] * e1[0]};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          go[ia][a] += dm * nf[a] - ge1[a] - ge2[a];
+          go[ib][a] += ge1[a];
+          go[ic][a] += ge2[a];
+          gpc[a] += dm * nf[a];      // the plane moves with p
+        }
+      }
+    }
+    constexpr int RGK = Kind<KIND>::RG;
+    dsig = m[RGK - 4];
+    drgb[0] = m[RGK - 3]; drgb[1] = m[RGK - 2]; drgb[2] = m[RGK - 1];
+    // densification statistic in pixel units at the centre's depth (reading 26/27)
+    gcr[0] = gpc[0] * (double)g.cz / (double)cam.fx;
+    gcr[1] = gpc[1] * (double)g.cz / (double)cam.fy;
+  } else if (KIND == OCTA) {
     double M[3][3], G[3][3], det;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
@@ -349,12 +498,17 @@ __device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_ca
     for (int r = 0; r < 3; ++r) ow[r] = (CT)dhf[j] * Rb[r];
 #pragma unroll
     for (int r = 0; r < 3; ++r) oc[r] = Wm[r][0] * ow[0] + Wm[r][1] * ow[1] + Wm[r][2] * ow[2];
+    if (EXACT) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) goc[a] = J[0][a] * go[j][0] + J[1][a] * go[j][1] + J[2][a] * go[j][2];
+      for (int a = 0; a < 3; ++a) goc[a] = (CT)go[j][a];
+    } else {
 #pragma unroll
-    for (int r = 0; r < 3; ++r)
+      for (int a = 0; a < 3; ++a) goc[a] = J[0][a] * go[j][0] + J[1][a] * go[j][1] + J[2][a] * go[j][2];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) gJ[r][a] += go[j][r] * oc[a];
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) gJ[r][a] += go[j][r] * oc[a];
+    }
 #pragma unroll
     for (int a = 0; a < 3; ++a) gow[a] = Wm[0][a] * goc[0] + Wm[1][a] * goc[1] + Wm[2][a] * goc[2];
     gdh[j] = Rb[0] * gow[0] + Rb[1] * gow[1] + Rb[2] * gow[2];
@@ -364,6 +518,10 @@ __device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_ca
       for (int cc = 0; cc < 3; ++cc) gR[r][cc] += (CT)dhf[j] * gow[r] * bj[cc];
   }
   CT gp[3];
+  if (EXACT) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) gp[a] = (CT)gpc[a];
+  } else {
 #pragma unroll
   for (int a = 0; a < 3; ++a) gp[a] = J[0][a] * gcr[0] + J[1][a] * gcr[1];   // c_ray.z gets no gradient
   gp[2] += gJ[0][0] * (-fx / pz2);
@@ -376,6 +534,7 @@ __device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_ca
   for (int k = 0; k < 3; ++k)
 #pragma unroll
     for (int mm = 0; mm < 3; ++mm) gp[mm] += gJ[2][k] * (((k == mm) ? 1.0f : 0.0f) - p[k] * p[mm] / (l * l)) / l;
+  }
   CT gc[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) gc[a] = Wm[0][a] * gp[0] + Wm[1][a] * gp[1] + Wm[2][a] * gp[2];
@@ -478,7 +637,7 @@ struct ItemRes {
 // items (contiguous in the list), expands the SH gradient sum_v Y(dir_v) gr_v in registers, and
 // read-modify-writes every feature gradient once.  No shared-memory float atomics (sm_100 has
 // none: they compile to CAS loops).
-template <int KIND, int DEG>
+template <int KIND, int DEG, bool EXACT>
 __global__ void __launch_bounds__(64) k_preprocess_bwd(lp_prims P, float kappa, ViewPack V, int rg_words,
                                                        lp_grads Gs) {
   constexpr int WARPS = 2, K = Kind<KIND>::K, NC = (DEG + 1) * (DEG + 1);
@@ -540,7 +699,7 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd(lp_prims P, float kappa, 
       const int ii = base + pl;
       float gpos[3] = {0.f, 0.f, 0.f}, grot[4] = {0.f, 0.f, 0.f, 0.f}, gdist[4] = {0.f, 0.f, 0.f, 0.f};
       float gop = 0.f, m2d = 0.f, gr[3] = {0.f, 0.f, 0.f}, dir[3] = {0.f, 0.f, 1.f};
-      view_feature_grad<KIND>(P, s_cam[v], kappa, ii, s_rg[v], gpos, grot, gdist, gop, m2d);
+      view_feature_grad<KIND, EXACT>(P, s_cam[v], kappa, ii, s_rg[v], gpos, grot, gdist, gop, m2d);
       if (Gs.sh || Gs.pos) sh_view_inputs<DEG>(P, s_cam[v], ii, s_rg[v], rg_words, gr, dir, gpos);
       float *res = s_res[w][it];
 #pragma unroll
@@ -610,7 +769,7 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd(lp_prims P, float kappa, 
 
 // ---------------------------------------------------------------------------------------------
 void launch_preprocess(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
-                       cudaStream_t st) {
+                       bool exact, cudaStream_t st) {
   if (P.n == 0 || n_views <= 0) return;
   const int grid = (P.n + 255) / 256;
   for (int v0 = 0; v0 < n_views; v0 += LP_PRE_MAXV) {
@@ -621,24 +780,29 @@ void launch_preprocess(const lp_prims &P, const lp_camera *cams, float kappa, co
       V.cam[v] = cams[s];
       V.frame[v] = frames[s];
     }
-    if (P.kind == LP_OCTAHEDRON) k_preprocess<LP_OCTAHEDRON><<<grid * V.nv, 256, 0, st>>>(P, kappa, V);
-    else k_preprocess<LP_TETRAHEDRON><<<grid * V.nv, 256, 0, st>>>(P, kappa, V);
+    if (P.kind == LP_OCTAHEDRON) {
+      if (exact) k_preprocess<LP_OCTAHEDRON, true><<<grid * V.nv, 256, 0, st>>>(P, kappa, V);
+      else k_preprocess<LP_OCTAHEDRON, false><<<grid * V.nv, 256, 0, st>>>(P, kappa, V);
+    } else {
+      if (exact) k_preprocess<LP_TETRAHEDRON, true><<<grid * V.nv, 256, 0, st>>>(P, kappa, V);
+      else k_preprocess<LP_TETRAHEDRON, false><<<grid * V.nv, 256, 0, st>>>(P, kappa, V);
+    }
   }
 }
 
-template <int KIND>
+template <int KIND, bool EXACT>
 static void bwd_deg(const lp_prims &P, float kappa, const ViewPack &V, int rg, const lp_grads &G, cudaStream_t st) {
   const int grid = (P.n + 63) / 64;
   switch (P.sh_degree) {
-    case 0: k_preprocess_bwd<KIND, 0><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
-    case 1: k_preprocess_bwd<KIND, 1><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
-    case 2: k_preprocess_bwd<KIND, 2><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
-    default: k_preprocess_bwd<KIND, 3><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
+    case 0: k_preprocess_bwd<KIND, 0, EXACT><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
+    case 1: k_preprocess_bwd<KIND, 1, EXACT><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
+    case 2: k_preprocess_bwd<KIND, 2, EXACT><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
+    default: k_preprocess_bwd<KIND, 3, EXACT><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
   }
 }
 
 void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
-                           const lp_grads &G, cudaStream_t st) {
+                           const lp_grads &G, bool exact, cudaStream_t st) {
   if (P.n == 0 || n_views <= 0) return;
   for (int v0 = 0; v0 < n_views; v0 += LP_MAXV) {
     ViewPack V;
@@ -649,8 +813,14 @@ void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa
       V.rgrad[v] = frames[s].rgrad;
       V.tt[v] = frames[s].tiles_touched;
     }
-    if (P.kind == LP_OCTAHEDRON) bwd_deg<LP_OCTAHEDRON>(P, kappa, V, frames[v0].rgrad_words, G, st);
-    else bwd_deg<LP_TETRAHEDRON>(P, kappa, V, frames[v0].rgrad_words, G, st);
+    const int rg = frames[v0].rgrad_words;
+    if (P.kind == LP_OCTAHEDRON) {
+      if (exact) bwd_deg<LP_OCTAHEDRON, true>(P, kappa, V, rg, G, st);
+      else bwd_deg<LP_OCTAHEDRON, false>(P, kappa, V, rg, G, st);
+    } else {
+      if (exact) bwd_deg<LP_TETRAHEDRON, true>(P, kappa, V, rg, G, st);
+      else bwd_deg<LP_TETRAHEDRON, false>(P, kappa, V, rg, G, st);
+    }
   }
 }
 

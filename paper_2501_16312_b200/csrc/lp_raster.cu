@@ -110,12 +110,17 @@ extern "C" int lp_debug_bwd_stats(unsigned long long *out, int reset) {
 // 128 threads, 2 pixels per thread: pixel k = 0 / 1 of a thread are (x, y) and (x, y + 4), so they
 // share dx and the bbox x test, and their chords are ONE paired evaluation (chord2: FFMA2 / FADD2
 // lanes, bitwise the scalar chord the backward replays).
-template <int KIND, bool STATS, bool AUX>
-__global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_raster_cfg cfg, float *__restrict__ image,
-                                                    float *__restrict__ depth, float *__restrict__ alpha) {
+// EXACT: the no-ray-space variant (App. D, reading 27): per-pixel perspective rays
+// r = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1) against the record's camera-space planes.
+template <int KIND, bool STATS, bool AUX, bool EXACT>
+__global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, lp_raster_cfg cfg,
+                                                    float *__restrict__ image, float *__restrict__ depth,
+                                                    float *__restrict__ alpha) {
   constexpr int NT = 128, PPT = 2;
   using KD = Kind<KIND>;
-  constexpr int RW = KD::RW, RW4 = RW / 4;
+  using ER = ExactRec<KIND>;
+  constexpr int RW = EXACT ? ER::W : KD::RW, RW4 = RW / 4, RS = KD::RS;
+  constexpr int SIGMA = EXACT ? ER::SIGMA : KD::SIGMA, RGB = EXACT ? ER::RGB : KD::RGB;
   __shared__ float4 s_rec[NT * RW4];
   __shared__ unsigned char s_list[NT / 32][NT];
   __shared__ unsigned long long s_stat[3];
@@ -147,6 +152,13 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_raster_cfg cf
     dep[k] = 0.f;
     dset[k] = false;
   }
+  // exact mode: the pixel rays (r_x shared by the pair, r_z = 1) and their lengths
+  const float rx = EXACT ? __fdiv_rn(fs(fx, cam.cx), cam.fx) : 0.f;
+  const float2 ry2 = EXACT ? make_float2(__fdiv_rn(fs(fy[0], cam.cy), cam.fy), __fdiv_rn(fs(fy[1], cam.cy), cam.fy))
+                           : make_float2(0.f, 0.f);
+  const float2 rn2 = EXACT ? make_float2(sqrtf(fmaf(rx, rx, fmaf(ry2.x, ry2.x, 1.f))),
+                                         sqrtf(fmaf(rx, rx, fmaf(ry2.y, ry2.y, 1.f))))
+                           : make_float2(1.f, 1.f);
   float wx0, wx1, wy0, wy1;
   warp_rect<NT>(threadIdx.x >> 5, tx, ty, wx0, wx1, wy0, wy1);
 
@@ -155,7 +167,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_raster_cfg cf
     const uint32_t e = b + threadIdx.x;
     if (e < end) {
       const uint32_t v = F.sorted_val[e];
-      const float4 *src = reinterpret_cast<const float4 *>(F.record + (size_t)v * RW);
+      const float4 *src = reinterpret_cast<const float4 *>(F.record + (size_t)v * RS);
 #pragma unroll
       for (int w = 0; w < RW4; ++w) s_rec[threadIdx.x * RW4 + w] = __ldg(src + w);
     }
@@ -176,10 +188,20 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_raster_cfg cf
       if (!__any_sync(0xffffffffu, any)) continue;
       if (!any) continue;
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
-      const float dx = fs(fx, rec[KD::CX]);
-      const float2 dy2 = fsub2(make_float2(fy[0], fy[1]), bc(rec[KD::CX + 1]));
-      float2 en2;
-      const float2 ch2 = chord2<KIND>(rec, dx, dy2, en2);
+      float2 ch2, en2;
+      if constexpr (EXACT) {
+        PlanesE2 P;
+        planesE2<KIND>(rec, rx, ry2, P);
+        float2 ex2;
+        const float pz = rec[ER::P + 2];
+        const float2 cht = chordE2_of(P, pz, en2, ex2);
+        ch2 = fmul2(cht, rn2);                         // Euclidean chord (negative: no hit)
+        en2 = fmul2(fadd2(en2, bc(pz)), rn2);          // entry distance from the camera
+      } else {
+        const float dx = fs(fx, rec[KD::CX]);
+        const float2 dy2 = fsub2(make_float2(fy[0], fy[1]), bc(rec[KD::CX + 1]));
+        ch2 = chord2<KIND>(rec, dx, dy2, en2);
+      }
       const float ch[PPT] = {ch2.x, ch2.y};
       const float enk[PPT] = {en2.x, en2.y};
 #pragma unroll
@@ -187,17 +209,21 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_raster_cfg cf
         if (!test[k]) continue;
         if (STATS) ++nbox;
         if (ch[k] > 0.f) {
-          const float E = transmit(rec[KD::SIGMA], ch[k]);
+          const float E = transmit(rec[SIGMA], ch[k]);
           const float o = 1.f - E;
           const float wgt = T[k] * o;
-          C[k][0] = fmaf(wgt, rec[KD::RGB + 0], C[k][0]);
-          C[k][1] = fmaf(wgt, rec[KD::RGB + 1], C[k][1]);
-          C[k][2] = fmaf(wgt, rec[KD::RGB + 2], C[k][2]);
+          C[k][0] = fmaf(wgt, rec[RGB + 0], C[k][0]);
+          C[k][1] = fmaf(wgt, rec[RGB + 1], C[k][1]);
+          C[k][2] = fmaf(wgt, rec[RGB + 2], C[k][2]);
           T[k] = T[k] * E;
           if (AUX && !dset[k] && T[k] < 0.5f) {      // cumulative opacity 1 - T > 0.5 (once per pixel)
             dset[k] = true;
-            const uint32_t id = F.sorted_val[b + (uint32_t)j];
-            dep[k] = fa(__uint_as_float(F.depth_key[id]), enk[k]);
+            if (EXACT) {
+              dep[k] = enk[k];
+            } else {
+              const uint32_t id = F.sorted_val[b + (uint32_t)j];
+              dep[k] = fa(__uint_as_float(F.depth_key[id]), enk[k]);
+            }
           }
           if (STATS) ++nhit;
           if (T[k] < cfg.t_stop) {       // include-then-stop (reading 9)
@@ -252,12 +278,17 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_raster_cfg cf
 // =============================================================================================
 // K4 backward
 // =============================================================================================
-template <int KIND, int NT>
-__global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_frame F, lp_raster_cfg cfg,
+// EXACT: the no-ray-space variant; per plane f the moments are (dL/dm_f, dL/dn_f) with
+// t = (m -+ 1)/k or m/k, k = n . r:  dt/dm = 1/k, dt/dn = -t r / k  (reading 27).
+template <int KIND, int NT, bool EXACT>
+__global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_frame F, lp_camera cam,
+                                                                      lp_raster_cfg cfg,
                                                                       const float *__restrict__ dL) {
   static_assert(NT == 128, "paired pixel evaluation assumes 2 pixels per thread");
   using KD = Kind<KIND>;
-  constexpr int RW = KD::RW, RW4 = RW / 4, PPT = 256 / NT, RG = KD::RG;
+  using ER = ExactRec<KIND>;
+  constexpr int RW = EXACT ? ER::W : KD::RW, RW4 = RW / 4, PPT = 256 / NT, RG = KD::RG, RS = KD::RS;
+  constexpr int SIGMA = EXACT ? ER::SIGMA : KD::SIGMA, RGB = EXACT ? ER::RGB : KD::RGB;
   constexpr int RGP = RG == 20 ? 20 : 28;      // padded row: 16-byte stores, conflict-free (RGP/4 odd)
   __shared__ float4 s_rec[NT * RW4];
   __shared__ unsigned char s_list[NT / 32][NT];
@@ -300,6 +331,13 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
   const uint32_t lmax = s_last;
   float wx0, wx1, wy0, wy1;
   warp_rect<NT>(threadIdx.x >> 5, tx, ty, wx0, wx1, wy0, wy1);
+  // exact mode: the pixel rays (bitwise the forward's)
+  const float rx = EXACT ? __fdiv_rn(fs(fx[0], cam.cx), cam.fx) : 0.f;
+  const float2 ry2 = EXACT ? make_float2(__fdiv_rn(fs(fy[0], cam.cy), cam.fy), __fdiv_rn(fs(fy[1], cam.cy), cam.fy))
+                           : make_float2(0.f, 0.f);
+  const float2 rn2 = EXACT ? make_float2(sqrtf(fmaf(rx, rx, fmaf(ry2.x, ry2.x, 1.f))),
+                                         sqrtf(fmaf(rx, rx, fmaf(ry2.y, ry2.y, 1.f))))
+                           : make_float2(1.f, 1.f);
 
   for (uint32_t bend = lmax; bend > start; bend = (bend - start > NT) ? bend - NT : start) {
     const uint32_t bstart = (bend - start > NT) ? bend - NT : start;
@@ -308,7 +346,7 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
     if (e < bend) {
       const uint32_t v = F.sorted_val[e];
       s_id[threadIdx.x] = v;
-      const float4 *src = reinterpret_cast<const float4 *>(F.record + (size_t)v * RW);
+      const float4 *src = reinterpret_cast<const float4 *>(F.record + (size_t)v * RS);
 #pragma unroll
       for (int w = 0; w < RW4; ++w) s_rec[threadIdx.x * RW4 + w] = __ldg(src + w);
     }
@@ -346,7 +384,57 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
 #pragma unroll
       for (int a = 0; a < RGP; ++a) acc[a] = 0.f;
       bool hit = false;
-      if (any) {
+      if (any && EXACT) {
+        // exact mode: paired plane parameters, entry / exit plane resolved for hit pixels only
+        PlanesE2 P;
+        planesE2<KIND>(rec, rx, ry2, P);
+        float2 en2, ex2;
+        const float2 ch2 = fmul2(chordE2_of(P, rec[ER::P + 2], en2, ex2), rn2);
+        float dxp;
+        float2 dyp2;
+        exact_d<KIND>(rec, rx, ry2, dxp, dyp2);
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const float ch = lane_k(ch2, k);
+          if (!test[k] || !(ch > 0.f)) continue;
+          hit = true;
+          int se, sx;
+          const float te = lane_k(en2, k), tx_ = lane_k(ex2, k);
+          trackE_k(P, k, te, tx_, se, sx);
+          const float sig = rec[SIGMA];
+          const float E = transmit(sig, ch);
+          const float o = 1.f - E;
+          const float Tk = T[k] * rcp_ftz(E);
+          float dLdo = 0.f;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            acc[RG - 3 + c] = fmaf(Tk * o, G[k][c], acc[RG - 3 + c]);
+            dLdo = fmaf(rec[RGB + c] - S[k][c], G[k][c], dLdo);
+            S[k][c] = fmaf(o, rec[RGB + c], E * S[k][c]);
+          }
+          dLdo *= Tk;
+          T[k] = Tk;
+          const float gE = E * dLdo;
+          acc[RG - 4] = fmaf(ch, gE, acc[RG - 4]);      // dL/dsigma = (Euclidean chord) E dL/do
+          const float ry = lane_k(ry2, k);
+          const float w = sig * gE * lane_k(rn2, k);    // dL/dt_exit = w, dL/dt_entry = -w
+          const float ike = plane_ik<KIND>(rec, se, rx, ry), ikx = plane_ik<KIND>(rec, sx, rx, ry);
+          // centred moments: dL/dm = dL/dt / k and dL/dn = -dL/dt (q - p) / k with
+          // q - p = tau r - d (tau = t - p_z, d = p - p_z r)
+          const float dyp = lane_k(dyp2, k);
+          const float ax = w * ikx, ae = -w * ike;
+          const float qx[3] = {fmaf(tx_, rx, -dxp), fmaf(tx_, ry, -dyp), tx_};
+          const float qe[3] = {fmaf(te, rx, -dxp), fmaf(te, ry, -dyp), te};
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            const float A = ((f == sx) ? ax : 0.f) + ((f == se) ? ae : 0.f);
+            acc[4 * f + 0] += A;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              acc[4 * f + 1 + c] -= ((f == sx) ? ax * qx[c] : 0.f) + ((f == se) ? ae * qe[c] : 0.f);
+          }
+        }
+      } else if (any) {
       // both pixels' entry / exit values as one paired evaluation (bitwise the forward's chord2);
       // the entry / exit slab is resolved only for pixels the primitive actually hits
       const float dx = fs(fx[0], rec[KD::CX]);
@@ -363,7 +451,7 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
         int se, sx;
         track_k<KIND>(P, k, lane_k(en2, k), lane_k(ex2, k), se, sx);
         const float dy = lane_k(dy2, k);
-        const float sig = rec[KD::SIGMA];
+        const float sig = rec[SIGMA];
         const float E = transmit(sig, ch);
         const float o = 1.f - E;
         const float Tk = T[k] * rcp_ftz(E);               // transmittance in front of this entry
@@ -371,8 +459,8 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           acc[RG - 3 + c] = fmaf(Tk * o, G[k][c], acc[RG - 3 + c]);   // dL/drgb
-          dLdo = fmaf(rec[KD::RGB + c] - S[k][c], G[k][c], dLdo);
-          S[k][c] = fmaf(o, rec[KD::RGB + c], E * S[k][c]);           // colour behind the previous entry
+          dLdo = fmaf(rec[RGB + c] - S[k][c], G[k][c], dLdo);
+          S[k][c] = fmaf(o, rec[RGB + c], E * S[k][c]);               // colour behind the previous entry
         }
         dLdo *= Tk;
         T[k] = Tk;
@@ -437,31 +525,44 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
 }
 
 // ---------------------------------------------------------------------------------------------
-template <bool STATS, bool AUX>
-static void fwd_k(const lp_frame &F, const lp_raster_cfg &cfg, float *image, float *depth, float *alpha,
-                  cudaStream_t st) {
+template <bool STATS, bool AUX, bool EXACT>
+static void fwd_k(const lp_frame &F, const lp_camera &cam, const lp_raster_cfg &cfg, float *image, float *depth,
+                  float *alpha, cudaStream_t st) {
   const int tiles = F.tiles_x * F.tiles_y;
   if (F.kind == LP_OCTAHEDRON)
-    k_raster_fwd<LP_OCTAHEDRON, STATS, AUX><<<tiles, 128, 0, st>>>(F, cfg, image, depth, alpha);
-  else k_raster_fwd<LP_TETRAHEDRON, STATS, AUX><<<tiles, 128, 0, st>>>(F, cfg, image, depth, alpha);
+    k_raster_fwd<LP_OCTAHEDRON, STATS, AUX, EXACT><<<tiles, 128, 0, st>>>(F, cam, cfg, image, depth, alpha);
+  else k_raster_fwd<LP_TETRAHEDRON, STATS, AUX, EXACT><<<tiles, 128, 0, st>>>(F, cam, cfg, image, depth, alpha);
 }
 
-void launch_raster_fwd(const lp_frame &F, const lp_raster_cfg &cfg, float *image, float *depth, float *alpha,
-                       cudaStream_t st) {
+template <bool EXACT>
+static void fwd_x(const lp_frame &F, const lp_camera &cam, const lp_raster_cfg &cfg, float *image, float *depth,
+                  float *alpha, cudaStream_t st) {
   const bool aux = depth || alpha;
   if (cfg.count_stats) {
-    if (aux) fwd_k<true, true>(F, cfg, image, depth, alpha, st);
-    else fwd_k<true, false>(F, cfg, image, depth, alpha, st);
+    if (aux) fwd_k<true, true, EXACT>(F, cam, cfg, image, depth, alpha, st);
+    else fwd_k<true, false, EXACT>(F, cam, cfg, image, depth, alpha, st);
   } else {
-    if (aux) fwd_k<false, true>(F, cfg, image, depth, alpha, st);
-    else fwd_k<false, false>(F, cfg, image, depth, alpha, st);
+    if (aux) fwd_k<false, true, EXACT>(F, cam, cfg, image, depth, alpha, st);
+    else fwd_k<false, false, EXACT>(F, cam, cfg, image, depth, alpha, st);
   }
 }
 
-void launch_raster_bwd(const lp_frame &F, const lp_raster_cfg &cfg, const float *dL, cudaStream_t st) {
+void launch_raster_fwd(const lp_frame &F, const lp_camera &cam, const lp_raster_cfg &cfg, float *image, float *depth,
+                       float *alpha, cudaStream_t st) {
+  if (cfg.exact) fwd_x<true>(F, cam, cfg, image, depth, alpha, st);
+  else fwd_x<false>(F, cam, cfg, image, depth, alpha, st);
+}
+
+void launch_raster_bwd(const lp_frame &F, const lp_camera &cam, const lp_raster_cfg &cfg, const float *dL,
+                       cudaStream_t st) {
   const int tiles = F.tiles_x * F.tiles_y;
-  if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, 128><<<tiles, 128, 0, st>>>(F, cfg, dL);
-  else k_raster_bwd<LP_TETRAHEDRON, 128><<<tiles, 128, 0, st>>>(F, cfg, dL);
+  if (cfg.exact) {
+    if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, 128, true><<<tiles, 128, 0, st>>>(F, cam, cfg, dL);
+    else k_raster_bwd<LP_TETRAHEDRON, 128, true><<<tiles, 128, 0, st>>>(F, cam, cfg, dL);
+  } else {
+    if (F.kind == LP_OCTAHEDRON) k_raster_bwd<LP_OCTAHEDRON, 128, false><<<tiles, 128, 0, st>>>(F, cam, cfg, dL);
+    else k_raster_bwd<LP_TETRAHEDRON, 128, false><<<tiles, 128, 0, st>>>(F, cam, cfg, dL);
+  }
 }
 
 }  // namespace lp

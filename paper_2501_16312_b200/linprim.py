@@ -41,7 +41,7 @@ class lp_camera(C.Structure):
 
 class lp_raster_cfg(C.Structure):
     _fields_ = [("aa_kernel", C.c_float), ("t_stop", C.c_float), ("bg", C.c_float * 3),
-                ("count_stats", C.c_int32)]
+                ("count_stats", C.c_int32), ("exact", C.c_int32)]
 
 
 class lp_frame(C.Structure):
@@ -223,11 +223,12 @@ def cameras(cams):
     return arr
 
 
-def raster_cfg(aa_kernel=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), count_stats=False) -> lp_raster_cfg:
+def raster_cfg(aa_kernel=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), count_stats=False, exact=False) -> lp_raster_cfg:
     c = lp_raster_cfg()
     c.aa_kernel, c.t_stop = float(aa_kernel), float(t_stop)
     c.bg[:] = [float(b) for b in bg]
     c.count_stats = 1 if count_stats else 0
+    c.exact = 1 if exact else 0
     return c
 
 

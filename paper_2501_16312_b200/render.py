@@ -122,12 +122,13 @@ class Renderer:
     """Forward / backward of the LinPrim tile rasterizer over a list of views (C-ABI calls only)."""
 
     def __init__(self, scene: DeviceScene, cams, aa_kernel=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), capacity=None,
-                 with_canon=False, count_stats=False, sync_capacity=True, sort_method=None):
+                 with_canon=False, count_stats=False, sync_capacity=True, sort_method=None, exact=False):
         self.scene = scene
         self.sort_method = L.LP_SORT_RADIX if sort_method is None else int(sort_method)
         self.cam_dicts = list(cams)
         self.cams = L.cameras(self.cam_dicts)
-        self.cfg = L.raster_cfg(aa_kernel, t_stop, bg, count_stats)
+        # exact: the "no ray space" variant (App. D, lp_raster_cfg.exact)
+        self.cfg = L.raster_cfg(aa_kernel, t_stop, bg, count_stats, exact)
         self.with_canon = with_canon
         self.sync_capacity = sync_capacity
         dev = scene.flat.device

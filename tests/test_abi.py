@@ -40,15 +40,15 @@ def test_library_exports_every_declared_symbol(L):
 
 
 def test_abi_version_and_status_strings(L):
-    assert L.lp_abi_version() == 1
+    assert L.lp_abi_version() == 2
     assert L.lp_status_string(L.LP_OK) == "ok"
     assert "capacity" in L.lp_status_string(L.LP_ERR_CAPACITY)
 
 
 def test_struct_sizes_match_header_layout(L):
-    # lp_camera: 9+3+5 floats + 2 ints = 76 B; lp_raster_cfg: 5 floats + 1 int = 24 B
+    # lp_camera: 9+3+5 floats + 2 ints = 76 B; lp_raster_cfg: 5 floats + 2 ints = 28 B
     assert C.sizeof(L.lp_camera) == 76
-    assert C.sizeof(L.lp_raster_cfg) == 24
+    assert C.sizeof(L.lp_raster_cfg) == 28
     assert C.sizeof(L.lp_prims) == 12 + 4 + 6 * 8
     assert C.sizeof(L.lp_adam_group) == 24
 
