@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--loss", default="l1ssim", choices=["l1ssim", "l1"],
                     help="training loss: 3DGS (1-0.2) L1 + 0.2 (1-SSIM) (P:212) or L1 only")
+    ap.add_argument("--exact", action="store_true",
+                    help="the paper's no-ray-space variant (App. D) instead of the EWA ray-space method")
     ap.add_argument("--streams", type=int, default=2, help="CUDA streams the views of a step are spread over")
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop (ncu --profile-from-start off) and exit")
@@ -156,13 +158,14 @@ def run_ours(args, rank, world, local_rank):
     tgt_scene["pos"] = (scene["pos"] + rng.normal(0, 0.01, scene["pos"].shape) *
                         scene["dist"].mean(0, keepdims=True)).astype(np.float32)
     tds = render.DeviceScene(tgt_scene, device=dev)
-    trend = render.Renderer(tds, [cams[v] for v in my_views])
+    trend = render.Renderer(tds, [cams[v] for v in my_views], exact=args.exact, aa_kernel=0.0 if args.exact else 0.1)
     targets = trend.forward()
     torch.cuda.synchronize()
     del trend, tds
 
     # counters pass (untimed): per-view E, iterated and intersected pairs
-    rr = render.Renderer(ds, [cams[v] for v in my_views], count_stats=True)
+    rr = render.Renderer(ds, [cams[v] for v in my_views], count_stats=True, exact=args.exact,
+                         aa_kernel=0.0 if args.exact else 0.1)
     img = torch.empty((len(my_views), 3, H, W), dtype=torch.float32, device=dev)
     rr.forward(image=img)
     torch.cuda.synchronize()
@@ -177,6 +180,7 @@ def run_ours(args, rank, world, local_rank):
 
     # the timed renderer: async binning (no host sync), capacity sized from the counters pass
     rend = render.Renderer(ds, [cams[v] for v in my_views], capacity=int(max(E) * 1.3) + 4096,
+                           exact=args.exact, aa_kernel=0.0 if args.exact else 0.1,
                            sync_capacity=False)
     st = torch.cuda.current_stream(dev)
     dL = torch.empty_like(img)
@@ -437,6 +441,7 @@ def run_ours(args, rank, world, local_rank):
         "iters_per_s": round(iters, 3),
         "config": {"workload": "C5: 1M octahedra, SH deg 3, 8 views 1600x1060, training step (views sharded)",
                    "loss": "3DGS 0.8 L1 + 0.2 (1 - SSIM)" if args.loss == "l1ssim" else "L1",
+                   "projection": "no ray space (App. D)" if args.exact else "EWA ray space",
                    "n_primitives": n, "kind": "octahedron", "sh_degree": 3, "global_batch_views": views_total,
                    "views_per_gpu": n_local, "width": W, "height": H, "parallelism": f"dp{world} (views)",
                    "l2": "inputs larger than L2: features+grads+Adam state = %.2f GB touched per step"
