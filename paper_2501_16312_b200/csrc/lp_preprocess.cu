@@ -16,9 +16,16 @@ __device__ __forceinline__ void warp_count(uint32_t *ctr, bool pred) {
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(ctr, (uint32_t)__popc(b));
 }
 
-// unclamped SH colour exactly as the forward computes it (fp32), shared by K1 and K5
+// unclamped SH colour exactly as the forward computes it (fp32), shared by K1 and K5.  DEG is the
+// compile-time SH degree: the (DEG+1)^2 x 3 coefficient loads are issued together, then summed in
+// basis order (acc = 0.5 + sum_k sh_k Y_k, one FFMA per term).
+template <int DEG>
 __device__ __forceinline__ void sh_colour_fp32(const lp_prims &P, int i, const lp_camera &cam, const float c[3],
                                                float raw[3]) {
+  constexpr int NC = (DEG + 1) * (DEG + 1);
+  float shv[NC * 3];
+#pragma unroll
+  for (int q = 0; q < NC * 3; ++q) shv[q] = P.sh[(size_t)q * P.n + i];
   const float cpx = -(cam.W[0] * cam.t[0] + cam.W[3] * cam.t[1] + cam.W[6] * cam.t[2]);
   const float cpy = -(cam.W[1] * cam.t[0] + cam.W[4] * cam.t[1] + cam.W[7] * cam.t[2]);
   const float cpz = -(cam.W[2] * cam.t[0] + cam.W[5] * cam.t[1] + cam.W[8] * cam.t[2]);
@@ -28,14 +35,12 @@ __device__ __forceinline__ void sh_colour_fp32(const lp_prims &P, int i, const l
   vy *= inv;
   vz *= inv;
   float Y[16];
-  sh_basis<float>(P.sh_degree, vx, vy, vz, Y);
-  const int ncoef = (P.sh_degree + 1) * (P.sh_degree + 1);
+  sh_basis<float>(DEG, vx, vy, vz, Y);
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
     float acc = 0.5f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k)   // static indices keep Y[] in registers
-      if (k < ncoef) acc += P.sh[((size_t)k * 3 + ch) * P.n + i] * Y[k];
+    for (int k = 0; k < NC; ++k) acc += shv[k * 3 + ch] * Y[k];
     raw[ch] = acc;
   }
 }
@@ -51,17 +56,17 @@ struct PreViews {
   int nv;
 };
 
-template <int KIND, bool EXACT>
+template <int KIND, bool EXACT, int DEG>
 __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_camera &cam, float kappa,
                                                 const lp_frame &F, int i);
 
-template <int KIND, bool EXACT>
+template <int KIND, bool EXACT, int DEG>
 __global__ void __launch_bounds__(256) k_preprocess(lp_prims P, float kappa, PreViews V) {
   // view-interleaved grid: the nv consecutive blocks of one primitive range run the nv views, so
   // the primitive features come from HBM once and from L2 for the other views
   const int v = blockIdx.x % V.nv;
   const int i = (blockIdx.x / V.nv) * blockDim.x + threadIdx.x;
-  preprocess_view<KIND, EXACT>(P, V.cam[v], kappa, V.frame[v], i);
+  preprocess_view<KIND, EXACT, DEG>(P, V.cam[v], kappa, V.frame[v], i);
 }
 
 // exact-mode record planes (App. D, reading 27), fp64 from the canonical fp32 geometry
@@ -121,7 +126,7 @@ __device__ __forceinline__ bool exact_planes(const Geom &g, float *rec) {
   }
 }
 
-template <int KIND, bool EXACT>
+template <int KIND, bool EXACT, int DEG>
 __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_camera &cam, float kappa,
                                                 const lp_frame &F, int i) {
   constexpr int K = Kind<KIND>::K, RW = Kind<KIND>::RW, RS = Kind<KIND>::RS;
@@ -173,7 +178,7 @@ __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_came
 
   // ---- SH colour
   float rgb[3];
-  sh_colour_fp32(P, i, cam, c, rgb);
+  sh_colour_fp32<DEG>(P, i, cam, c, rgb);
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) rgb[ch] = fmaxf(rgb[ch], 0.f);
 
@@ -223,10 +228,10 @@ __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_came
     octa_slabs(g.off, S);
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-      const double rz = S.r[s][2];
-      rec[KD::SLAB + 3 * s] = S.ok ? (float)(-S.r[s][0] / rz) : 0.f;
-      rec[KD::SLAB + 1 + 3 * s] = S.ok ? (float)(-S.r[s][1] / rz) : 0.f;
-      rec[KD::SLAB + 2 + 3 * s] = S.ok ? (float)(1.0 / fabs(rz)) : -1.f;   // h = -1: never intersected
+      const double irz = 1.0 / S.r[s][2];   // one fp64 division per slab (K5 uses the same)
+      rec[KD::SLAB + 3 * s] = S.ok ? (float)(-S.r[s][0] * irz) : 0.f;
+      rec[KD::SLAB + 1 + 3 * s] = S.ok ? (float)(-S.r[s][1] * irz) : 0.f;
+      rec[KD::SLAB + 2 + 3 * s] = S.ok ? (float)fabs(irz) : -1.f;   // h = -1: never intersected
     }
   } else {
     TetraPlanes T;
@@ -595,7 +600,7 @@ __device__ __forceinline__ void sh_view_inputs(const lp_prims &P, const lp_camer
   float raw[3];
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) gr[ch] = rgrad[(size_t)(rg_words - 3 + ch) * n + i];
-  sh_colour_fp32(P, i, cam, c, raw);   // the forward's exact fp32 colour decides the clamp
+  sh_colour_fp32<DEG>(P, i, cam, c, raw);   // the forward's exact fp32 colour decides the clamp
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch)
     if (raw[ch] < 0.f) gr[ch] = 0.f;
@@ -768,6 +773,16 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd(lp_prims P, float kappa, 
 }
 
 // ---------------------------------------------------------------------------------------------
+template <int KIND, bool EXACT>
+static void pre_deg(const lp_prims &P, float kappa, const PreViews &V, int grid, cudaStream_t st) {
+  switch (P.sh_degree) {
+    case 0: k_preprocess<KIND, EXACT, 0><<<grid, 256, 0, st>>>(P, kappa, V); break;
+    case 1: k_preprocess<KIND, EXACT, 1><<<grid, 256, 0, st>>>(P, kappa, V); break;
+    case 2: k_preprocess<KIND, EXACT, 2><<<grid, 256, 0, st>>>(P, kappa, V); break;
+    default: k_preprocess<KIND, EXACT, 3><<<grid, 256, 0, st>>>(P, kappa, V); break;
+  }
+}
+
 void launch_preprocess(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
                        bool exact, cudaStream_t st) {
   if (P.n == 0 || n_views <= 0) return;
@@ -781,11 +796,11 @@ void launch_preprocess(const lp_prims &P, const lp_camera *cams, float kappa, co
       V.frame[v] = frames[s];
     }
     if (P.kind == LP_OCTAHEDRON) {
-      if (exact) k_preprocess<LP_OCTAHEDRON, true><<<grid * V.nv, 256, 0, st>>>(P, kappa, V);
-      else k_preprocess<LP_OCTAHEDRON, false><<<grid * V.nv, 256, 0, st>>>(P, kappa, V);
+      if (exact) pre_deg<LP_OCTAHEDRON, true>(P, kappa, V, grid * V.nv, st);
+      else pre_deg<LP_OCTAHEDRON, false>(P, kappa, V, grid * V.nv, st);
     } else {
-      if (exact) k_preprocess<LP_TETRAHEDRON, true><<<grid * V.nv, 256, 0, st>>>(P, kappa, V);
-      else k_preprocess<LP_TETRAHEDRON, false><<<grid * V.nv, 256, 0, st>>>(P, kappa, V);
+      if (exact) pre_deg<LP_TETRAHEDRON, true>(P, kappa, V, grid * V.nv, st);
+      else pre_deg<LP_TETRAHEDRON, false>(P, kappa, V, grid * V.nv, st);
     }
   }
 }

@@ -9,14 +9,24 @@ WANT = ["Duration", "SM Frequency", "DRAM Throughput", "Memory Throughput", "Com
         "Warp Cycles Per Issued Instruction", "Block Size", "Grid Size", "Static Shared Memory Per Block"]
 
 
-def main(rep):
+def main(rep, kernel=None):
+    """First captured launch of `kernel` (substring of the name; default: the first launch)."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h = rows[0]
     ki, mi, vi, ui = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    idi = h.index("ID") if "ID" in h else None
     seen = set()
     name = None
+    launch = None
     for r in rows[1:]:
+        if kernel is not None and kernel not in r[ki].split("(")[0]:
+            continue
+        if idi is not None:
+            if launch is None:
+                launch = r[idi]
+            elif r[idi] != launch:
+                continue
         if name is None:
             name = r[ki]
             print(name[:120])
@@ -26,4 +36,4 @@ def main(rep):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)
