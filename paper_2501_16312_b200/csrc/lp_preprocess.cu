@@ -179,8 +179,10 @@ __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_came
   // ---- SH colour
   float rgb[3];
   sh_colour_fp32<DEG>(P, i, cam, c, rgb);
+  // clamp max(0, .); a clamped channel is stored as -0.0 so the backward reads the clamp
+  // decision from the record's sign bit instead of re-evaluating the SH colour
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) rgb[ch] = fmaxf(rgb[ch], 0.f);
+  for (int ch = 0; ch < 3; ++ch) rgb[ch] = rgb[ch] < 0.f ? -0.f : rgb[ch];
 
   // ---- raster record
   using KD = Kind<KIND>;
@@ -259,11 +261,21 @@ __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_came
 // feature gradients are accumulated in registers and written once per call, and a primitive
 // invisible in one view usually has work in another (better SIMT utilisation).
 // =============================================================================================
-constexpr int LP_MAXV = 8;
+// views per K5 launch and resident K5 blocks per SM asked of the register allocator (measured on
+// C5: 4 views x 8 blocks (128 registers, a few spills) beats 8 x 1 (196 registers, 40 KB smem)
+// by 8 %; -DLP_K5_MAXV / -DLP_K5_MINB override)
+#ifndef LP_K5_MAXV
+#define LP_K5_MAXV 4
+#endif
+#ifndef LP_K5_MINB
+#define LP_K5_MINB 8
+#endif
+constexpr int LP_MAXV = LP_K5_MAXV;
 struct ViewPack {
   lp_camera cam[LP_MAXV];
   const float *rgrad[LP_MAXV];
   const uint32_t *tt[LP_MAXV];
+  const float *rec[LP_MAXV];   // the view's raster records: the stored colour's sign bit is the clamp
   int nv;
 };
 
@@ -592,18 +604,18 @@ __device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_ca
 // owner lane), plus the view-direction term of the centre gradient.
 template <int DEG>
 __device__ __forceinline__ void sh_view_inputs(const lp_prims &P, const lp_camera &cam, int i,
-                                               const float *__restrict__ rgrad, int rg_words, float gr[3],
-                                               float dir[3], float gpos[3]) {
+                                               const float *__restrict__ rgrad, int rg_words,
+                                               const float *__restrict__ rec_rgb, float gr[3], float dir[3],
+                                               float gpos[3]) {
   constexpr int NC = (DEG + 1) * (DEG + 1);
   const int n = P.n;
   const float c[3] = {P.pos[i], P.pos[n + i], P.pos[2 * n + i]};
-  float raw[3];
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) gr[ch] = rgrad[(size_t)(rg_words - 3 + ch) * n + i];
-  sh_colour_fp32<DEG>(P, i, cam, c, raw);   // the forward's exact fp32 colour decides the clamp
+  // the forward's clamp decision, stored by K1 as the colour's sign bit (-0.0: clamped)
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch)
-    if (raw[ch] < 0.f) gr[ch] = 0.f;
+    if (signbit(rec_rgb[ch])) gr[ch] = 0.f;
   const float cpx = -(cam.W[0] * cam.t[0] + cam.W[3] * cam.t[1] + cam.W[6] * cam.t[2]);
   const float cpy = -(cam.W[1] * cam.t[0] + cam.W[4] * cam.t[1] + cam.W[7] * cam.t[2]);
   const float cpz = -(cam.W[2] * cam.t[0] + cam.W[5] * cam.t[1] + cam.W[8] * cam.t[2]);
@@ -643,7 +655,7 @@ struct ItemRes {
 // read-modify-writes every feature gradient once.  No shared-memory float atomics (sm_100 has
 // none: they compile to CAS loops).
 template <int KIND, int DEG, bool EXACT>
-__global__ void __launch_bounds__(64) k_preprocess_bwd(lp_prims P, float kappa, ViewPack V, int rg_words,
+__global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, float kappa, ViewPack V, int rg_words,
                                                        lp_grads Gs) {
   constexpr int WARPS = 2, K = Kind<KIND>::K, NC = (DEG + 1) * (DEG + 1);
   __shared__ lp_camera s_cam[LP_MAXV];
@@ -705,7 +717,11 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd(lp_prims P, float kappa, 
       float gpos[3] = {0.f, 0.f, 0.f}, grot[4] = {0.f, 0.f, 0.f, 0.f}, gdist[4] = {0.f, 0.f, 0.f, 0.f};
       float gop = 0.f, m2d = 0.f, gr[3] = {0.f, 0.f, 0.f}, dir[3] = {0.f, 0.f, 1.f};
       view_feature_grad<KIND, EXACT>(P, s_cam[v], kappa, ii, s_rg[v], gpos, grot, gdist, gop, m2d);
-      if (Gs.sh || Gs.pos) sh_view_inputs<DEG>(P, s_cam[v], ii, s_rg[v], rg_words, gr, dir, gpos);
+      if (Gs.sh || Gs.pos) {
+        constexpr int RGBW = EXACT ? ExactRec<KIND>::RGB : Kind<KIND>::RGB;
+        const float *rgb = V.rec[v] + (size_t)ii * Kind<KIND>::RS + RGBW;
+        sh_view_inputs<DEG>(P, s_cam[v], ii, s_rg[v], rg_words, rgb, gr, dir, gpos);
+      }
       float *res = s_res[w][it];
 #pragma unroll
       for (int a = 0; a < 3; ++a) res[ItemRes::POS + a] = gpos[a];
@@ -827,6 +843,7 @@ void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa
       V.cam[v] = cams[s];
       V.rgrad[v] = frames[s].rgrad;
       V.tt[v] = frames[s].tiles_touched;
+      V.rec[v] = frames[s].record;
     }
     const int rg = frames[v0].rgrad_words;
     if (P.kind == LP_OCTAHEDRON) {
