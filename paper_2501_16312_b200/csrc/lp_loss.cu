@@ -12,9 +12,12 @@
 // there (zero outside the image), runs the window again on the G maps for the core and writes
 // dL/dx.  HBM traffic is the minimum 12 B per pixel-channel (read x, y; write dL/dx); the kernel
 // is FP32-FMA bound (~290 FMA per pixel-channel).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "lp_kernels.h"
 #include "lp_x2.cuh"
@@ -273,6 +276,295 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim(const float *__restrict__ i
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// TMA-fed persistent variant (used when the image rows are 16-byte aligned, W % 4 == 0): one CTA
+// loops over (plane, tile) work items; the x and y input boxes (10-pixel halo, zero fill outside
+// the image done by the tensor-map OOB rule) arrive by cp.async.bulk.tensor into a double buffer,
+// the next item's boxes in flight while the current one is computed.  The box starts 12 columns
+// left of the tile (56 x 52): a TMA box's innermost start coordinate must be a multiple of
+// 16 bytes when it is negative (measured: other negative x starts fault), so the 52-wide window
+// sits at box column 2.
+// ---------------------------------------------------------------------------------------------
+namespace {
+constexpr int BW = RI + 4;           // 56: box width (start 12 columns left of the tile)
+constexpr int BX = 2;                // box column of window column 0
+constexpr int BOXF = BW * RI;        // 2912 floats = 11648 B (a multiple of 128 B)
+struct LossSmemT {
+  float box[2][2][BOXF];             // [buffer][x | y]
+  union {
+    struct {
+      float2 h01[RI][RA];
+      float2 h23[RI][RA];
+      float h4[RI][RA];
+    } a;
+    struct {
+      float2 h01[RA][TS];
+      float h2[RA][TS];
+    } b;
+  } u;
+  float2 g01[RA][RA + 1];
+  float g2[RA][RA + 1];
+  unsigned long long bar[2];
+  float red[LT / 32];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                            unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+}  // namespace
+
+__global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__ CUtensorMap map_x,
+                                                         const __grid_constant__ CUtensorMap map_y,
+                                                         float *__restrict__ dL, float *__restrict__ loss_sum, int H,
+                                                         int W, int tiles_x, int tiles_per_plane, int items,
+                                                         float lam, float scale, Win win) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  LossSmemT &S = *reinterpret_cast<LossSmemT *>(smem_raw);
+  const int tid = threadIdx.x;
+  constexpr uint32_t BOX_BYTES = BW * RI * 4;
+  if (tid == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int item, int buf) {
+    const int plane = item / tiles_per_plane, tile = item % tiles_per_plane;
+    const int tx0 = (tile % tiles_x) * TS, ty0 = (tile / tiles_x) * TS;
+    mbar_expect_tx(&S.bar[buf], 2 * BOX_BYTES);
+    tma_load_3d(S.box[buf][0], &map_x, tx0 - 2 * RAD - BX, ty0 - 2 * RAD, plane, &S.bar[buf]);
+    tma_load_3d(S.box[buf][1], &map_y, tx0 - 2 * RAD - BX, ty0 - 2 * RAD, plane, &S.bar[buf]);
+  };
+  if (tid == 0 && (int)blockIdx.x < items) issue(blockIdx.x, 0);
+  float lsum = 0.f;
+  uint32_t phase[2] = {0u, 0u};
+  int buf = 0;
+  for (int item = blockIdx.x; item < items; item += gridDim.x, buf ^= 1) {
+    if (tid == 0 && item + (int)gridDim.x < items) issue(item + gridDim.x, buf ^ 1);
+    mbar_wait(&S.bar[buf], phase[buf]);
+    phase[buf] ^= 1u;
+    const float *X = S.box[buf][0], *Y = S.box[buf][1];
+    const int plane = item / tiles_per_plane, tile = item % tiles_per_plane;
+    const int tx0 = (tile % tiles_x) * TS, ty0 = (tile / tiles_x) * TS;
+    float *D = dL + (size_t)plane * H * W;
+
+    // ---- stage 2: horizontal window sums of the five products, 52 rows x 42 cols
+    {
+      constexpr int CH = 6, NCH = RA / CH;
+      for (int it = tid; it < RI * NCH; it += LT) {
+        const int r = it / NCH, c0 = (it % NCH) * CH;
+        float2 a01[CH], a23[CH];
+        float a4[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          a01[j] = a23[j] = make_float2(0.f, 0.f);
+          a4[j] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < CH + TAPS - 1; ++k) {
+          const float2 v01 = make_float2(X[r * BW + BX + c0 + k], Y[r * BW + BX + c0 + k]);
+          const float2 v23 = fmul2(v01, v01);
+          const float v4 = v01.x * v01.y;
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int t = k - j;
+            if (t >= 0 && t < TAPS) {
+              a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+              a23[j] = ffma2(bc(win.g[t]), v23, a23[j]);
+              a4[j] = fmaf(win.g[t], v4, a4[j]);
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          S.u.a.h01[r][c0 + j] = a01[j];
+          S.u.a.h23[r][c0 + j] = a23[j];
+          S.u.a.h4[r][c0 + j] = a4[j];
+        }
+      }
+    }
+    __syncthreads();
+    // ---- stage 3: vertical sums -> S and the G maps on the 42 x 42 region
+    {
+      constexpr int CH = 6, NCH = RA / CH;
+      for (int it = tid; it < RA * NCH; it += LT) {
+        const int c = it % RA, r0 = (it / RA) * CH;
+        float2 a01[CH], a23[CH];
+        float a4[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          a01[j] = a23[j] = make_float2(0.f, 0.f);
+          a4[j] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < CH + TAPS - 1; ++k) {
+          const float2 v01 = S.u.a.h01[r0 + k][c], v23 = S.u.a.h23[r0 + k][c];
+          const float v4 = S.u.a.h4[r0 + k][c];
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int t = k - j;
+            if (t >= 0 && t < TAPS) {
+              a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+              a23[j] = ffma2(bc(win.g[t]), v23, a23[j]);
+              a4[j] = fmaf(win.g[t], v4, a4[j]);
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int r = r0 + j;
+          const int gy = ty0 - RAD + r, gx = tx0 - RAD + c;
+          float gmv = 0.f, gxy = 0.f, gxx = 0.f;
+          if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+            const float mx = a01[j].x, my = a01[j].y;
+            const float vx = a23[j].x - mx * mx, vy = a23[j].y - my * my, cxy = a4[j] - mx * my;
+            const float A1 = 2.f * mx * my + C1, A2 = 2.f * cxy + C2;
+            const float B1 = mx * mx + my * my + C1, B2 = vx + vy + C2;
+            const float iB1 = __fdividef(1.f, B1), iB2 = __fdividef(1.f, B2);
+            const float ssim = A1 * A2 * iB1 * iB2;
+            gmv = 2.f * my * (A2 - A1) * iB1 * iB2 - 2.f * mx * ssim * (iB1 - iB2);
+            gxy = 2.f * A1 * iB1 * iB2;
+            gxx = -ssim * iB2;
+            if (r >= RAD && r < RAD + TS && c >= RAD && c < RAD + TS) lsum += lam * (1.f - ssim);
+          }
+          S.g01[r][c] = make_float2(gmv, gxy);
+          S.g2[r][c] = gxx;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- stage 4: horizontal window sums of the G maps
+    {
+      constexpr int CH = 4, NCH = TS / CH;
+      for (int it = tid; it < RA * NCH; it += LT) {
+        const int r = it / NCH, c0 = (it % NCH) * CH;
+        float2 a01[CH];
+        float a2[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          a01[j] = make_float2(0.f, 0.f);
+          a2[j] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < CH + TAPS - 1; ++k) {
+          const float2 v01 = S.g01[r][c0 + k];
+          const float v2 = S.g2[r][c0 + k];
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int t = k - j;
+            if (t >= 0 && t < TAPS) {
+              a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+              a2[j] = fmaf(win.g[t], v2, a2[j]);
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          S.u.b.h01[r][c0 + j] = a01[j];
+          S.u.b.h2[r][c0 + j] = a2[j];
+        }
+      }
+    }
+    __syncthreads();
+    // ---- stage 5: vertical sums on the core, combine with L1, write dL/dx
+    {
+      constexpr int CH = 4, NCH = TS / CH;
+      for (int it = tid; it < TS * NCH; it += LT) {
+        const int c = it % TS, r0 = (it / TS) * CH;
+        float2 a01[CH];
+        float a2[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          a01[j] = make_float2(0.f, 0.f);
+          a2[j] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < CH + TAPS - 1; ++k) {
+          const float2 v01 = S.u.b.h01[r0 + k][c];
+          const float v2 = S.u.b.h2[r0 + k][c];
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int t = k - j;
+            if (t >= 0 && t < TAPS) {
+              a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+              a2[j] = fmaf(win.g[t], v2, a2[j]);
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int gy = ty0 + r0 + j, gx = tx0 + c;
+          if (gy < H && gx < W) {
+            const int bi = (r0 + j + 2 * RAD) * BW + BX + c + 2 * RAD;
+            const float x = X[bi], y = Y[bi];
+            const float d = x - y;
+            const float sg = (float)((d > 0.f) - (d < 0.f));
+            const float dS = a01[j].x + y * a01[j].y + 2.f * x * a2[j];
+            D[(size_t)gy * W + gx] = scale * ((1.f - lam) * sg - lam * dS);
+            lsum += (1.f - lam) * fabsf(d);
+          }
+        }
+      }
+    }
+    __syncthreads();   // every thread is done with box[buf] and the stage buffers
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  if ((tid & 31) == 0) S.red[tid >> 5] = lsum;
+  __syncthreads();
+  if (tid == 0) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < LT / 32; ++w) t += S.red[w];
+    atomicAdd(loss_sum, scale * t);
+  }
+}
+
+static bool make_box_map(CUtensorMap *map, const float *base, int planes, int H, int W) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return false;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)planes};
+  const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * H * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)BW, (cuuint32_t)RI, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void launch_loss_ssim(const float *img, const float *tgt, float *dL, float *loss_sum, int n_planes, int H, int W,
                       float lam, float scale, cudaStream_t st) {
   if (n_planes <= 0 || H <= 0 || W <= 0) return;
@@ -284,6 +576,26 @@ void launch_loss_ssim(const float *img, const float *tgt, float *dL, float *loss
   }
   for (int k = 0; k < TAPS; ++k) win.g[k] = (float)(g[k] / s);
   const int tiles_x = (W + TS - 1) / TS, tiles_y = (H + TS - 1) / TS;
+  // TMA path: rows 16-byte aligned (W % 4 == 0) and 16-byte aligned bases
+  const bool aligned = (W % 4) == 0 && ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(tgt)) & 15) == 0;
+  static const bool tma_off = getenv("LP_LOSS_NO_TMA") != nullptr;   // measurement knob
+  CUtensorMap mx, my;
+  if (aligned && !tma_off && make_box_map(&mx, img, n_planes, H, W) && make_box_map(&my, tgt, n_planes, H, W)) {
+    const size_t smem = sizeof(LossSmemT);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_loss_ssim_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    const int items = tiles_x * tiles_y * n_planes;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = items < 2 * sms ? items : 2 * sms;
+    k_loss_ssim_tma<<<grid, LT, smem, st>>>(mx, my, dL, loss_sum, H, W, tiles_x, tiles_x * tiles_y, items, lam, scale,
+                                            win);
+    return;
+  }
   const size_t smem = sizeof(LossSmem);
   static bool attr = false;
   if (!attr) {
