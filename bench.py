@@ -51,7 +51,7 @@ def parse():
                     help="training loss: 3DGS (1-0.2) L1 + 0.2 (1-SSIM) (P:212) or L1 only")
     ap.add_argument("--exact", action="store_true",
                     help="the paper's no-ray-space variant (App. D) instead of the EWA ray-space method")
-    ap.add_argument("--streams", type=int, default=2, help="CUDA streams the views of a step are spread over")
+    ap.add_argument("--streams", type=int, default=4, help="CUDA streams the views of a step are spread over")
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop (ncu --profile-from-start off) and exit")
     return ap.parse_args()
