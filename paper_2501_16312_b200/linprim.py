@@ -24,6 +24,7 @@ LP_TILE = 16
 LP_CNT_ENTRIES, LP_CNT_OVERFLOW, LP_CNT_INVALID, LP_CNT_FRUSTUM, LP_CNT_VISIBLE = 0, 1, 2, 3, 4
 LP_CNT_ITERATED, LP_CNT_INTERSECTED, LP_CNT_INBOX, LP_NUM_COUNTERS = 8, 10, 12, 16
 LP_SORT_BUCKET, LP_SORT_RADIX = 0, 1
+LP_ABI_VERSION = 2            # include/linprim.h; the loaded library must match the structs below
 
 _p = C.c_void_p
 
@@ -95,6 +96,8 @@ for _name, (_res, _args) in _sig.items():
     _f.argtypes = _args
 
 EXPORTS = tuple(_sig)
+if _lib.lp_abi_version() != LP_ABI_VERSION:
+    raise ImportError(f"{LIB_PATH} has ABI {_lib.lp_abi_version()}, this binding expects {LP_ABI_VERSION}; rebuild")
 
 
 class LinPrimError(RuntimeError):
