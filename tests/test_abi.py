@@ -90,3 +90,9 @@ def test_no_oracle_in_product_path():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "lpo_" not in txt, f
+
+
+def test_graft_entry_build_is_consistent():
+    """__graft_entry__.build() (the driver's build check) succeeds against the built library."""
+    import __graft_entry__
+    __graft_entry__.build()
