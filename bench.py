@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override the primitive count (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-zero", action="store_true", help=argparse.SUPPRESS)   # exercise the sharded path at N = 1
+    ap.add_argument("--no-zero", action="store_true",
+                    help="N > 1: allreduce + replicated Adam instead of reduce-scatter + sharded Adam + all-gather")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--loss", default="l1ssim", choices=["l1ssim", "l1"],
                     help="training loss: 3DGS (1-0.2) L1 + 0.2 (1-SSIM) (P:212) or L1 only")
@@ -150,7 +153,11 @@ def run_ours(args, rank, world, local_rank):
     n_views = len(cams)
     W, H = cams[0]["width"], cams[0]["height"]
     my_views = train.shard_views(n_views, rank, world)
-    ds = render.DeviceScene(scene, device=dev)
+    # N > 1: sharded optimizer (reduce-scatter, Adam on 1/N of the parameters, all-gather)
+    zero = (world > 1 or args.force_zero) and not args.no_zero
+    total = sum(sz for _, sz in train.section_sizes(scene["kind"], scene["pos"].shape[1], scene["sh_degree"]))
+    lo, hi, chunk = train.shard_range(total, rank, world)
+    ds = render.DeviceScene(scene, device=dev, pad_to=world * chunk if zero else 0)
 
     # synthetic targets: the same scene with jittered centres, rendered once at setup
     rng = np.random.default_rng(1234)
@@ -187,11 +194,13 @@ def run_ours(args, rank, world, local_rank):
     n_local = len(my_views)
     total_steps = args.warmup + args.steps
     loss_buf = torch.zeros(2 * total_steps + 64, dtype=torch.float32, device=dev)
-    m = torch.zeros_like(ds.flat)
-    v = torch.zeros_like(ds.flat)
+    m = torch.zeros(chunk if zero else ds.flat.numel(), dtype=torch.float32, device=dev)
+    v = torch.zeros_like(m)
+    gshard = torch.zeros(chunk, dtype=torch.float32, device=dev) if zero else None
     # paper's learning rates; position 1.6e-4 x extent (3DGS), distances 2.6^-1 1e-4 x extent
     n = ds.n
     groups = train.lr_groups(ds.offsets, n, extent=4.0)
+    sgroups = train.shard_groups(groups, lo, hi) if zero else None
     scale = 1.0 / (3.0 * W * H * n_views)
     cams_c = rend.cams
     ev_names = ["sort", "fwd", "loss", "rbwd"]         # per view
@@ -250,10 +259,19 @@ def run_ours(args, rank, world, local_rank):
         # preprocess backward fused over this rank's views (feature + SH gradients written once)
         L.lp_preprocess_bwd(ds.prims, ca_all, rend.cfg, fa_all, ds.grads, st)
         rec(S, 2, st)
-        if world > 1:
-            train.allreduce_gradients(ds.grad, world)
+        if world > 1 or zero:
+            if zero:
+                train.reduce_scatter_gradients(ds.grad_padded, gshard, world)
+                ds.grad_padded.zero_()
+            else:
+                train.allreduce_gradients(ds.grad, world)
         rec(S, 3, st)
-        L.lp_adam_step(ds.flat, ds.grad, m, v, groups, 0.9, 0.999, 1e-15, si + 1, st, zero_grad=True)
+        if zero:   # Adam on this rank's shard, then the all-gather of the parameters (in the "adam" stage)
+            L.lp_adam_step(ds.flat_padded[rank * chunk:(rank + 1) * chunk], gshard, m, v, sgroups, 0.9, 0.999, 1e-15,
+                           si + 1, st, zero_grad=False)
+            train.all_gather_params(ds.flat_padded, rank, chunk)
+        else:
+            L.lp_adam_step(ds.flat, ds.grad, m, v, groups, 0.9, 0.999, 1e-15, si + 1, st, zero_grad=True)
         rec(S, 4, st)
 
     def barrier():
@@ -350,7 +368,7 @@ def run_ours(args, rank, world, local_rank):
         # gradients read-modified-written once per call
         "pbwd_all_views": ("k_preprocess_bwd+k_sh_bwd", "hbm", 4 * n * n_local + vis * n_local * 4 * RG + n * 3 * Fb),
         "pre_all_views": ("k_preprocess", "hbm", n * Fb + n_local * (n * 24 + vis * 4 * RW)),
-        "adam": ("k_adam", "hbm", 32 * ds.flat.numel()),
+        "adam": ("k_adam", "hbm", 32 * (chunk if zero else ds.flat.numel())),
         # separable 11-tap window: 5 products x 2 directions x 11 + 3 G maps x 2 x 11 FMA + ~30 for
         # S and the G maps per pixel-channel; L1 only: 12 B per pixel-channel
         "loss": ("k_loss_ssim", "alu", 206 * 3 * W * H) if args.loss == "l1ssim" else ("k_l1_grad", "hbm", 12 * 3 * W * H),
@@ -443,7 +461,7 @@ def run_ours(args, rank, world, local_rank):
                    "loss": "3DGS 0.8 L1 + 0.2 (1 - SSIM)" if args.loss == "l1ssim" else "L1",
                    "projection": "no ray space (App. D)" if args.exact else "EWA ray space",
                    "n_primitives": n, "kind": "octahedron", "sh_degree": 3, "global_batch_views": views_total,
-                   "views_per_gpu": n_local, "width": W, "height": H, "parallelism": f"dp{world} (views)",
+                   "views_per_gpu": n_local, "width": W, "height": H, "parallelism": f"dp{world} (views)" + (", sharded Adam (reduce-scatter / all-gather)" if zero else ""),
                    "l2": "inputs larger than L2: features+grads+Adam state = %.2f GB touched per step"
                          % (ds.flat.numel() * 4 * 5 / 1e9),
                    "tile_list_entries_per_view": E, "iterated_pairs_per_px": round(I_tot / (n_local * W * H), 2),
@@ -537,7 +555,8 @@ def main():
             print(json.dumps(out))
         return
     import torch
-    if world > 1:
+    use_dist = world > 1 or args.force_zero
+    if use_dist:
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
@@ -549,7 +568,7 @@ def main():
             scene, cams, _ = ctx
             out["cpu_baseline"] = cpu_baseline(scene, cams)
         print(json.dumps(out))
-    if world > 1:
+    if use_dist:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()

@@ -19,15 +19,21 @@ from .train import section_sizes
 class DeviceScene:
     """Primitive features + gradient sinks in flat device buffers."""
 
-    def __init__(self, scene: dict, device="cuda", filter3d=None):
+    def __init__(self, scene: dict, device="cuda", filter3d=None, pad_to: int = 0):
         self.kind = int(scene["kind"])
         self.sh_degree = int(scene["sh_degree"])
         self.n = int(scene["pos"].shape[1])
         self.K = 3 if self.kind == L.LP_OCTAHEDRON else 4
         secs = section_sizes(self.kind, self.n, self.sh_degree)
         total = sum(s for _, s in secs)
-        self.flat = torch.empty(total, dtype=torch.float32, device=device)
-        self.grad = torch.zeros(total, dtype=torch.float32, device=device)
+        self.total = total
+        # pad_to: allocate the flat buffers padded (sharded optimizer: world * chunk elements); the
+        # padding is zero and never read by the kernels
+        alloc = max(total, int(pad_to))
+        self.flat_padded = torch.zeros(alloc, dtype=torch.float32, device=device)
+        self.grad_padded = torch.zeros(alloc, dtype=torch.float32, device=device)
+        self.flat = self.flat_padded[:total]
+        self.grad = self.grad_padded[:total]
         self.offsets = {}
         o = 0
         for name, size in secs:

@@ -48,3 +48,46 @@ def allreduce_gradients(flat_grad, world: int):
         import torch.distributed as dist
         dist.all_reduce(flat_grad, op=dist.ReduceOp.SUM)
     return flat_grad
+
+
+# ---------------------------------------------------------------------------------------------
+# sharded optimizer (N > 1): reduce-scatter the flat gradient, Adam on the rank's shard only,
+# all-gather the parameters -- the allreduce's wire bytes, 1/N of the Adam work and Adam state
+# per rank (SURVEY §8e variant).
+# ---------------------------------------------------------------------------------------------
+def shard_range(total: int, rank: int, world: int, align: int = 4):
+    """(lo, hi, chunk): the rank's [lo, hi) of a flat buffer of `total` elements split into `world`
+    equal chunks of `chunk` elements (a multiple of `align`, so the float4 Adam path applies); the
+    buffer is padded to world * chunk, the padding belongs to the last ranks."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    per = -(-total // world)
+    chunk = -(-per // align) * align
+    lo = min(rank * chunk, total)
+    hi = min(lo + chunk, total)
+    return lo, hi, chunk
+
+
+def shard_groups(groups, lo: int, hi: int) -> list:
+    """Adam groups (begin, end, lr) clipped to [lo, hi) and re-based to the shard start."""
+    out = []
+    for b, e, lr in groups:
+        b2, e2 = max(int(b), lo), min(int(e), hi)
+        if b2 < e2:
+            out.append((b2 - lo, e2 - lo, lr))
+    return out
+
+
+def reduce_scatter_gradients(flat_grad_padded, grad_shard, world: int):
+    """grad_shard (chunk elements) <- this rank's chunk of the SUM over ranks of flat_grad_padded."""
+    import torch.distributed as dist
+    dist.reduce_scatter_tensor(grad_shard, flat_grad_padded, op=dist.ReduceOp.SUM)
+    return grad_shard
+
+
+def all_gather_params(flat_padded, rank: int, chunk: int):
+    """Every rank's updated chunk into every rank's padded parameter buffer (in place: the input is
+    this rank's chunk of the output)."""
+    import torch.distributed as dist
+    dist.all_gather_into_tensor(flat_padded, flat_padded[rank * chunk:(rank + 1) * chunk])
+    return flat_padded

@@ -86,3 +86,77 @@ def test_two_rank_gloo_allreduce_matches_single_process(tmp_path):
     ref = _flat_grad(scene, cams, range(N_VIEWS))
     assert np.allclose(g0, ref, rtol=1e-12, atol=1e-18)    # == the single-process sum over all views
     assert np.abs(ref).max() > 0
+
+
+# ---------------------------------------------------------------- sharded optimizer (N > 1)
+
+def _adam_ref(p, g, m, v, groups, step, b1=0.9, b2=0.999, eps=1e-15):
+    """Plain per-element Adam with bias correction over the listed groups (test reference)."""
+    bc1, bc2 = 1 - b1 ** step, 1 - b2 ** step
+    for b, e, lr in groups:
+        m[b:e] = b1 * m[b:e] + (1 - b1) * g[b:e]
+        v[b:e] = b2 * v[b:e] + (1 - b2) * g[b:e] * g[b:e]
+        p[b:e] = p[b:e] - lr * (m[b:e] / bc1) / (torch.sqrt(v[b:e] / bc2) + eps)
+
+
+@pytest.mark.parametrize("total,world", [(1000, 2), (1003, 2), (7, 4), (4096, 8), (13, 3)])
+def test_shard_range_partitions_the_buffer(total, world):
+    seen = np.zeros(total, np.int32)
+    chunks = set()
+    for r in range(world):
+        lo, hi, chunk = train.shard_range(total, r, world)
+        assert chunk % 4 == 0 and world * chunk >= total
+        assert lo == min(r * chunk, total) and hi - lo <= chunk
+        seen[lo:hi] += 1
+        chunks.add(chunk)
+    assert len(chunks) == 1 and np.all(seen == 1)
+
+
+def test_shard_groups_clip_and_rebase():
+    groups = [(0, 10, 1.0), (10, 25, 2.0), (25, 40, 3.0)]
+    assert train.shard_groups(groups, 8, 20) == [(0, 2, 1.0), (2, 12, 2.0)]
+    assert train.shard_groups(groups, 30, 32) == [(0, 2, 3.0)]
+    assert train.shard_groups(groups, 40, 48) == []
+
+
+def _zero_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    scene, cams = _scene()
+    n, kind, deg = scene["pos"].shape[1], scene["kind"], scene["sh_degree"]
+    off = train.flat_offsets(kind, n, deg)
+    total = max(e for _, e in off.values())
+    lo, hi, chunk = train.shard_range(total, rank, world)
+    g = torch.zeros(world * chunk, dtype=torch.float32)
+    g[:total] = torch.from_numpy(_flat_grad(scene, cams, train.shard_views(N_VIEWS, rank, world))).float()
+    p = torch.zeros(world * chunk, dtype=torch.float32)
+    p[:total] = torch.linspace(-1, 1, total)
+    gs = torch.zeros(chunk, dtype=torch.float32)
+    train.reduce_scatter_gradients(g, gs, world)
+    m, v = torch.zeros(chunk), torch.zeros(chunk)
+    groups = train.shard_groups(train.lr_groups(off, n), lo, hi)
+    _adam_ref(p[rank * chunk:(rank + 1) * chunk], gs, m, v, groups, step=1)
+    train.all_gather_params(p, rank, chunk)
+    np.save(os.path.join(out_dir, f"p{rank}.npy"), p[:total].numpy())
+    dist.destroy_process_group()
+
+
+def test_two_rank_sharded_adam_matches_allreduce_adam(tmp_path):
+    """reduce-scatter + Adam on the rank's shard + all-gather == allreduce + replicated Adam."""
+    world = 2
+    mp.spawn(_zero_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    p0, p1 = np.load(tmp_path / "p0.npy"), np.load(tmp_path / "p1.npy")
+    assert np.array_equal(p0, p1)
+    scene, cams = _scene()
+    n, kind, deg = scene["pos"].shape[1], scene["kind"], scene["sh_degree"]
+    off = train.flat_offsets(kind, n, deg)
+    total = max(e for _, e in off.values())
+    g = torch.zeros(total, dtype=torch.float32)
+    for r in range(world):   # the float32 sum of the two ranks' gradients, as the collective forms it
+        g += torch.from_numpy(_flat_grad(scene, cams, train.shard_views(N_VIEWS, r, world))).float()
+    p = torch.linspace(-1, 1, total)
+    m, v = torch.zeros(total), torch.zeros(total)
+    _adam_ref(p, g, m, v, train.lr_groups(off, n), step=1)
+    assert np.array_equal(p0, p.numpy())
+    assert np.abs(p0 - np.linspace(-1, 1, total)).max() > 1e-4   # the step moved the parameters
