@@ -578,20 +578,68 @@ __device__ __forceinline__ const float *plane_n(const float *rec, int f) {
   return KIND == LP_OCTAHEDRON ? rec + 4 + 3 * f : rec + 4 + 4 * f;
 }
 
+// The thread's two pixel rays r = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1) (same x), their lengths, and the
+// screen offsets x+0.5-cx, y+0.5-cy as unevaluated sums hi + lo (exact): d below needs them to
+// ~1e-7 px relative accuracy, not the ~6e-8 relative accuracy of a rounded r (a rounded r is off by
+// ~1e-6 at depth 15 -- visible as 5e-4 transmittance on a 3 mm primitive with sigma 290).
+struct ExactRay {
+  float rx;
+  float2 ry2, rn2;
+  float sxh, sxl, syh[2], syl[2];
+  float fxc, fyc, ifx, ify;
+};
+
+__device__ __forceinline__ void two_diff(float a, float b, float &s, float &e) {   // s + e = a - b exactly
+  s = fs(a, b);
+  const float bv = fs(s, a);          // = -b up to the rounding of s
+  const float av = fs(s, bv);
+  e = fa(fs(a, av), fs(-b, bv));
+}
+
+__device__ __forceinline__ ExactRay make_ray(const lp_camera &cam, float px, float py0, float py1) {
+  ExactRay R;
+  R.rx = __fdiv_rn(fs(px, cam.cx), cam.fx);
+  R.ry2 = make_float2(__fdiv_rn(fs(py0, cam.cy), cam.fy), __fdiv_rn(fs(py1, cam.cy), cam.fy));
+  R.rn2 = make_float2(sqrtf(fmaf(R.rx, R.rx, fmaf(R.ry2.x, R.ry2.x, 1.f))),
+                      sqrtf(fmaf(R.rx, R.rx, fmaf(R.ry2.y, R.ry2.y, 1.f))));
+  two_diff(px, cam.cx, R.sxh, R.sxl);
+  two_diff(py0, cam.cy, R.syh[0], R.syl[0]);
+  two_diff(py1, cam.cy, R.syh[1], R.syl[1]);
+  R.fxc = cam.fx;
+  R.fyc = cam.fy;
+  R.ifx = __frcp_rn(cam.fx);
+  R.ify = __frcp_rn(cam.fy);
+  return R;
+}
+
+// (p_c f - p_z s) / f with the two products split exactly (FMA) and s = sh + sl: the offset
+// p_c - p_z r_c of the centre from the pixel ray at the centre's depth, accurate to a few ulp of
+// itself even though p_c f and p_z s nearly cancel
+__device__ __forceinline__ float ray_offset(float pc, float pz, float f, float sh, float sl, float inv_f) {
+  const float ah = fm(pc, f), al = __fmaf_rn(pc, f, -ah);
+  const float bh = fm(pz, sh);
+  float bl = __fmaf_rn(pz, sh, -bh);
+  bl = __fmaf_rn(pz, sl, bl);
+  return fm(fa(fs(ah, bh), fs(al, bl)), inv_f);
+}
+
 // per-pixel offsets of the centre from the pixel ray at depth p_z: d = p - p_z r (d_z = 0)
 template <int KIND>
-__device__ __forceinline__ void exact_d(const float *rec, float rx, float2 ry2, float &dx, float2 &dy2) {
+__device__ __forceinline__ void exact_d(const float *rec, const ExactRay &R, float &dx, float2 &dy2) {
   using ER = ExactRec<KIND>;
   const float px = rec[ER::P], py = rec[ER::P + 1], pz = rec[ER::P + 2];
-  dx = __fmaf_rn(-pz, rx, px);
-  dy2 = ffma2(bc(-pz), ry2, bc(py));
+  dx = ray_offset(px, pz, R.fxc, R.sxh, R.sxl, R.ifx);
+  dy2 = make_float2(ray_offset(py, pz, R.fyc, R.syh[0], R.syl[0], R.ify),
+                    ray_offset(py, pz, R.fyc, R.syh[1], R.syl[1], R.ify));
 }
 
 template <int KIND>
-__device__ __forceinline__ void planesE2(const float *rec, float rx, float2 ry2, PlanesE2 &P) {
+__device__ __forceinline__ void planesE2(const float *rec, const ExactRay &R, PlanesE2 &P) {
+  const float rx = R.rx;
+  const float2 ry2 = R.ry2;
   float dx;
   float2 dy2;
-  exact_d<KIND>(rec, rx, ry2, dx, dy2);
+  exact_d<KIND>(rec, R, dx, dy2);
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
     const float *n = plane_n<KIND>(rec, f);

@@ -152,13 +152,10 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
     dep[k] = 0.f;
     dset[k] = false;
   }
-  // exact mode: the pixel rays (r_x shared by the pair, r_z = 1) and their lengths
-  const float rx = EXACT ? __fdiv_rn(fs(fx, cam.cx), cam.fx) : 0.f;
-  const float2 ry2 = EXACT ? make_float2(__fdiv_rn(fs(fy[0], cam.cy), cam.fy), __fdiv_rn(fs(fy[1], cam.cy), cam.fy))
-                           : make_float2(0.f, 0.f);
-  const float2 rn2 = EXACT ? make_float2(sqrtf(fmaf(rx, rx, fmaf(ry2.x, ry2.x, 1.f))),
-                                         sqrtf(fmaf(rx, rx, fmaf(ry2.y, ry2.y, 1.f))))
-                           : make_float2(1.f, 1.f);
+  // exact mode: the pixel rays (r_x shared by the pair, r_z = 1), their lengths and exact offsets
+  ExactRay RY;
+  if (EXACT) RY = make_ray(cam, fx, fy[0], fy[1]);
+  const float2 rn2 = EXACT ? RY.rn2 : make_float2(1.f, 1.f);
   float wx0, wx1, wy0, wy1;
   warp_rect<NT>(threadIdx.x >> 5, tx, ty, wx0, wx1, wy0, wy1);
 
@@ -191,7 +188,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
       float2 ch2, en2;
       if constexpr (EXACT) {
         PlanesE2 P;
-        planesE2<KIND>(rec, rx, ry2, P);
+        planesE2<KIND>(rec, RY, P);
         float2 ex2;
         const float pz = rec[ER::P + 2];
         const float2 cht = chordE2_of(P, pz, en2, ex2);
@@ -332,12 +329,11 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
   float wx0, wx1, wy0, wy1;
   warp_rect<NT>(threadIdx.x >> 5, tx, ty, wx0, wx1, wy0, wy1);
   // exact mode: the pixel rays (bitwise the forward's)
-  const float rx = EXACT ? __fdiv_rn(fs(fx[0], cam.cx), cam.fx) : 0.f;
-  const float2 ry2 = EXACT ? make_float2(__fdiv_rn(fs(fy[0], cam.cy), cam.fy), __fdiv_rn(fs(fy[1], cam.cy), cam.fy))
-                           : make_float2(0.f, 0.f);
-  const float2 rn2 = EXACT ? make_float2(sqrtf(fmaf(rx, rx, fmaf(ry2.x, ry2.x, 1.f))),
-                                         sqrtf(fmaf(rx, rx, fmaf(ry2.y, ry2.y, 1.f))))
-                           : make_float2(1.f, 1.f);
+  ExactRay RY;
+  if (EXACT) RY = make_ray(cam, fx[0], fy[0], fy[1]);
+  const float rx = EXACT ? RY.rx : 0.f;
+  const float2 ry2 = EXACT ? RY.ry2 : make_float2(0.f, 0.f);
+  const float2 rn2 = EXACT ? RY.rn2 : make_float2(1.f, 1.f);
 
   for (uint32_t bend = lmax; bend > start; bend = (bend - start > NT) ? bend - NT : start) {
     const uint32_t bstart = (bend - start > NT) ? bend - NT : start;
@@ -387,12 +383,12 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
       if (any && EXACT) {
         // exact mode: paired plane parameters, entry / exit plane resolved for hit pixels only
         PlanesE2 P;
-        planesE2<KIND>(rec, rx, ry2, P);
+        planesE2<KIND>(rec, RY, P);
         float2 en2, ex2;
         const float2 ch2 = fmul2(chordE2_of(P, rec[ER::P + 2], en2, ex2), rn2);
         float dxp;
         float2 dyp2;
-        exact_d<KIND>(rec, rx, ry2, dxp, dyp2);
+        exact_d<KIND>(rec, RY, dxp, dyp2);
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
           const float ch = lane_k(ch2, k);

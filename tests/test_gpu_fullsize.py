@@ -31,8 +31,10 @@ def _sample_tiles(gx, gy, k, seed):
     return np.sort(rng.choice(gx * gy, size=min(k, gx * gy), replace=False))
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
-def test_fullsize_sampled_parity(cfg):
+@pytest.mark.parametrize("cfg,exact", [("C2", False), ("C3", False), ("C4", False), ("C5", False), ("C3", True),
+                                       ("C2", True)])
+def test_fullsize_sampled_parity(cfg, exact):
+    """exact: the no-ray-space variant (f3) at the same full size, no 2D filter."""
     import torch
     scene, cams = scenegen.make_scene(cfg, seed=0)
     cam = cams[0]
@@ -53,9 +55,10 @@ def test_fullsize_sampled_parity(cfg):
     pix = np.concatenate(pix).astype(np.int32)
 
     osc = oscene(scene)
-    pre = oracle.preprocess(osc, cam, kappa=0.1, mode=0)
+    kappa = 0.0 if exact else 0.1
+    pre = oracle.preprocess(osc, cam, kappa=kappa, mode=0, exact=exact)
     keys, vals, ranges = oracle.bin_tiles(pre, W, H, tile_mask=mask_t)
-    f0 = oracle.render(osc, cam, pre, vals, ranges, pix=pix)
+    f0 = oracle.render(osc, cam, pre, vals, ranges, pix=pix, exact=exact)
     stop_mask = np.zeros((H, W), bool)
     stop_mask.reshape(-1)[pix] = f0.m_stop.reshape(-1)[pix] < PT.STOP_MARGIN
     G = np.zeros((3, H, W), np.float32)
@@ -65,7 +68,7 @@ def test_fullsize_sampled_parity(cfg):
     sel &= ~stop_mask.reshape(-1)
     G.reshape(3, -1)[:, sel] = Gs.reshape(3, -1)[:, sel]
 
-    ds, r, img = PT.gpu_run(scene, [cam], G=G)
+    ds, r, img = PT.gpu_run(scene, [cam], G=G, kappa=kappa, exact=exact)
     got = PT.frame_arrays(r, 0, n, K)
     # ---- per-primitive outputs, all primitives, bit-exact
     assert np.array_equal(got["tiles_touched"], pre.tiles_touched)
@@ -97,8 +100,8 @@ def test_fullsize_sampled_parity(cfg):
     assert np.abs(im - ref)[:, ok].max() <= PT.IMG_TOL
     assert np.array_equal(got["n_proc"].reshape(-1)[pix][ok], f0.n_proc.reshape(-1)[pix][ok])
     # ---- gradients (dL/dC non-zero only on the sampled pixels)
-    fb = oracle.render(osc, cam, pre, vals, ranges, pix=pix, dL_dimage=G)
-    g = oracle.preprocess_bwd(osc, cam, pre, fb)
+    fb = oracle.render(osc, cam, pre, vals, ranges, pix=pix, dL_dimage=G, exact=exact)
+    g = oracle.preprocess_bwd(osc, cam, pre, fb, exact=exact)
     flagged = fb.face_margin < PT.FACE_MARGIN
     gd = ds.grad_dict()
     for name, refg, fl in (("pos", g.pos, flagged), ("rot", g.rot, flagged), ("dist", g.dist, flagged),
