@@ -87,3 +87,25 @@ def test_exact_differs_from_ray_space():
     b = render.Renderer(ds, [cam], aa_kernel=0.0, exact=True).forward().cpu().numpy()
     torch.cuda.synchronize()
     assert np.abs(a - b).max() > 1e-3
+
+
+@pytest.mark.parametrize("kind", [OCTA, TETRA])
+@pytest.mark.parametrize("seed", range(3))
+def test_exact_edge_scenes(kind, seed):
+    """The ray-space edge cases (tile-border stragglers, off-screen, behind the camera, inside znear,
+    sub-pixel, huge, alpha ~ 0, duplicate depths, invalid inputs, axis-aligned faces; image size not a
+    multiple of 16) through the no-ray-space variant."""
+    scene, cam = scenegen.edge_scene(kind, seed=seed)
+    full_parity(scene, cam, kappa=0.0, seed=seed, exact=True, max_flagged=0.1)
+
+
+def test_exact_empty_and_single():
+    import torch
+    scene, cam = scenegen.small_scene(OCTA, 50, seed=1, width=40, height=30)
+    scene["pos"][2] = -5.0
+    ds, r, img = PT.gpu_run(scene, [cam], G=np.ones((3, 30, 40), np.float32), bg=(0.25, 0.5, 0.75), kappa=0.0,
+                            exact=True)
+    assert torch.allclose(img[0, 0], torch.full_like(img[0, 0], 0.25))
+    assert float(ds.grad.abs().max()) == 0.0
+    scene, cam = scenegen.small_scene(TETRA, 1, seed=2, width=1, height=1)
+    full_parity(scene, cam, kappa=0.0, seed=1, exact=True)
