@@ -11,7 +11,8 @@ f32 = np.float32
 K_TETRA = f32(0.57735026918962576451)
 
 
-def canonical(scene, cam, kappa=0.1, filter3d=None):
+def canonical(scene, cam, kappa=0.1, filter3d=None, exact=False):
+    """exact: the no-ray-space variant's canonical geometry (DESIGN.md §3 "exact mode")."""
     kind = scene["kind"]
     K = 3 if kind == 0 else 4
     n = scene["pos"].shape[1]
@@ -66,12 +67,31 @@ def canonical(scene, cam, kappa=0.1, filter3d=None):
         off = np.zeros((K, 3, n), f32)
         for j in range(K):
             oc = [(Wm[r, 0] * ow[j][0] + Wm[r, 1] * ow[j][1]) + Wm[r, 2] * ow[j][2] for r in range(3)]
-            off[j, 0] = J00 * oc[0] + J02 * oc[2]
-            off[j, 1] = J11 * oc[1] + J12 * oc[2]
-            off[j, 2] = (J20 * oc[0] + J21 * oc[1]) + J22 * oc[2]
+            if exact:
+                off[j, 0], off[j, 1], off[j, 2] = oc
+            else:
+                off[j, 0] = J00 * oc[0] + J02 * oc[2]
+                off[j, 1] = J11 * oc[1] + J12 * oc[2]
+                off[j, 2] = (J20 * oc[0] + J21 * oc[1]) + J22 * oc[2]
+        if exact:
+            verts = []
+            for j in range(K):
+                verts.append([p[r] + off[j, r] for r in range(3)])
+                if kind == 0:
+                    verts.append([p[r] - off[j, r] for r in range(3)])
+            behind = np.zeros(n, bool)
+            us, ws = [], []
+            for v in verts:
+                behind |= ~(v[2] > 0)
+                us.append(fx * (v[0] / v[2]) + cx)
+                ws.append(fy * (v[1] / v[2]) + cy)
+            us, ws = np.stack(us), np.stack(ws)
+            lo = [np.where(behind, f32(-2), us.min(0)), np.where(behind, f32(-2), ws.min(0))]
+            hi = [np.where(behind, f32(Wd + 2), us.max(0)), np.where(behind, f32(Hd + 2), ws.max(0))]
+            crx, cry = p[0], p[1]
         h = f32(0.5) * f32(kappa)
         ar = np.arange(n)
-        for ax in range(2):
+        for ax in range(2 if not exact else 0):
             if kind == 0:
                 a = np.abs(off[:, ax])
                 jm = np.argmax(a, axis=0)           # first max
@@ -82,8 +102,9 @@ def canonical(scene, cam, kappa=0.1, filter3d=None):
                 kmax = np.argmax(off[:, ax], axis=0)
                 off[kmin, ax, ar] = off[kmin, ax, ar] - h
                 off[kmax, ax, ar] = off[kmax, ax, ar] + h
-        lo, hi = [], []
-        for ax, c in ((0, crx), (1, cry)):
+        if not exact:
+            lo, hi = [], []
+        for ax, c in (((0, crx), (1, cry)) if not exact else ()):
             if kind == 0:
                 m = np.abs(off[:, ax]).max(0)
                 lo.append(c - m)

@@ -174,3 +174,20 @@ def test_ray_space_vertex_error_is_second_order():
         errs.append(e)
     slopes = [math.log(errs[i] / errs[i + 1]) / math.log(2) for i in range(3)]
     assert all(abs(sl - 2) < 0.2 for sl in slopes), (errs, slopes)
+
+
+@pytest.mark.parametrize("kind", [OCTA, TETRA])
+def test_exact_canonical_matches_numpy_arbiter(kind):
+    """The exact-mode canonical fp32 geometry: oracle == NumPy float32, bit for bit."""
+    from tests.canonical_np import canonical
+    scene, c = scenegen.small_scene(kind, 3000, seed=8, width=123, height=77, depth=(0.6, 9.0), size=(0.05, 1.2))
+    pre = oracle.preprocess(oscene(scene), c, kappa=0.0, mode=0, exact=True)
+    ref = canonical(scene, c, kappa=0.0, exact=True)
+    assert np.array_equal(pre.flag, ref["flag"])
+    assert np.array_equal(pre.tiles_touched, ref["tiles_touched"])
+    assert np.array_equal(pre.rect, ref["rect"])
+    assert np.array_equal(pre.depth_key, ref["depth_key"])
+    assert np.array_equal(pre.canon.view(np.uint32), ref["canon"].view(np.uint32))
+    # the whole-screen case occurs
+    full = (pre.flag == 0) & (pre.tiles_touched == ((123 + 15) // 16) * ((77 + 15) // 16))
+    assert full.sum() > 0
