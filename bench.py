@@ -538,7 +538,8 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": round(1000 * tot_s / args.steps, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C5: 1M octahedra, SH deg 3, 8 views 1600x1060, training step (views sharded)",
-                       "sample_per_step": f"{band} rows x 1600 px of one view (fwd+bwd), views round-robin"},
+                       "sample_per_step": f"{band} rows x 1600 px of one view (fwd+bwd; a seeded upstream gradient "
+                                          f"stands in for the loss gradient), views round-robin"},
             "cpu_baseline": {"value": round(value, 6), "unit": "Mpixel/s", "cores": os.cpu_count(),
                              "kind": "oracle", "sample": f"{band}-row band per step, {args.steps} steps"},
             "e2e": {"value": round(value, 6), "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
