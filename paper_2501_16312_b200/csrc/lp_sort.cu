@@ -279,13 +279,28 @@ void launch_scan_tiles(const lp_frame &F, int n, cudaStream_t st) {
 // ---------------------------------------------------------------------------------------------
 constexpr int EMIT_TILE = 2048;
 
-__device__ __forceinline__ int last_leq(const uint32_t *__restrict__ a, int n, uint32_t x) {   // max j: a[j] <= x
+// max j: a[j] <= x for a non-decreasing a with a[0] <= x, by one warp: 32 probes per round narrow
+// the interval 32-fold, so ~4 dependent global loads instead of ~20 (the search is the latency
+// chain at the head of every k_emit block)
+__device__ __forceinline__ int warp_last_leq(const uint32_t *__restrict__ a, int n, uint32_t x) {
+  const int lane = threadIdx.x & 31;
   int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a[mid] <= x) lo = mid; else hi = mid - 1;
+  while (hi - lo >= 32) {
+    const int step = (hi - lo + 31) / 32;
+    const int probe = min(lo + (lane + 1) * step, hi);
+    const unsigned m = __ballot_sync(0xffffffffu, a[probe] <= x);
+    if (m == 0u) {
+      hi = lo + step - 1;
+    } else {
+      const int last = 31 - __clz(m);
+      const int nlo = min(lo + (last + 1) * step, hi);
+      if (last < 31) hi = min(hi, nlo + step - 1);
+      lo = nlo;
+    }
   }
-  return lo;
+  const int probe = lo + lane;
+  const unsigned m = __ballot_sync(0xffffffffu, probe <= hi && a[probe] <= x);
+  return lo + 31 - __clz(m);
 }
 
 __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ order, const uint32_t *__restrict__ offsets,
@@ -295,34 +310,66 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ order
   __shared__ uint32_t s_off[EMIT_TILE];
   __shared__ uint32_t s_id[EMIT_TILE];
   __shared__ ushort4 s_rect[EMIT_TILE];
+  __shared__ int s_own[EMIT_TILE];
+  __shared__ int s_wmax[8];
   __shared__ int s_j0, s_cnt;
   const int64_t E = item_count(E_dev, capacity);
   const int64_t e0 = (int64_t)blockIdx.x * EMIT_TILE;
   if (e0 >= E) return;
   const int64_t e1 = e0 + EMIT_TILE < E ? e0 + EMIT_TILE : E;
-  if (threadIdx.x == 0) {
-    const int j0 = last_leq(offsets, n, (uint32_t)e0);
-    const int j1 = last_leq(offsets, n, (uint32_t)(e1 - 1));
-    s_j0 = j0;
-    s_cnt = j1 - j0 + 1;   // every primitive in the range owns >= 1 entry, so s_cnt <= EMIT_TILE
+  if (threadIdx.x < 64) {   // warp 0 finds the first primitive of the range, warp 1 the last
+    const int j = warp_last_leq(offsets, n, (uint32_t)(threadIdx.x < 32 ? e0 : e1 - 1));
+    if (threadIdx.x == 0) s_j0 = j;
+    if (threadIdx.x == 32) s_cnt = j;
   }
   __syncthreads();
+  if (threadIdx.x == 0) s_cnt = s_cnt - s_j0 + 1;   // every primitive in the range owns >= 1 entry: <= EMIT_TILE
+  __syncthreads();
   const int j0 = s_j0, cnt = s_cnt;
+  const int len = (int)(e1 - e0);
+  // owner of every output slot: heads (each primitive's first entry) then a block-wide prefix max
+  // (the primitives' offsets increase with their index, so the owner of slot e is the last head <= e)
+  for (int k = threadIdx.x; k < EMIT_TILE; k += blockDim.x) s_own[k] = 0;
+  __syncthreads();
   for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
     const uint32_t i = order[j0 + q];
-    s_off[q] = offsets[j0 + q];
+    const uint32_t off = offsets[j0 + q];
+    s_off[q] = off;
     s_id[q] = i;
     s_rect[q] = rect[i];
+    const int64_t pos = (int64_t)off - e0;
+    if (pos > 0 && pos < len) atomicMax(&s_own[pos], q);   // slot 0 belongs to q = 0 (its head may precede e0)
+  }
+  __syncthreads();
+  {
+    constexpr int PER = EMIT_TILE / 256;   // 8 consecutive slots per thread
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    int v[PER], run = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      run = max(run, s_own[t * PER + k]);
+      v[k] = run;
+    }
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = max(incl, y);
+    }
+    if (lane == 31) s_wmax[w] = incl;
+    int excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = 0;
+    __syncthreads();
+    int wpre = 0;
+    for (int k = 0; k < w; ++k) wpre = max(wpre, s_wmax[k]);
+    const int pre = max(excl, wpre);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) s_own[t * PER + k] = max(v[k], pre);
   }
   __syncthreads();
   for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    int lo = 0, hi = cnt - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_off[mid] <= (uint32_t)e) lo = mid; else hi = mid - 1;
-    }
-    const uint32_t k = (uint32_t)e - s_off[lo];
-    const ushort4 r = s_rect[lo];
+    const int lo = s_own[e - e0];
+    const uint32_t k = (uint32_t)e - s_off[lo];    const ushort4 r = s_rect[lo];
     const uint32_t rw = (uint32_t)r.z - r.x + 1;
     const uint32_t ty = r.y + k / rw, tx = r.x + k % rw;
     tile_key[e] = ty * (uint32_t)tiles_x + tx;
