@@ -17,7 +17,10 @@ void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa
 
 // K2 (lp_sort.cu)
 constexpr int SORT_THREADS = 256;
-constexpr int SORT_ITEMS = 8;
+#ifndef LP_SORT_ITEMS
+#define LP_SORT_ITEMS 8      // keys per thread of a radix block (measurement knob -DLP_SORT_ITEMS)
+#endif
+constexpr int SORT_ITEMS = LP_SORT_ITEMS;
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;   // keys per radix block
 constexpr int SCAN_TILE = 2048;                        // elements per scan block
 size_t radix_hist_words(int64_t max_items);
