@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 2
+#define LP_ABI_VERSION 3
 #define LP_TILE 16            /* 16 x 16 pixel tiles */
 
 typedef enum {
@@ -108,6 +108,9 @@ typedef struct {
   uint32_t *tile_cursor;      /* [tiles] bucket fill cursors (bucket sort) */
   int32_t   sort_method;      /* LP_SORT_RADIX (default set by lp_frame_init) or LP_SORT_BUCKET; caller may change
                                  before lp_preprocess (K1 fills the bucket method's rect grid only when selected) */
+  uint32_t *hitmask;          /* [4][capacity/32 + 2] per warp of a tile, one bit per tile-list entry: the forward
+                                 sets it when the entry intersected one of the warp's pixels; the backward
+                                 replays only those entries */
 } lp_frame;
 
 /* lp_bin_sort methods; both produce the identical (tile, depth, id) order. */

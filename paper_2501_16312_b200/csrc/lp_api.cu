@@ -23,7 +23,7 @@ inline int offsets_k(int kind) { return kind == LP_OCTAHEDRON ? 3 : 4; }
 struct Layout {
   size_t tiles_touched, rect, depth_key, record, prim_key, prim_key_alt, prim_order, prim_order_alt, offsets, tile_key,
       tile_key_alt, entry_val, entry_val_alt, ranges, sort_hist, scan_tmp, counters, T_final, n_proc, rgrad, canon,
-      tile_diff, tile_cursor, total;
+      tile_diff, tile_cursor, hitmask, total;
 };
 
 Layout layout(int kind, int64_t n, int w, int h, int64_t cap, int canon) {
@@ -57,6 +57,7 @@ Layout layout(int kind, int64_t n, int w, int h, int64_t cap, int canon) {
   const int64_t gx = (w + LP_TILE - 1) / LP_TILE, gy = (h + LP_TILE - 1) / LP_TILE;
   L.tile_diff = take(4 * (gx + 1) * (gy + 1));
   L.tile_cursor = take(4 * tiles);
+  L.hitmask = take(4 * 4 * hit_words(cc));
   L.total = o;
   return L;
 }
@@ -152,6 +153,7 @@ lp_status lp_frame_init(lp_frame *F, void *workspace, size_t bytes, int32_t kind
   F->tile_diff = reinterpret_cast<int32_t *>(b + L.tile_diff);
   F->tile_cursor = reinterpret_cast<uint32_t *>(b + L.tile_cursor);
   F->sort_method = LP_SORT_RADIX;   // measured faster on C5
+  F->hitmask = reinterpret_cast<uint32_t *>(b + L.hitmask);
   return LP_OK;
 }
 

@@ -7,6 +7,10 @@
 
 namespace lp {
 
+// words per warp row of lp_frame.hitmask (one bit per tile-list entry, +2 so a 128-entry batch at
+// any bit offset stays inside the row)
+__host__ __device__ inline int64_t hit_words(int64_t capacity) { return (capacity + 31) / 32 + 2; }
+
 // K1 / K5 (lp_preprocess.cu)
 // exact: the no-ray-space variant (App. D, reading 27)
 void launch_preprocess(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,

@@ -100,6 +100,16 @@ extern "C" int lp_debug_bwd_stats(unsigned long long *out, int reset) {
 #define BWD_STAT(i, v) do { } while (0)
 #endif
 
+// the forward's hit bits of 32 consecutive entries [bit0, bit0 + 32) into warp row w of the hit mask
+// (once per batch; kept out of line so its 64-bit address math does not occupy registers across the
+// record loop)
+__device__ __noinline__ void write_hit_word(uint32_t *hitmask, int64_t capacity, int w, uint32_t bit0, uint32_t m) {
+  uint32_t *row = hitmask + (size_t)w * hit_words(capacity);
+  const uint32_t wd = bit0 >> 5, sh = bit0 & 31u;
+  atomicOr(row + wd, m << sh);
+  if (sh) atomicOr(row + wd + 1, m >> (32u - sh));
+}
+
 // =============================================================================================
 // K3 forward
 // =============================================================================================
@@ -124,6 +134,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
   __shared__ float4 s_rec[NT * RW4];
   __shared__ unsigned char s_list[NT / 32][NT];
   __shared__ unsigned long long s_stat[3];
+  __shared__ uint32_t s_hitw[NT / 32][NT / 32];
 
   const int tile = blockIdx.x;
   const int tx = tile % F.tiles_x, ty = tile / F.tiles_x;
@@ -171,11 +182,14 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
     __syncthreads();
     if (__all_sync(0xffffffffu, done[0] && done[1])) continue;
     const int cnt = (int)min((uint32_t)NT, end - b);
+    const int wrp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane < NT / 32) s_hitw[wrp][lane] = 0u;         // the warp's hit bits of the batch records
+    __syncwarp();
     // per-warp sub-list: the batch records whose bbox reaches the warp's pixels, in list order
     // (each lane tests NT/32 records; convexity: outside the vertex bbox the chord is <= 0)
-    const int nl = warp_sublist<NT, RW4>(s_rec, cnt, wx0, wx1, wy0, wy1, s_list[threadIdx.x >> 5]);
+    const int nl = warp_sublist<NT, RW4>(s_rec, cnt, wx0, wx1, wy0, wy1, s_list[wrp]);
     for (int q = 0; q < nl; ++q) {
-      const int j = s_list[threadIdx.x >> 5][q];
+      const int j = s_list[wrp][q];
       const float4 bb = s_rec[j * RW4];
       const bool inx = fabsf(fx - bb.x) <= bb.z;
       bool test[PPT];
@@ -201,6 +215,9 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
       }
       const float ch[PPT] = {ch2.x, ch2.y};
       const float enk[PPT] = {en2.x, en2.y};
+      // the forward's hits of this record -> the warp's hit bits (every hitting lane ORs the same bit
+      // into the same shared word: identical read-modify-writes, no lost bits)
+      if ((test[0] && ch[0] > 0.f) || (test[1] && ch[1] > 0.f)) s_hitw[wrp][j >> 5] |= 1u << (j & 31);
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         if (!test[k]) continue;
@@ -229,6 +246,12 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
           }
         }
       }
+    }
+    // this batch's hit bits of the warp -> the global per-warp bit row (entry index = bit index)
+    __syncwarp();
+    if (lane < NT / 32) {
+      const uint32_t m = s_hitw[wrp][lane];
+      if (m) write_hit_word(F.hitmask, F.capacity, wrp, b + 32u * (uint32_t)lane, m);
     }
   }
 
@@ -352,18 +375,40 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
     for (int k = 0; k < PPT; ++k) act = act || (last[k] > bstart);
     if (!__any_sync(0xffffffffu, act)) continue;
     const int w = threadIdx.x >> 5;
-    const int nl = warp_sublist<NT, RW4>(s_rec, (int)(bend - bstart), wx0, wx1, wy0, wy1, s_list[w]);
-    BWD_STAT(0, nl);
+    // the entries of this batch that hit one of the warp's pixels in the forward (its hit bits):
+    // no rect / bbox tests and no chord evaluation of entries that miss every pixel of the warp
+    uint32_t hb[NT / 32];
+    {
+      const uint32_t *row = F.hitmask + (size_t)w * hit_words(F.capacity);
+      uint32_t mine = 0u;
+      if (lane < NT / 32) {
+        const uint32_t bit0 = bstart + 32u * lane, wd = bit0 >> 5, sh = bit0 & 31u;
+        mine = row[wd] >> sh;
+        if (sh) mine |= row[wd + 1] << (32u - sh);
+        const int rem = (int)(bend - bstart) - 32 * lane;   // records of this word inside the batch
+        if (rem < 32) mine = rem <= 0 ? 0u : (mine & ((1u << rem) - 1u));
+      }
+#pragma unroll
+      for (int i = 0; i < NT / 32; ++i) hb[i] = __shfl_sync(0xffffffffu, mine, i);
+    }
+    BWD_STAT(0, __popc(hb[0]) + __popc(hb[1]) + __popc(hb[2]) + __popc(hb[3]));
 
-    for (int q = nl - 1; q >= 0; --q) {
-      const int j = s_list[w][q];
+#pragma unroll 1
+    for (int wi = NT / 32 - 1; wi >= 0; --wi) {
+    uint32_t bits = hb[0];
+#pragma unroll
+    for (int i = 1; i < NT / 32; ++i)
+      if (wi == i) bits = hb[i];
+    while (bits) {
+      const int bt = 31 - __clz(bits);
+      bits &= ~(1u << bt);
+      const int j = 32 * wi + bt;
       const uint32_t ej = bstart + (uint32_t)j;
-      // bbox reject per pixel: pixels outside the bbox have chord <= 0 (the forward's hit set)
-      const float4 bb = s_rec[j * RW4];
+      // a pixel outside the primitive has chord <= 0; the forward stopped pixel k after last[k]
       bool test[PPT], any = false;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        test[k] = ej < last[k] && in_bbox(bb, fx[k], fy[k]);
+        test[k] = ej < last[k];
         any = any || test[k];
       }
       if (!__any_sync(0xffffffffu, any)) continue;
@@ -517,6 +562,7 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
       }
       __syncwarp();
     }
+    }
   }
 }
 
@@ -545,6 +591,7 @@ static void fwd_x(const lp_frame &F, const lp_camera &cam, const lp_raster_cfg &
 
 void launch_raster_fwd(const lp_frame &F, const lp_camera &cam, const lp_raster_cfg &cfg, float *image, float *depth,
                        float *alpha, cudaStream_t st) {
+  cudaMemsetAsync(F.hitmask, 0, sizeof(uint32_t) * 4 * (size_t)hit_words(F.capacity), st);   // the backward's hit bits
   if (cfg.exact) fwd_x<true>(F, cam, cfg, image, depth, alpha, st);
   else fwd_x<false>(F, cam, cfg, image, depth, alpha, st);
 }
