@@ -123,11 +123,7 @@ __device__ __noinline__ void write_hit_word(uint32_t *hitmask, int64_t capacity,
 // EXACT: the no-ray-space variant (App. D, reading 27): per-pixel perspective rays
 // r = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1) against the record's camera-space planes.
 template <int KIND, bool STATS, bool AUX, bool EXACT>
-#ifdef LP_FWD_MINB   // measurement knob: resident forward CTAs per SM asked of the register allocator
-__global__ void __launch_bounds__(128, LP_FWD_MINB) k_raster_fwd(
-#else
-__global__ void __launch_bounds__(128) k_raster_fwd(
-#endiflp_frame F, lp_camera cam, lp_raster_cfg cfg,
+__global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, lp_raster_cfg cfg,
                                                     float *__restrict__ image, float *__restrict__ depth,
                                                     float *__restrict__ alpha) {
   constexpr int NT = 128, PPT = 2;
