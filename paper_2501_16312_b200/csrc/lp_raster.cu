@@ -9,8 +9,9 @@
 //
 // Backward: the same lists in reverse.  Per (pixel, entry) with chord > 0 it recovers T_k = T/E,
 // runs the blend backward and the chord backward (App. E, in slab/plane
-// moment form), accumulates <= 22 moments per thread, then a shared-memory column sum over the
-// hit lanes and one RED.F32 per moment per (warp, primitive) into rgrad[moment][n].
+// moment form) into its lane's compacted shared-memory row (<= 22 moments; one 16-byte
+// read-modify-write per entry / exit plane), then a column sum over the hit lanes and one
+// RED.F32 per moment per (warp, primitive) into rgrad[moment][n].
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -134,7 +135,6 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
   __shared__ float4 s_rec[NT * RW4];
   __shared__ unsigned char s_list[NT / 32][NT];
   __shared__ unsigned long long s_stat[3];
-  __shared__ uint32_t s_hitw[NT / 32][NT / 32];
 
   const int tile = blockIdx.x;
   const int tx = tile % F.tiles_x, ty = tile / F.tiles_x;
@@ -183,8 +183,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
     if (__all_sync(0xffffffffu, done[0] && done[1])) continue;
     const int cnt = (int)min((uint32_t)NT, end - b);
     const int wrp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane < NT / 32) s_hitw[wrp][lane] = 0u;         // the warp's hit bits of the batch records
-    __syncwarp();
+    uint32_t hitw = 0u;                                 // lane L < NT/32: the warp's hit bits of records 32L..
     // per-warp sub-list: the batch records whose bbox reaches the warp's pixels, in list order
     // (each lane tests NT/32 records; convexity: outside the vertex bbox the chord is <= 0)
     const int nl = warp_sublist<NT, RW4>(s_rec, cnt, wx0, wx1, wy0, wy1, s_list[wrp]);
@@ -197,7 +196,6 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
       for (int k = 0; k < PPT; ++k) test[k] = !done[k] && inx && fabsf(fy[k] - bb.y) <= bb.w;
       const bool any = test[0] || test[1];
       if (!__any_sync(0xffffffffu, any)) continue;
-      if (!any) continue;
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
       float2 ch2, en2;
       if constexpr (EXACT) {
@@ -215,9 +213,9 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
       }
       const float ch[PPT] = {ch2.x, ch2.y};
       const float enk[PPT] = {en2.x, en2.y};
-      // the forward's hits of this record -> the warp's hit bits (every hitting lane ORs the same bit
-      // into the same shared word: identical read-modify-writes, no lost bits)
-      if ((test[0] && ch[0] > 0.f) || (test[1] && ch[1] > 0.f)) s_hitw[wrp][j >> 5] |= 1u << (j & 31);
+      // the forward's hits of this record -> the warp's hit bits (held by lane j / 32)
+      const bool hit = (test[0] && ch[0] > 0.f) || (test[1] && ch[1] > 0.f);
+      if (__any_sync(0xffffffffu, hit) && lane == (j >> 5)) hitw |= 1u << (j & 31);
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         if (!test[k]) continue;
@@ -248,11 +246,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
       }
     }
     // this batch's hit bits of the warp -> the global per-warp bit row (entry index = bit index)
-    __syncwarp();
-    if (lane < NT / 32) {
-      const uint32_t m = s_hitw[wrp][lane];
-      if (m) write_hit_word(F.hitmask, F.capacity, wrp, b + 32u * (uint32_t)lane, m);
-    }
+    if (hitw) write_hit_word(F.hitmask, F.capacity, wrp, b + 32u * (uint32_t)lane, hitw);
   }
 
   const size_t HW = (size_t)W * H;
@@ -311,7 +305,6 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
   constexpr int SIGMA = EXACT ? ER::SIGMA : KD::SIGMA, RGB = EXACT ? ER::RGB : KD::RGB;
   constexpr int RGP = RG == 20 ? 20 : 28;      // padded row: 16-byte stores, conflict-free (RGP/4 odd)
   __shared__ float4 s_rec[NT * RW4];
-  __shared__ unsigned char s_list[NT / 32][NT];
   __shared__ __align__(16) float s_red[NT / 32][32][RGP];
   __shared__ uint32_t s_id[NT];
   __shared__ uint32_t s_last;
@@ -421,128 +414,128 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
       }
 #endif
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
-      float acc[RGP];
-#pragma unroll
-      for (int a = 0; a < RGP; ++a) acc[a] = 0.f;
-      bool hit = false;
-      if (any && EXACT) {
-        // exact mode: paired plane parameters, entry / exit plane resolved for hit pixels only
-        PlanesE2 P;
-        planesE2<KIND>(rec, RY, P);
-        float2 en2, ex2;
-        const float2 ch2 = fmul2(chordE2_of(P, rec[ER::P + 2], en2, ex2), rn2);
-        float dxp;
-        float2 dyp2;
+      // the warp's pixels this entry hits (chord > 0 before the forward's stop): their lanes get a
+      // compacted shared-memory row [dsigma, drgb | per-plane moments] that the pixels update in
+      // place (one 16-byte read-modify-write per entry / exit plane, no per-plane selects)
+      float2 ch2, en2, ex2;
+      float dx = 0.f, dxp = 0.f;
+      float2 dy2 = make_float2(0.f, 0.f), dyp2 = make_float2(0.f, 0.f);
+      PlanesE2 PE;
+      Planes2<KIND> PR;
+      if (EXACT) {
+        planesE2<KIND>(rec, RY, PE);
+        ch2 = fmul2(chordE2_of(PE, rec[ER::P + 2], en2, ex2), rn2);
         exact_d<KIND>(rec, RY, dxp, dyp2);
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          const float ch = lane_k(ch2, k);
-          if (!test[k] || !(ch > 0.f)) continue;
-          hit = true;
-          int se, sx;
-          const float te = lane_k(en2, k), tx_ = lane_k(ex2, k);
-          trackE_k(P, k, te, tx_, se, sx);
-          const float sig = rec[SIGMA];
-          const float E = transmit(sig, ch);
-          const float o = 1.f - E;
-          const float Tk = T[k] * rcp_ftz(E);
-          float dLdo = 0.f;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            acc[RG - 3 + c] = fmaf(Tk * o, G[k][c], acc[RG - 3 + c]);
-            dLdo = fmaf(rec[RGB + c] - S[k][c], G[k][c], dLdo);
-            S[k][c] = fmaf(o, rec[RGB + c], E * S[k][c]);
-          }
-          dLdo *= Tk;
-          T[k] = Tk;
-          const float gE = E * dLdo;
-          acc[RG - 4] = fmaf(ch, gE, acc[RG - 4]);      // dL/dsigma = (Euclidean chord) E dL/do
-          const float ry = lane_k(ry2, k);
-          const float w = sig * gE * lane_k(rn2, k);    // dL/dt_exit = w, dL/dt_entry = -w
-          const float ike = plane_ik<KIND>(rec, se, rx, ry), ikx = plane_ik<KIND>(rec, sx, rx, ry);
-          // centred moments: dL/dm = dL/dt / k and dL/dn = -dL/dt (q - p) / k with
-          // q - p = tau r - d (tau = t - p_z, d = p - p_z r)
-          const float dyp = lane_k(dyp2, k);
-          const float ax = w * ikx, ae = -w * ike;
-          const float qx[3] = {fmaf(tx_, rx, -dxp), fmaf(tx_, ry, -dyp), tx_};
-          const float qe[3] = {fmaf(te, rx, -dxp), fmaf(te, ry, -dyp), te};
-#pragma unroll
-          for (int f = 0; f < 4; ++f) {
-            const float A = ((f == sx) ? ax : 0.f) + ((f == se) ? ae : 0.f);
-            acc[4 * f + 0] += A;
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-              acc[4 * f + 1 + c] -= ((f == sx) ? ax * qx[c] : 0.f) + ((f == se) ? ae * qe[c] : 0.f);
-          }
-        }
-      } else if (any) {
-      // both pixels' entry / exit values as one paired evaluation (bitwise the forward's chord2);
-      // the entry / exit slab is resolved only for pixels the primitive actually hits
-      const float dx = fs(fx[0], rec[KD::CX]);
-      const float2 dy2 = fsub2(make_float2(fy[0], fy[1]), bc(rec[KD::CX + 1]));
-      Planes2<KIND> P;
-      planes2<KIND>(rec, dx, dy2, P);
-      float2 en2, ex2;
-      const float2 ch2 = chord2_of<KIND>(P, en2, ex2);
+      } else {
+        dx = fs(fx[0], rec[KD::CX]);
+        dy2 = fsub2(make_float2(fy[0], fy[1]), bc(rec[KD::CX + 1]));
+        planes2<KIND>(rec, dx, dy2, PR);
+        ch2 = chord2_of<KIND>(PR, en2, ex2);
+      }
+      bool hk[PPT], hit = false;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        const float ch = lane_k(ch2, k);
-        if (!test[k] || !(ch > 0.f)) continue;
-        hit = true;
-        int se, sx;
-        track_k<KIND>(P, k, lane_k(en2, k), lane_k(ex2, k), se, sx);
-        const float dy = lane_k(dy2, k);
-        const float sig = rec[SIGMA];
-        const float E = transmit(sig, ch);
-        const float o = 1.f - E;
-        const float Tk = T[k] * rcp_ftz(E);               // transmittance in front of this entry
-        float dLdo = 0.f;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          acc[RG - 3 + c] = fmaf(Tk * o, G[k][c], acc[RG - 3 + c]);   // dL/drgb
-          dLdo = fmaf(rec[RGB + c] - S[k][c], G[k][c], dLdo);
-          S[k][c] = fmaf(o, rec[RGB + c], E * S[k][c]);               // colour behind the previous entry
-        }
-        dLdo *= Tk;
-        T[k] = Tk;
-        const float gE = E * dLdo;
-        acc[RG - 4] = fmaf(ch, gE, acc[RG - 4]);          // dL/dsigma = chord E dL/do
-        const float g = sig * gE;                          // dL/d exit = g, dL/d entry = -g
-        if (KIND == OCTA) {
-#pragma unroll
-          for (int s = 0; s < 4; ++s) {
-            const float gx = (s == sx) ? g : 0.f, gn = (s == se) ? g : 0.f;
-            const float ws = gx - gn, us = gx + gn;
-            acc[4 * s + 0] = fmaf(ws, dx, acc[4 * s + 0]);
-            acc[4 * s + 1] = fmaf(ws, dy, acc[4 * s + 1]);
-            acc[4 * s + 2] += ws;
-            acc[4 * s + 3] += us;
-          }
-        } else {
-#pragma unroll
-          for (int s = 0; s < 6; ++s) {
-            const float ws = (s == sx) ? g : ((s == se) ? -g : 0.f);
-            acc[3 * s + 0] += ws;
-            acc[3 * s + 1] = fmaf(ws, dx, acc[3 * s + 1]);
-            acc[3 * s + 2] = fmaf(ws, dy, acc[3 * s + 2]);
-          }
-        }
+        hk[k] = test[k] && lane_k(ch2, k) > 0.f;
+        hit = hit || hk[k];
       }
-      }
-      // per-(warp, primitive) reduction of the <= 22 moments, one RED.F32 per moment: the hit
-      // lanes stage their moments in compacted shared-memory rows, lane m < RG sums column m
-      // over the h rows (2 instructions per row, 4 independent partial sums)
       const unsigned hm = __ballot_sync(0xffffffffu, hit);
       if (!hm) continue;
       BWD_STAT(2, 1);
       BWD_STAT(3, __popc(hm));
+      float *row = &s_red[w][__popc(hm & ((1u << lane) - 1u))][0];
+      if (hit) {
+#pragma unroll
+        for (int a = 1; a < RGP / 4; ++a) reinterpret_cast<float4 *>(row)[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 tail = make_float4(0.f, 0.f, 0.f, 0.f);   // dsigma, dr, dg, db
+        const float sig = rec[SIGMA];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          if (!hk[k]) continue;
+          const float ch = lane_k(ch2, k), te = lane_k(en2, k), tx_ = lane_k(ex2, k);
+          int se, sx;
+          if (EXACT) trackE_k(PE, k, te, tx_, se, sx);
+          else track_k<KIND>(PR, k, te, tx_, se, sx);
+          const float E = transmit(sig, ch);
+          const float o = 1.f - E;
+          const float Tk = T[k] * rcp_ftz(E);               // transmittance in front of this entry
+          float dLdo = 0.f;
+          tail.y = fmaf(Tk * o, G[k][0], tail.y);           // dL/drgb
+          tail.z = fmaf(Tk * o, G[k][1], tail.z);
+          tail.w = fmaf(Tk * o, G[k][2], tail.w);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            dLdo = fmaf(rec[RGB + c] - S[k][c], G[k][c], dLdo);
+            S[k][c] = fmaf(o, rec[RGB + c], E * S[k][c]);   // colour behind the previous entry
+          }
+          dLdo *= Tk;
+          T[k] = Tk;
+          const float gE = E * dLdo;
+          tail.x = fmaf(ch, gE, tail.x);                    // dL/dsigma = chord E dL/do
+          float4 *slot = reinterpret_cast<float4 *>(row + 4);
+          if (EXACT) {
+            // centred moments: dL/dm = dL/dt / k and dL/dn = -dL/dt (q - p) / k with
+            // q - p = tau r - d (tau = t - p_z, d = p - p_z r)
+            const float ry = lane_k(ry2, k), dyp = lane_k(dyp2, k);
+            const float wt = sig * gE * lane_k(rn2, k);    // dL/dt_exit = wt, dL/dt_entry = -wt
+            const float ax = wt * plane_ik<KIND>(rec, sx, rx, ry), ae = -wt * plane_ik<KIND>(rec, se, rx, ry);
+            const float qx0 = fmaf(tx_, rx, -dxp), qx1 = fmaf(tx_, ry, -dyp);
+            const float qe0 = fmaf(te, rx, -dxp), qe1 = fmaf(te, ry, -dyp);
+            if (se == sx) {
+              float4 m = slot[sx];
+              m.x += ax + ae;
+              m.y -= ax * qx0 + ae * qe0;
+              m.z -= ax * qx1 + ae * qe1;
+              m.w -= ax * tx_ + ae * te;
+              slot[sx] = m;
+            } else {                                       // distinct slots: both loads first
+              float4 m = slot[sx], n = slot[se];
+              m.x += ax;
+              m.y -= ax * qx0;
+              m.z -= ax * qx1;
+              m.w -= ax * tx_;
+              n.x += ae;
+              n.y -= ae * qe0;
+              n.z -= ae * qe1;
+              n.w -= ae * te;
+              slot[sx] = m;
+              slot[se] = n;
+            }
+          } else if (KIND == OCTA) {
+            // slab s: (dL/da, dL/db, dL/dc, dL/dhalf) += (w dx, w dy, w, u) with w = gx - gn, u = gx + gn
+            const float g = sig * gE, dy = lane_k(dy2, k);   // dL/d exit = g, dL/d entry = -g
+            if (se == sx) {
+              slot[sx].w += g + g;
+            } else {                                       // distinct slots: both loads first
+              float4 m = slot[sx], n = slot[se];
+              m.x = fmaf(g, dx, m.x);
+              m.y = fmaf(g, dy, m.y);
+              m.z += g;
+              m.w += g;
+              n.x = fmaf(-g, dx, n.x);
+              n.y = fmaf(-g, dy, n.y);
+              n.z -= g;
+              n.w += g;
+              slot[sx] = m;
+              slot[se] = n;
+            }
+          } else {
+            const float g = sig * gE, dy = lane_k(dy2, k);
+            float *px = row + 4 + 3 * sx, *pe = row + 4 + 3 * se;
+            const float x0 = px[0], x1 = px[1], x2 = px[2], e0 = pe[0], e1 = pe[1], e2 = pe[2];
+            px[0] = x0 + g;
+            px[1] = fmaf(g, dx, x1);
+            px[2] = fmaf(g, dy, x2);
+            pe[0] = e0 - g;
+            pe[1] = fmaf(-g, dx, e1);
+            pe[2] = fmaf(-g, dy, e2);
+          }
+        }
+        reinterpret_cast<float4 *>(row)[0] = tail;
+      }
+      // per-(warp, primitive) reduction of the <= 22 moments, one RED.F32 per moment: lane m < RG
+      // sums column m over the h rows (2 instructions per row, 4 independent partial sums)
       const uint32_t id = s_id[j];
       const int h = __popc(hm);
-      if (hit) {
-        float4 *row = reinterpret_cast<float4 *>(&s_red[w][__popc(hm & ((1u << lane) - 1u))][0]);
-#pragma unroll
-        for (int a = 0; a < RGP / 4; ++a) row[a] = make_float4(acc[4 * a], acc[4 * a + 1], acc[4 * a + 2], acc[4 * a + 3]);
-      }
       __syncwarp();
       if (lane < RG) {
         const float *col = &s_red[w][0][lane];
@@ -558,7 +551,9 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
         if (q + 1 < h) s1 += col[(q + 1) * RGP];
         if (q + 2 < h) s2 += col[(q + 2) * RGP];
         const float sum = (s0 + s1) + (s2 + s3);
-        if (sum != 0.f) atomicAdd(F.rgrad + (size_t)lane * F.n + id, sum);
+        // row column m holds moment m - 4 (m >= 4) or dsigma / drgb (m < 4) = rgrad rows RG-4..RG-1
+        const int out = lane < 4 ? RG - 4 + lane : lane - 4;
+        if (sum != 0.f) atomicAdd(F.rgrad + (size_t)out * F.n + id, sum);
       }
       __syncwarp();
     }
