@@ -61,7 +61,7 @@ struct LossSmem {
 __global__ void __launch_bounds__(LT, 2) k_loss_ssim(const float *__restrict__ img, const float *__restrict__ tgt,
                                                      float *__restrict__ dL, float *__restrict__ loss_sum, int H,
                                                      int W, int tiles_x, float lam, float scale, Win win) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   LossSmem &S = *reinterpret_cast<LossSmem *>(smem_raw);
   const int tid = threadIdx.x;
   const int tile = blockIdx.x;

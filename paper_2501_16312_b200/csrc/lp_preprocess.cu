@@ -307,7 +307,6 @@ __device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_ca
   double dsig, drgb[3];
   if (EXACT) {
     // planes n . q = m (+-1 for slabs); moments per plane f: (dL/dm, dL/dn.x, dL/dn.y, dL/dn.z)
-    const double pc[3] = {(double)g.crx, (double)g.cry, (double)g.cz};
     if (KIND == OCTA) {
       double M[3][3], G[3][3], det;
 #pragma unroll
@@ -624,7 +623,8 @@ __device__ __forceinline__ void sh_view_inputs(const lp_prims &P, const lp_camer
   dir[0] = d[0] / nv;
   dir[1] = d[1] / nv;
   dir[2] = d[2] / nv;
-  if (DEG == 0 || (gr[0] == 0.f && gr[1] == 0.f && gr[2] == 0.f)) return;
+  if constexpr (DEG == 0) return;
+  if (gr[0] == 0.f && gr[1] == 0.f && gr[2] == 0.f) return;
   float wk[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
@@ -741,9 +741,24 @@ __global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, f
   __syncwarp();
   if (!vm) return;
   // ---- phase B: owner lane sums its items and writes its primitive's gradients once
+  // the old values of the non-SH feature gradients, loaded up front (independent round trips; the
+  // compiler cannot move these loads past the stores below, which may alias)
   float acc[ItemRes::M2D + 1];
 #pragma unroll
-  for (int a = 0; a <= ItemRes::M2D; ++a) acc[a] = 0.f;
+  for (int a = 0; a < 3; ++a) acc[ItemRes::POS + a] = Gs.pos ? Gs.pos[(size_t)a * n + i] : 0.f;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) acc[ItemRes::ROT + a] = Gs.rot ? Gs.rot[(size_t)a * n + i] : 0.f;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) acc[ItemRes::DIST + a] = (Gs.dist && a < K) ? Gs.dist[(size_t)a * n + i] : 0.f;
+  acc[ItemRes::OP] = Gs.opacity ? Gs.opacity[i] : 0.f;
+  acc[ItemRes::M2D] = Gs.mean2d_abs ? Gs.mean2d_abs[i] : 0.f;
+  float sum[ItemRes::M2D + 1];
+#pragma unroll
+  for (int a = 0; a <= ItemRes::M2D; ++a) sum[a] = 0.f;
+  if (Gs.sh) {   // the SH gradient rows of the warp's primitives: on their way to L1 during the sums
+#pragma unroll
+    for (int q = 0; q < 3 * NC; ++q) asm volatile("prefetch.global.L1 [%0];" ::"l"(Gs.sh + (size_t)q * n + i));
+  }
   float gs[3][NC];
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch)
@@ -752,7 +767,7 @@ __global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, f
   for (int it = first; it < first + c; ++it) {
     const float *res = s_res[w][it];
 #pragma unroll
-    for (int a = 0; a <= ItemRes::M2D; ++a) acc[a] += res[a];
+    for (int a = 0; a <= ItemRes::M2D; ++a) sum[a] += res[a];
     const float gr[3] = {res[ItemRes::GR], res[ItemRes::GR + 1], res[ItemRes::GR + 2]};
     if (gr[0] == 0.f && gr[1] == 0.f && gr[2] == 0.f) continue;
     float Y[16];
@@ -764,18 +779,18 @@ __global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, f
   }
   if (Gs.pos) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] += acc[ItemRes::POS + a];
+    for (int a = 0; a < 3; ++a) Gs.pos[(size_t)a * n + i] = acc[ItemRes::POS + a] + sum[ItemRes::POS + a];
   }
   if (Gs.rot) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a) Gs.rot[(size_t)a * n + i] += acc[ItemRes::ROT + a];
+    for (int a = 0; a < 4; ++a) Gs.rot[(size_t)a * n + i] = acc[ItemRes::ROT + a] + sum[ItemRes::ROT + a];
   }
   if (Gs.dist) {
 #pragma unroll
-    for (int a = 0; a < K; ++a) Gs.dist[(size_t)a * n + i] += acc[ItemRes::DIST + a];
+    for (int a = 0; a < K; ++a) Gs.dist[(size_t)a * n + i] = acc[ItemRes::DIST + a] + sum[ItemRes::DIST + a];
   }
-  if (Gs.opacity) Gs.opacity[i] += acc[ItemRes::OP];
-  if (Gs.mean2d_abs) Gs.mean2d_abs[i] += acc[ItemRes::M2D];
+  if (Gs.opacity) Gs.opacity[i] = acc[ItemRes::OP] + sum[ItemRes::OP];
+  if (Gs.mean2d_abs) Gs.mean2d_abs[i] = acc[ItemRes::M2D] + sum[ItemRes::M2D];
   if (Gs.sh) {
     // all loads first, then the stores (the compiler cannot reorder loads past stores that may alias)
     float old[3 * NC];
