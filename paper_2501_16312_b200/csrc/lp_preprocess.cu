@@ -279,22 +279,19 @@ struct ViewPack {
   int nv;
 };
 
-// one view's contribution; false if the view has no raster gradient for primitive i.
+// one view's contribution of primitive i (a visible primitive: finite geometry).
 // EXACT: the no-ray-space moments (per plane: dL/dm, dL/dn) -> camera-space offsets and centre.
 template <int KIND, bool EXACT>
-__device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_camera &cam, float kappa, int i,
+__device__ __forceinline__ void view_feature_grad(const lp_prims &P, const lp_camera &cam, float kappa, int i,
                                                   const float *__restrict__ rgrad, float gpos[3], float grot[4],
                                                   float gdist[4], float &gop, float &m2d) {
   constexpr int K = Kind<KIND>::K, RG = Kind<KIND>::RG;
   const int n = P.n;
+  // (no early exit on all-zero moments: the items are (primitive, view) pairs with a raster
+  // gradient, and without a branch on the moments the feature loads below overlap theirs)
   float m[RG];
-  bool any = false;
 #pragma unroll
-  for (int a = 0; a < RG; ++a) {
-    m[a] = rgrad[(size_t)a * n + i];
-    any |= (m[a] != 0.f);
-  }
-  if (!any) return false;
+  for (int a = 0; a < RG; ++a) m[a] = rgrad[(size_t)a * n + i];
 
   Geom g;
   float dhf[4], qf[4], cf[3];
@@ -592,10 +589,9 @@ __device__ __forceinline__ bool view_feature_grad(const lp_prims &P, const lp_ca
     const CT dsda = 0.99f / ((1.0f - 0.99f * alpha) * 2.0f * md);
     gop += (float)(dsig * dsda * alpha * (1.0f - alpha));
   }
-  // (SH coefficients and the view-direction term of the centre: k_sh_bwd)
+  // (SH coefficients and the view-direction term of the centre: sh_view_inputs)
 #pragma unroll
   for (int a = 0; a < 3; ++a) gpos[a] += (float)gc[a];
-  return true;
 }
 
 // SH inputs of one (primitive, view) item: the clamp-masked colour gradient gr and the view
