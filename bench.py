@@ -381,9 +381,10 @@ def run_ours(args, rank, world, local_rank):
         else:
             ach, pk, unit = amount / sec / 1e9, hbm_peak, "GB/s"
         tr = traffic_db.get(kname)
+        # traffic: ncu dram read + write bytes per launch of this kernel (profiles/traffic.json), or null
         rooflines[key] = {"kernel": kname, "bound": bound, "achieved": round(ach, 3), "peak": round(pk, 3),
-                          "unit": unit, "frac": round(ach / pk, 4), "ms": round(stage_ms[key], 4),
-                          "traffic": tr, "algorithmic_per_launch": int(amount)}
+                          "unit": unit, "frac": round(ach / pk, 4), "traffic": tr["traffic_bytes"] if tr else None,
+                          "ms": round(stage_ms[key], 4), "traffic_detail": tr, "algorithmic_per_launch": int(amount)}
     per_step = {k: stage_ms[k] * (1 if k in ("pbwd_all_views", "pre_all_views", "adam") else n_local) for k in work}
     dom = max(work, key=lambda k: per_step[k])        # the kernel with the largest share of the step
     for k in rooflines:
