@@ -675,11 +675,13 @@ __global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, f
     for (int v = 0; v < LP_MAXV; ++v)
       if (v < V.nv && V.tt[v][i] != 0) vis |= 1u << v;
     if (Gs.vis_count && vis) Gs.vis_count[i] += (float)__popc(vis);   // densification denominator
+    // (not gated by vis: the raster scratch of a view is zeroed per frame, so an invisible
+    // primitive's probe is 0 anyway, and the probe loads overlap the tiles_touched loads)
     float probe[LP_MAXV];
 #pragma unroll
     for (int v = 0; v < LP_MAXV; ++v) {
       probe[v] = 0.f;
-      if ((vis >> v) & 1u) {
+      if (v < V.nv) {
         const float *rg = V.rgrad[v] + (size_t)(rg_words - 4) * n + i;   // dsigma, drgb
         probe[v] = fabsf(rg[0]) + fabsf(rg[n]) + fabsf(rg[2 * n]) + fabsf(rg[3 * n]);
       }
