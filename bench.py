@@ -219,7 +219,7 @@ def run_ours(args, rank, world, local_rank):
         if evl is not None:
             evl[j].record(stream)
 
-    def step(si, events=None, tgt=None, serial=False):
+    def step(si, events=None, tgt=None, serial=False, tgt_ready=None):
         tg = targets if tgt is None else tgt
         S = events[n_local] if events is not None else None
         # preprocess of all local views in one launch (each primitive's features read once)
@@ -244,6 +244,8 @@ def run_ours(args, rank, world, local_rank):
             rec(ev, 1, sx)
             L.lp_render_fwd(ca, rend.cfg, fa, img[i], sx)
             rec(ev, 2, sx)
+            if tgt_ready is not None:          # e2e: this view's target has arrived from the host
+                sx.wait_event(tgt_ready[i])
             if args.loss == "l1":
                 L.lp_l1_grad(img[i], tg[i], dL[i], loss_buf[si:si + 1], scale, sx)
             else:
@@ -399,13 +401,14 @@ def run_ours(args, rank, world, local_rank):
     e2e = None
     if not args.no_e2e:
         # every step: H2D of that step's targets from pinned memory (prefetched one step ahead on a
-        # copy stream into a double buffer) and a D2H read of that step's loss (pinned ring; the host
-        # waits for step k's loss while step k+1 is already queued)
+        # copy stream into a double buffer, one copy + event per view so a view's loss waits only for
+        # its own target) and a D2H read of that step's loss (pinned ring; the host waits for step
+        # k's loss while step k+1 is already queued)
         host_t = torch.empty(targets.shape, dtype=torch.float32, pin_memory=True)
         host_t.copy_(targets)
         dev_t = [torch.empty_like(targets), torch.empty_like(targets)]
         cp = torch.cuda.Stream(dev)
-        copied = [torch.cuda.Event(), torch.cuda.Event()]
+        copied = [[torch.cuda.Event() for _ in range(n_local)] for _ in range(2)]
         freed = [torch.cuda.Event(), torch.cuda.Event()]
         loss_host = torch.zeros(args.steps, dtype=torch.float32, pin_memory=True)
         read = [torch.cuda.Event() for _ in range(args.steps)]
@@ -413,22 +416,25 @@ def run_ours(args, rank, world, local_rank):
         loss_buf.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+
+        def copy_in(b):
+            with torch.cuda.stream(cp):
+                for i in range(n_local):
+                    dev_t[b][i].copy_(host_t[i], non_blocking=True)
+                    copied[b][i].record(cp)
+
         barrier()
         e0.record(st)
         cp.wait_stream(st)
-        with torch.cuda.stream(cp):
-            dev_t[0].copy_(host_t, non_blocking=True)
-        copied[0].record(cp)
+        copy_in(0)
         losses = []
         for k in range(args.steps):
             b = k & 1
             if k + 1 < args.steps:
-                cp.wait_event(freed[1 - b]) if k >= 1 else None
-                with torch.cuda.stream(cp):
-                    dev_t[1 - b].copy_(host_t, non_blocking=True)
-                copied[1 - b].record(cp)
-            st.wait_event(copied[b])
-            step(base + k, tgt=dev_t[b])
+                if k >= 1:
+                    cp.wait_event(freed[1 - b])
+                copy_in(1 - b)
+            step(base + k, tgt=dev_t[b], tgt_ready=copied[b])
             freed[b].record(st)
             loss_host[k:k + 1].copy_(loss_buf[base + k:base + k + 1], non_blocking=True)
             read[k].record(st)
