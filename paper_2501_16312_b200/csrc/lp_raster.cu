@@ -75,9 +75,10 @@ __device__ __forceinline__ int warp_sublist(const float4 *s_rec, int cnt, float 
 }
 
 // resident CTAs per SM the backward asks the register allocator for (LP_BWD_BLOCKS overrides at
-// build time): 7 x 128 threads allows 72 registers (measured best; 6 -> 80 is spill-free but slower)
+// build time): 6 x 128 threads allows 80 registers (measured on C5 with the shared-row moments:
+// 6 -> 0.613 ms, 7 (72 registers) -> 0.616, 8 (64) -> 0.616)
 #ifndef LP_BWD_BLOCKS
-#define LP_BWD_BLOCKS 7
+#define LP_BWD_BLOCKS 6
 #endif
 // (tetrahedra: 29.7 KB of shared memory per CTA fits at most 7 per SM)
 #define BWD_MIN_BLOCKS(kind, nt) \
