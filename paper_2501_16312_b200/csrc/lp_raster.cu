@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
   const int W = F.width, H = F.height;
   if (threadIdx.x < 3) s_stat[threadIdx.x] = 0ull;
 
-  float fy[PPT], T[PPT], C[PPT][3], dep[PPT];
+  float fy[PPT], dep[PPT];
+  float2 T2 = make_float2(1.f, 1.f), C2[3];   // transmittance and colour of the two pixels (lane k = pixel k)
   uint32_t nproc[PPT];
   bool done[PPT], inside[PPT], dset[PPT];
   uint32_t nhit = 0, nbox = 0;
@@ -157,13 +158,13 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
     inside[k] = x < W && y < H;
     fx = (float)x + 0.5f;
     fy[k] = (float)y + 0.5f;
-    T[k] = 1.f;
-    C[k][0] = C[k][1] = C[k][2] = 0.f;
     done[k] = !inside[k];
     nproc[k] = end - start;
     dep[k] = 0.f;
     dset[k] = false;
   }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) C2[c] = make_float2(0.f, 0.f);
   // exact mode: the pixel rays (r_x shared by the pair, r_z = 1), their lengths and exact offsets
   ExactRay RY;
   if (EXACT) RY = make_ray(cam, fx, fy[0], fy[1]);
@@ -212,37 +213,40 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
         const float2 dy2 = fsub2(make_float2(fy[0], fy[1]), bc(rec[KD::CX + 1]));
         ch2 = chord2<KIND>(rec, dx, dy2, en2);
       }
-      const float ch[PPT] = {ch2.x, ch2.y};
       const float enk[PPT] = {en2.x, en2.y};
+      bool hk[PPT];
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) hk[k] = test[k] && lane_k(ch2, k) > 0.f;
+      if (STATS) nbox += (uint32_t)test[0] + (uint32_t)test[1];
       // the forward's hits of this record -> the warp's hit bits (held by lane j / 32)
-      const bool hit = (test[0] && ch[0] > 0.f) || (test[1] && ch[1] > 0.f);
-      if (__any_sync(0xffffffffu, hit) && lane == (j >> 5)) hitw |= 1u << (j & 31);
+      if (!__any_sync(0xffffffffu, hk[0] || hk[1])) continue;
+      if (lane == (j >> 5)) hitw |= 1u << (j & 31);
+      // both pixels composited as f32x2 pairs; a pixel this record does not hit gets chord 0 ->
+      // E = 1, o = 0, leaving its T and colour bitwise unchanged
+      {
+        const float sig = rec[SIGMA];
+        const float2 E = make_float2(transmit(sig, hk[0] ? ch2.x : 0.f), transmit(sig, hk[1] ? ch2.y : 0.f));
+        const float2 wgt = fmul2(T2, fsub2(bc(1.f), E));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) C2[c] = ffma2(wgt, bc(rec[RGB + c]), C2[c]);
+        T2 = fmul2(T2, E);
+      }
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        if (!test[k]) continue;
-        if (STATS) ++nbox;
-        if (ch[k] > 0.f) {
-          const float E = transmit(rec[SIGMA], ch[k]);
-          const float o = 1.f - E;
-          const float wgt = T[k] * o;
-          C[k][0] = fmaf(wgt, rec[RGB + 0], C[k][0]);
-          C[k][1] = fmaf(wgt, rec[RGB + 1], C[k][1]);
-          C[k][2] = fmaf(wgt, rec[RGB + 2], C[k][2]);
-          T[k] = T[k] * E;
-          if (AUX && !dset[k] && T[k] < 0.5f) {      // cumulative opacity 1 - T > 0.5 (once per pixel)
-            dset[k] = true;
-            if (EXACT) {
-              dep[k] = enk[k];
-            } else {
-              const uint32_t id = F.sorted_val[b + (uint32_t)j];
-              dep[k] = fa(__uint_as_float(F.depth_key[id]), enk[k]);
-            }
+        if (!hk[k]) continue;
+        if (AUX && !dset[k] && lane_k(T2, k) < 0.5f) {   // cumulative opacity 1 - T > 0.5 (once per pixel)
+          dset[k] = true;
+          if (EXACT) {
+            dep[k] = enk[k];
+          } else {
+            const uint32_t id = F.sorted_val[b + (uint32_t)j];
+            dep[k] = fa(__uint_as_float(F.depth_key[id]), enk[k]);
           }
-          if (STATS) ++nhit;
-          if (T[k] < cfg.t_stop) {       // include-then-stop (reading 9)
-            done[k] = true;
-            nproc[k] = b + (uint32_t)j - start + 1;
-          }
+        }
+        if (STATS) ++nhit;
+        if (lane_k(T2, k) < cfg.t_stop) {   // include-then-stop (reading 9)
+          done[k] = true;
+          nproc[k] = b + (uint32_t)j - start + 1;
         }
       }
     }
@@ -257,14 +261,15 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
     if (!inside[k]) continue;
     const int x = (int)fx, y = (int)fy[k];
     const size_t p = (size_t)y * W + x;
-    image[p] = fmaf(T[k], cfg.bg[0], C[k][0]);
-    image[HW + p] = fmaf(T[k], cfg.bg[1], C[k][1]);
-    image[2 * HW + p] = fmaf(T[k], cfg.bg[2], C[k][2]);
-    F.T_final[p] = T[k];
+    const float Tk = lane_k(T2, k);
+    image[p] = fmaf(Tk, cfg.bg[0], lane_k(C2[0], k));
+    image[HW + p] = fmaf(Tk, cfg.bg[1], lane_k(C2[1], k));
+    image[2 * HW + p] = fmaf(Tk, cfg.bg[2], lane_k(C2[2], k));
+    F.T_final[p] = Tk;
     F.n_proc[p] = nproc[k];
     if (AUX) {
       if (depth) depth[p] = dep[k];
-      if (alpha) alpha[p] = 1.f - T[k];
+      if (alpha) alpha[p] = 1.f - Tk;
     }
     it += nproc[k];
   }
