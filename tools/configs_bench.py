@@ -1,0 +1,142 @@
+"""Per-config measurement of the single-view configs C1-C4 (SURVEY §8d "per-config reporting").
+
+For each config: one view, the C-ABI calls of the hot path timed separately with CUDA events on the
+launching stream, L2 flushed (a 2 x L2 write) before every iteration, median over --iters after
+--warmup:
+
+  fwd      = lp_preprocess + lp_bin_sort + lp_render_fwd              (render-only frame)
+  fwd+bwd  = fwd + lp_raster_bwd + lp_preprocess_bwd                  (seeded upstream G ~ N(0,1)/(3HW))
+
+Prints one JSON line per config (Mpixel/s, FPS, per-call ms, the tile-list / pair counters, the
+raster kernels' ALU-model fraction as in bench.py) and with --out appends them to a file.
+
+  python tools/configs_bench.py [C1 C2 C3 C4] [--iters 20] [--warmup 5] [--exact] [--out FILE]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402  (work model, clock sampler)
+from paper_2501_16312_b200 import linprim as L  # noqa: E402
+from paper_2501_16312_b200 import render, scenegen  # noqa: E402
+
+RENDER_ONLY = {"C4"}        # BASELINE configs[3]: "render-only FPS"
+
+
+def run(name, iters, warmup, exact):
+    dev = torch.device("cuda", 0)
+    scene, cams = scenegen.make_scene(name, seed=0)
+    cam = cams[0]
+    W, H = cam["width"], cam["height"]
+    ds = render.DeviceScene(scene, device=dev)
+    kw = dict(exact=exact, aa_kernel=0.0 if exact else 0.1)
+    # counters pass (untimed)
+    rr = render.Renderer(ds, [cam], count_stats=True, **kw)
+    rr.forward()
+    torch.cuda.synchronize()
+    s = rr.counters(0)
+    E = int(s[L.LP_CNT_ENTRIES])
+    I_ = int(s[8]) | (int(s[9]) << 32)
+    X_ = int(s[10]) | (int(s[11]) << 32)
+    B_ = int(s[12]) | (int(s[13]) << 32)
+    vis = int(s[L.LP_CNT_VISIBLE])
+    del rr
+    rend = render.Renderer(ds, [cam], capacity=int(E * 1.3) + 4096, sync_capacity=False, **kw)
+    st = torch.cuda.current_stream(dev)
+    img = torch.empty((1, 3, H, W), dtype=torch.float32, device=dev)
+    G = torch.from_numpy(scenegen.upstream_grad(W, H, seed=0)).to(dev).reshape(1, 3, H, W).contiguous()
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(2 * l2 // 4 + 1024, dtype=torch.float32, device=dev)
+    ca = rend._cams([0])
+    fa = render.frames_array(rend.frames)
+    bwd = name not in RENDER_ONLY
+    names = ["pre", "sort", "fwd"] + (["rbwd", "pbwd"] if bwd else [])
+
+    def once(ev=None):
+        def rec(j):
+            if ev is not None:
+                ev[j].record(st)
+        rec(0)
+        L.lp_preprocess(ds.prims, ca, rend.cfg, fa, st)
+        rec(1)
+        L.lp_bin_sort(ca, fa, st, None)
+        rec(2)
+        L.lp_render_fwd(ca, rend.cfg, fa, img[0], st)
+        rec(3)
+        if bwd:
+            L.lp_raster_bwd(ca, rend.cfg, fa, G[0], st)
+            rec(4)
+            L.lp_preprocess_bwd(ds.prims, ca, rend.cfg, fa, ds.grads, st)
+            rec(5)
+
+    for _ in range(warmup):
+        flush.fill_(1.0)
+        once()
+    torch.cuda.synchronize()
+    c = L.lp_frame_counters(rend.frames[0].c, st)
+    assert c[L.LP_CNT_OVERFLOW] == 0, "tile-list capacity overflow"
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)] for _ in range(iters)]
+    clocks = bench.ClockSampler(0)
+    clocks.start()
+    for k in range(iters):
+        flush.fill_(1.0)
+        once(evs[k])
+        ds.grad.zero_()
+    torch.cuda.synchronize()
+    clocks.stop()
+    per = {nm: statistics.median(e[j].elapsed_time(e[j + 1]) for e in evs) for j, nm in enumerate(names)}
+    fwd_ms = statistics.median(e[0].elapsed_time(e[3]) for e in evs)
+    out = {"workload": name, "kind": "octahedron" if ds.kind == 0 else "tetrahedron", "n_primitives": ds.n,
+           "sh_degree": ds.sh_degree, "width": W, "height": H,
+           "projection": "no ray space (App. D)" if exact else "EWA ray space",
+           "l2": "flushed (2 x L2 write) before every iteration", "iters": iters, "warmup": warmup,
+           "fwd_ms": round(fwd_ms, 4), "fwd_mpix_s": round(W * H / (fwd_ms * 1e-3) / 1e6, 2),
+           "render_fps": round(1000.0 / fwd_ms, 1)}
+    if bwd:
+        fb_ms = statistics.median(e[0].elapsed_time(e[5]) for e in evs)
+        out.update({"fwd_bwd_ms": round(fb_ms, 4), "fwd_bwd_mpix_s": round(W * H / (fb_ms * 1e-3) / 1e6, 2),
+                    "iters_per_s": round(1000.0 / fb_ms, 1)})
+    out["calls_ms"] = {k: round(v, 4) for k, v in per.items()}
+    alu_peak = 148 * 128 * 1965.0 * 1e6
+    out["raster_fwd_alu_frac"] = round(bench.fp32_ops(ds.kind, I_, B_, X_, False) / (per["fwd"] * 1e-3) / alu_peak, 4)
+    if bwd:
+        out["raster_bwd_alu_frac"] = round(bench.fp32_ops(ds.kind, I_, B_, X_, True) / (per["rbwd"] * 1e-3) / alu_peak, 4)
+    out["counters"] = {"tile_list_entries": E, "visible_primitives": vis,
+                       "iterated_pairs_per_px": round(I_ / (W * H), 2),
+                       "in_bbox_pairs_per_px": round(B_ / (W * H), 2),
+                       "intersected_pairs_per_px": round(X_ / (W * H), 2)}
+    out["clocks"] = clocks.summary()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="*", default=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--exact", action="store_true")
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    torch.cuda.set_device(0)
+    for name in a.configs:
+        r = run(name, a.iters, a.warmup, a.exact)
+        line = json.dumps(r)
+        print(line, flush=True)
+        if a.out:
+            with open(a.out, "a") as f:
+                f.write(line + "\n")
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
