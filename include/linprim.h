@@ -84,7 +84,7 @@ typedef struct {
   int32_t kind, n, width, height, tiles_x, tiles_y;
   int64_t capacity;           /* maximum tile-list entries */
   int32_t record_words;       /* record stride in floats (24 octa, 28 tetra) */
-  int32_t rgrad_words;        /* floats per primitive in rgrad (20 octa, 22 tetra) */
+  int32_t rgrad_words;        /* rgrad row stride in floats (24: dsigma, drgb, 16 octa / 18 tetra moments, pad) */
   uint32_t *tiles_touched;    /* [n] */
   uint16_t *rect;             /* [n][4] tile rect tx0, ty0, tx1, ty1 (inclusive), zeros if none */
   uint32_t *depth_key;        /* [n] float bits of l = |p| (0 if culled / invalid) */
@@ -102,7 +102,7 @@ typedef struct {
   uint32_t *counters;         /* [16] device counters, see LP_CNT_* */
   float    *T_final;          /* [H][W] final transmittance */
   uint32_t *n_proc;           /* [H][W] tile-list entries processed per pixel (from the tile's start) */
-  float    *rgrad;            /* [rgrad_words][n] raster-gradient scratch of the backward */
+  float    *rgrad;            /* [n][rgrad_words] raster-gradient scratch of the backward, one row per primitive */
   float    *canon;            /* [n][2 + 3K] canonical fp32 cr_x, cr_y, offsets (debug; NULL unless requested) */
   int32_t  *tile_diff;        /* [(tiles_y+1)][(tiles_x+1)] 2-D difference counts of the tile rects (bucket sort) */
   uint32_t *tile_cursor;      /* [tiles] bucket fill cursors (bucket sort) */

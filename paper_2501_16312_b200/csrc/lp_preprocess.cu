@@ -289,9 +289,22 @@ __device__ __forceinline__ void view_feature_grad(const lp_prims &P, const lp_ca
   const int n = P.n;
   // (no early exit on all-zero moments: the items are (primitive, view) pairs with a raster
   // gradient, and without a branch on the moments the feature loads below overlap theirs)
+  // the primitive's rgrad row (dsigma, drgb | moments) -> m[moments..., dsigma, drgb]
   float m[RG];
+  {
+    const float4 *row = reinterpret_cast<const float4 *>(rgrad + (size_t)i * LP_RGS);
+    float t[4 * ((RG + 3) / 4)];
 #pragma unroll
-  for (int a = 0; a < RG; ++a) m[a] = rgrad[(size_t)a * n + i];
+    for (int q = 0; q < (RG + 3) / 4; ++q) {
+      const float4 x = row[q];
+      t[4 * q] = x.x;
+      t[4 * q + 1] = x.y;
+      t[4 * q + 2] = x.z;
+      t[4 * q + 3] = x.w;
+    }
+#pragma unroll
+    for (int a = 0; a < RG; ++a) m[a] = a < RG - 4 ? t[a + 4] : t[a - (RG - 4)];
+  }
 
   Geom g;
   float dhf[4], qf[4], cf[3];
@@ -606,7 +619,7 @@ __device__ __forceinline__ void sh_view_inputs(const lp_prims &P, const lp_camer
   const int n = P.n;
   const float c[3] = {P.pos[i], P.pos[n + i], P.pos[2 * n + i]};
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) gr[ch] = rgrad[(size_t)(rg_words - 3 + ch) * n + i];
+  for (int ch = 0; ch < 3; ++ch) gr[ch] = rgrad[(size_t)i * LP_RGS + 1 + ch];   // row: dsigma, drgb | moments
   // the forward's clamp decision, stored by K1 as the colour's sign bit (-0.0: clamped)
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch)
@@ -682,8 +695,8 @@ __global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, f
     for (int v = 0; v < LP_MAXV; ++v) {
       probe[v] = 0.f;
       if (v < V.nv) {
-        const float *rg = V.rgrad[v] + (size_t)(rg_words - 4) * n + i;   // dsigma, drgb
-        probe[v] = fabsf(rg[0]) + fabsf(rg[n]) + fabsf(rg[2 * n]) + fabsf(rg[3 * n]);
+        const float4 rg = *reinterpret_cast<const float4 *>(V.rgrad[v] + (size_t)i * LP_RGS);   // dsigma, drgb
+        probe[v] = fabsf(rg.x) + fabsf(rg.y) + fabsf(rg.z) + fabsf(rg.w);
       }
     }
 #pragma unroll
