@@ -60,8 +60,13 @@ template <int KIND, bool EXACT, int DEG>
 __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_camera &cam, float kappa,
                                                 const lp_frame &F, int i);
 
+// resident K1 blocks per SM asked of the register allocator (-DLP_PRE_MINB overrides): 4 x 256
+// threads = 64 registers (70 unconstrained, 3 blocks)
+#ifndef LP_PRE_MINB
+#define LP_PRE_MINB 4
+#endif
 template <int KIND, bool EXACT, int DEG>
-__global__ void __launch_bounds__(256) k_preprocess(lp_prims P, float kappa, PreViews V) {
+__global__ void __launch_bounds__(256, LP_PRE_MINB) k_preprocess(lp_prims P, float kappa, PreViews V) {
   // view-interleaved grid: the nv consecutive blocks of one primitive range run the nv views, so
   // the primitive features come from HBM once and from L2 for the other views
   const int v = blockIdx.x % V.nv;
