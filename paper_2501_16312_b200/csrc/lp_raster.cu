@@ -191,13 +191,23 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
     const int nl = warp_sublist<NT, RW4>(s_rec, cnt, wx0, wx1, wy0, wy1, s_list[wrp]);
     for (int q = 0; q < nl; ++q) {
       const int j = s_list[wrp][q];
-      const float4 bb = s_rec[j * RW4];
-      const bool inx = fabsf(fx - bb.x) <= bb.z;
       bool test[PPT];
+      if (STATS || EXACT) {
+        // per-pixel bbox test (the in-bbox counter; exact mode: degenerate records are marked by an
+        // empty bbox only)
+        const float4 bb = s_rec[j * RW4];
+        const bool inx = fabsf(fx - bb.x) <= bb.z;
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) test[k] = !done[k] && inx && fabsf(fy[k] - bb.y) <= bb.w;
-      const bool any = test[0] || test[1];
-      if (!__any_sync(0xffffffffu, any)) continue;
+        for (int k = 0; k < PPT; ++k) test[k] = !done[k] && inx && fabsf(fy[k] - bb.y) <= bb.w;
+        if (!__any_sync(0xffffffffu, test[0] || test[1])) continue;
+      } else {
+        // ray space: no per-pixel bbox test -- the record's bbox reaches the warp's pixel rectangle
+        // (sub-list), and outside the primitive the chord is <= 0 (the backward's hit test is
+        // chord > 0 alone); a warp whose pixels all stopped skips the compositing and leaves at the
+        // next batch
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) test[k] = !done[k];
+      }
       const float *rec = reinterpret_cast<const float *>(&s_rec[j * RW4]);
       float2 ch2, en2;
       if constexpr (EXACT) {
