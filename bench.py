@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--exact", action="store_true",
                     help="the paper's no-ray-space variant (App. D) instead of the EWA ray-space method")
     ap.add_argument("--streams", type=int, default=4, help="CUDA streams the views of a step are spread over")
+    ap.add_argument("--split-pre", action=argparse.BooleanOptionalAction, default=True,
+                    help="preprocess the first --streams views in their own launch so their binning overlaps "
+                         "the preprocess of the others")
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop (ncu --profile-from-start off) and exit")
     return ap.parse_args()
@@ -213,7 +216,14 @@ def run_ours(args, rank, world, local_rank):
     n_str = max(1, min(args.streams, n_local))
     streams = [st] + [torch.cuda.Stream(dev) for _ in range(n_str - 1)]
     fork = torch.cuda.Event()
+    fork2 = torch.cuda.Event()
     joins = [torch.cuda.Event() for _ in streams[1:]]
+    # --split-pre: the views run on n_str auxiliary streams, the preprocess in two launches on `st`
+    aux = [torch.cuda.Stream(dev) for _ in range(n_str)] if args.split_pre else []
+    joins_aux = [torch.cuda.Event() for _ in aux]
+    pre_cams = [rend._cams(list(range(n_str))), rend._cams(list(range(n_str, n_local)))]
+    pre_frames = [render.frames_array([rend.frames[i] for i in range(n_str)]),
+                  render.frames_array([rend.frames[i] for i in range(n_str, n_local)])]
 
     def rec(evl, j, stream):
         if evl is not None:
@@ -226,17 +236,32 @@ def run_ours(args, rank, world, local_rank):
         rec(S, 0, st)
         for i in range(n_local):
             fa_all[i] = fa_view[i][0]
-        L.lp_preprocess(ds.prims, ca_all, rend.cfg, fa_all, st)
-        for i in range(n_local):
-            fa_view[i][0] = fa_all[i]
-        rec(S, 1, st)
         strs = [st] if serial else streams
-        if len(strs) > 1:
+        split = not serial and args.split_pre and n_local > len(strs)
+        if split:
+            # preprocess in two launches: the first wave of views (one per stream) starts binning
+            # while the second launch preprocesses the remaining views
+            nf = len(strs)
+            L.lp_preprocess(ds.prims, pre_cams[0], rend.cfg, pre_frames[0], st)
+            fork.record(st)
+            L.lp_preprocess(ds.prims, pre_cams[1], rend.cfg, pre_frames[1], st)
+            fork2.record(st)
+            for i in range(n_local):
+                fa_view[i][0] = pre_frames[0][i] if i < nf else pre_frames[1][i - nf]
+        else:
+            L.lp_preprocess(ds.prims, ca_all, rend.cfg, fa_all, st)
+            for i in range(n_local):
+                fa_view[i][0] = fa_all[i]
+        rec(S, 1, st)
+        if len(strs) > 1 and not split:
             fork.record(st)
             for s_ in strs[1:]:
                 s_.wait_event(fork)
         for i in range(n_local):
             sx = strs[i % len(strs)]
+            if split:
+                sx = aux[i % len(aux)]
+                sx.wait_event(fork if i < len(strs) else fork2)
             ca, fa = ca_view[i], fa_view[i]
             ev = events[i] if events is not None else None
             rec(ev, 0, sx)
@@ -254,7 +279,11 @@ def run_ours(args, rank, world, local_rank):
             L.lp_raster_bwd(ca, rend.cfg, fa, dL[i], sx)
             rec(ev, 4, sx)
             fa_all[i] = fa[0]
-        if len(strs) > 1:
+        if split:
+            for j, s_ in enumerate(aux):
+                joins_aux[j].record(s_)
+                st.wait_event(joins_aux[j])
+        elif len(strs) > 1:
             for j, s_ in enumerate(strs[1:]):
                 joins[j].record(s_)
                 st.wait_event(joins[j])
