@@ -459,11 +459,24 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
       BWD_STAT(2, 1);
       BWD_STAT(3, __popc(hm));
       float *row = &s_red[w][__popc(hm & ((1u << lane) - 1u))][0];
+      // sigma and colour into registers once per entry, by every lane (one broadcast load; inside
+      // the hit lanes' loop the compiler re-reads them after every shared store to the rows)
+      float sig, rgbv[3];
+      if constexpr (SIGMA % 4 == 0 && RGB == SIGMA + 1) {
+        const float4 v = reinterpret_cast<const float4 *>(rec)[SIGMA / 4];
+        sig = v.x;
+        rgbv[0] = v.y;
+        rgbv[1] = v.z;
+        rgbv[2] = v.w;
+      } else {
+        sig = rec[SIGMA];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) rgbv[c] = rec[RGB + c];
+      }
       if (hit) {
 #pragma unroll
         for (int a = 1; a < RGP / 4; ++a) reinterpret_cast<float4 *>(row)[a] = make_float4(0.f, 0.f, 0.f, 0.f);
         float4 tail = make_float4(0.f, 0.f, 0.f, 0.f);   // dsigma, dr, dg, db
-        const float sig = rec[SIGMA];
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
           if (!hk[k]) continue;
@@ -480,8 +493,8 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
           tail.w = fmaf(Tk * o, G[k][2], tail.w);
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            dLdo = fmaf(rec[RGB + c] - S[k][c], G[k][c], dLdo);
-            S[k][c] = fmaf(o, rec[RGB + c], E * S[k][c]);   // colour behind the previous entry
+            dLdo = fmaf(rgbv[c] - S[k][c], G[k][c], dLdo);
+            S[k][c] = fmaf(o, rgbv[c], E * S[k][c]);        // colour behind the previous entry
           }
           dLdo *= Tk;
           T[k] = Tk;
