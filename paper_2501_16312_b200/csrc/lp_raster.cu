@@ -56,22 +56,60 @@ __device__ __forceinline__ bool rect_hits_bbox(const float4 &bb, float x0, float
 
 // Build the warp's ordered sub-list of batch records [0, cnt) whose bbox reaches its rectangle.
 // Lane l tests records l, l+32, ...; returns the list length (warp-uniform).
-template <int NT, int RW4>
-__device__ __forceinline__ int warp_sublist(const float4 *s_rec, int cnt, float x0, float x1, float y0, float y1,
-                                            unsigned char *list) {
+// WM: the records' per-warp masks s_wm (octahedron_warp_mask) replace the bbox test.
+template <int NT, int RW4, bool WM>
+__device__ __forceinline__ int warp_sublist(const float4 *s_rec, const unsigned char *s_wm, int cnt, float x0,
+                                            float x1, float y0, float y1, unsigned char *list) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   int n = 0;
 #pragma unroll
   for (int r = 0; r < NT; r += 32) {
     const int j = r + lane;
-    const bool ov = j < cnt && rect_hits_bbox(s_rec[j * RW4], x0, x1, y0, y1);
+    const bool ov = j < cnt && (WM ? ((s_wm[j] >> (threadIdx.x >> 5)) & 1u) != 0
+                                   : rect_hits_bbox(s_rec[j * RW4], x0, x1, y0, y1));
     const unsigned m = __ballot_sync(0xffffffffu, ov);
     if (ov) list[n + __popc(m & lt)] = (unsigned char)j;
     n += __popc(m);
   }
   __syncwarp();
   return n;
+}
+
+// Which of the CTA's four 8x8 warp rectangles (NT = 128: warp w at (8 (w & 1), 8 (w >> 1)) in the
+// tile) the octahedron's screen footprint can reach: the record's bbox against each rectangle, then
+// the separating-axis test against the six strips that bound the footprint,
+//   chord(D) > 0  =>  |(b_s - b_t) D.x + (g_s - g_t) D.y| < h_s + h_t   for every slab pair {s, t}
+// (min_s (L_s + h_s) > max_t (L_t - h_t) with L = b D.x + g D.y, D relative to the centre).  A
+// rectangle with centre D_c and half-size 3.5 misses strip {s, t} if |a . D_c| > h_s + h_t +
+// 3.5 (|a.x| + |a.y|); the bound is widened by 1e-4 relative plus 1e-5 of the evaluated terms so fp32
+// rounding never drops a record with a hit.  Computed once per staged record by its staging thread
+// (instead of a bbox test per warp): on C5 about half of the bbox sub-list entries hit no pixel of
+// the warp.
+__device__ __forceinline__ unsigned octahedron_warp_mask(const float4 *r, int tx, int ty) {
+  const float4 bb = r[0];
+  const float b[4] = {r[1].x, r[1].w, r[2].z, r[3].y};
+  const float g[4] = {r[1].y, r[2].x, r[2].w, r[3].z};
+  const float h[4] = {r[1].z, r[2].y, r[3].x, r[3].w};
+  const float dcx = (float)(tx * LP_TILE) + 4.f - bb.x, dcy = (float)(ty * LP_TILE) + 4.f - bb.y;
+  unsigned m = 0u;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const float ox = (w & 1) ? 8.f : 0.f, oy = (w & 2) ? 8.f : 0.f;
+    if (fabsf(dcx + ox) <= bb.z + 3.5f && fabsf(dcy + oy) <= bb.w + 3.5f) m |= 1u << w;
+  }
+  const float K = 1e-5f * (fabsf(dcx) + fabsf(dcy) + 16.f);
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+#pragma unroll
+    for (int t = s + 1; t < 4; ++t) {
+      const float ax = b[s] - b[t], ay = g[s] - g[t], aa = fabsf(ax) + fabsf(ay);
+      const float e = fmaf(aa, K, (h[s] + h[t] + 3.5f * aa) * 1.0001f);
+      const float v0 = fmaf(ax, dcx, ay * dcy), v1 = fmaf(8.f, ax, v0), v2 = fmaf(8.f, ay, v0), v3 = fmaf(8.f, ay, v1);
+      m &= (fabsf(v0) <= e ? 1u : 0u) | (fabsf(v1) <= e ? 2u : 0u) | (fabsf(v2) <= e ? 4u : 0u) |
+           (fabsf(v3) <= e ? 8u : 0u);
+    }
+  return m;
 }
 
 // resident CTAs per SM the backward asks the register allocator for (LP_BWD_BLOCKS overrides at
@@ -135,7 +173,10 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
   constexpr int SIGMA = EXACT ? ER::SIGMA : KD::SIGMA, RGB = EXACT ? ER::RGB : KD::RGB;
   __shared__ float4 s_rec[NT * RW4];
   __shared__ unsigned char s_list[NT / 32][NT];
+  __shared__ unsigned char s_wm[NT];
   __shared__ unsigned long long s_stat[3];
+  // per-record warp masks (footprint strips) for the ray-space octahedron; the bbox test otherwise
+  constexpr bool WM = KIND == LP_OCTAHEDRON && !EXACT && !STATS && NT == 128;
 
   const int tile = blockIdx.x;
   const int tx = tile % F.tiles_x, ty = tile / F.tiles_x;
@@ -178,8 +219,12 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
     if (e < end) {
       const uint32_t v = F.sorted_val[e];
       const float4 *src = reinterpret_cast<const float4 *>(F.record + (size_t)v * RS);
+      float4 rv[RW4];
 #pragma unroll
-      for (int w = 0; w < RW4; ++w) s_rec[threadIdx.x * RW4 + w] = __ldg(src + w);
+      for (int w = 0; w < RW4; ++w) rv[w] = __ldg(src + w);
+#pragma unroll
+      for (int w = 0; w < RW4; ++w) s_rec[threadIdx.x * RW4 + w] = rv[w];
+      if constexpr (WM) s_wm[threadIdx.x] = (unsigned char)octahedron_warp_mask(rv, tx, ty);
     }
     __syncthreads();
     if (__all_sync(0xffffffffu, done[0] && done[1])) continue;
@@ -188,7 +233,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
     uint32_t hitw = 0u;                                 // lane L < NT/32: the warp's hit bits of records 32L..
     // per-warp sub-list: the batch records whose bbox reaches the warp's pixels, in list order
     // (each lane tests NT/32 records; convexity: outside the vertex bbox the chord is <= 0)
-    const int nl = warp_sublist<NT, RW4>(s_rec, cnt, wx0, wx1, wy0, wy1, s_list[wrp]);
+    const int nl = warp_sublist<NT, RW4, WM>(s_rec, s_wm, cnt, wx0, wx1, wy0, wy1, s_list[wrp]);
     for (int q = 0; q < nl; ++q) {
       const int j = s_list[wrp][q];
       bool test[PPT];
