@@ -112,6 +112,37 @@ __device__ __forceinline__ unsigned octahedron_warp_mask(const float4 *r, int tx
   return m;
 }
 
+// The same for a tetrahedron: chord(D) > 0 needs every back plane above every front plane,
+//   (A_b - A_f) + (B_b - B_f) D.x + (C_b - C_f) D.y > 0   (front slots 0-2, back slots 3-5),
+// so a rectangle misses the footprint if for some pair the maximum of that plane over it is < 0.
+__device__ __forceinline__ unsigned tetrahedron_warp_mask(const float4 *r, int tx, int ty) {
+  const float4 bb = r[0];
+  const float cx = r[1].x, cy = r[1].y;
+  const float w_[24] = {r[1].z, r[1].w, r[2].x, r[2].y, r[2].z, r[2].w, r[3].x, r[3].y, r[3].z, r[3].w, r[4].x,
+                        r[4].y, r[4].z, r[4].w, r[5].x, r[5].y, r[5].z, r[5].w, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const float X = (float)(tx * LP_TILE) + 4.f, Y = (float)(ty * LP_TILE) + 4.f;
+  const float dbx = X - bb.x, dby = Y - bb.y, dcx = X - cx, dcy = Y - cy;
+  unsigned m = 0u;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const float ox = (w & 1) ? 8.f : 0.f, oy = (w & 2) ? 8.f : 0.f;
+    if (fabsf(dbx + ox) <= bb.z + 3.5f && fabsf(dby + oy) <= bb.w + 3.5f) m |= 1u << w;
+  }
+  const float K = 1e-5f * (fabsf(dcx) + fabsf(dcy) + 16.f);
+#pragma unroll
+  for (int f = 0; f < 3; ++f)
+#pragma unroll
+    for (int bk = 3; bk < 6; ++bk) {
+      const float dA = w_[3 * bk] - w_[3 * f], dB = w_[3 * bk + 1] - w_[3 * f + 1], dC = w_[3 * bk + 2] - w_[3 * f + 2];
+      const float aa = fabsf(dB) + fabsf(dC);
+      const float tol = fmaf(aa, K, 1e-4f * (fabsf(w_[3 * bk]) + fabsf(w_[3 * f]) + 3.5f * aa));
+      const float lim = -(dA + 3.5f * aa + tol);   // keep warp w if dB D.x + dC D.y >= lim at its centre
+      const float v0 = fmaf(dB, dcx, dC * dcy), v1 = fmaf(8.f, dB, v0), v2 = fmaf(8.f, dC, v0), v3 = fmaf(8.f, dC, v1);
+      m &= (v0 >= lim ? 1u : 0u) | (v1 >= lim ? 2u : 0u) | (v2 >= lim ? 4u : 0u) | (v3 >= lim ? 8u : 0u);
+    }
+  return m;
+}
+
 // resident CTAs per SM the backward asks the register allocator for (LP_BWD_BLOCKS overrides at
 // build time): 6 x 128 threads allows 80 registers (measured on C5 with the shared-row moments:
 // 6 -> 0.613 ms, 7 (72 registers) -> 0.616, 8 (64) -> 0.616)
@@ -176,7 +207,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
   __shared__ unsigned char s_wm[NT];
   __shared__ unsigned long long s_stat[3];
   // per-record warp masks (footprint strips) for the ray-space octahedron; the bbox test otherwise
-  constexpr bool WM = KIND == LP_OCTAHEDRON && !EXACT && !STATS && NT == 128;
+  constexpr bool WM = !EXACT && !STATS && NT == 128;
 
   const int tile = blockIdx.x;
   const int tx = tile % F.tiles_x, ty = tile / F.tiles_x;
@@ -224,7 +255,8 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
       for (int w = 0; w < RW4; ++w) rv[w] = __ldg(src + w);
 #pragma unroll
       for (int w = 0; w < RW4; ++w) s_rec[threadIdx.x * RW4 + w] = rv[w];
-      if constexpr (WM) s_wm[threadIdx.x] = (unsigned char)octahedron_warp_mask(rv, tx, ty);
+      if constexpr (WM && KIND == LP_OCTAHEDRON) s_wm[threadIdx.x] = (unsigned char)octahedron_warp_mask(rv, tx, ty);
+      if constexpr (WM && KIND == LP_TETRAHEDRON) s_wm[threadIdx.x] = (unsigned char)tetrahedron_warp_mask(rv, tx, ty);
     }
     __syncthreads();
     if (__all_sync(0xffffffffu, done[0] && done[1])) continue;
