@@ -484,8 +484,11 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": int(host_t.numel() * 4 * world), "d2h_bytes_per_step": 4 * world,
                "ms_per_step": round(e2e_step, 3), "loss_last": losses[-1]}
 
-    # + one fused preprocess backward and one Adam per step
-    launches = args.steps * (n_local * launches_per_view(n, rend.frames[0].c.tiles_x * rend.frames[0].c.tiles_y) + 3)  # + K1, K5, Adam
+    # + the preprocess launches (8 views per launch; two with --split-pre), the preprocess backward
+    # (4 views per launch, LP_K5_MAXV) and one Adam per step
+    n_pre = 2 if (args.split_pre and n_local > n_str) else math.ceil(n_local / 8)
+    launches = args.steps * (n_local * launches_per_view(n, rend.frames[0].c.tiles_x * rend.frames[0].c.tiles_y) +
+                             n_pre + math.ceil(n_local / 4) + 1)
 
     out = {
         "metric": "fwd+bwd Mpixel/s (C5 training step: 8 views, fwd+bwd+allreduce+Adam)",
