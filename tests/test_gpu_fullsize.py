@@ -109,3 +109,36 @@ def test_fullsize_sampled_parity(cfg, exact):
         ok_g, worst, rep = PT.grad_close(name, gd[name].cpu().numpy().reshape(refg.shape), refg, fl)
         assert ok_g, rep
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
+def test_forward_warp_masks_drop_no_hit(cfg):
+    """The forward's per-record warp masks (footprint strips) only skip records that hit
+    no pixel of the warp: the timed forward (masks) and the counting forward (bbox sub-list + per-pixel
+    bbox test, count_stats) give bit-identical image, T_final and n_proc at full size, and the
+    backward fed by either one's hit bits gives bit-identical gradients."""
+    import torch
+    from paper_2501_16312_b200 import render
+    scene, cams = scenegen.make_scene(cfg, seed=0)
+    cam = cams[0]
+    W, H = cam["width"], cam["height"]
+    ds = render.DeviceScene(scene)
+    G = torch.from_numpy(scenegen.upstream_grad(W, H, seed=3)).cuda().reshape(1, 3, H, W).contiguous()
+    outs = []
+    for stats in (False, True):
+        r = render.Renderer(ds, [cam], count_stats=stats)
+        img = r.forward()
+        ds.grad.zero_()
+        r.backward(G)
+        torch.cuda.synchronize()
+        f = r.frames[0]
+        outs.append((img.cpu().numpy(), f.buf("T_final", W * H, torch.float32).cpu().numpy(),
+                     f.buf("n_proc", W * H, torch.int32).cpu().numpy(),
+                     {k: ds.view(k, grad=True).cpu().numpy() for k in ds.offsets}))
+    for a, b, name in zip(outs[0][:3], outs[1][:3], ("image", "T_final", "n_proc")):
+        assert np.array_equal(a, b), f"{cfg}: {name} differs between the masked and the counting forward"
+    # the backward's float atomics are order-dependent: equal up to accumulation order (the parity
+    # bar per feature group, DESIGN.md §9)
+    for k, a in outs[0][3].items():
+        b = outs[1][3][k]
+        assert np.all(np.abs(a - b) <= 1e-3 * np.abs(b) + 1e-5 * np.abs(b).max()), f"{cfg}: grad {k}"
