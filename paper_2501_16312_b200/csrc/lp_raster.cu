@@ -1,9 +1,10 @@
 // lp_raster.cu -- K3 forward raster (rows a8-a9) and K4 backward raster (rows a10-a11).
 //
 // One CTA per 16x16 tile.  A CTA walks its tile's sorted list in batches of NT records: each
-// thread stages one record (80 B octa / 96 B tetra, gathered by primitive id) into shared
-// memory, then every thread evaluates the whole batch for its PPT pixels, reading each record
-// with broadcast LDS.128.  The per-pair work is the slab / Cyrus-Beck chord:
+// thread stages one record (80 B octa / 112 B tetra, gathered by primitive id) into shared
+// memory and marks which of the four 8x8 warp rectangles its footprint reaches; each warp then
+// evaluates its sub-list of the batch for its pixels (2 per thread), reading each record with
+// broadcast LDS.128.  The per-pair work is the slab / Cyrus-Beck chord:
 // ~26 FP32 instructions per (pixel, octahedron), ~19 per (pixel, tetrahedron), plus ~10 per
 // intersected pair for the opacity and compositing.
 //
@@ -56,7 +57,7 @@ __device__ __forceinline__ bool rect_hits_bbox(const float4 &bb, float x0, float
 
 // Build the warp's ordered sub-list of batch records [0, cnt) whose bbox reaches its rectangle.
 // Lane l tests records l, l+32, ...; returns the list length (warp-uniform).
-// WM: the records' per-warp masks s_wm (octahedron_warp_mask) replace the bbox test.
+// WM: the records' per-warp masks s_wm (octahedron_ / tetrahedron_warp_mask) replace the bbox test.
 template <int NT, int RW4, bool WM>
 __device__ __forceinline__ int warp_sublist(const float4 *s_rec, const unsigned char *s_wm, int cnt, float x0,
                                             float x1, float y0, float y1, unsigned char *list) {
@@ -189,7 +190,7 @@ __device__ __noinline__ void write_hit_word(uint32_t *hitmask, int64_t capacity,
 // either pointer may be null.
 //
 // 128 threads, 2 pixels per thread: pixel k = 0 / 1 of a thread are (x, y) and (x, y + 4), so they
-// share dx and the bbox x test, and their chords are ONE paired evaluation (chord2: FFMA2 / FADD2
+// share dx, and their chords are ONE paired evaluation (chord2: FFMA2 / FADD2
 // lanes, bitwise the scalar chord the backward replays).
 // EXACT: the no-ray-space variant (App. D, reading 27): per-pixel perspective rays
 // r = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1) against the record's camera-space planes.
@@ -206,7 +207,8 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
   __shared__ unsigned char s_list[NT / 32][NT];
   __shared__ unsigned char s_wm[NT];
   __shared__ unsigned long long s_stat[3];
-  // per-record warp masks (footprint strips) for the ray-space octahedron; the bbox test otherwise
+  // per-record warp masks (footprint strips) in ray space; the bbox test in the counting and the
+  // no-ray-space variants
   constexpr bool WM = !EXACT && !STATS && NT == 128;
 
   const int tile = blockIdx.x;
@@ -263,8 +265,8 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
     const int cnt = (int)min((uint32_t)NT, end - b);
     const int wrp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t hitw = 0u;                                 // lane L < NT/32: the warp's hit bits of records 32L..
-    // per-warp sub-list: the batch records whose bbox reaches the warp's pixels, in list order
-    // (each lane tests NT/32 records; convexity: outside the vertex bbox the chord is <= 0)
+    // per-warp sub-list: the batch records whose footprint (WM) or bbox reaches the warp's pixels, in
+    // list order (convexity: outside the footprint / vertex bbox the chord is <= 0)
     const int nl = warp_sublist<NT, RW4, WM>(s_rec, s_wm, cnt, wx0, wx1, wy0, wy1, s_list[wrp]);
     for (int q = 0; q < nl; ++q) {
       const int j = s_list[wrp][q];
