@@ -144,6 +144,16 @@ __device__ __forceinline__ unsigned tetrahedron_warp_mask(const float4 *r, int t
   return m;
 }
 
+// 16-byte global -> shared copies that bypass the registers (cp.async, L2 only): the backward
+// stages the next batch's records while it processes the current one
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // resident CTAs per SM the backward asks the register allocator for (LP_BWD_BLOCKS overrides at
 // build time): 6 x 128 threads allows 80 registers (measured on C5 with the shared-row moments:
 // 6 -> 0.613 ms, 7 (72 registers) -> 0.616, 8 (64) -> 0.616)
@@ -399,9 +409,9 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
   constexpr int RW = EXACT ? ER::W : KD::RW, RW4 = RW / 4, PPT = 256 / NT, RG = KD::RG, RS = KD::RS;
   constexpr int SIGMA = EXACT ? ER::SIGMA : KD::SIGMA, RGB = EXACT ? ER::RGB : KD::RGB;
   constexpr int RGP = RG == 20 ? 20 : 28;      // padded row: 16-byte stores, conflict-free (RGP/4 odd)
-  __shared__ float4 s_rec[NT * RW4];
+  __shared__ float4 s_rec2[2][NT * RW4];   // double-buffered batch records (cp.async)
   __shared__ __align__(16) float s_red[NT / 32][32][RGP];
-  __shared__ uint32_t s_id[NT];
+  __shared__ uint32_t s_id2[2][NT];
   __shared__ uint32_t s_last;
 
   const int tile = blockIdx.x;
@@ -446,18 +456,39 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
   const float2 ry2 = EXACT ? RY.ry2 : make_float2(0.f, 0.f);
   const float2 rn2 = EXACT ? RY.rn2 : make_float2(1.f, 1.f);
 
-  for (uint32_t bend = lmax; bend > start; bend = (bend - start > NT) ? bend - NT : start) {
-    const uint32_t bstart = (bend - start > NT) ? bend - NT : start;
-    __syncthreads();
-    const uint32_t e = bstart + threadIdx.x;
-    if (e < bend) {
-      const uint32_t v = F.sorted_val[e];
-      s_id[threadIdx.x] = v;
-      const float4 *src = reinterpret_cast<const float4 *>(F.record + (size_t)v * RS);
+  // batches walk the list backwards: batch [bstart(bend), bend), the next one ends at bstart
+  auto bstart_of = [&](uint32_t be) { return (be - start > NT) ? be - NT : start; };
+  // this thread's entry of the batch ending at `be` (its primitive id; false if none)
+  auto entry_of = [&](uint32_t be, uint32_t &v) {
+    if (be <= start) return false;
+    const uint32_t e = bstart_of(be) + threadIdx.x;
+    if (e >= be) return false;
+    v = F.sorted_val[e];
+    return true;
+  };
+  auto stage = [&](int bf, uint32_t v) {
+    s_id2[bf][threadIdx.x] = v;
+    const float4 *src = reinterpret_cast<const float4 *>(F.record + (size_t)v * RS);
 #pragma unroll
-      for (int w = 0; w < RW4; ++w) s_rec[threadIdx.x * RW4 + w] = __ldg(src + w);
-    }
-    __syncthreads();
+    for (int w = 0; w < RW4; ++w) cp_async16(&s_rec2[bf][threadIdx.x * RW4 + w], src + w);
+  };
+  // prologue: the first batch in flight, the second batch's primitive id loaded
+  uint32_t vcur = 0, vnext = 0;
+  if (entry_of(lmax, vcur)) stage(0, vcur);
+  cp_async_commit();
+  bool has_next = entry_of(bstart_of(lmax), vnext);
+  int buf = 0;
+  for (uint32_t bend = lmax; bend > start; bend = bstart_of(bend), buf ^= 1) {
+    const uint32_t bstart = bstart_of(bend);
+    cp_async_wait_all();
+    __syncthreads();   // this batch landed for every thread; every thread is done with the other buffer
+    // the next batch's records into the other buffer (their ids were loaded one batch ago), and
+    // the id of the batch after it
+    if (has_next) stage(buf ^ 1, vnext);
+    cp_async_commit();
+    has_next = bstart > start && entry_of(bstart_of(bstart), vnext);
+    const float4 *s_rec = s_rec2[buf];
+    const uint32_t *s_id = s_id2[buf];
     bool act = false;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) act = act || (last[k] > bstart);
