@@ -21,6 +21,7 @@
 namespace lp {
 
 constexpr int RADIX = 256;
+constexpr int RADIX_FUSE_BLOCKS = 64;   // up to this many scatter blocks the per-digit scan is fused in
 constexpr int WARPS = SORT_THREADS / 32;
 
 __device__ __forceinline__ int64_t item_count(const uint32_t *n_dev, int64_t n_host) {
@@ -93,6 +94,9 @@ __global__ void __launch_bounds__(1024) k_radix_scan(uint32_t *__restrict__ hist
   if (threadIdx.x == 0) tot[blockIdx.x] = carry;
 }
 
+// FUSED (few blocks): hist holds the raw per-block digit counts (no k_radix_scan launch); each
+// block sums its own prefix and the digit totals from them (<= RADIX_FUSE_BLOCKS loads per digit).
+template <bool FUSED>
 __global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(const uint32_t *__restrict__ keys_in,
                                                                 const uint32_t *__restrict__ vals_in,
                                                                 uint32_t *__restrict__ keys_out,
@@ -150,10 +154,23 @@ __global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(const uint32_t *
     const uint32_t ex = block_exclusive_scan(run, s_warp, total);
     s_local[d] = ex;
     // global start of digit d = (keys of smaller digits, all blocks) + (digit d, earlier blocks)
-    const uint32_t tsum = tot[d];
+    uint32_t tsum, pre;
+    if (FUSED) {
+      tsum = 0;
+      pre = 0;
+      const uint32_t *row = hist + (size_t)d * nblk;
+      for (int b2 = 0; b2 < nblk; ++b2) {
+        const uint32_t c = row[b2];
+        tsum += c;
+        pre += b2 < (int)blockIdx.x ? c : 0u;
+      }
+    } else {
+      tsum = tot[d];
+      pre = hist[(size_t)d * nblk + blockIdx.x];
+    }
     uint32_t gtotal;
     const uint32_t gex = block_exclusive_scan(tsum, s_warp, gtotal);
-    s_base[d] = gex + hist[(size_t)d * nblk + blockIdx.x];
+    s_base[d] = gex + pre;
   }
   __syncthreads();
 #pragma unroll
@@ -191,8 +208,12 @@ int radix_sort_pairs(uint32_t *keys, uint32_t *keys_alt, uint32_t *vals, uint32_
     uint32_t *ki = flip ? keys_alt : keys, *vi = flip ? vals_alt : vals;
     uint32_t *ko = flip ? keys : keys_alt, *vo = flip ? vals : vals_alt;
     k_radix_hist<<<nblk, SORT_THREADS, 0, st>>>(ki, n_dev, n_max, shift, hist, nblk);
-    k_radix_scan<<<RADIX, 1024, 0, st>>>(hist, nblk, tot);
-    k_radix_scatter<<<nblk, SORT_THREADS, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, hist, tot, nblk);
+    if (nblk <= RADIX_FUSE_BLOCKS) {   // small sorts: two launches per pass instead of three
+      k_radix_scatter<true><<<nblk, SORT_THREADS, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, hist, tot, nblk);
+    } else {
+      k_radix_scan<<<RADIX, 1024, 0, st>>>(hist, nblk, tot);
+      k_radix_scatter<false><<<nblk, SORT_THREADS, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, hist, tot, nblk);
+    }
     flip ^= 1;
   }
   return flip;
