@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--exact", action="store_true",
                     help="the paper's no-ray-space variant (App. D) instead of the EWA ray-space method")
     ap.add_argument("--streams", type=int, default=4, help="CUDA streams the views of a step are spread over")
+    ap.add_argument("--assign", action=argparse.BooleanOptionalAction, default=True,
+                    help="preprocess backward SETS the step's gradient (lp_preprocess_bwd_assign) instead of "
+                         "accumulating into a zeroed one")
     ap.add_argument("--split-pre", action=argparse.BooleanOptionalAction, default=True,
                     help="preprocess the first --streams views in their own launch so their binning overlaps "
                          "the preprocess of the others")
@@ -288,12 +291,15 @@ def run_ours(args, rank, world, local_rank):
                 joins[j].record(s_)
                 st.wait_event(joins[j])
         # preprocess backward fused over this rank's views (feature + SH gradients written once)
-        L.lp_preprocess_bwd(ds.prims, ca_all, rend.cfg, fa_all, ds.grads, st)
+        # (assign: the step's gradient is SET here, so nothing zeroes it after the optimizer)
+        (L.lp_preprocess_bwd_assign if args.assign else L.lp_preprocess_bwd)(ds.prims, ca_all, rend.cfg, fa_all,
+                                                                             ds.grads, st)
         rec(S, 2, st)
         if world > 1 or zero:
             if zero:
                 train.reduce_scatter_gradients(ds.grad_padded, gshard, world)
-                ds.grad_padded.zero_()
+                if not args.assign:
+                    ds.grad_padded.zero_()
             else:
                 train.allreduce_gradients(ds.grad, world)
         rec(S, 3, st)
@@ -302,7 +308,7 @@ def run_ours(args, rank, world, local_rank):
                            si + 1, st, zero_grad=False)
             train.all_gather_params(ds.flat_padded, rank, chunk)
         else:
-            L.lp_adam_step(ds.flat, ds.grad, m, v, groups, 0.9, 0.999, 1e-15, si + 1, st, zero_grad=True)
+            L.lp_adam_step(ds.flat, ds.grad, m, v, groups, 0.9, 0.999, 1e-15, si + 1, st, zero_grad=not args.assign)
         rec(S, 4, st)
 
     def barrier():

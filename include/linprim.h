@@ -207,6 +207,14 @@ lp_status lp_raster_bwd(const lp_camera *cams, int32_t n_views, const lp_raster_
 lp_status lp_preprocess_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_views,
                             const lp_raster_cfg *cfg, lp_frame *frames, const lp_grads *grads, void *stream);
 
+/* lp_preprocess_bwd with ASSIGN semantics for the feature gradients: grads.pos/rot/dist/opacity/sh
+ * are SET to the sum over these n_views (every primitive written, zero where no view has a raster
+ * gradient; the old contents are never read), so a training step that starts with this call needs no
+ * gradient zeroing (lp_adam_step with zero_grad = 0).  grads.mean2d_abs / vis_count still accumulate.
+ * Same arguments, layout and errors as lp_preprocess_bwd. */
+lp_status lp_preprocess_bwd_assign(const lp_prims *prims, const lp_camera *cams, int32_t n_views,
+                                   const lp_raster_cfg *cfg, lp_frame *frames, const lp_grads *grads, void *stream);
+
 /* Copy the frame's counters to host (synchronises the stream). */
 lp_status lp_frame_counters(const lp_frame *frame, uint32_t *host_counters /* [LP_NUM_COUNTERS] words */,
                             void *stream);

@@ -284,7 +284,7 @@ lp_status lp_render_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_
     launch_raster_bwd(frames[v], cams[v], *cfg, dL_dimage + off, st);
     off += (size_t)3 * cams[v].width * cams[v].height;
   }
-  launch_preprocess_bwd(*prims, cams, cfg->aa_kernel, frames, n_views, *grads, cfg->exact != 0, st);
+  launch_preprocess_bwd(*prims, cams, cfg->aa_kernel, frames, n_views, *grads, cfg->exact != 0, false, st);
   return last_error();
 }
 
@@ -303,16 +303,26 @@ lp_status lp_raster_bwd(const lp_camera *cams, int32_t n_views, const lp_raster_
   return last_error();
 }
 
-lp_status lp_preprocess_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg,
-                            lp_frame *frames, const lp_grads *grads, void *stream) {
+static lp_status preprocess_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg,
+                                lp_frame *frames, const lp_grads *grads, bool assign, void *stream) {
   if (check_prims(prims) != LP_OK || !cams || !cfg || !frames || !grads || n_views < 0) return LP_ERR_ARG;
   for (int v = 0; v < n_views; ++v) {
     if (!valid_cam(cams[v]) || !frame_matches(frames[v], cams[v]) || !frames[v].sorted_val) return LP_ERR_ARG;
     if (frames[v].kind != prims->kind || frames[v].n != prims->n) return LP_ERR_ARG;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  launch_preprocess_bwd(*prims, cams, cfg->aa_kernel, frames, n_views, *grads, cfg->exact != 0, st);
+  launch_preprocess_bwd(*prims, cams, cfg->aa_kernel, frames, n_views, *grads, cfg->exact != 0, assign, st);
   return last_error();
+}
+
+lp_status lp_preprocess_bwd(const lp_prims *prims, const lp_camera *cams, int32_t n_views, const lp_raster_cfg *cfg,
+                            lp_frame *frames, const lp_grads *grads, void *stream) {
+  return preprocess_bwd(prims, cams, n_views, cfg, frames, grads, false, stream);
+}
+
+lp_status lp_preprocess_bwd_assign(const lp_prims *prims, const lp_camera *cams, int32_t n_views,
+                                   const lp_raster_cfg *cfg, lp_frame *frames, const lp_grads *grads, void *stream) {
+  return preprocess_bwd(prims, cams, n_views, cfg, frames, grads, true, stream);
 }
 
 lp_status lp_frame_counters(const lp_frame *F, uint32_t *host, void *stream) {

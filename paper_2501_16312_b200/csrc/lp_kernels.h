@@ -17,7 +17,7 @@ void launch_preprocess(const lp_prims &P, const lp_camera *cams, float kappa, co
                        bool exact, cudaStream_t st);
 // fused over the views of one call (chunks of 8): feature / SH gradients written once per chunk
 void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
-                           const lp_grads &G, bool exact, cudaStream_t st);
+                           const lp_grads &G, bool exact, bool assign, cudaStream_t st);
 
 // K2 (lp_sort.cu)
 constexpr int SORT_THREADS = 256;

@@ -669,8 +669,12 @@ struct ItemRes {
 // read-modify-writes every feature gradient once.  No shared-memory float atomics (sm_100 has
 // none: they compile to CAS loops).
 template <int KIND, int DEG, bool EXACT>
+// assign: the feature gradients are SET (=) instead of accumulated (+=): every primitive's gradient
+// is written (zeros where no view has a raster gradient), no old gradient is read -- the first pack
+// of a step whose optimizer consumed (and need not zero) the previous step's gradients.  The
+// densification statistics (mean2d_abs, vis_count) accumulate either way.
 __global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, float kappa, ViewPack V, int rg_words,
-                                                       lp_grads Gs) {
+                                                       lp_grads Gs, bool assign) {
   constexpr int WARPS = 2, K = Kind<KIND>::K, NC = (DEG + 1) * (DEG + 1);
   __shared__ lp_camera s_cam[LP_MAXV];
   __shared__ const float *s_rg[LP_MAXV];
@@ -716,7 +720,7 @@ __global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, f
     if (lane >= o) incl += y;
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
-  if (total == 0) return;
+  if (total == 0 && !assign) return;   // (assign: the warp's gradients are still written, as zeros)
   const int first = incl - c;   // this lane's items are [first, first + c)
   {
     int slot = first;
@@ -755,23 +759,42 @@ __global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, f
     }
   }
   __syncwarp();
-  if (!vm) return;
+  if (!vm) {
+    if (assign && i < n) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (Gs.pos) Gs.pos[(size_t)a * n + i] = 0.f;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (Gs.rot) Gs.rot[(size_t)a * n + i] = 0.f;
+#pragma unroll
+      for (int a = 0; a < K; ++a)
+        if (Gs.dist) Gs.dist[(size_t)a * n + i] = 0.f;
+      if (Gs.opacity) Gs.opacity[i] = 0.f;
+      if (Gs.sh) {
+#pragma unroll
+        for (int q = 0; q < 3 * NC; ++q) Gs.sh[(size_t)q * n + i] = 0.f;
+      }
+    }
+    return;
+  }
   // ---- phase B: owner lane sums its items and writes its primitive's gradients once
   // the old values of the non-SH feature gradients, loaded up front (independent round trips; the
   // compiler cannot move these loads past the stores below, which may alias)
   float acc[ItemRes::M2D + 1];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) acc[ItemRes::POS + a] = Gs.pos ? Gs.pos[(size_t)a * n + i] : 0.f;
+  for (int a = 0; a < 3; ++a) acc[ItemRes::POS + a] = (Gs.pos && !assign) ? Gs.pos[(size_t)a * n + i] : 0.f;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) acc[ItemRes::ROT + a] = Gs.rot ? Gs.rot[(size_t)a * n + i] : 0.f;
+  for (int a = 0; a < 4; ++a) acc[ItemRes::ROT + a] = (Gs.rot && !assign) ? Gs.rot[(size_t)a * n + i] : 0.f;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) acc[ItemRes::DIST + a] = (Gs.dist && a < K) ? Gs.dist[(size_t)a * n + i] : 0.f;
-  acc[ItemRes::OP] = Gs.opacity ? Gs.opacity[i] : 0.f;
+  for (int a = 0; a < 4; ++a)
+    acc[ItemRes::DIST + a] = (Gs.dist && a < K && !assign) ? Gs.dist[(size_t)a * n + i] : 0.f;
+  acc[ItemRes::OP] = (Gs.opacity && !assign) ? Gs.opacity[i] : 0.f;
   acc[ItemRes::M2D] = Gs.mean2d_abs ? Gs.mean2d_abs[i] : 0.f;
   float sum[ItemRes::M2D + 1];
 #pragma unroll
   for (int a = 0; a <= ItemRes::M2D; ++a) sum[a] = 0.f;
-  if (Gs.sh) {   // the SH gradient rows of the warp's primitives: on their way to L1 during the sums
+  if (Gs.sh && !assign) {   // the SH gradient rows of the warp's primitives: on their way to L1 during the sums
 #pragma unroll
     for (int q = 0; q < 3 * NC; ++q) asm volatile("prefetch.global.L1 [%0];" ::"l"(Gs.sh + (size_t)q * n + i));
   }
@@ -811,7 +834,7 @@ __global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, f
     // all loads first, then the stores (the compiler cannot reorder loads past stores that may alias)
     float old[3 * NC];
 #pragma unroll
-    for (int q = 0; q < 3 * NC; ++q) old[q] = Gs.sh[(size_t)q * n + i];
+    for (int q = 0; q < 3 * NC; ++q) old[q] = assign ? 0.f : Gs.sh[(size_t)q * n + i];
 #pragma unroll
     for (int k = 0; k < NC; ++k)
 #pragma unroll
@@ -853,18 +876,19 @@ void launch_preprocess(const lp_prims &P, const lp_camera *cams, float kappa, co
 }
 
 template <int KIND, bool EXACT>
-static void bwd_deg(const lp_prims &P, float kappa, const ViewPack &V, int rg, const lp_grads &G, cudaStream_t st) {
+static void bwd_deg(const lp_prims &P, float kappa, const ViewPack &V, int rg, const lp_grads &G, bool assign,
+                    cudaStream_t st) {
   const int grid = (P.n + 63) / 64;
   switch (P.sh_degree) {
-    case 0: k_preprocess_bwd<KIND, 0, EXACT><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
-    case 1: k_preprocess_bwd<KIND, 1, EXACT><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
-    case 2: k_preprocess_bwd<KIND, 2, EXACT><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
-    default: k_preprocess_bwd<KIND, 3, EXACT><<<grid, 64, 0, st>>>(P, kappa, V, rg, G); break;
+    case 0: k_preprocess_bwd<KIND, 0, EXACT><<<grid, 64, 0, st>>>(P, kappa, V, rg, G, assign); break;
+    case 1: k_preprocess_bwd<KIND, 1, EXACT><<<grid, 64, 0, st>>>(P, kappa, V, rg, G, assign); break;
+    case 2: k_preprocess_bwd<KIND, 2, EXACT><<<grid, 64, 0, st>>>(P, kappa, V, rg, G, assign); break;
+    default: k_preprocess_bwd<KIND, 3, EXACT><<<grid, 64, 0, st>>>(P, kappa, V, rg, G, assign); break;
   }
 }
 
 void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
-                           const lp_grads &G, bool exact, cudaStream_t st) {
+                           const lp_grads &G, bool exact, bool assign, cudaStream_t st) {
   if (P.n == 0 || n_views <= 0) return;
   for (int v0 = 0; v0 < n_views; v0 += LP_MAXV) {
     ViewPack V;
@@ -878,11 +902,11 @@ void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa
     }
     const int rg = frames[v0].rgrad_words;
     if (P.kind == LP_OCTAHEDRON) {
-      if (exact) bwd_deg<LP_OCTAHEDRON, true>(P, kappa, V, rg, G, st);
-      else bwd_deg<LP_OCTAHEDRON, false>(P, kappa, V, rg, G, st);
+      if (exact) bwd_deg<LP_OCTAHEDRON, true>(P, kappa, V, rg, G, assign && v0 == 0, st);
+      else bwd_deg<LP_OCTAHEDRON, false>(P, kappa, V, rg, G, assign && v0 == 0, st);
     } else {
-      if (exact) bwd_deg<LP_TETRAHEDRON, true>(P, kappa, V, rg, G, st);
-      else bwd_deg<LP_TETRAHEDRON, false>(P, kappa, V, rg, G, st);
+      if (exact) bwd_deg<LP_TETRAHEDRON, true>(P, kappa, V, rg, G, assign && v0 == 0, st);
+      else bwd_deg<LP_TETRAHEDRON, false>(P, kappa, V, rg, G, assign && v0 == 0, st);
     }
   }
 }

@@ -83,6 +83,8 @@ _sig = {
                                 _p, _p]),
     "lp_preprocess_bwd": (C.c_int, [C.POINTER(lp_prims), C.POINTER(lp_camera), C.c_int32,
                                     C.POINTER(lp_raster_cfg), C.POINTER(lp_frame), C.POINTER(lp_grads), _p]),
+    "lp_preprocess_bwd_assign": (C.c_int, [C.POINTER(lp_prims), C.POINTER(lp_camera), C.c_int32,
+                                    C.POINTER(lp_raster_cfg), C.POINTER(lp_frame), C.POINTER(lp_grads), _p]),
     "lp_frame_counters": (C.c_int, [C.POINTER(lp_frame), C.POINTER(C.c_uint32), _p]),
     "lp_l1_grad": (C.c_int, [_p, _p, _p, _p, C.c_int64, C.c_float, _p]),
     "lp_filter3d": (C.c_int, [_p, C.c_int32, _p, C.c_int32, C.c_float, _p, _p]),
@@ -173,6 +175,11 @@ def lp_raster_bwd(cams, cfg, frames, dL_dimage, stream):
 def lp_preprocess_bwd(prims, cams, cfg, frames, grads, stream):
     return _check(_lib.lp_preprocess_bwd(C.byref(prims), cams, len(cams), C.byref(cfg), frames, C.byref(grads),
                                          _stream(stream)), "lp_preprocess_bwd")
+
+
+def lp_preprocess_bwd_assign(prims, cams, cfg, frames, grads, stream):
+    return _check(_lib.lp_preprocess_bwd_assign(C.byref(prims), cams, len(cams), C.byref(cfg), frames, C.byref(grads),
+                                         _stream(stream)), "lp_preprocess_bwd_assign")
 
 
 def lp_frame_counters(frame, stream) -> np.ndarray:

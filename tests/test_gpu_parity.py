@@ -171,6 +171,39 @@ def test_multi_view_call_and_accumulation():
     assert ok, rep
 
 
+@pytest.mark.parametrize("n_views", [1, 6])
+def test_preprocess_bwd_assign_equals_zeroed_accumulate(n_views):
+    """lp_preprocess_bwd_assign (every primitive's feature gradient SET, the old contents never read;
+    6 views = two view packs: the second one accumulates) gives bit for bit what lp_preprocess_bwd
+    gives on a zeroed gradient, from the same raster moments; densification statistics accumulate."""
+    import torch
+    from paper_2501_16312_b200 import linprim as L
+    from paper_2501_16312_b200 import render
+    scene, cams = scenegen.make_scene("C5", seed=1, n=4000)
+    cams = [dict(c, width=80, height=64, cx=np.float32(40), cy=np.float32(32),
+                 fx=np.float32(69.3), fy=np.float32(69.3)) for c in cams[:n_views]]
+    ds = render.DeviceScene(scene)
+    ds.track_mean2d()
+    r = render.Renderer(ds, cams)
+    img = r.forward()
+    G = torch.from_numpy(scenegen.upstream_grad(80, 64, seed=2, n_views=n_views)).cuda().contiguous()
+    st = torch.cuda.current_stream()
+    fa = render.frames_array(r.frames)
+    ca = r._cams(list(range(n_views)))
+    L.lp_raster_bwd(ca, r.cfg, fa, G, st)
+    ds.grad.zero_()
+    L.lp_preprocess_bwd(ds.prims, ca, r.cfg, fa, ds.grads, st)
+    ref = ds.grad.clone()
+    m2d_ref = ds.mean2d.clone()
+    ds.grad.fill_(7.0)                      # stale garbage: must be overwritten, never read
+    L.lp_preprocess_bwd_assign(ds.prims, ca, r.cfg, fa, ds.grads, st)
+    torch.cuda.synchronize()
+    assert torch.equal(ds.grad, ref)
+    # the statistics accumulated over both calls (equal up to the summation order of the packs)
+    assert torch.allclose(ds.mean2d, 2 * m2d_ref, rtol=1e-6, atol=0)
+    assert img.shape[0] == n_views and float(ref.abs().sum()) > 0
+
+
 def test_capacity_error_and_async_overflow_flag():
     import ctypes as C
 
