@@ -84,7 +84,7 @@ typedef struct {
   int32_t kind, n, width, height, tiles_x, tiles_y;
   int64_t capacity;           /* maximum tile-list entries */
   int32_t record_words;       /* record stride in floats (24 octa, 28 tetra) */
-  int32_t rgrad_words;        /* rgrad row stride in floats (24: dsigma, drgb, 16 octa / 18 tetra moments, pad) */
+  int32_t rgrad_words;        /* rgrad row stride in floats (20 octa: dsigma, drgb, 16 moments; 24 tetra: 18 moments + pad) */
   uint32_t *tiles_touched;    /* [n] */
   uint16_t *rect;             /* [n][4] tile rect tx0, ty0, tx1, ty1 (inclusive), zeros if none */
   uint32_t *depth_key;        /* [n] float bits of l = |p| (0 if culled / invalid) */

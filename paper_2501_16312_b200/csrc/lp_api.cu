@@ -17,7 +17,9 @@ inline size_t up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 // record stride (words): room for both the ray-space and the exact-mode record
 inline int record_words(int kind) { return kind == LP_OCTAHEDRON ? Kind<LP_OCTAHEDRON>::RS : Kind<LP_TETRAHEDRON>::RS; }
-inline int rgrad_words(int) { return LP_RGS; }   // row stride of the [n][LP_RGS] scratch
+inline int rgrad_words(int kind) {   // row stride of the [n][rgrad_words] scratch
+  return kind == LP_OCTAHEDRON ? lp_rgs<LP_OCTAHEDRON>() : lp_rgs<LP_TETRAHEDRON>();
+}
 inline int offsets_k(int kind) { return kind == LP_OCTAHEDRON ? 3 : 4; }
 
 struct Layout {

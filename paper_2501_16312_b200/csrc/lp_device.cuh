@@ -28,11 +28,11 @@ template <int KIND> struct Kind;
 // ~6 instructions before the slab / plane evaluation.
 //   octahedron (20 words): bx=cx by=cy hx hy | (b g h) x 4 slabs | sigma r g b
 //   tetrahedron (28 words): bx by hx hy | cx cy | (A B C) x 6 slots | sigma r g b
-// raster-gradient scratch row stride (floats): rgrad is [n][LP_RGS], one row per primitive laid out
+// raster-gradient scratch row stride (floats): rgrad is [n][lp_rgs], one row per primitive laid out
 // as the backward's shared-memory row: dsigma, drgb (3), then the RG - 4 plane moments, then padding.
 // A (warp, primitive) reduction's <= 22 RED.F32 then land in 3 consecutive 32-byte sectors
 // instead of one sector per moment.
-constexpr int LP_RGS = 24;
+template <int KIND> __host__ __device__ constexpr int lp_rgs() { return KIND == LP_OCTAHEDRON ? 20 : 24; }   // 80 B / 96 B rows
 template <> struct Kind<LP_OCTAHEDRON> {
   static constexpr int K = 3;          // offset vectors (vertices are c +- o_j)
   static constexpr int RW = 20;        // record words (ray space)

@@ -297,7 +297,7 @@ __device__ __forceinline__ void view_feature_grad(const lp_prims &P, const lp_ca
   // the primitive's rgrad row (dsigma, drgb | moments) -> m[moments..., dsigma, drgb]
   float m[RG];
   {
-    const float4 *row = reinterpret_cast<const float4 *>(rgrad + (size_t)i * LP_RGS);
+    const float4 *row = reinterpret_cast<const float4 *>(rgrad + (size_t)i * lp_rgs<KIND>());
     float t[4 * ((RG + 3) / 4)];
 #pragma unroll
     for (int q = 0; q < (RG + 3) / 4; ++q) {
@@ -624,7 +624,7 @@ __device__ __forceinline__ void sh_view_inputs(const lp_prims &P, const lp_camer
   const int n = P.n;
   const float c[3] = {P.pos[i], P.pos[n + i], P.pos[2 * n + i]};
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) gr[ch] = rgrad[(size_t)i * LP_RGS + 1 + ch];   // row: dsigma, drgb | moments
+  for (int ch = 0; ch < 3; ++ch) gr[ch] = rgrad[(size_t)i * rg_words + 1 + ch];   // row: dsigma, drgb | moments
   // the forward's clamp decision, stored by K1 as the colour's sign bit (-0.0: clamped)
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch)
@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, f
     for (int v = 0; v < LP_MAXV; ++v) {
       probe[v] = 0.f;
       if (v < V.nv) {
-        const float4 rg = *reinterpret_cast<const float4 *>(V.rgrad[v] + (size_t)i * LP_RGS);   // dsigma, drgb
+        const float4 rg = *reinterpret_cast<const float4 *>(V.rgrad[v] + (size_t)i * lp_rgs<KIND>());   // dsigma, drgb
         probe[v] = fabsf(rg.x) + fabsf(rg.y) + fabsf(rg.z) + fabsf(rg.w);
       }
     }

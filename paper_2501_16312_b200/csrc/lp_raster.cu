@@ -12,7 +12,7 @@
 // runs the blend backward and the chord backward (App. E, in slab/plane
 // moment form) into its lane's compacted shared-memory row (<= 22 moments; one 16-byte
 // read-modify-write per entry / exit plane), then a column sum over the hit lanes and one
-// RED.F32 per moment per (warp, primitive) into the primitive's rgrad row rgrad[n][LP_RGS].
+// RED.F32 per moment per (warp, primitive) into the primitive's rgrad row rgrad[n][lp_rgs].
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -691,8 +691,8 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
         if (q + 2 < h) s2 += col[(q + 2) * RGP];
         const float sum = (s0 + s1) + (s2 + s3);
         // the shared row's layout is the rgrad row's (dsigma, drgb | moments): the h-row column sums
-        // land in one primitive's 96-byte row (3 sectors per RED instruction)
-        if (sum != 0.f) atomicAdd(F.rgrad + (size_t)id * LP_RGS + lane, sum);
+        // land in one primitive's 80 / 96-byte row (3 sectors per RED instruction)
+        if (sum != 0.f) atomicAdd(F.rgrad + (size_t)id * lp_rgs<KIND>() + lane, sum);
       }
       __syncwarp();
     }
