@@ -172,8 +172,7 @@ lp_status lp_preprocess(const lp_prims *prims, const lp_camera *cams, int32_t n_
     lp_frame &F = frames[v];
     F.sorted_tile = F.sorted_val = nullptr;
     cudaMemsetAsync(F.counters, 0, 4 * LP_NUM_COUNTERS, st);
-    // the backward's raster-moment scratch is consumed once per preprocess
-    cudaMemsetAsync(F.rgrad, 0, 4 * (size_t)F.rgrad_words * (F.n > 0 ? F.n : 1), st);
+    // (the backward's raster-moment scratch rows are zeroed by k_preprocess itself)
     if (F.sort_method == LP_SORT_BUCKET)
       cudaMemsetAsync(F.tile_diff, 0, 4 * (size_t)(F.tiles_x + 1) * (F.tiles_y + 1), st);
   }

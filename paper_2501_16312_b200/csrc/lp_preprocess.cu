@@ -145,6 +145,13 @@ __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_came
   warp_count(F.counters + LP_CNT_FRUSTUM, inb && g.flag == 0);
   warp_count(F.counters + LP_CNT_VISIBLE, inb && g.tiles > 0);
   if (!inb) return;
+  {
+    // the backward's raster-moment row of this (primitive, view) starts at zero (instead of a
+    // separate memset of the whole scratch per view)
+    float4 *row = reinterpret_cast<float4 *>(F.rgrad + (size_t)i * lp_rgs<KIND>());
+#pragma unroll
+    for (int q = 0; q < lp_rgs<KIND>() / 4; ++q) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 
   const bool ok = g.flag == 0;
   F.tiles_touched[i] = g.tiles;
