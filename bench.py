@@ -405,7 +405,8 @@ def run_ours(args, rank, world, local_rank):
         # gradients read-modified-written once per call
         "pbwd_all_views": ("k_preprocess_bwd", "hbm", 4 * n * n_local + vis * n_local * 4 * RG + n * 3 * Fb),
         "pre_all_views": ("k_preprocess", "hbm", n * Fb + n_local * (n * 24 + vis * 4 * RW)),
-        "adam": ("k_adam", "hbm", 32 * (chunk if zero else ds.flat.numel())),
+        # read p, g, m, v; write p, m, v (and g = 0 without --assign)
+        "adam": ("k_adam", "hbm", (28 if args.assign else 32) * (chunk if zero else ds.flat.numel())),
         # separable 11-tap window: 5 products x 2 directions x 11 + 3 G maps x 2 x 11 FMA + ~30 for
         # S and the G maps per pixel-channel; L1 only: 12 B per pixel-channel
         "loss": ("k_loss_ssim_tma", "alu", 206 * 3 * W * H) if args.loss == "l1ssim" else ("k_l1_grad", "hbm", 12 * 3 * W * H),
