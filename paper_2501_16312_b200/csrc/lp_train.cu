@@ -160,6 +160,10 @@ __global__ void __launch_bounds__(256) k_adam(float *__restrict__ p, float *__re
   }
 }
 
+// grid cap of the Adam kernel: blocks per SM and group (-DLP_ADAM_BPSM overrides)
+#ifndef LP_ADAM_BPSM
+#define LP_ADAM_BPSM 8
+#endif
 void launch_adam(float *p, float *g, float *m, float *v, const lp_adam_group *groups, int ng, float b1, float b2,
                  float eps, int step, bool zero_grad, cudaStream_t st) {
   for (int base = 0; base < ng; base += 8) {
@@ -175,7 +179,7 @@ void launch_adam(float *p, float *g, float *m, float *v, const lp_adam_group *gr
     for (int k = G.n; k < 8; ++k) { G.begin[k] = G.end[k] = 0; G.lr[k] = 0.f; }
     const float bc1 = 1.f - powf(b1, (float)step), bc2 = 1.f - powf(b2, (float)step);
     const int64_t want = (longest / 4 + 255) / 256 + 1;
-    const int gx = (int)(want < 148 * 8 ? want : 148 * 8);
+    const int gx = (int)(want < 148 * LP_ADAM_BPSM ? want : 148 * LP_ADAM_BPSM);
     k_adam<<<dim3(gx, G.n), 256, 0, st>>>(p, g, m, v, G, b1, b2, eps, bc1, bc2, zero_grad);
   }
 }
