@@ -10,7 +10,8 @@ launching stream, L2 flushed (a 2 x L2 write) before every iteration, median ove
 Prints one JSON line per config (Mpixel/s, FPS, per-call ms, the tile-list / pair counters, the
 raster kernels' ALU-model fraction as in bench.py) and with --out appends them to a file.
 
-  python tools/configs_bench.py [C1 C2 C3 C4] [--iters 20] [--warmup 5] [--exact] [--out FILE]
+  python tools/configs_bench.py [C1 C2 C3 C4] [--iters 20] [--warmup 5] [--exact] [--size-mult 0.5 1 2]
+                                [--out FILE]
 """
 from __future__ import annotations
 
@@ -33,9 +34,9 @@ from paper_2501_16312_b200 import render, scenegen  # noqa: E402
 RENDER_ONLY = {"C4"}        # BASELINE configs[3]: "render-only FPS"
 
 
-def run(name, iters, warmup, exact):
+def run(name, iters, warmup, exact, size_mult=1.0):
     dev = torch.device("cuda", 0)
-    scene, cams = scenegen.make_scene(name, seed=0)
+    scene, cams = scenegen.make_scene(name, seed=0, size_scale=scenegen.DEFAULT_SIZE_SCALE * size_mult)
     cam = cams[0]
     W, H = cam["width"], cam["height"]
     ds = render.DeviceScene(scene, device=dev)
@@ -98,7 +99,7 @@ def run(name, iters, warmup, exact):
     fwd_ms = statistics.median(e[0].elapsed_time(e[3]) for e in evs)
     out = {"workload": name, "kind": "octahedron" if ds.kind == 0 else "tetrahedron", "n_primitives": ds.n,
            "sh_degree": ds.sh_degree, "width": W, "height": H,
-           "projection": "no ray space (App. D)" if exact else "EWA ray space",
+           "projection": "no ray space (App. D)" if exact else "EWA ray space", "size_mult": size_mult,
            "l2": "flushed (2 x L2 write) before every iteration", "iters": iters, "warmup": warmup,
            "fwd_ms": round(fwd_ms, 4), "fwd_mpix_s": round(W * H / (fwd_ms * 1e-3) / 1e6, 2),
            "render_fps": round(1000.0 / fwd_ms, 1)}
@@ -126,16 +127,19 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--size-mult", type=float, nargs="*", default=[1.0],
+                    help="primitive size scale multipliers (SURVEY §8d sensitivity sweep: 0.5 1 2)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     for name in a.configs:
-        r = run(name, a.iters, a.warmup, a.exact)
-        line = json.dumps(r)
-        print(line, flush=True)
-        if a.out:
-            with open(a.out, "a") as f:
-                f.write(line + "\n")
-        torch.cuda.empty_cache()
+        for sm in a.size_mult:
+            r = run(name, a.iters, a.warmup, a.exact, sm)
+            line = json.dumps(r)
+            print(line, flush=True)
+            if a.out:
+                with open(a.out, "a") as f:
+                    f.write(line + "\n")
+            torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":
