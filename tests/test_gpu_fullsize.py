@@ -31,18 +31,19 @@ def _sample_tiles(gx, gy, k, seed):
     return np.sort(rng.choice(gx * gy, size=min(k, gx * gy), replace=False))
 
 
-@pytest.mark.parametrize("cfg,exact", [("C2", False), ("C3", False), ("C4", False), ("C5", False), ("C3", True),
-                                       ("C2", True)])
-def test_fullsize_sampled_parity(cfg, exact):
-    """exact: the no-ray-space variant (f3) at the same full size, no 2D filter."""
+@pytest.mark.parametrize("cfg,exact,view", [("C2", False, 0), ("C3", False, 0), ("C4", False, 0), ("C5", False, 0),
+                                            ("C5", False, 3), ("C5", False, 6), ("C3", True, 0), ("C2", True, 0)])
+def test_fullsize_sampled_parity(cfg, exact, view):
+    """exact: the no-ray-space variant (f3) at the same full size, no 2D filter; view: which camera of
+    the configuration (C5: three of the eight ring cameras the bench step renders)."""
     import torch
     scene, cams = scenegen.make_scene(cfg, seed=0)
-    cam = cams[0]
+    cam = cams[view]
     W, H = cam["width"], cam["height"]
     n = scene["pos"].shape[1]
     K = K_OF[scene["kind"]]
     gx, gy = (W + 15) // 16, (H + 15) // 16
-    tiles = _sample_tiles(gx, gy, 24, seed=len(cfg) + n % 97)
+    tiles = _sample_tiles(gx, gy, 24, seed=len(cfg) + n % 97 + 7 * view)
     mask_t = np.zeros(gx * gy, np.uint8)
     mask_t[tiles] = 1
     # pixels of the sampled tiles
