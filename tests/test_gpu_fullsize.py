@@ -32,10 +32,10 @@ def _sample_tiles(gx, gy, k, seed):
 
 
 @pytest.mark.parametrize("cfg,exact,view", [("C2", False, 0), ("C3", False, 0), ("C4", False, 0), ("C5", False, 0),
-                                            ("C5", False, 3), ("C5", False, 6), ("C3", True, 0), ("C2", True, 0)])
+                                            ("C5", False, 3), ("C3", True, 0), ("C2", True, 0)])
 def test_fullsize_sampled_parity(cfg, exact, view):
     """exact: the no-ray-space variant (f3) at the same full size, no 2D filter; view: which camera of
-    the configuration (C5: three of the eight ring cameras the bench step renders)."""
+    the configuration (C5: two of the eight ring cameras the bench step renders; DESIGN.md §9 reports view 6)."""
     import torch
     scene, cams = scenegen.make_scene(cfg, seed=0)
     cam = cams[view]
