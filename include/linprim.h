@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 3
+#define LP_ABI_VERSION 4
 #define LP_TILE 16            /* 16 x 16 pixel tiles */
 
 typedef enum {
@@ -68,7 +68,9 @@ typedef struct {
 
 typedef struct {
   float aa_kernel;            /* 2D anti-aliasing filter kernel kappa in pixels (0.1), 0 disables */
-  float t_stop;               /* stop once transmittance T < t_stop (1e-3), 0 disables */
+  float t_stop;               /* stop once transmittance T < t_stop (1e-3); values below 2^-100 (0
+                                 included) act as 2^-100, where no fp32 image changes any more (DESIGN.md
+                                 reading 28) */
   float bg[3];                /* background colour (reading 14) */
   int32_t count_stats;        /* 1: count iterated / intersected pairs into the frame counters */
   int32_t exact;              /* 0: EWA ray space (the method); 1: the "no ray space" variant
@@ -111,6 +113,11 @@ typedef struct {
   uint32_t *hitmask;          /* [4][capacity/32 + 2] per warp of a tile, one bit per tile-list entry: the forward
                                  sets it when the entry intersected one of the warp's pixels; the backward
                                  replays only those entries */
+  float    *T_last;           /* [H][W] T in front of the entry that stopped the pixel (= T_final if it never
+                                 stopped): the backward's first recovered T, never divided by a tiny E */
+  float    *T_ckpt;           /* [tiles + capacity/128 + 2][128][2] the pixels' T in front of every 128-entry
+                                 batch of their tile list after the first (forward); the backward restarts its
+                                 T = T_after / E recovery from these, so no division chain spans two batches */
 } lp_frame;
 
 /* lp_bin_sort methods; both produce the identical (tile, depth, id) order. */

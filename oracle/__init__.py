@@ -66,7 +66,7 @@ class _Camera(C.Structure):
 class _Pre(C.Structure):
     _fields_ = [("flag", C.c_void_p), ("tiles_touched", C.c_void_p), ("rect", C.c_void_p),
                 ("depth_key", C.c_void_p), ("geom", C.c_void_p), ("canon", C.c_void_p),
-                ("sigma", C.c_void_p), ("sigma_den", C.c_void_p), ("rgb", C.c_void_p)]
+                ("sigma", C.c_void_p), ("sigma_den", C.c_void_p), ("rgb", C.c_void_p), ("rgb_raw", C.c_void_p)]
 
 
 class _RenderCfg(C.Structure):
@@ -126,10 +126,12 @@ class Pre:
     sigma: np.ndarray
     sigma_den: np.ndarray
     rgb: np.ndarray
+    rgb_raw: np.ndarray = None     # SH colour before the clamp (clamp-decision margins in the parity tests)
 
     def c(self):
         p = _Pre()
-        for f in ("flag", "tiles_touched", "rect", "depth_key", "geom", "canon", "sigma", "sigma_den", "rgb"):
+        for f in ("flag", "tiles_touched", "rect", "depth_key", "geom", "canon", "sigma", "sigma_den", "rgb",
+                  "rgb_raw"):
             setattr(p, f, _ptr(getattr(self, f)))
         return p
 
@@ -143,7 +145,7 @@ def preprocess(scene: Scene, cam, kappa=0.1, mode=0, den_override=None, exact=Fa
               rect=np.zeros((n, 4), np.int32), depth_key=np.zeros(n, np.uint32),
               geom=np.zeros((n, 3 + 3 * K), np.float64), canon=np.zeros((n, 2 + 3 * K), np.float32),
               sigma=np.zeros(n, np.float64), sigma_den=np.zeros(n, np.float64),
-              rgb=np.zeros((n, 3), np.float64))
+              rgb=np.zeros((n, 3), np.float64), rgb_raw=np.zeros((n, 3), np.float64))
     den = None if den_override is None else np.ascontiguousarray(den_override, np.float64)
     s, c, p = scene.c(), camera(cam), out.c()
     rc = lib().lpo_preprocess(C.byref(s), C.byref(c), C.c_float(kappa), C.c_int32(mode), C.c_int32(1 if exact else 0),
@@ -189,10 +191,14 @@ class RenderOut:
     depth: np.ndarray = None       # depth mode: entry distance at cumulative opacity > 0.5, else 0
     m_depth: np.ndarray = None     # min |ln(T_after / 0.5)| over the pixel's hits
     alpha: np.ndarray = None       # alpha mode: 1 - T_final
+    # conditioning bounds (bounds=True): first-order fp32 error of drgb / dsigma / dv (lpo.h)
+    bnd_rgb: np.ndarray = None
+    bnd_sigma: np.ndarray = None
+    bnd_dv: np.ndarray = None
 
 
 def render(scene: Scene, cam, pre: Pre, vals, ranges, bg=(0.0, 0.0, 0.0), t_stop=1e-3,
-           pix=None, dL_dimage=None, brute=False, exact=False) -> RenderOut:
+           pix=None, dL_dimage=None, brute=False, exact=False, bounds=False) -> RenderOut:
     """MTIA rasterisation of the requested pixels (all when pix is None), optional backward."""
     W, H = int(cam["width"]), int(cam["height"])
     n = scene.n
@@ -215,6 +221,10 @@ def render(scene: Scene, cam, pre: Pre, vals, ranges, bg=(0.0, 0.0, 0.0), t_stop
         out.dsigma = np.zeros(n, np.float64)
         out.drgb = np.zeros((n, 3), np.float64)
         out.face_margin = np.full(n, np.inf)
+        if bounds:
+            out.bnd_rgb = np.zeros((n, 3), np.float64)
+            out.bnd_sigma = np.zeros(n, np.float64)
+            out.bnd_dv = np.zeros((n, NV, 3), np.float64)
     vals = np.ascontiguousarray(vals, np.uint32)
     ranges = np.ascontiguousarray(ranges, np.int64)
     s, c, p = scene.c(), camera(cam), pre.c()
@@ -226,7 +236,8 @@ def render(scene: Scene, cam, pre: Pre, vals, ranges, bg=(0.0, 0.0, 0.0), t_stop
                           C.c_void_p(_ptr(out.dv)), C.c_void_p(_ptr(out.dsigma)),
                           C.c_void_p(_ptr(out.drgb)), C.c_void_p(_ptr(out.face_margin)),
                           C.c_void_p(_ptr(out.counters)), C.c_void_p(_ptr(out.depth)),
-                          C.c_void_p(_ptr(out.m_depth)))
+                          C.c_void_p(_ptr(out.m_depth)), C.c_void_p(_ptr(out.bnd_rgb)),
+                          C.c_void_p(_ptr(out.bnd_sigma)), C.c_void_p(_ptr(out.bnd_dv)))
     assert rc == 0
     out.alpha = 1.0 - out.T_final
     return out
@@ -277,18 +288,19 @@ class Forward:
 
 
 def forward(scene, cam, kappa=0.1, mode=0, bg=(0, 0, 0), t_stop=1e-3, pix=None, den_override=None,
-            dL_dimage=None, tile_mask=None, brute=False, exact=False) -> Forward:
+            dL_dimage=None, tile_mask=None, brute=False, exact=False, bounds=False) -> Forward:
     pre = preprocess(scene, cam, kappa=kappa, mode=mode, den_override=den_override, exact=exact)
     keys, vals, ranges = bin_tiles(pre, cam["width"], cam["height"], tile_mask=tile_mask)
     out = render(scene, cam, pre, vals, ranges, bg=bg, t_stop=t_stop, pix=pix, dL_dimage=dL_dimage,
-                 brute=brute, exact=exact)
+                 brute=brute, exact=exact, bounds=bounds)
     return Forward(pre, keys, vals, ranges, out)
 
 
 def forward_backward(scene, cam, dL_dimage, kappa=0.1, mode=0, bg=(0, 0, 0), t_stop=1e-3, pix=None,
-                     den_override=None, tile_mask=None, exact=False):
+                     den_override=None, tile_mask=None, exact=False, bounds=False):
     f = forward(scene, cam, kappa=kappa, mode=mode, bg=bg, t_stop=t_stop, pix=pix,
-                den_override=den_override, dL_dimage=dL_dimage, tile_mask=tile_mask, exact=exact)
+                den_override=den_override, dL_dimage=dL_dimage, tile_mask=tile_mask, exact=exact,
+                bounds=bounds)
     g = preprocess_bwd(scene, cam, f.pre, f.out, den_override=den_override, exact=exact)
     return f, g
 
@@ -328,3 +340,13 @@ def mtia3_grad(A, B, C_, r):
     lib().lpo_mtia3_grad(C.c_void_p(A.ctypes.data), C.c_void_p(B.ctypes.data), C.c_void_p(C_.ctypes.data),
                          C.c_void_p(r.ctypes.data), C.c_void_p(dt.ctypes.data))
     return dt
+
+
+def feature_bounds(scene: Scene, cam, pre: Pre, r: RenderOut, exact=False) -> Grads:
+    """Conditioning bounds of the feature gradients (test tolerances only): the render's
+    bnd_rgb / bnd_sigma / bnd_dv chained to the features by the same preprocess backward, in
+    absolute value."""
+    b = RenderOut(image=None, T_final=None, n_proc=None, m_stop=None, m_face=None, counters=None,
+                  dv=r.bnd_dv, dsigma=r.bnd_sigma, drgb=r.bnd_rgb)
+    g = preprocess_bwd(scene, cam, pre, b, exact=exact)
+    return Grads(*(np.abs(getattr(g, k)) for k in ("pos", "rot", "dist", "opacity", "sh")))

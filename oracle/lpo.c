@@ -208,6 +208,7 @@ int lpo_preprocess(const lpo_scene *s, const lpo_camera *cam, float kappa, int32
         for (int k = 0; k < ncoef; ++k) acc += (double)s->sh[((size_t)k * 3 + ch) * n + i] * Y[k];
         acc += 0.5;
         rgb[ch] = acc > 0.0 ? acc : 0.0;
+        if (out->rgb_raw) out->rgb_raw[(size_t)i * 3 + ch] = acc;
       }
     }
     out->sigma[i] = sig;
@@ -408,6 +409,7 @@ typedef struct {
   double o, chord, E, T_before;
   int f_in, f_out;
   double u_in, v_in, d_in, u_out, v_out, d_out;
+  double dc, eT;   /* conditioning (test tolerances only): fp32 chord error scale, relative T error in front */
 } hit_rec;
 
 /* exact (App. D): r = perspective ray of the pixel, depths are ray parameters t, and the chord
@@ -442,7 +444,8 @@ static void primitive_hit(int kind, const double *geo, double rx, double ry, dou
 }
 
 static void add_face_grad(int kind, const double *geo, int f, double u, double v, double d,
-                          double rx, double ry, double dLdi, double *dvp, int exact, const double r[3])
+                          double rx, double ry, double dLdi, double *dvp, int exact, const double r[3],
+                          int absval)
 {
   double V[6][3];
   vertices(kind, geo, V);
@@ -460,6 +463,7 @@ static void add_face_grad(int kind, const double *geo, int f, double u, double v
   for (int k = 0; k < 3; ++k)
     for (int a = 0; a < 3; ++a) {
       double val = dLdi * di[k][a];
+      if (absval) val = fabs(val);
 #pragma omp atomic
       dvp[idx[k] * 3 + a] += val;
     }
@@ -487,7 +491,8 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
                const lpo_render_cfg *cfg, const int32_t *pix, int64_t npix,
                double *image, double *T_final, int32_t *n_proc, double *m_stop, double *m_face,
                const float *dL_dimage, double *dv, double *dsigma, double *drgb,
-               double *face_margin, int64_t *counters, double *depth, double *m_depth)
+               double *face_margin, int64_t *counters, double *depth, double *m_depth,
+               double *bnd_rgb, double *bnd_sigma, double *bnd_dv)
 {
   const int W = cam->width, H = cam->height, gx = (W + LPO_TILE - 1) / LPO_TILE;
   const int kind = s->kind, K = noffs(kind), G = 3 + 3 * K, NV = nverts(kind);
@@ -527,7 +532,7 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
         list = sorted_vals + ranges[2 * t];
         cnt = ranges[2 * t + 1] - ranges[2 * t];
       }
-      double T = 1.0, C[3] = {0, 0, 0}, ms = DBL_MAX, mf = DBL_MAX, dep = 0.0, md = DBL_MAX;
+      double T = 1.0, C[3] = {0, 0, 0}, ms = DBL_MAX, mf = DBL_MAX, dep = 0.0, md = DBL_MAX, eT = 0.0;
       int dep_set = 0;
       int64_t nh = 0, np = 0;
       for (int64_t e = 0; e < cnt; ++e) {
@@ -547,6 +552,28 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
         if (nh == cap) { cap *= 2; hits = (hit_rec *)realloc(hits, sizeof(hit_rec) * (size_t)cap); }
         hit_rec *h = &hits[nh++];
         h->prim = i; h->o = o; h->chord = chord; h->E = E; h->T_before = T;
+        {
+          /* Conditioning of the chord in fp32 (test tolerances only): an fp32
+             evaluation of i2 - i1 from the primitive's centre-relative geometry carries an absolute
+             error of a few units in the last place of the depths it subtracts, |i - z_c| and the
+             primitive's own depth extent; 8 ulp (2^-20) of their sum.  eT: the relative error this
+             puts on T of the entries behind (sum of sigma dc). */
+          double zc, Z = 0.0;
+          if (exact) {
+            zc = sqrt(geo[0] * geo[0] + geo[1] * geo[1] + geo[2] * geo[2]);
+            for (int j = 0; j < K; ++j) {
+              const double *oj = geo + 3 + 3 * j;
+              double nj = sqrt(oj[0] * oj[0] + oj[1] * oj[1] + oj[2] * oj[2]);
+              if (nj > Z) Z = nj;
+            }
+          } else {
+            zc = geo[2];
+            for (int j = 0; j < K; ++j) if (fabs(geo[3 + 3 * j + 2]) > Z) Z = fabs(geo[3 + 3 * j + 2]);
+          }
+          h->dc = 0x1p-20 * (fabs(i1 - zc) + fabs(i1 + chord - zc) + 2.0 * Z);
+          h->eT = eT;
+          eT += sig * h->dc;
+        }
         h->f_in = f_in; h->u_in = u_in; h->v_in = v_in; h->d_in = d_in;
         h->f_out = f_out; h->u_out = u_out; h->v_out = v_out; h->d_out = d_out;
         double m1 = bary_margin(u_in, v_in), m2 = bary_margin(u_out, v_out);
@@ -561,10 +588,13 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
           if (m < md) md = m;
           if (!dep_set && 1.0 - T > 0.5) { dep = i1; dep_set = 1; }
         }
-        if (cfg->t_stop > 0.0f) {
-          double m = fabs(log(T / (double)cfg->t_stop));
+        {
+          /* include-then-stop (reading 9); a threshold below 2^-100 (0 included) acts as 2^-100
+             (reading 28: no fp32 image changes below it) */
+          const double ts = cfg->t_stop > 0x1p-100f ? (double)cfg->t_stop : 0x1p-100;
+          double m = fabs(log(T / ts));
           if (m < ms) ms = m;
-          if (T < (double)cfg->t_stop) break;   /* include-then-stop (reading 9) */
+          if (T < ts) break;
         }
       }
       for (int ch = 0; ch < 3; ++ch) C[ch] += T * cfg->bg[ch];
@@ -581,19 +611,35 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
       if (dL_dimage) {
         /* blend backward: S = colour behind k incl. background */
         double Gc[3] = {dL_dimage[p], dL_dimage[HW + p], dL_dimage[2 * HW + p]};
-        double S[3] = {cfg->bg[0], cfg->bg[1], cfg->bg[2]};
+        double S[3] = {cfg->bg[0], cfg->bg[1], cfg->bg[2]}, eS[3] = {0, 0, 0};
         for (int64_t k = nh - 1; k >= 0; --k) {
           const hit_rec *h = &hits[k];
           const int i = h->prim;
           const double *rgb = pre->rgb + (size_t)i * 3;
-          double dLdo = 0.0;
+          double dLdo = 0.0, edo = 0.0;
+          const double eo = pre->sigma[i] * h->E * h->dc;   /* error of o from the chord's */
           for (int ch = 0; ch < 3; ++ch) {
             double val = h->T_before * h->o * Gc[ch];
 #pragma omp atomic
             drgb[(size_t)i * 3 + ch] += val;
             dLdo += h->T_before * (rgb[ch] - S[ch]) * Gc[ch];
+            edo += h->T_before * eS[ch] * fabs(Gc[ch]);
+            if (bnd_rgb) {
+              double b = h->T_before * fabs(Gc[ch]) * (eo + h->o * h->eT);
+#pragma omp atomic
+              bnd_rgb[(size_t)i * 3 + ch] += b;
+            }
           }
-          for (int ch = 0; ch < 3; ++ch) S[ch] = h->o * rgb[ch] + (1.0 - h->o) * S[ch];
+          edo += fabs(dLdo) * h->eT;
+          for (int ch = 0; ch < 3; ++ch) {
+            eS[ch] = fabs(rgb[ch] - S[ch]) * eo + (1.0 - h->o) * eS[ch];
+            S[ch] = h->o * rgb[ch] + (1.0 - h->o) * S[ch];
+          }
+          if (bnd_sigma) {
+            double b = h->E * (fabs(dLdo) * h->dc * (1.0 + pre->sigma[i] * h->chord) + h->chord * edo);
+#pragma omp atomic
+            bnd_sigma[i] += b;
+          }
           /* o = 1 - exp(-sigma (i2 - i1)) */
           double sig = pre->sigma[i];
           double ds = h->chord * h->E * dLdo;
@@ -602,8 +648,15 @@ int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
           double g = sig * h->E * dLdo;     /* dL/d i2 = g, dL/d i1 = -g */
           const double *geo = pre->geom + (size_t)i * G;
           double *dvp = dv + (size_t)i * NV * 3;
-          add_face_grad(kind, geo, h->f_in, h->u_in, h->v_in, h->d_in, rx, ry, -g, dvp, exact, rv);
-          add_face_grad(kind, geo, h->f_out, h->u_out, h->v_out, h->d_out, rx, ry, g, dvp, exact, rv);
+          add_face_grad(kind, geo, h->f_in, h->u_in, h->v_in, h->d_in, rx, ry, -g, dvp, exact, rv, 0);
+          add_face_grad(kind, geo, h->f_out, h->u_out, h->v_out, h->d_out, rx, ry, g, dvp, exact, rv, 0);
+          if (bnd_dv) {
+            /* first-order error of g = sigma E dL/do from the chord and T errors */
+            const double eg = sig * h->E * (fabs(dLdo) * sig * h->dc + edo);
+            double *bvp = bnd_dv + (size_t)i * NV * 3;
+            add_face_grad(kind, geo, h->f_in, h->u_in, h->v_in, h->d_in, rx, ry, eg, bvp, exact, rv, 1);
+            add_face_grad(kind, geo, h->f_out, h->u_out, h->v_out, h->d_out, rx, ry, eg, bvp, exact, rv, 1);
+          }
           if (face_margin) {
             double m = bary_margin(h->u_in, h->v_in), m2 = bary_margin(h->u_out, h->v_out);
             if (m2 < m) m = m2;

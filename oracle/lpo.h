@@ -64,6 +64,8 @@ typedef struct {
   double   *sigma;         /* [n] Eq. 1 */
   double   *sigma_den;     /* [n] 2 * min(dhat), the frozen denominator */
   double   *rgb;           /* [n][3] clamped SH colour */
+  double   *rgb_raw;       /* [n][3] SH colour before the clamp max(0, .) (may be NULL): parity tests use
+                              it to find clamp decisions within rounding of 0 */
 } lpo_pre;
 
 /* Preprocess every primitive.  mode 0 = canonical fp32 geometry, 1 = fp64 geometry.
@@ -85,7 +87,8 @@ int64_t lpo_bin(int32_t n, const uint32_t *tiles_touched, const int32_t *rect,
 
 typedef struct {
   float bg[3];
-  float t_stop;           /* stop once T < t_stop (include-then-stop), 0 disables */
+  float t_stop;           /* stop once T < t_stop (include-then-stop); below 2^-100 (0 included) it acts as
+                             2^-100 (reading 28) */
   int32_t brute;          /* 1: ignore tiling, every valid primitive in (key, id) order */
   int32_t exact;          /* 1: geometry from lpo_preprocess(exact = 1); per-pixel perspective rays
                              r = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1) against the camera-space faces by
@@ -106,13 +109,18 @@ typedef struct {
  * hit, whose scale is the camera distance |p|) of the first composited primitive after which
  * 1 - T > 0.5, else 0 (the invalid marker, reading 24); m_depth[H][W] = min over the pixel's
  * hits of |ln(T_after / 0.5)| (how far the 0.5 decision is from flipping).  Either may be NULL.
+ * Conditioning bounds (test tolerances only; each may be NULL; += like the gradients):
+ * bnd_rgb[n][3], bnd_sigma[n], bnd_dv[n][V][3] receive, per primitive, the first-order error that
+ * an fp32 evaluation of the same method puts on drgb, dsigma and dv through the chord's rounding
+ * (8 ulp of the centre-relative depths it subtracts) and the resulting T errors.
  * Returns 0 or -1. */
 int lpo_render(const lpo_scene *s, const lpo_camera *cam, const lpo_pre *pre,
                const uint32_t *sorted_vals, const int64_t *ranges,
                const lpo_render_cfg *cfg, const int32_t *pix, int64_t npix,
                double *image, double *T_final, int32_t *n_proc, double *m_stop, double *m_face,
                const float *dL_dimage, double *dv, double *dsigma, double *drgb,
-               double *face_margin, int64_t *counters, double *depth, double *m_depth);
+               double *face_margin, int64_t *counters, double *depth, double *m_depth,
+               double *bnd_rgb, double *bnd_sigma, double *bnd_dv);
 
 /* Chain ray-space gradients to the world features (+= into SoA fp64 gradients with the
  * same layout as the features).  Primitives with flag != 0 receive nothing.

@@ -25,7 +25,7 @@ inline int offsets_k(int kind) { return kind == LP_OCTAHEDRON ? 3 : 4; }
 struct Layout {
   size_t tiles_touched, rect, depth_key, record, prim_key, prim_key_alt, prim_order, prim_order_alt, offsets, tile_key,
       tile_key_alt, entry_val, entry_val_alt, ranges, sort_hist, scan_tmp, counters, T_final, n_proc, rgrad, canon,
-      tile_diff, tile_cursor, hitmask, total;
+      tile_diff, tile_cursor, hitmask, T_last, T_ckpt, total;
 };
 
 Layout layout(int kind, int64_t n, int w, int h, int64_t cap, int canon) {
@@ -60,6 +60,8 @@ Layout layout(int kind, int64_t n, int w, int h, int64_t cap, int canon) {
   L.tile_diff = take(4 * (gx + 1) * (gy + 1));
   L.tile_cursor = take(4 * tiles);
   L.hitmask = take(4 * 4 * hit_words(cc));
+  L.T_last = take(4 * hw);
+  L.T_ckpt = take(8 * 128 * (size_t)ckpt_slots(tiles, cc));
   L.total = o;
   return L;
 }
@@ -156,6 +158,8 @@ lp_status lp_frame_init(lp_frame *F, void *workspace, size_t bytes, int32_t kind
   F->tile_cursor = reinterpret_cast<uint32_t *>(b + L.tile_cursor);
   F->sort_method = LP_SORT_RADIX;   // measured faster on C5
   F->hitmask = reinterpret_cast<uint32_t *>(b + L.hitmask);
+  F->T_last = reinterpret_cast<float *>(b + L.T_last);
+  F->T_ckpt = reinterpret_cast<float *>(b + L.T_ckpt);
   return LP_OK;
 }
 

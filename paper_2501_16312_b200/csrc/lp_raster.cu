@@ -227,9 +227,10 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
   const int W = F.width, H = F.height;
   if (threadIdx.x < 3) s_stat[threadIdx.x] = 0ull;
 
-  float fy[PPT], dep[PPT];
+  float fy[PPT], dep[PPT], tlast[PPT];
   float2 T2 = make_float2(1.f, 1.f), C2[3];   // transmittance and colour of the two pixels (lane k = pixel k)
   uint32_t nproc[PPT];
+  const float tstop = effective_t_stop(cfg.t_stop);
   bool done[PPT], inside[PPT], dset[PPT];
   uint32_t nhit = 0, nbox = 0;
   float fx;
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
     done[k] = !inside[k];
     nproc[k] = end - start;
     dep[k] = 0.f;
+    tlast[k] = 1.f;
     dset[k] = false;
   }
 #pragma unroll
@@ -258,6 +260,8 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
 
   for (uint32_t b = start; b < end; b += NT) {
     if (__syncthreads_and(done[0] && done[1])) break;   // also protects s_rec from the previous batch
+    // the pixels' T in front of this batch: the backward restarts its T recovery here
+    if (b > start) *(ckpt_at(F.T_ckpt, tile, start, b) + threadIdx.x) = T2;
     const uint32_t e = b + threadIdx.x;
     if (e < end) {
       const uint32_t v = F.sorted_val[e];
@@ -321,11 +325,13 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
       if (!__any_sync(0xffffffffu, hk[0] || hk[1])) continue;
       if (lane == (j >> 5)) hitw |= 1u << (j & 31);
       // both pixels composited as f32x2 pairs; a pixel this record does not hit gets chord 0 ->
-      // E = 1, o = 0, leaving its T and colour bitwise unchanged
+      // x = 0, E = 1, o = 0, leaving its T and colour bitwise unchanged
+      const float2 Tin = T2;
       {
         const float sig = rec[SIGMA];
-        const float2 E = make_float2(transmit(sig, hk[0] ? ch2.x : 0.f), transmit(sig, hk[1] ? ch2.y : 0.f));
-        const float2 wgt = fmul2(T2, fsub2(bc(1.f), E));
+        const float2 X = make_float2(hk[0] ? optical_depth(sig, ch2.x) : 0.f, hk[1] ? optical_depth(sig, ch2.y) : 0.f);
+        const float2 E = make_float2(transmit_x(X.x), transmit_x(X.y));
+        const float2 wgt = fmul2(T2, opacity_x2(X, E));
 #pragma unroll
         for (int c = 0; c < 3; ++c) C2[c] = ffma2(wgt, bc(rec[RGB + c]), C2[c]);
         T2 = fmul2(T2, E);
@@ -343,9 +349,10 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
           }
         }
         if (STATS) ++nhit;
-        if (lane_k(T2, k) < cfg.t_stop) {   // include-then-stop (reading 9)
+        if (lane_k(T2, k) < tstop) {   // include-then-stop (readings 9, 28)
           done[k] = true;
           nproc[k] = b + (uint32_t)j - start + 1;
+          tlast[k] = lane_k(Tin, k);   // T in front of the stopping entry (the backward's start)
         }
       }
     }
@@ -365,6 +372,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
     image[HW + p] = fmaf(Tk, cfg.bg[1], lane_k(C2[1], k));
     image[2 * HW + p] = fmaf(Tk, cfg.bg[2], lane_k(C2[2], k));
     F.T_final[p] = Tk;
+    F.T_last[p] = Tk < tstop ? tlast[k] : Tk;
     F.n_proc[p] = nproc[k];
     if (AUX) {
       if (depth) depth[p] = dep[k];
@@ -426,6 +434,11 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
 
   float fx[PPT], fy[PPT], T[PPT], S[PPT][3], G[PPT][3];
   uint32_t last[PPT];
+  // T[k]: the pixel's transmittance in front of the hit entry processed last (the next one in list
+  // order); fresh[k]: T[k] is already the T in front of the upcoming hit (no division).  A stopped
+  // pixel starts from T_last (T in front of its stopping entry), every other one from T_final.
+  bool fresh[PPT];
+  const float tstop = effective_t_stop(cfg.t_stop);
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     int x, y;
@@ -436,7 +449,9 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
     fx[k] = (float)x + 0.5f;
     fy[k] = (float)y + 0.5f;
     const size_t p = in ? (size_t)y * W + x : 0;
-    T[k] = in ? F.T_final[p] : 1.f;
+    const float tf = in ? F.T_final[p] : 1.f;
+    fresh[k] = tf < tstop;                          // stopped (include-then-stop)
+    T[k] = fresh[k] ? F.T_last[p] : tf;
     last[k] = in ? start + F.n_proc[p] : start;     // entries [start, last) were processed
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -456,8 +471,9 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
   const float2 ry2 = EXACT ? RY.ry2 : make_float2(0.f, 0.f);
   const float2 rn2 = EXACT ? RY.rn2 : make_float2(1.f, 1.f);
 
-  // batches walk the list backwards: batch [bstart(bend), bend), the next one ends at bstart
-  auto bstart_of = [&](uint32_t be) { return (be - start > NT) ? be - NT : start; };
+  // batches walk the list backwards, aligned with the forward's (entries [start + 128 i, start +
+  // 128 (i + 1)), the top one cut at lmax): batch [bstart(bend), bend), the next one ends at bstart
+  auto bstart_of = [&](uint32_t be) { return be > start ? start + (((be - 1u - start) / NT) * NT) : start; };
   // this thread's entry of the batch ending at `be` (its primitive id; false if none)
   auto entry_of = [&](uint32_t be, uint32_t &v) {
     if (be <= start) return false;
@@ -489,10 +505,24 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
     has_next = bstart > start && entry_of(bstart_of(bstart), vnext);
     const float4 *s_rec = s_rec2[buf];
     const uint32_t *s_id = s_id2[buf];
-    bool act = false;
+    bool act = false, after = false;
 #pragma unroll
-    for (int k = 0; k < PPT; ++k) act = act || (last[k] > bstart);
+    for (int k = 0; k < PPT; ++k) {
+      act = act || (last[k] > bstart);
+      after = after || (last[k] > bend);
+    }
     if (!__any_sync(0xffffffffu, act)) continue;
+    // re-anchor the T recovery at the forward's checkpoint in front of the next batch: the
+    // divisions T / E never chain across more than one 128-entry batch
+    if (after) {
+      const float2 c = *(ckpt_at(F.T_ckpt, tile, start, bend) + threadIdx.x);
+#pragma unroll
+      for (int k = 0; k < PPT; ++k)
+        if (last[k] > bend) {
+          T[k] = lane_k(c, k);
+          fresh[k] = false;
+        }
+    }
     const int w = threadIdx.x >> 5;
     // the entries of this batch that hit one of the warp's pixels in the forward (its hit bits):
     // no rect / bbox tests and no chord evaluation of entries that miss every pixel of the warp
@@ -594,9 +624,11 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
           int se, sx;
           if (EXACT) trackE_k(PE, k, te, tx_, se, sx);
           else track_k<KIND>(PR, k, te, tx_, se, sx);
-          const float E = transmit(sig, ch);
-          const float o = 1.f - E;
-          const float Tk = T[k] * rcp_ftz(E);               // transmittance in front of this entry
+          const float x = optical_depth(sig, ch);
+          const float E = transmit_x(x);
+          const float o = opacity_x(x, E);
+          const float Tk = fresh[k] ? T[k] : T[k] * rcp_ftz(E);   // transmittance in front of this entry
+          fresh[k] = false;
           float dLdo = 0.f;
           tail.y = fmaf(Tk * o, G[k][0], tail.y);           // dL/drgb
           tail.z = fmaf(Tk * o, G[k][1], tail.z);

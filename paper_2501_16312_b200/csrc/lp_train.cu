@@ -106,81 +106,111 @@ void launch_filter3d(const float *pos, int n, const lp_camera *cams, int nc, flo
   k_filter3d<<<(n + 255) / 256, 256, 0, st>>>(pos, n, cams, nc, kappa, out);
 }
 
+// ---------------------------------------------------------------------------------------------
+// C5: fused Adam over the flat parameter buffer, one CTA per ADAM_TILE-element tile of a
+// group.  The bias corrections are folded on the host (the textbook update
+//   p -= lr (m / bc1) / (sqrt(v / bc2) + eps)  ==  p -= step m / (sqrt(v) + eps_hat)
+// with step = lr sqrt(bc2) / bc1 and eps_hat = eps sqrt(bc2), bc_i = 1 - beta_i^t), so an element
+// costs 2 FFMA + 2 FMUL + sqrt + reciprocal.  Tiles never straddle groups: the float4 body covers
+// the tile's 16-byte aligned part and threads 0-2 take its (at most 3 + 3) ragged elements.
+constexpr int ADAM_THREADS = 256;
+constexpr int ADAM_VEC = 4;                                   // float4 per thread per tile
+constexpr int64_t ADAM_TILE = (int64_t)ADAM_THREADS * ADAM_VEC * 4;
+
 struct AdamGroups {
-  int64_t begin[8], end[8];
-  float lr[8];
+  int64_t begin[8], end[8], tile0[9];                         // tile0: first tile of each group (prefix)
+  float step[8], eps_hat[8];
   int n;
 };
 
-__global__ void __launch_bounds__(256) k_adam(float *__restrict__ p, float *__restrict__ g, float *__restrict__ m,
-                                              float *__restrict__ v, AdamGroups G, float b1, float b2, float eps,
-                                              float bc1, float bc2, bool zero_grad) {
-  const int gi = blockIdx.y;
-  const int64_t b = G.begin[gi], e = G.end[gi];
-  const float lr = G.lr[gi];
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  auto upd = [&](float pp, float gg, float &mm, float &vv) {
-    mm = fmaf(b1, mm, (1.f - b1) * gg);
-    vv = fmaf(b2, vv, (1.f - b2) * gg * gg);
-    return pp - lr * (mm / bc1) / (sqrtf(vv / bc2) + eps);
-  };
-  // float4 body over the 16-byte aligned part of [b, e), scalar head / tail
+__device__ __forceinline__ float adam_elem(float p, float g, float &m, float &v, float b1, float b2, float om1,
+                                           float om2, float step, float eps_hat) {
+  m = fmaf(b1, m, om1 * g);
+  v = fmaf(b2, v, om2 * g * g);
+  return fmaf(-step, __fdividef(m, sqrtf(v) + eps_hat), p);
+}
+
+__global__ void __launch_bounds__(ADAM_THREADS) k_adam(float *__restrict__ p, float *__restrict__ g,
+                                                       float *__restrict__ m, float *__restrict__ v,
+                                                       const AdamGroups G, float b1, float b2, bool zero_grad) {
+  const int64_t tile = blockIdx.x;
+  int gi = 0;
+  while (gi + 1 < G.n && tile >= G.tile0[gi + 1]) ++gi;       // block-uniform, <= 7 compares
+  const int64_t b = G.begin[gi] + (tile - G.tile0[gi]) * ADAM_TILE;
+  const int64_t e = min(b + ADAM_TILE, G.end[gi]);
+  // 1 - beta is exact in fp32 for beta in [0.5, 1] (Sterbenz): the complement of the caller's fp32 beta
+  const float step = G.step[gi], eh = G.eps_hat[gi], om1 = 1.f - b1, om2 = 1.f - b2;
   const int64_t b4 = (b + 3) & ~int64_t(3), e4 = e & ~int64_t(3);
   if (b4 < e4) {
-    float4 *p4 = reinterpret_cast<float4 *>(p + b4), *g4 = reinterpret_cast<float4 *>(g + b4);
-    float4 *m4 = reinterpret_cast<float4 *>(m + b4), *v4 = reinterpret_cast<float4 *>(v + b4);
-    const int64_t n4 = (e4 - b4) / 4;
-    for (int64_t i = tid; i < n4; i += stride) {
-      float4 pp = p4[i], gg = g4[i], mm = m4[i], vv = v4[i];
-      pp.x = upd(pp.x, gg.x, mm.x, vv.x);
-      pp.y = upd(pp.y, gg.y, mm.y, vv.y);
-      pp.z = upd(pp.z, gg.z, mm.z, vv.z);
-      pp.w = upd(pp.w, gg.w, mm.w, vv.w);
-      p4[i] = pp;
-      m4[i] = mm;
-      v4[i] = vv;
-      if (zero_grad) g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t q0 = b4 >> 2, nq = (e4 - b4) >> 2;
+    float4 *p4 = reinterpret_cast<float4 *>(p) + q0, *g4 = reinterpret_cast<float4 *>(g) + q0;
+    float4 *m4 = reinterpret_cast<float4 *>(m) + q0, *v4 = reinterpret_cast<float4 *>(v) + q0;
+    float4 pp[ADAM_VEC], gg[ADAM_VEC], mm[ADAM_VEC], vv[ADAM_VEC];
+#pragma unroll
+    for (int k = 0; k < ADAM_VEC; ++k) {                     // all loads in flight first
+      const int64_t i = threadIdx.x + (int64_t)k * ADAM_THREADS;
+      if (i < nq) {
+        pp[k] = p4[i];
+        gg[k] = g4[i];
+        mm[k] = m4[i];
+        vv[k] = v4[i];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < ADAM_VEC; ++k) {
+      const int64_t i = threadIdx.x + (int64_t)k * ADAM_THREADS;
+      if (i < nq) {
+        pp[k].x = adam_elem(pp[k].x, gg[k].x, mm[k].x, vv[k].x, b1, b2, om1, om2, step, eh);
+        pp[k].y = adam_elem(pp[k].y, gg[k].y, mm[k].y, vv[k].y, b1, b2, om1, om2, step, eh);
+        pp[k].z = adam_elem(pp[k].z, gg[k].z, mm[k].z, vv[k].z, b1, b2, om1, om2, step, eh);
+        pp[k].w = adam_elem(pp[k].w, gg[k].w, mm[k].w, vv[k].w, b1, b2, om1, om2, step, eh);
+        p4[i] = pp[k];
+        m4[i] = mm[k];
+        v4[i] = vv[k];
+        if (zero_grad) g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
   }
-  const int64_t head_end = b4 < e ? b4 : e;
-  for (int64_t i = b + tid; i < head_end; i += stride) {
-    float mm = m[i], vv = v[i];
-    p[i] = upd(p[i], g[i], mm, vv);
-    m[i] = mm;
-    v[i] = vv;
-    if (zero_grad) g[i] = 0.f;
+  // ragged elements: [b, b4) and [e4, e) when the tile has an aligned body, else all of [b, e)
+  int64_t i = -1;
+  const int t = threadIdx.x;
+  if (b4 < e4) {
+    if (t < 3) i = b + t < b4 ? b + t : -1;
+    else if (t < 6) i = e4 + (t - 3) < e ? e4 + (t - 3) : -1;
+  } else if (t < 6) {
+    i = b + t < e ? b + t : -1;
   }
-  for (int64_t i = (e4 > b ? (e4 > head_end ? e4 : head_end) : e) + tid; i < e; i += stride) {
+  if (i >= 0) {
     float mm = m[i], vv = v[i];
-    p[i] = upd(p[i], g[i], mm, vv);
+    p[i] = adam_elem(p[i], g[i], mm, vv, b1, b2, om1, om2, step, eh);
     m[i] = mm;
     v[i] = vv;
     if (zero_grad) g[i] = 0.f;
   }
 }
 
-// grid cap of the Adam kernel: blocks per SM and group (-DLP_ADAM_BPSM overrides)
-#ifndef LP_ADAM_BPSM
-#define LP_ADAM_BPSM 8
-#endif
 void launch_adam(float *p, float *g, float *m, float *v, const lp_adam_group *groups, int ng, float b1, float b2,
                  float eps, int step, bool zero_grad, cudaStream_t st) {
+  // bias corrections in double on the host (Kingma & Ba, Alg. 1)
+  const double bc1 = 1.0 - pow((double)b1, (double)step), bc2 = 1.0 - pow((double)b2, (double)step);
   for (int base = 0; base < ng; base += 8) {
     AdamGroups G;
-    G.n = ng - base < 8 ? ng - base : 8;
-    int64_t longest = 1;
-    for (int k = 0; k < G.n; ++k) {
-      G.begin[k] = groups[base + k].begin;
-      G.end[k] = groups[base + k].end;
-      G.lr[k] = groups[base + k].lr;
-      if (G.end[k] - G.begin[k] > longest) longest = G.end[k] - G.begin[k];
+    G.n = 0;
+    int64_t tiles = 0;
+    for (int k = 0; k < 8 && base + k < ng; ++k) {
+      const lp_adam_group &gr = groups[base + k];
+      if (gr.end <= gr.begin) continue;
+      G.begin[G.n] = gr.begin;
+      G.end[G.n] = gr.end;
+      G.tile0[G.n] = tiles;
+      G.step[G.n] = (float)((double)gr.lr * sqrt(bc2) / bc1);
+      G.eps_hat[G.n] = (float)((double)eps * sqrt(bc2));
+      tiles += (gr.end - gr.begin + ADAM_TILE - 1) / ADAM_TILE;
+      ++G.n;
     }
-    for (int k = G.n; k < 8; ++k) { G.begin[k] = G.end[k] = 0; G.lr[k] = 0.f; }
-    const float bc1 = 1.f - powf(b1, (float)step), bc2 = 1.f - powf(b2, (float)step);
-    const int64_t want = (longest / 4 + 255) / 256 + 1;
-    const int gx = (int)(want < 148 * LP_ADAM_BPSM ? want : 148 * LP_ADAM_BPSM);
-    k_adam<<<dim3(gx, G.n), 256, 0, st>>>(p, g, m, v, G, b1, b2, eps, bc1, bc2, zero_grad);
+    if (G.n == 0) continue;
+    G.tile0[G.n] = tiles;
+    k_adam<<<(unsigned)tiles, ADAM_THREADS, 0, st>>>(p, g, m, v, G, b1, b2, zero_grad);
   }
 }
 

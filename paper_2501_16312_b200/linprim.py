@@ -24,7 +24,7 @@ LP_TILE = 16
 LP_CNT_ENTRIES, LP_CNT_OVERFLOW, LP_CNT_INVALID, LP_CNT_FRUSTUM, LP_CNT_VISIBLE = 0, 1, 2, 3, 4
 LP_CNT_ITERATED, LP_CNT_INTERSECTED, LP_CNT_INBOX, LP_NUM_COUNTERS = 8, 10, 12, 16
 LP_SORT_BUCKET, LP_SORT_RADIX = 0, 1
-LP_ABI_VERSION = 3            # include/linprim.h; the loaded library must match the structs below
+LP_ABI_VERSION = 4            # include/linprim.h; the loaded library must match the structs below
 
 _p = C.c_void_p
 
@@ -53,7 +53,7 @@ class lp_frame(C.Structure):
                            "prim_order", "prim_order_alt", "offsets", "tile_key", "tile_key_alt", "entry_val",
                            "entry_val_alt", "sorted_tile", "sorted_val", "ranges", "sort_hist", "scan_tmp",
                            "counters", "T_final", "n_proc", "rgrad", "canon", "tile_diff", "tile_cursor")] + \
-        [("sort_method", C.c_int32), ("hitmask", _p)]
+        [("sort_method", C.c_int32), ("hitmask", _p), ("T_last", _p), ("T_ckpt", _p)]
 
 
 class lp_adam_group(C.Structure):

@@ -92,5 +92,5 @@ def test_densification_statistics(kind):
         flagged |= fb.out.face_margin < PT.FACE_MARGIN
         assert (fb.out.m_stop < PT.STOP_MARGIN).mean() < 0.01
     assert np.array_equal(cnt, ref_c)
-    ok, worst, rep = PT.grad_close("mean2d_abs", m2d, ref_m, flagged)
+    ok, worst, rep, _ = PT.grad_close("mean2d_abs", m2d, ref_m, flagged)
     assert ok, rep

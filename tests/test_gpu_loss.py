@@ -53,7 +53,7 @@ def test_loss_and_grad_vs_oracle(V, H, W, seed, lam):
     L_ref, G_ref = OL.batch_loss_and_grad(x.astype(np.float64), y.astype(np.float64), lam)
     L_got, G_got = run(x, y, lam)
     assert abs(L_got - L_ref) <= 1e-5 * abs(L_ref), (L_got, L_ref)
-    ok, worst, rep = PT.grad_close("dL/dimage", G_got, G_ref)
+    ok, worst, rep, _ = PT.grad_close("dL/dimage", G_got, G_ref)
     assert ok, rep
 
 

@@ -58,7 +58,7 @@ def check_binning(got, pre, cam):
 
 
 def full_parity(scene, cam, kappa=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), seed=0, grads=True, filter3d=None,
-                max_masked=0.01, max_flagged=0.05, exact=False, loose=0.1):
+                max_masked=0.01, max_flagged=0.03, exact=False, loose=0.1):
     W, H = cam["width"], cam["height"]
     osc = oscene(scene, filter3d)
     f0 = oracle.forward(osc, cam, kappa=kappa, t_stop=t_stop, bg=bg, exact=exact)
@@ -76,19 +76,17 @@ def full_parity(scene, cam, kappa=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), seed=0, 
     assert got["counters"][8] == int(f0.out.n_proc.sum()) or mask.any()
     if not grads:
         return
-    fb, g = oracle.forward_backward(osc, cam, G, kappa=kappa, t_stop=t_stop, bg=bg, exact=exact)
+    fb, g = oracle.forward_backward(osc, cam, G, kappa=kappa, t_stop=t_stop, bg=bg, exact=exact, bounds=True)
+    gb = oracle.feature_bounds(osc, cam, fb.pre, fb.out, exact=exact)
     flagged = fb.out.face_margin < PT.FACE_MARGIN
     touched = np.isfinite(fb.out.face_margin)
     assert flagged.sum() <= max(2, max_flagged * touched.sum()), f"flagged {flagged.sum()} of {touched.sum()}"
-    gd = ds.grad_dict()
-    n = scene["pos"].shape[1]
-    reports = []
-    for name, ref, fl in (("pos", g.pos, flagged), ("rot", g.rot, flagged), ("dist", g.dist, flagged),
-                          ("opacity", g.opacity, None), ("sh", g.sh, None)):
-        got_g = gd[name].cpu().numpy().reshape(ref.shape)
-        ok, worst, rep = PT.grad_close(name, got_g, ref, fl, loose=loose)
-        reports.append(rep)
-        assert ok, "; ".join(reports)
+    ok, worst, reports, n_cond, n_clamp = PT.check_gradients(ds.grad_dict(), g, gb, fb.pre, flagged, loose=loose)
+    import os
+    PT.log(os.environ.get("PYTEST_CURRENT_TEST", "full_parity").split(" ")[0].split("::")[-1], pixels=W * H,
+           masked_px=int(mask.sum()), hit_prims=int(touched.sum()), flagged=int(flagged.sum()), clamp=n_clamp,
+           cond_elems=n_cond, worst=worst)
+    assert ok, "; ".join(reports)
     return reports
 
 
@@ -167,7 +165,7 @@ def test_multi_view_call_and_accumulation():
         f, g = oracle.forward_backward(osc, cams[v], G[v])
         assert np.abs(img[v].cpu().numpy() - f.out.image).max() <= PT.IMG_TOL
         tot = g.opacity if tot is None else tot + g.opacity
-    ok, worst, rep = PT.grad_close("opacity", ds.grad_dict()["opacity"].cpu().numpy(), tot)
+    ok, worst, rep, _ = PT.grad_close("opacity", ds.grad_dict()["opacity"].cpu().numpy(), tot)
     assert ok, rep
 
 

@@ -239,3 +239,36 @@ def test_counters_and_pixel_subset():
         y, x = divmod(int(p), 50)
         assert np.array_equal(sub.out.image[:, y, x], full.out.image[:, y, x])
         assert sub.out.n_proc[y, x] == full.out.n_proc[y, x]
+
+
+# ---------------------------------------------------------------- conditioning bounds
+
+def test_conditioning_bound_closed_form_and_silhouette_growth():
+    """The oracle's first-order fp32 error of drgb (test tolerances only): on the centre ray of an
+    on-axis octahedron the entry / exit are at -d_z / +d_z from the centre and the depth extent is
+    d_z, so dc = 2^-20 (d_z + d_z + 2 d_z) and bnd_rgb_c = |G_c| sigma E dc exactly (T = 1 in
+    front, no error carried).  Near the silhouette the bound relative to the pixel's own colour
+    gradient grows like 1 / chord (the chord is a difference of two depths that do not shrink)."""
+    c = dict(cam(64, 48), cx=np.float32(32.5), cy=np.float32(24.5))
+    dz = 0.5
+    s = one_prim(OCTA, (0, 0, 5.0), (1, 0, 0, 0), (0.4, 0.6, dz), logit=0.3)
+    G = np.zeros((3, 48, 64), np.float32)
+    G[:, 24, 32] = (0.5, -1.0, 2.0)
+    f, g = oracle.forward_backward(oscene(s), c, G, kappa=0.0, mode=1, t_stop=0.0, bounds=True)
+    sig = f.pre.sigma[0]
+    chord = 2 * dz
+    E = math.exp(-sig * chord)
+    dc = 2.0 ** -20 * 4 * dz
+    np.testing.assert_allclose(f.out.bnd_rgb[0], np.abs(G[:, 24, 32]) * sig * E * dc, rtol=1e-9)
+    assert np.all(f.out.bnd_rgb >= 0) and np.all(f.out.bnd_sigma >= 0) and np.all(f.out.bnd_dv >= 0)
+    # relative bound |bnd_rgb / drgb| at the centre vs at a pixel near the footprint's edge
+    rel = []
+    for x in (32, None):
+        G2 = np.zeros((3, 48, 64), np.float32)
+        if x is None:   # the last pixel of row 24 still hit (smallest chord along the row)
+            ch = chord_image(s, c)[0][24]
+            x = int(np.nonzero(ch > 0)[0].max())
+        G2[:, 24, x] = 1.0
+        f2, _ = oracle.forward_backward(oscene(s), c, G2, kappa=0.0, mode=1, t_stop=0.0, bounds=True)
+        rel.append(f2.out.bnd_rgb[0, 0] / abs(f2.out.drgb[0, 0]))
+    assert rel[1] > 3 * rel[0]
