@@ -2,16 +2,18 @@
 """bench.py -- LinPrim (arXiv 2501.16312) training-step benchmark on B200.
 
 Workload (BASELINE.json configs[4], the config its metric "fwd+bwd Mpixel/s and train iters/s at
-1/2/4/8 B200" is quoted on): 1M octahedra, SH degree 3, a batch of 8 views at 1600x1060, one
-training step = one lp_preprocess over all local views; for each local view lp_bin_sort ->
-lp_render_fwd -> lp_loss_grad (3DGS L1 + SSIM; --loss l1 for L1 only) -> lp_raster_bwd (views
-spread over --streams CUDA streams); one
-lp_preprocess_bwd over all local views; then (N > 1) one NCCL allreduce of the flat gradient;
-then one fused Adam (lp_adam_step, also zeroing the gradient).  Views are sharded views[r::N] over
-ranks (strong scaling, fixed global batch of 8).
+1/2/4/8 B200" is quoted on): 1M octahedra, SH degree 3, a batch of 8 views at 1600x1060.  One step
+is paper_2501_16312_b200.step.TrainStep: lp_preprocess of the local views; per view lp_bin_sort ->
+lp_render_fwd -> lp_loss_grad (3DGS L1 + SSIM) -> lp_raster_bwd (views over --streams CUDA
+streams); lp_preprocess_bwd_assign over the local views; N > 1: ONE NCCL all_reduce of the flat
+fp32 gradient (north_star; --sharded: reduce-scatter + sharded Adam + all-gather instead); the
+fused Adam (P:213, learning rates P:1169-1185).  Views are sharded views[r::N] over ranks (strong
+scaling of the fixed global batch of 8).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-  torchrun --nproc-per-node N bench.py --gpus N ...
+      --gpus N > 1 without WORLD_SIZE in the environment re-launches itself through
+      torch.distributed.run with N ranks (127.0.0.1); under torchrun --gpus must equal WORLD_SIZE.
+  python bench.py --gpus 2 --dry-run      (CPU: spawns the ranks over gloo and reports them; no GPU)
 
 --impl reference times the CPU oracle (oracle/, plain C fp64) on a bounded pixel sample of the
 same workload on the host cores (rank 0 only).
@@ -22,6 +24,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,10 +37,11 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 WORKLOAD = "C5"
+METRIC = "fwd+bwd Mpixel/s (C5 training step: 8 views, fwd+bwd+allreduce+Adam)"
 PAPER_FPS_CONTEXT = "paper (RTX 3090, forward only): octahedra 14.6 ms ScanNet++ 1752x1168, 34.6 ms Mip-NeRF360"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -46,9 +50,11 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override the primitive count (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--force-zero", action="store_true", help=argparse.SUPPRESS)   # exercise the sharded path at N = 1
-    ap.add_argument("--no-zero", action="store_true",
-                    help="N > 1: allreduce + replicated Adam instead of reduce-scatter + sharded Adam + all-gather")
+    ap.add_argument("--sharded", action="store_true",
+                    help="N > 1: reduce-scatter + Adam on 1/N of the parameters + all-gather instead of the "
+                         "single allreduce + replicated Adam")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch the ranks and check the process group over gloo on CPU; no GPU work")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--loss", default="l1ssim", choices=["l1ssim", "l1"],
                     help="training loss: 3DGS (1-0.2) L1 + 0.2 (1-SSIM) (P:212) or L1 only")
@@ -63,7 +69,7 @@ def parse():
                          "the preprocess of the others")
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop (ncu --profile-from-start off) and exit")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 # ------------------------------------------------------------------------------ clocks sampler
@@ -122,26 +128,36 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-# ------------------------------------------------------------------------------ work model
+# ------------------------------------------------------------------------------ work models
+#
+# Algorithmic work per launch.  Each raster kernel's fraction is reported under two
+# models side by side; `frac` is SURVEY §8(d)'s:
+#   K3 forward (lane instr.): §8(d) 28 I + 9 X (octa) / 16 I + 9 X (tetra);  builder 6 I + 24 B + 11 X (tetra 19 B)
+#   K4 backward:              §8(d) 36 I_b + 50 X + 32 W_h + 20 A with I_b = I (the pairs a reverse walk of
+#                             the processed lists visits);  builder 6 I + 30 B + 61 X (tetra 25 B)
+#   I iterated, B in-bbox, X intersected (pixel, entry) pairs; W_h (warp, entry) and A (tile, entry) pairs
+#   with a hit -- all counted by the untimed count_stats pass (LP_CNT_*).
+# HBM kernels (bytes per launch): K1 N F + v (24 N + 4 RW V_vis); K5 4 N v + 4 RG V_vis v + 3 N F (v views
+#   of the launch); K2 (lp_bin_sort, per view) §8(d) (24 + 24 P) E + 24 N with P = ceil(key bits / 8) 8-bit
+#   passes of the (tile|depth) key; Adam 28 B per parameter (32 without --assign).
 
-def fp32_ops(kind, iterated, inbox, intersected, backward):
-    """Algorithmic FP32-pipe lane instructions: every iterated (pixel, entry) pair
-    costs the bbox reject (2 FADD + 2 FSETP|abs + vote ~ 6); a pair inside the bbox costs the chord
-    (octahedron 4 x (FMUL FFMA 2 FADD 2 FMNMX) - 2 + 2 FADD = 24, tetrahedron 6 x 2 FFMA + 4 FMNMX
-    + 3 = 19); an intersected pair costs opacity + compositing (11).  The backward replays the same
-    and adds the argmax tracking (+6 per in-bbox pair) and 61 per intersected pair (blend backward
-    + slab/plane moments)."""
+def raster_work(kind, c, backward, model):
+    I, B, X, Wh, A = c["I"], c["B"], c["X"], c["Wh"], c["A"]
+    if model == "survey":
+        if not backward:
+            return (28 if kind == 0 else 16) * I + 9 * X
+        return 36 * I + 50 * X + 32 * Wh + 20 * A
     chord = 24 if kind == 0 else 19
     if not backward:
-        return 6 * iterated + chord * inbox + 11 * intersected
-    return 6 * iterated + (chord + 6) * inbox + 61 * intersected
+        return 6 * I + chord * B + 11 * X
+    return 6 * I + (chord + 6) * B + 61 * X
 
 
-def launches_per_view(n, tiles):
-    bits = max(1, math.ceil(math.log2(tiles)))
-    tile_passes = math.ceil(bits / 8)
-    sort_prims = 4 * 3
-    return sort_prims + 3 + 1 + 3 * tile_passes + 1 + 1 + 1 + 1   # depth sort | scan | emit | tile sort | ranges | fwd | l1 | raster bwd
+def load_json(path):
+    try:
+        return json.load(open(path))
+    except Exception:
+        return {}
 
 
 # ------------------------------------------------------------------------------ our implementation
@@ -151,7 +167,7 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2501_16312_b200 import linprim as L
-    from paper_2501_16312_b200 import render, scenegen, train
+    from paper_2501_16312_b200 import render, scenegen, step as S, train
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -159,11 +175,9 @@ def run_ours(args, rank, world, local_rank):
     n_views = len(cams)
     W, H = cams[0]["width"], cams[0]["height"]
     my_views = train.shard_views(n_views, rank, world)
-    # N > 1: sharded optimizer (reduce-scatter, Adam on 1/N of the parameters, all-gather)
-    zero = (world > 1 or args.force_zero) and not args.no_zero
-    total = sum(sz for _, sz in train.section_sizes(scene["kind"], scene["pos"].shape[1], scene["sh_degree"]))
-    lo, hi, chunk = train.shard_range(total, rank, world)
-    ds = render.DeviceScene(scene, device=dev, pad_to=world * chunk if zero else 0)
+    my_cams = [cams[v] for v in my_views]
+    kappa = 0.0 if args.exact else 0.1
+    ds = S.device_scene(scene, dev, world, args.sharded)
 
     # synthetic targets: the same scene with jittered centres, rendered once at setup
     rng = np.random.default_rng(1234)
@@ -171,169 +185,51 @@ def run_ours(args, rank, world, local_rank):
     tgt_scene["pos"] = (scene["pos"] + rng.normal(0, 0.01, scene["pos"].shape) *
                         scene["dist"].mean(0, keepdims=True)).astype(np.float32)
     tds = render.DeviceScene(tgt_scene, device=dev)
-    trend = render.Renderer(tds, [cams[v] for v in my_views], exact=args.exact, aa_kernel=0.0 if args.exact else 0.1)
-    targets = trend.forward()
+    targets = render.Renderer(tds, my_cams, exact=args.exact, aa_kernel=kappa).forward()
     torch.cuda.synchronize()
-    del trend, tds
+    del tds
 
-    # counters pass (untimed): per-view E, iterated and intersected pairs
-    rr = render.Renderer(ds, [cams[v] for v in my_views], count_stats=True, exact=args.exact,
-                         aa_kernel=0.0 if args.exact else 0.1)
-    img = torch.empty((len(my_views), 3, H, W), dtype=torch.float32, device=dev)
-    rr.forward(image=img)
+    # counters pass (untimed): per view E, I, B, X, W_h, A, visible primitives
+    rr = render.Renderer(ds, my_cams, count_stats=True, exact=args.exact, aa_kernel=kappa)
+    rr.forward()
     torch.cuda.synchronize()
     stats = [rr.counters(i) for i in range(len(my_views))]
-    caps = [rr.frames[i].capacity for i in range(len(my_views))]
     del rr
-    E = [int(s[L.LP_CNT_ENTRIES]) for s in stats]
-    it = [int(s[8]) | (int(s[9]) << 32) for s in stats]
-    hit = [int(s[10]) | (int(s[11]) << 32) for s in stats]
-    box = [int(s[12]) | (int(s[13]) << 32) for s in stats]
-    frustum = [int(s[L.LP_CNT_FRUSTUM]) for s in stats]
+    u64 = lambda s, k: int(s[k]) | (int(s[k + 1]) << 32)
+    cnt = {"E": [int(s[L.LP_CNT_ENTRIES]) for s in stats], "I": [u64(s, L.LP_CNT_ITERATED) for s in stats],
+           "X": [u64(s, L.LP_CNT_INTERSECTED) for s in stats], "B": [u64(s, L.LP_CNT_INBOX) for s in stats],
+           "Wh": [int(s[L.LP_CNT_WARP_HITS]) for s in stats], "A": [int(s[L.LP_CNT_TILE_HITS]) for s in stats],
+           "vis": [int(s[L.LP_CNT_VISIBLE]) for s in stats], "frustum": [int(s[L.LP_CNT_FRUSTUM]) for s in stats]}
 
-    # the timed renderer: async binning (no host sync), capacity sized from the counters pass
-    rend = render.Renderer(ds, [cams[v] for v in my_views], capacity=int(max(E) * 1.3) + 4096,
-                           exact=args.exact, aa_kernel=0.0 if args.exact else 0.1,
-                           sync_capacity=False)
-    st = torch.cuda.current_stream(dev)
-    dL = torch.empty_like(img)
-    n_local = len(my_views)
+    ts = S.TrainStep(ds, my_cams, n_views, targets=targets, loss=args.loss, streams=args.streams,
+                     split_pre=args.split_pre, assign=args.assign, exact=args.exact,
+                     capacity=int(max(cnt["E"]) * 1.3) + 4096, world=world, rank=rank, sharded=args.sharded,
+                     loss_slots=2 * (args.warmup + 3 * args.steps) + 64)
+    st = ts.st
+    n_local = ts.n_local
     total_steps = args.warmup + args.steps
-    loss_buf = torch.zeros(2 * total_steps + 64, dtype=torch.float32, device=dev)
-    m = torch.zeros(chunk if zero else ds.flat.numel(), dtype=torch.float32, device=dev)
-    v = torch.zeros_like(m)
-    gshard = torch.zeros(chunk, dtype=torch.float32, device=dev) if zero else None
-    # paper's learning rates; position 1.6e-4 x extent (3DGS), distances 2.6^-1 1e-4 x extent
-    n = ds.n
-    groups = train.lr_groups(ds.offsets, n, extent=4.0)
-    sgroups = train.shard_groups(groups, lo, hi) if zero else None
-    scale = 1.0 / (3.0 * W * H * n_views)
-    cams_c = rend.cams
-    ev_names = ["sort", "fwd", "loss", "rbwd"]         # per view
-    fa_all = render.frames_array(rend.frames)
-    ca_all = rend._cams(list(range(n_local)))
-    fa_view = [render.frames_array([rend.frames[i]]) for i in range(n_local)]
-    ca_view = [rend._cams([i]) for i in range(n_local)]
-    # views run round-robin on `--streams` CUDA streams so one view's sort kernels overlap another
-    # view's raster (views are independent between the fused preprocess and preprocess backward)
-    n_str = max(1, min(args.streams, n_local))
-    streams = [st] + [torch.cuda.Stream(dev) for _ in range(n_str - 1)]
-    fork = torch.cuda.Event()
-    fork2 = torch.cuda.Event()
-    joins = [torch.cuda.Event() for _ in streams[1:]]
-    # --split-pre: the views run on n_str auxiliary streams, the preprocess in two launches on `st`
-    aux = [torch.cuda.Stream(dev) for _ in range(n_str)] if args.split_pre else []
-    joins_aux = [torch.cuda.Event() for _ in aux]
-    pre_cams = [rend._cams(list(range(n_str))), rend._cams(list(range(n_str, n_local)))]
-    pre_frames = [render.frames_array([rend.frames[i] for i in range(n_str)]),
-                  render.frames_array([rend.frames[i] for i in range(n_str, n_local)])]
-
-    def rec(evl, j, stream):
-        if evl is not None:
-            evl[j].record(stream)
-
-    def step(si, events=None, tgt=None, serial=False, tgt_ready=None):
-        tg = targets if tgt is None else tgt
-        S = events[n_local] if events is not None else None
-        # preprocess of all local views in one launch (each primitive's features read once)
-        rec(S, 0, st)
-        for i in range(n_local):
-            fa_all[i] = fa_view[i][0]
-        strs = [st] if serial else streams
-        split = not serial and args.split_pre and n_local > len(strs)
-        if split:
-            # preprocess in two launches: the first wave of views (one per stream) starts binning
-            # while the second launch preprocesses the remaining views
-            nf = len(strs)
-            L.lp_preprocess(ds.prims, pre_cams[0], rend.cfg, pre_frames[0], st)
-            fork.record(st)
-            L.lp_preprocess(ds.prims, pre_cams[1], rend.cfg, pre_frames[1], st)
-            fork2.record(st)
-            for i in range(n_local):
-                fa_view[i][0] = pre_frames[0][i] if i < nf else pre_frames[1][i - nf]
-        else:
-            L.lp_preprocess(ds.prims, ca_all, rend.cfg, fa_all, st)
-            for i in range(n_local):
-                fa_view[i][0] = fa_all[i]
-        rec(S, 1, st)
-        if len(strs) > 1 and not split:
-            fork.record(st)
-            for s_ in strs[1:]:
-                s_.wait_event(fork)
-        for i in range(n_local):
-            sx = strs[i % len(strs)]
-            if split:
-                sx = aux[i % len(aux)]
-                sx.wait_event(fork if i < len(strs) else fork2)
-            ca, fa = ca_view[i], fa_view[i]
-            ev = events[i] if events is not None else None
-            rec(ev, 0, sx)
-            L.lp_bin_sort(ca, fa, sx, None)
-            rec(ev, 1, sx)
-            L.lp_render_fwd(ca, rend.cfg, fa, img[i], sx)
-            rec(ev, 2, sx)
-            if tgt_ready is not None:          # e2e: this view's target has arrived from the host
-                sx.wait_event(tgt_ready[i])
-            if args.loss == "l1":
-                L.lp_l1_grad(img[i], tg[i], dL[i], loss_buf[si:si + 1], scale, sx)
-            else:
-                L.lp_loss_grad(img[i], tg[i], dL[i], loss_buf[si:si + 1], 0.2, scale, sx)
-            rec(ev, 3, sx)
-            L.lp_raster_bwd(ca, rend.cfg, fa, dL[i], sx)
-            rec(ev, 4, sx)
-            fa_all[i] = fa[0]
-        if split:
-            for j, s_ in enumerate(aux):
-                joins_aux[j].record(s_)
-                st.wait_event(joins_aux[j])
-        elif len(strs) > 1:
-            for j, s_ in enumerate(strs[1:]):
-                joins[j].record(s_)
-                st.wait_event(joins[j])
-        # preprocess backward fused over this rank's views (feature + SH gradients written once)
-        # (assign: the step's gradient is SET here, so nothing zeroes it after the optimizer)
-        (L.lp_preprocess_bwd_assign if args.assign else L.lp_preprocess_bwd)(ds.prims, ca_all, rend.cfg, fa_all,
-                                                                             ds.grads, st)
-        rec(S, 2, st)
-        if world > 1 or zero:
-            if zero:
-                train.reduce_scatter_gradients(ds.grad_padded, gshard, world)
-                if not args.assign:
-                    ds.grad_padded.zero_()
-            else:
-                train.allreduce_gradients(ds.grad, world)
-        rec(S, 3, st)
-        if zero:   # Adam on this rank's shard, then the all-gather of the parameters (in the "adam" stage)
-            L.lp_adam_step(ds.flat_padded[rank * chunk:(rank + 1) * chunk], gshard, m, v, sgroups, 0.9, 0.999, 1e-15,
-                           si + 1, st, zero_grad=False)
-            train.all_gather_params(ds.flat_padded, rank, chunk)
-        else:
-            L.lp_adam_step(ds.flat, ds.grad, m, v, groups, 0.9, 0.999, 1e-15, si + 1, st, zero_grad=not args.assign)
-        rec(S, 4, st)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    def check_overflow(where):
+        assert not ts.overflowed(), f"tile-list capacity overflow ({where})"
+
     for s in range(args.warmup):
-        step(s)
+        ts.run(s)
     barrier()
     if args.profile_step:
         torch.cuda.profiler.start()
-        step(args.warmup)
+        ts.run(args.warmup)
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
         return None, None
-    # overflow check after warm-up (async binning must not have truncated)
-    for i in range(n_local):
-        c = rend.counters(i)
-        assert c[L.LP_CNT_OVERFLOW] == 0, "tile-list capacity overflow in the timed renderer"
+    check_overflow("warm-up")
 
     vis = [s for s in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if s.strip().isdigit()]
     clocks = ClockSampler(int(vis[local_rank]) if local_rank < len(vis) else local_rank)
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(n_local)] + [
-        [torch.cuda.Event(enable_timing=True) for _ in range(5)]] for _ in range(args.steps)]
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     clocks.start()
@@ -342,24 +238,27 @@ def run_ours(args, rank, world, local_rank):
     wall0 = time.perf_counter()
     t0.record(st)
     for k in range(args.steps):
-        step(args.warmup + k)
+        ts.run(args.warmup + k)
     t1.record(st)
     barrier()
     wall = time.perf_counter() - wall0
     clocks.stop()
-    ms = t0.elapsed_time(t1)
-    ms_t = torch.tensor([ms], device=dev)
+    check_overflow("timed loop")     # Adam moved the scene during the timed steps
+    ms_t = torch.tensor([t0.elapsed_time(t1)], device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    ms_step = ms_max / args.steps
+    ms_step = float(ms_t.item()) / args.steps
 
-    # per-stage averages (ms per view-call): an attribution region of the same K steps run with the
-    # views serialised on one stream and CUDA events around every stage
+    # ---------------- attribution: the same K steps with the views serialised on one stream and CUDA
+    # events around every stage (per view: sort, fwd, loss, raster bwd; per step: pre, pbwd, collective, adam)
+    ev_names = ["sort", "fwd", "loss", "rbwd"]
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(n_local)] +
+           [[torch.cuda.Event(enable_timing=True) for _ in range(5)]] for _ in range(args.steps)]
     barrier()
     for k in range(args.steps):
-        step(args.warmup + k, evs[k], serial=True)
+        ts.run(total_steps + k, t=args.warmup + k + 1, events=evs[k], serial=True)
     barrier()
+    check_overflow("attribution loop")
     stage = {nm: [] for nm in ev_names}
     pre, pb, ar, ad = [], [], [], []
     for k in range(args.steps):
@@ -367,79 +266,106 @@ def run_ours(args, rank, world, local_rank):
             e = evs[k][i]
             for j, nm in enumerate(ev_names):
                 stage[nm].append(e[j].elapsed_time(e[j + 1]))
-        S = evs[k][n_local]
-        pre.append(S[0].elapsed_time(S[1]))
-        pb.append(evs[k][n_local - 1][4].elapsed_time(S[2]))
-        ar.append(S[2].elapsed_time(S[3]))
-        ad.append(S[3].elapsed_time(S[4]))
+        Sv = evs[k][n_local]
+        pre.append(Sv[0].elapsed_time(Sv[1]))
+        pb.append(evs[k][n_local - 1][4].elapsed_time(Sv[2]))
+        ar.append(Sv[2].elapsed_time(Sv[3]))
+        ad.append(Sv[3].elapsed_time(Sv[4]))
     stage_ms = {nm: statistics.mean(vals) for nm, vals in stage.items()}
     stage_ms["pre_all_views"] = statistics.mean(pre)
     stage_ms["pbwd_all_views"] = statistics.mean(pb)
-    stage_ms["allreduce"] = statistics.mean(ar)
+    stage_ms["collective"] = statistics.mean(ar)
     stage_ms["adam"] = statistics.mean(ad)
     serial_step_ms = statistics.mean(evs[k][n_local][0].elapsed_time(evs[k][n_local][4]) for k in range(args.steps))
 
-    # rooflines of the single-kernel stages; the dominant one is reported as "roofline"
+    # ---------------- standalone all-reduce busbw probe of the step's gradient buffer (N > 1)
+    probe = None
+    if world > 1:
+        buf = torch.empty_like(ds.grad_padded)
+        buf.fill_(1.0)
+        for _ in range(3):
+            dist.all_reduce(buf)
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        a0.record(st)
+        for _ in range(reps):
+            dist.all_reduce(buf)
+        a1.record(st)
+        barrier()
+        t = torch.tensor([a0.elapsed_time(a1) / reps], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item()) * 1e-3
+        nbytes = buf.numel() * 4
+        algbw = nbytes / sec / 1e9
+        probe = {"bytes": nbytes, "ms": round(sec * 1e3, 4), "algbw_gbs": round(algbw, 1),
+                 "busbw_gbs": round(algbw * 2 * (world - 1) / world, 1), "nvlink_peak_gbs": 900.0,
+                 "step_collective_ms": round(stage_ms["collective"], 4)}
+        del buf
+
+    # ---------------- rooflines: per LAUNCH algorithmic work / per-launch time
     kind = ds.kind
-    I_tot, X_tot, B_tot = sum(it), sum(hit), sum(box)
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    alu_peak = 148 * 128 * 1965.0 * 1e6 / 1e12                          # T FP32 lane-instr/s at max SM clock
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"))
+    hbm_peak = float(peaks.get("hbm_gbs", 6550.0))
+    clk_max = float(peaks.get("sm_max_mhz", 1965.0))
+    alu_peak = 148 * 128 * clk_max * 1e6 / 1e12            # T FP32 lane-instr/s (nominal: unit counts x max clock)
+    ncu_db = load_json(os.path.join(ROOT, "profiles", "round2", "ncu_kernels.json"))
     K = ds.K
-    RG, RW = (20, 20) if kind == 0 else (22, 28)
+    RG, RW = (20, 20) if kind == 0 else (24, 28)
     ncoef = (ds.sh_degree + 1) ** 2
-    Fb = 4 * (3 + 4 + K + 1 + 3 * ncoef)                                # feature bytes per primitive
-    vis = statistics.mean([int(s[L.LP_CNT_VISIBLE]) for s in stats])
-    traffic_db = {}
-    prof_path = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof_path):
-        try:
-            traffic_db = json.load(open(prof_path))
-        except Exception:
-            traffic_db = {}
+    Fb = 4 * (3 + 4 + K + 1 + 3 * ncoef)                    # feature bytes per primitive
+    n = ds.n
+    mean = lambda k: statistics.mean(cnt[k])
+    per_view = {k: mean(k) for k in ("I", "B", "X", "Wh", "A", "E", "vis")}
+    tiles = ts.frames[0].c.tiles_x * ts.frames[0].c.tiles_y
+    key_bits = 32 + max(1, math.ceil(math.log2(tiles)))
+    P = math.ceil(key_bits / 8)
+    n_pre_launch = 2 if (args.split_pre and n_local > ts.n_str) else math.ceil(n_local / 8)
+    n_k5_launch = math.ceil(n_local / 4)
+    v_pre, v_k5 = n_local / n_pre_launch, n_local / n_k5_launch
+    params = ts.chunk if ts.sharded else ds.flat.numel()
+    # (kernel, bound, per-launch amount [§8(d)], per-launch amount [builder] or None, per-launch ms, launches/step)
     work = {
-        "fwd": ("k_raster_fwd", "alu", fp32_ops(kind, I_tot / n_local, B_tot / n_local, X_tot / n_local, False)),
-        "rbwd": ("k_raster_bwd", "alu", fp32_ops(kind, I_tot / n_local, B_tot / n_local, X_tot / n_local, True)),
-        # fused over the rank's views: tiles_touched + rgrad per view, features read and feature
-        # gradients read-modified-written once per call
-        "pbwd_all_views": ("k_preprocess_bwd", "hbm", 4 * n * n_local + vis * n_local * 4 * RG + n * 3 * Fb),
-        "pre_all_views": ("k_preprocess", "hbm", n * Fb + n_local * (n * 24 + vis * 4 * RW)),
-        # read p, g, m, v; write p, m, v (and g = 0 without --assign)
-        "adam": ("k_adam", "hbm", (28 if args.assign else 32) * (chunk if zero else ds.flat.numel())),
-        # separable 11-tap window: 5 products x 2 directions x 11 + 3 G maps x 2 x 11 FMA + ~30 for
-        # S and the G maps per pixel-channel; L1 only: 12 B per pixel-channel
-        "loss": ("k_loss_ssim_tma", "alu", 206 * 3 * W * H) if args.loss == "l1ssim" else ("k_l1_grad", "hbm", 12 * 3 * W * H),
+        "rbwd": ("k_raster_bwd", "alu", raster_work(kind, per_view, True, "survey"),
+                 raster_work(kind, per_view, True, "builder"), stage_ms["rbwd"], n_local),
+        "fwd": ("k_raster_fwd", "alu", raster_work(kind, per_view, False, "survey"),
+                raster_work(kind, per_view, False, "builder"), stage_ms["fwd"], n_local),
+        "pre_all_views": ("k_preprocess", "hbm", n * Fb + v_pre * (n * 24 + per_view["vis"] * 4 * RW), None,
+                          stage_ms["pre_all_views"] / n_pre_launch, n_pre_launch),
+        "pbwd_all_views": ("k_preprocess_bwd", "hbm", 4 * n * v_k5 + per_view["vis"] * v_k5 * 4 * RG + n * 3 * Fb,
+                           None, stage_ms["pbwd_all_views"] / n_k5_launch, n_k5_launch),
+        "sort": ("lp_bin_sort (K2)", "hbm", (24 + 24 * P) * per_view["E"] + 24 * n, None, stage_ms["sort"], n_local),
+        "adam": ("k_adam", "hbm", (28 if args.assign else 32) * params, None, stage_ms["adam"], 1),
+        "loss": (("k_loss_ssim_tma", "alu", 206 * 3 * W * H, None, stage_ms["loss"], n_local) if args.loss == "l1ssim"
+                 else ("k_l1_grad", "hbm", 12 * 3 * W * H, None, stage_ms["loss"], n_local)),
     }
     rooflines = {}
-    for key, (kname, bound, amount) in work.items():
-        sec = stage_ms[key] * 1e-3
+    for key, (kname, bound, amount, amount_b, ms_l, nl) in work.items():
+        sec = ms_l * 1e-3
         if bound == "alu":
             ach, pk, unit = amount / sec / 1e12, alu_peak, "T FP32 lane-instr/s"
         else:
             ach, pk, unit = amount / sec / 1e9, hbm_peak, "GB/s"
-        tr = traffic_db.get(kname)
-        # traffic: ncu dram read + write bytes per launch of this kernel (profiles/traffic.json), or null
-        rooflines[key] = {"kernel": kname, "bound": bound, "achieved": round(ach, 3), "peak": round(pk, 3),
-                          "unit": unit, "frac": round(ach / pk, 4), "traffic": tr["traffic_bytes"] if tr else None,
-                          "ms": round(stage_ms[key], 4), "traffic_detail": tr, "algorithmic_per_launch": int(amount)}
-    per_step = {k: stage_ms[k] * (1 if k in ("pbwd_all_views", "pre_all_views", "adam") else n_local) for k in work}
-    dom = max(work, key=lambda k: per_step[k])        # the kernel with the largest share of the step
-    for k in rooflines:
-        rooflines[k]["ms_per_step"] = round(per_step[k], 4)
+        nc = ncu_db.get(kname.split(" ")[0], {})
+        r = {"kernel": kname, "bound": bound, "achieved": round(ach, 3), "peak": round(pk, 3), "unit": unit,
+             "frac": round(ach / pk, 4), "traffic": nc.get("traffic_bytes"), "ms": round(ms_l, 4),
+             "algorithmic_per_launch": int(amount), "launches_per_step": nl,
+             "ms_per_step": round(ms_l * nl, 4)}
+        if amount_b is not None:
+            r["frac_builder_model"] = round(amount_b / sec / 1e12 / pk, 4)
+        if nc.get("thread_inst_executed") and bound == "alu":
+            r["frac_ncu_executed"] = round(nc["thread_inst_executed"] / sec / 1e12 / pk, 4)
+        if bound == "hbm" and nc.get("traffic_bytes"):
+            r["traffic_over_algorithmic"] = round(nc["traffic_bytes"] / amount, 3)
+        rooflines[key] = r
+    dom = max(rooflines, key=lambda k: rooflines[k]["ms_per_step"])
 
-    views_total = n_views
-    mpix = views_total * W * H / 1e6
+    mpix = n_views * W * H / 1e6
     value = mpix / (ms_step * 1e-3)
-    iters = 1000.0 / ms_step
 
     # ---------------- e2e: host (pinned) targets copied in and the loss read back every step
     e2e = None
     if not args.no_e2e:
-        # every step: H2D of that step's targets from pinned memory (prefetched one step ahead on a
-        # copy stream into a double buffer, one copy + event per view so a view's loss waits only for
-        # its own target) and a D2H read of that step's loss (pinned ring; the host waits for step
-        # k's loss while step k+1 is already queued)
         host_t = torch.empty(targets.shape, dtype=torch.float32, pin_memory=True)
         host_t.copy_(targets)
         dev_t = [torch.empty_like(targets), torch.empty_like(targets)]
@@ -448,8 +374,7 @@ def run_ours(args, rank, world, local_rank):
         freed = [torch.cuda.Event(), torch.cuda.Event()]
         loss_host = torch.zeros(args.steps, dtype=torch.float32, pin_memory=True)
         read = [torch.cuda.Event() for _ in range(args.steps)]
-        base = total_steps
-        loss_buf.zero_()
+        base = total_steps + args.steps
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
 
@@ -470,9 +395,9 @@ def run_ours(args, rank, world, local_rank):
                 if k >= 1:
                     cp.wait_event(freed[1 - b])
                 copy_in(1 - b)
-            step(base + k, tgt=dev_t[b], tgt_ready=copied[b])
+            ts.run(base + k, t=args.warmup + args.steps + k + 1, tgt=dev_t[b], tgt_ready=copied[b])
             freed[b].record(st)
-            loss_host[k:k + 1].copy_(loss_buf[base + k:base + k + 1], non_blocking=True)
+            loss_host[k:k + 1].copy_(ts.loss_buf[base + k:base + k + 1], non_blocking=True)
             read[k].record(st)
             if k >= 1:
                 read[k - 1].synchronize()
@@ -481,8 +406,8 @@ def run_ours(args, rank, world, local_rank):
         read[args.steps - 1].synchronize()
         losses.append(float(loss_host[args.steps - 1]))
         barrier()
-        e2e_ms = e0.elapsed_time(e1)
-        t = torch.tensor([e2e_ms], device=dev)
+        check_overflow("e2e loop")
+        t = torch.tensor([e0.elapsed_time(e1)], device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_step = float(t.item()) / args.steps
@@ -491,40 +416,40 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": int(host_t.numel() * 4 * world), "d2h_bytes_per_step": 4 * world,
                "ms_per_step": round(e2e_step, 3), "loss_last": losses[-1]}
 
-    # + the preprocess launches (8 views per launch; two with --split-pre), the preprocess backward
-    # (4 views per launch, LP_K5_MAXV) and one Adam per step
-    n_pre = 2 if (args.split_pre and n_local > n_str) else math.ceil(n_local / 8)
-    launches = args.steps * (n_local * launches_per_view(n, rend.frames[0].c.tiles_x * rend.frames[0].c.tiles_y) +
-                             n_pre + math.ceil(n_local / 4) + 1)
-
+    mode = ("sharded Adam (reduce-scatter / all-gather)" if ts.sharded else "one NCCL all_reduce + replicated Adam") \
+        if world > 1 else "single GPU"
     out = {
-        "metric": "fwd+bwd Mpixel/s (C5 training step: 8 views, fwd+bwd+allreduce+Adam)",
+        "metric": METRIC,
         "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (seeded scenegen, BASELINE configs[4] shape; random-init features)",
-        "iters_per_s": round(iters, 3),
+        "iters_per_s": round(1000.0 / ms_step, 3),
         "config": {"workload": "C5: 1M octahedra, SH deg 3, 8 views 1600x1060, training step (views sharded)",
                    "loss": "3DGS 0.8 L1 + 0.2 (1 - SSIM)" if args.loss == "l1ssim" else "L1",
                    "projection": "no ray space (App. D)" if args.exact else "EWA ray space",
-                   "n_primitives": n, "kind": "octahedron", "sh_degree": 3, "global_batch_views": views_total,
-                   "views_per_gpu": n_local, "width": W, "height": H, "parallelism": f"dp{world} (views)" + (", sharded Adam (reduce-scatter / all-gather)" if zero else ""),
+                   "n_primitives": n, "kind": "octahedron", "sh_degree": 3, "global_batch_views": n_views,
+                   "views_per_gpu": n_local, "width": W, "height": H,
+                   "parallelism": f"dp{world} (views), {mode}",
                    "l2": "inputs larger than L2: features+grads+Adam state = %.2f GB touched per step"
                          % (ds.flat.numel() * 4 * 5 / 1e9),
-                   "tile_list_entries_per_view": E, "iterated_pairs_per_px": round(I_tot / (n_local * W * H), 2),
-                   "intersected_pairs_per_px": round(X_tot / (n_local * W * H), 2),
-                   "in_bbox_pairs_per_px": round(B_tot / (n_local * W * H), 2),
-                   "frustum_primitives_per_view": frustum, "capacity": caps},
-        "streams": n_str,
+                   "tile_list_entries_per_view": cnt["E"],
+                   "iterated_pairs_per_px": round(sum(cnt["I"]) / (n_local * W * H), 2),
+                   "intersected_pairs_per_px": round(sum(cnt["X"]) / (n_local * W * H), 2),
+                   "in_bbox_pairs_per_px": round(sum(cnt["B"]) / (n_local * W * H), 2),
+                   "warp_hit_pairs_per_view": cnt["Wh"], "tile_hit_pairs_per_view": cnt["A"],
+                   "frustum_primitives_per_view": cnt["frustum"], "capacity": [f.capacity for f in ts.frames]},
+        "streams": ts.n_str,
         "stages_ms_per_view": {k: round(v, 4) for k, v in stage_ms.items()},
         "serial_step_ms": round(serial_step_ms, 3),
-        "roofline": dict(rooflines[dom], peak_source="measured HBM copy (MEASURED_PEAKS.json)" if
-                         work[dom][1] == "hbm" else "148 SM x 128 FP32 lanes x 1965 MHz (B200_PROFILING unit counts)"),
+        "roofline": dict(rooflines[dom], peak_source=(
+            "measured HBM copy (MEASURED_PEAKS.json)" if rooflines[dom]["bound"] == "hbm" else
+            "nominal: 148 SM x 128 FP32 lanes x %.0f MHz (B200_PROFILING unit counts; no measured FP32 peak)" % clk_max)),
         "rooflines": rooflines,
-        "e2e": e2e, "gpu_launches": launches, "wall_s_timed": round(wall, 3),
+        "allreduce_probe": probe,
+        "e2e": e2e, "gpu_launches": ts.kernel_launches() * args.steps, "wall_s_timed": round(wall, 3),
         "context": PAPER_FPS_CONTEXT,
     }
-    clk = clocks.summary()
-    out["clocks"] = clk
+    out["clocks"] = clocks.summary()
     return out, (scene, cams, my_views)
 
 
@@ -591,34 +516,83 @@ def run_reference(args, rank, world):
             "e2e": {"value": round(value, 6), "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run with N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "4"))
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args, rank, world):
+    """Process-group check without GPU work: every rank joins over gloo and contributes its rank."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.zeros(world, dtype=torch.int64)
+    t[rank] = 1 + rank
+    if world > 1:
+        dist.all_reduce(t)
+    from paper_2501_16312_b200 import train
+    out = {"dry_run": True, "n_gpus": world, "ranks_seen": [int(x) - 1 for x in t.tolist()],
+           "views_per_rank": [train.shard_views(8, r, world) for r in range(world)]}
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        sys.exit(relaunch(args))
+    world = int(env_world or "1")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a number "
+                                   f"for a different GPU count"}), flush=True)
+        sys.exit(2)
+    if args.dry_run:
+        return dry_run(args, rank, world)
     if args.impl == "reference":
         out = run_reference(args, rank, world)
         if out is not None:
-            print(json.dumps(out))
+            print(json.dumps(out), flush=True)
         return
     import torch
-    use_dist = world > 1 or args.force_zero
-    if use_dist:
+    if torch.cuda.device_count() < local_rank + 1:
+        raise SystemExit(f"rank {rank}: {torch.cuda.device_count()} visible GPUs, local rank {local_rank} has none")
+    if world > 1:
         import torch.distributed as dist
+        if rank == 0:                      # NCCL init lines (rank count, NVLS / ring) on stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out, ctx = run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
     if out is None:
         return
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             scene, cams, _ = ctx
             out["cpu_baseline"] = cpu_baseline(scene, cams)
-        print(json.dumps(out))
-    if use_dist:
-        import torch.distributed as dist
-        dist.barrier()
-        dist.destroy_process_group()
+        print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":

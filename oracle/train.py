@@ -97,19 +97,32 @@ def flat(grads: "oracle.Grads"):
 
 
 def c5_step(scene: "oracle.Scene", cams, targets, groups, m, v, t, lam=oloss.LAMBDA, kappa=0.1, t_stop=1e-3,
-            bg=(0.0, 0.0, 0.0), b1=0.9, b2=0.999, eps=1e-15):
+            bg=(0.0, 0.0, 0.0), b1=0.9, b2=0.999, eps=1e-15, bounds=False, face_margin=2e-5, clamp_margin=1e-6,
+            mode=0):
     """One training iteration over the views `cams`.  Returns a dict with the loss, the
     images [V,3,H,W], dL/dimage [V,3,H,W], the summed flat gradient, the new flat parameters, m, v
-    and the per-view forward results (for margins)."""
-    fwd = [oracle.forward(scene, c, kappa=kappa, t_stop=t_stop, bg=bg) for c in cams]
+    and the per-view forward results.  bounds=True adds (test tolerances only) the summed flat
+    conditioning bound of the gradient, the primitives any view flags for an entry / exit face within
+    `face_margin` of switching, and the (primitive, channel) colour clamps within `clamp_margin`.
+    mode: geometry precision of oracle.preprocess (0 canonical fp32, 1 fp64 for finite differences)."""
+    fwd = [oracle.forward(scene, c, kappa=kappa, t_stop=t_stop, bg=bg, mode=mode) for c in cams]
     X = np.stack([f.out.image for f in fwd])
     L, dL = oloss.batch_loss_and_grad(X, np.asarray(targets, np.float64), lam)
-    gsum = None
+    gsum = bsum = None
+    flagged = clamp = None
     for f, c, d in zip(fwd, cams, dL):
         rb = oracle.render(scene, c, f.pre, f.vals, f.ranges, bg=bg, t_stop=t_stop,
-                           dL_dimage=d.astype(np.float32))
+                           dL_dimage=d.astype(np.float32), bounds=bounds)
         gv = flat(oracle.preprocess_bwd(scene, c, f.pre, rb))
         gsum = gv if gsum is None else gsum + gv
+        if bounds:
+            bv = flat(oracle.feature_bounds(scene, c, f.pre, rb))
+            bsum = bv if bsum is None else bsum + bv
+            fl = rb.face_margin < face_margin
+            cl = (np.abs(f.pre.rgb_raw) < clamp_margin) & (f.pre.flag == 0)[:, None]
+            flagged = fl if flagged is None else flagged | fl
+            clamp = cl if clamp is None else clamp | cl
     p0 = np.concatenate([np.asarray(getattr(scene, k), np.float64).reshape(-1) for k in SECTIONS])
     p1, m1, v1 = adam_step(p0, gsum, m, v, groups, t, b1, b2, eps)
-    return {"loss": L, "images": X, "dL": dL, "grad": gsum, "p": p1, "m": m1, "v": v1, "fwd": fwd}
+    return {"loss": L, "images": X, "dL": dL, "grad": gsum, "p0": p0, "p": p1, "m": m1, "v": v1, "fwd": fwd,
+            "bound": bsum, "flagged": flagged, "clamp": clamp}

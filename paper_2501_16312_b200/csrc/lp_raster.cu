@@ -755,11 +755,39 @@ static void fwd_x(const lp_frame &F, const lp_camera &cam, const lp_raster_cfg &
   }
 }
 
+// count_stats: the backward's work counters from the forward's hit bits (SURVEY §8d K4 model):
+// W_h = (warp, entry) pairs with a hit (popcount of the four warp rows), A = (tile, entry) pairs
+// with a hit in any warp (popcount of their OR; entries of different tiles are disjoint)
+__global__ void __launch_bounds__(256) k_hit_stats(const uint32_t *__restrict__ hitmask, int64_t words_per_row,
+                                                   uint32_t *__restrict__ counters) {
+  const int64_t nw = ((int64_t)min(counters[LP_CNT_ENTRIES], (uint32_t)(words_per_row - 2) * 32u) + 31) / 32;
+  uint32_t wh = 0, a = 0;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t r0 = hitmask[w], r1 = hitmask[words_per_row + w], r2 = hitmask[2 * words_per_row + w],
+                   r3 = hitmask[3 * words_per_row + w];
+    wh += __popc(r0) + __popc(r1) + __popc(r2) + __popc(r3);
+    a += __popc(r0 | r1 | r2 | r3);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    wh += __shfl_xor_sync(0xffffffffu, wh, o);
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(counters + LP_CNT_WARP_HITS, wh);
+    atomicAdd(counters + LP_CNT_TILE_HITS, a);
+  }
+}
+
 void launch_raster_fwd(const lp_frame &F, const lp_camera &cam, const lp_raster_cfg &cfg, float *image, float *depth,
                        float *alpha, cudaStream_t st) {
   cudaMemsetAsync(F.hitmask, 0, sizeof(uint32_t) * 4 * (size_t)hit_words(F.capacity), st);   // the backward's hit bits
   if (cfg.exact) fwd_x<true>(F, cam, cfg, image, depth, alpha, st);
   else fwd_x<false>(F, cam, cfg, image, depth, alpha, st);
+  if (cfg.count_stats) {
+    cudaMemsetAsync(F.counters + LP_CNT_WARP_HITS, 0, 8, st);
+    k_hit_stats<<<148, 256, 0, st>>>(F.hitmask, hit_words(F.capacity), F.counters);
+  }
 }
 
 void launch_raster_bwd(const lp_frame &F, const lp_camera &cam, const lp_raster_cfg &cfg, const float *dL,

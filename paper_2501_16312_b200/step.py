@@ -1,0 +1,194 @@
+"""The C5 training iteration: the launch sequence of one step over this
+rank's views -- host-side sequencing of C-ABI calls only (streams, events, the one collective).
+
+Per step:
+  lp_preprocess of all local views (two launches with split_pre so the first wave bins early)
+  per local view, round-robin over `streams` CUDA streams:
+      lp_bin_sort -> lp_render_fwd -> lp_loss_grad (3DGS L1 + SSIM) | lp_l1_grad -> lp_raster_bwd
+  lp_preprocess_bwd_assign over all local views (the step's gradient is SET: no zeroing pass)
+  N > 1: ONE NCCL all_reduce(SUM) of the flat fp32 gradient (north_star), then the replicated
+         fused Adam (lp_adam_step) -- or, with sharded=True, reduce_scatter + Adam on this rank's
+         chunk + all_gather of the parameters (same wire bytes, 1/N of the Adam work)
+bench.py times exactly this object; tests/test_gpu_step.py compares one step of it with
+oracle/train.py.c5_step.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import linprim as L
+from . import render, train
+
+
+def device_scene(scene, device, world=1, sharded=False):
+    """DeviceScene padded for the sharded optimizer when it is used (world * chunk elements)."""
+    total = sum(sz for _, sz in train.section_sizes(scene["kind"], scene["pos"].shape[1], scene["sh_degree"]))
+    _, _, chunk = train.shard_range(total, 0, world)
+    return render.DeviceScene(scene, device=device, pad_to=world * chunk if sharded and world > 1 else 0)
+
+
+class TrainStep:
+    """One training iteration of LinPrim over the local views `cams` of a global batch of
+    `n_views_total` views (views[r::N] on rank r)."""
+
+    def __init__(self, ds: render.DeviceScene, cams, n_views_total, *, targets=None, loss="l1ssim", lam=0.2,
+                 streams=4, split_pre=True, assign=True, exact=False, capacity=None, world=1, rank=0,
+                 sharded=False, extent=4.0, betas=(0.9, 0.999), eps=1e-15, loss_slots=256, aa_kernel=None):
+        dev = ds.flat.device
+        self.ds, self.dev = ds, dev
+        self.n_local = len(cams)
+        self.world, self.rank = world, rank
+        self.sharded = bool(sharded) and world > 1
+        self.loss_kind, self.lam = loss, lam
+        self.assign, self.split_pre = assign, split_pre
+        self.betas, self.eps = betas, eps
+        W, H = cams[0]["width"], cams[0]["height"]
+        self.W, self.H = W, H
+        kappa = (0.0 if exact else 0.1) if aa_kernel is None else aa_kernel
+        self.rend = render.Renderer(ds, cams, capacity=capacity, exact=exact, aa_kernel=kappa, sync_capacity=False)
+        self.img = torch.empty((self.n_local, 3, H, W), dtype=torch.float32, device=dev)
+        self.dL = torch.empty_like(self.img)
+        self.targets = targets
+        self.loss_buf = torch.zeros(loss_slots, dtype=torch.float32, device=dev)
+        self.scale = 1.0 / (3.0 * W * H * n_views_total)       # mean over views of the per-view means
+        groups = train.lr_groups(ds.offsets, ds.n, extent=extent)
+        self.groups = groups
+        if self.sharded:
+            lo, hi, chunk = train.shard_range(ds.total, rank, world)
+            self.chunk = chunk
+            self.sgroups = train.shard_groups(groups, lo, hi)
+            self.m = torch.zeros(chunk, dtype=torch.float32, device=dev)
+            self.gshard = torch.zeros(chunk, dtype=torch.float32, device=dev)
+        else:
+            self.m = torch.zeros(ds.flat.numel(), dtype=torch.float32, device=dev)
+        self.v = torch.zeros_like(self.m)
+        st = torch.cuda.current_stream(dev)
+        self.st = st
+        n = self.n_local
+        rend = self.rend
+        self.fa_all = render.frames_array(rend.frames)
+        self.ca_all = rend._cams(list(range(n)))
+        self.fa_view = [render.frames_array([rend.frames[i]]) for i in range(n)]
+        self.ca_view = [rend._cams([i]) for i in range(n)]
+        self.n_str = max(1, min(streams, n))
+        self.streams = [st] + [torch.cuda.Stream(dev) for _ in range(self.n_str - 1)]
+        self.fork, self.fork2 = torch.cuda.Event(), torch.cuda.Event()
+        self.joins = [torch.cuda.Event() for _ in self.streams[1:]]
+        self.aux = [torch.cuda.Stream(dev) for _ in range(self.n_str)] if split_pre else []
+        self.joins_aux = [torch.cuda.Event() for _ in self.aux]
+        ns = self.n_str
+        self.pre_cams = [rend._cams(list(range(min(ns, n)))), rend._cams(list(range(min(ns, n), n)))]
+        self.pre_frames = [render.frames_array([rend.frames[i] for i in range(min(ns, n))]),
+                           render.frames_array([rend.frames[i] for i in range(min(ns, n), n)])]
+
+    # ------------------------------------------------------------------------------------------
+    @property
+    def frames(self):
+        return self.rend.frames
+
+    def counters(self, i):
+        return self.rend.counters(i)
+
+    def overflowed(self):
+        """True if any local view's tile list overflowed its capacity (async binning; synchronises)."""
+        return any(int(self.counters(i)[L.LP_CNT_OVERFLOW]) != 0 for i in range(self.n_local))
+
+    def kernel_launches(self):
+        """Launches of liblinprim kernels one step enqueues (bench.py's gpu_launches claim)."""
+        import math
+        F = self.rend.frames[0].c
+        tiles = F.tiles_x * F.tiles_y
+        tile_passes = math.ceil(max(1, math.ceil(math.log2(tiles))) / 8)
+        per_view = 4 * 3 + 3 + 1 + 3 * tile_passes + 1 + 1 + 1 + 1   # depth sort|scan|emit|tile sort|ranges|fwd|loss|rbwd
+        n_pre = 2 if (self.split_pre and self.n_local > self.n_str) else math.ceil(self.n_local / 8)
+        return self.n_local * per_view + n_pre + math.ceil(self.n_local / 4) + 1
+
+    # ------------------------------------------------------------------------------------------
+    def run(self, si, t=None, tgt=None, events=None, serial=False, tgt_ready=None):
+        """Enqueue one step on the current stream.  si: loss slot; t: Adam step (default si + 1);
+        tgt: [n_local,3,H,W] device targets (default self.targets); events: per-view + step events
+        (bench attribution); serial: all views on one stream; tgt_ready: per-view events the loss
+        waits for (e2e host copies)."""
+        L_ = L
+        st = self.st
+        n_local = self.n_local
+        tg = self.targets if tgt is None else tgt
+        t = si + 1 if t is None else t
+        S = events[n_local] if events is not None else None
+
+        def rec(evl, j, stream):
+            if evl is not None:
+                evl[j].record(stream)
+
+        rec(S, 0, st)
+        for i in range(n_local):
+            self.fa_all[i] = self.fa_view[i][0]
+        strs = [st] if serial else self.streams
+        split = not serial and self.split_pre and n_local > len(strs)
+        if split:
+            nf = len(strs)
+            L_.lp_preprocess(self.ds.prims, self.pre_cams[0], self.rend.cfg, self.pre_frames[0], st)
+            self.fork.record(st)
+            L_.lp_preprocess(self.ds.prims, self.pre_cams[1], self.rend.cfg, self.pre_frames[1], st)
+            self.fork2.record(st)
+            for i in range(n_local):
+                self.fa_view[i][0] = self.pre_frames[0][i] if i < nf else self.pre_frames[1][i - nf]
+        else:
+            L_.lp_preprocess(self.ds.prims, self.ca_all, self.rend.cfg, self.fa_all, st)
+            for i in range(n_local):
+                self.fa_view[i][0] = self.fa_all[i]
+        rec(S, 1, st)
+        if len(strs) > 1 and not split:
+            self.fork.record(st)
+            for s_ in strs[1:]:
+                s_.wait_event(self.fork)
+        for i in range(n_local):
+            sx = strs[i % len(strs)]
+            if split:
+                sx = self.aux[i % len(self.aux)]
+                sx.wait_event(self.fork if i < len(strs) else self.fork2)
+            ca, fa = self.ca_view[i], self.fa_view[i]
+            ev = events[i] if events is not None else None
+            rec(ev, 0, sx)
+            L_.lp_bin_sort(ca, fa, sx, None)
+            rec(ev, 1, sx)
+            L_.lp_render_fwd(ca, self.rend.cfg, fa, self.img[i], sx)
+            rec(ev, 2, sx)
+            if tgt_ready is not None:
+                sx.wait_event(tgt_ready[i])
+            if self.loss_kind == "l1":
+                L_.lp_l1_grad(self.img[i], tg[i], self.dL[i], self.loss_buf[si:si + 1], self.scale, sx)
+            else:
+                L_.lp_loss_grad(self.img[i], tg[i], self.dL[i], self.loss_buf[si:si + 1], self.lam, self.scale, sx)
+            rec(ev, 3, sx)
+            L_.lp_raster_bwd(ca, self.rend.cfg, fa, self.dL[i], sx)
+            rec(ev, 4, sx)
+            self.fa_all[i] = fa[0]
+        if split:
+            for j, s_ in enumerate(self.aux):
+                self.joins_aux[j].record(s_)
+                st.wait_event(self.joins_aux[j])
+        elif len(strs) > 1:
+            for j, s_ in enumerate(strs[1:]):
+                self.joins[j].record(s_)
+                st.wait_event(self.joins[j])
+        ds = self.ds
+        (L_.lp_preprocess_bwd_assign if self.assign else L_.lp_preprocess_bwd)(ds.prims, self.ca_all, self.rend.cfg,
+                                                                               self.fa_all, ds.grads, st)
+        rec(S, 2, st)
+        b1, b2 = self.betas
+        if self.sharded:
+            train.reduce_scatter_gradients(ds.grad_padded, self.gshard, self.world)
+            if not self.assign:
+                ds.grad_padded.zero_()
+            rec(S, 3, st)
+            c = self.chunk
+            L_.lp_adam_step(ds.flat_padded[self.rank * c:(self.rank + 1) * c], self.gshard, self.m, self.v,
+                            self.sgroups, b1, b2, self.eps, t, st, zero_grad=False)
+            train.all_gather_params(ds.flat_padded, self.rank, c)
+        else:
+            train.allreduce_gradients(ds.grad, self.world)
+            rec(S, 3, st)
+            L_.lp_adam_step(ds.flat, ds.grad, self.m, self.v, self.groups, b1, b2, self.eps, t, st,
+                            zero_grad=not self.assign)
+        rec(S, 4, st)

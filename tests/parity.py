@@ -91,15 +91,17 @@ def grad_close(name, got, ref, flagged=None, rtol=GRAD_RTOL, atol_rel=GRAD_ATOL_
 CLAMP_MARGIN = 1e-6     # |SH colour before max(0, .)| below this: the clamp may flip in fp32 (both valid; seen: 9.5e-9)
 
 
-def check_gradients(gd, g, gb, pre, flagged, loose=1e-1):
+def check_gradients(gd, g, gb, pre, flagged, loose=1e-1, clamp=None):
     """All five feature-gradient groups of the CUDA path (gd, torch) against the oracle's (g), with
     the oracle's conditioning bounds gb (oracle.feature_bounds, or None).  A colour channel whose
     clamp decision is within rounding of 0 is excluded from the SH comparison and its primitive
     flagged (the SH direction term of its position gradient flips with it).
     Returns (worst ratio per group, report strings, elements that needed the conditioning term,
-    clamp-margin channels); asserts nothing."""
-    clamp = np.abs(pre.rgb_raw) < CLAMP_MARGIN if pre.rgb_raw is not None else np.zeros((len(pre.flag), 3), bool)
-    clamp &= (pre.flag == 0)[:, None]
+    clamp-margin channels); asserts nothing.  clamp: precomputed [n, 3] clamp-margin mask (a multi-view
+    step: the union over views), else taken from pre.rgb_raw."""
+    if clamp is None:
+        clamp = np.abs(pre.rgb_raw) < CLAMP_MARGIN
+        clamp &= (pre.flag == 0)[:, None]
     fl = flagged | clamp.any(1)
     worst, reps, n_cond = {}, [], 0
     ok_all = True

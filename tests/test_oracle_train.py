@@ -83,3 +83,57 @@ def test_update_sensitivity_by_finite_differences():
     pp = otr.adam_step(np.zeros(n), g + h, m, v, groups, 4, eps=1e-12)[0]
     pm = otr.adam_step(np.zeros(n), g - h, m, v, groups, 4, eps=1e-12)[0]
     np.testing.assert_allclose(np.abs((pp - pm) / (2 * h)), s, rtol=1e-5)
+
+
+def test_c5_step_gradient_is_the_batch_loss_derivative():
+    """c5_step's summed gradient (loss -> per-view dL/dimage -> render backward -> preprocess backward
+    -> sum over views) equals central finite differences of the batch loss (the mean of the per-view
+    3DGS losses) w.r.t. features, on a tiny two-view scene in fp64 geometry; and the returned
+    parameters are adam_step of that gradient."""
+    from oracle import loss as oloss
+    from paper_2501_16312_b200 import scenegen
+    from tests.helpers import oscene
+    scene, cams = scenegen.make_scene("C5", seed=3, n=400)
+    cams = [dict(c, width=24, height=20, cx=np.float32(12), cy=np.float32(10), fx=np.float32(14.0),
+                 fy=np.float32(14.0)) for c in cams[:2]]
+    osc = oscene(scene)
+    imgs = np.stack([oracle.forward(osc, c, kappa=0.0, mode=1, t_stop=0.0).out.image for c in cams])
+    rng = np.random.default_rng(0)
+    targets = imgs + rng.choice([-1, 1], imgs.shape) * rng.uniform(0.05, 0.1, imgs.shape)
+    n = scene["pos"].shape[1]
+    groups = otr.lr_table(oracle.OCTA, n, 3, 4.0)
+    z = np.zeros(groups[-1][1])
+    r = otr.c5_step(osc, cams, targets, groups, z, z, 1, kappa=0.0, t_stop=0.0, mode=1)
+
+    def batch_loss(sc):
+        X = np.stack([oracle.forward(sc, c, kappa=0.0, mode=1, t_stop=0.0).out.image for c in cams])
+        return oloss.batch_loss_and_grad(X, targets)[0]
+
+    off = otr.offsets(oracle.OCTA, n, 3)
+    go = np.abs(r["grad"][off["opacity"][0]:off["opacity"][1]])
+    touched = np.argsort(-go)[:3]
+    touched = touched[go[touched] > 0]
+    assert touched.size >= 2
+    checked = 0
+    for i in touched:
+        for name, comp in (("opacity", None), ("pos", 0), ("sh", 0)):
+            sc = {k: np.array(v, copy=True) for k, v in scene.items() if isinstance(v, np.ndarray)}
+            sc.update(kind=scene["kind"], sh_degree=scene["sh_degree"])
+            arr = sc[name]
+            idx = (i,) if comp is None else ((comp, i) if arr.ndim == 2 else (0, comp, i))
+            h = 1e-3 if name != "pos" else 1e-4
+            base = float(arr[idx])
+            vals = []
+            for sgn in (1, -1):
+                arr[idx] = np.float32(base + sgn * h)
+                vals.append(batch_loss(oscene(sc)))
+            arr[idx] = np.float32(base)
+            hh = (np.float64(np.float32(base + h)) - np.float64(np.float32(base - h))) / 2
+            fd = (vals[0] - vals[1]) / (2 * hh)
+            flat_i = off[name][0] + (np.ravel_multi_index(idx, arr.shape))
+            an = r["grad"][flat_i]
+            assert abs(fd - an) <= 2e-3 * abs(an) + 1e-9, (name, i, fd, an)
+            checked += 1
+    assert checked >= 6
+    p1, _, _ = otr.adam_step(r["p0"], r["grad"], z, z, groups, 1)
+    np.testing.assert_array_equal(p1, r["p"])
