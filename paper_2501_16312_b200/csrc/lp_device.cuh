@@ -726,34 +726,26 @@ __device__ __forceinline__ float optical_depth(float sigma, float chord) { retur
 __device__ __forceinline__ float transmit_x(float x) { return ex2_ftz(fm(-x, 1.44269504f)); }
 __device__ __forceinline__ float transmit(float sigma, float chord) { return transmit_x(optical_depth(sigma, chord)); }
 
-// opacity o = 1 - exp(-x) = -expm1(-x) to ~4e-7 relative for every x >= 0.  1 - E cancels
+// opacity o = 1 - exp(-x) = -expm1(-x) to ~4e-6 relative for every x >= 0.  1 - E cancels
 // for small x: an E near 1 carries ex2.approx's ~2^-22 relative error into o as 2^-22 / x (a
 // primitive with x = 1e-4 got o wrong by 0.3 %, and its colour gradient sum_p T o G -- strongly
-// cancelling under a random-sign upstream -- by the same factor).  Below x = 0.5, o is the Taylor
-// series of -expm1(-x) to degree 8 in Horner form (truncation x^8 / 9! < 1.1e-8 relative); above
-// it 1 - E loses at most E / o < 1.6 of E's relative error.
+// cancelling under a random-sign upstream -- by the same factor).  Below x = 1/16, o is the Taylor
+// series of -expm1(-x) to degree 4 in Horner form (truncation x^4 / 5! < 1.3e-7 relative); above
+// it 1 - E loses at most E / o < 16 times E's relative error.
 __device__ __forceinline__ float opacity_x(float x, float E) {
-  float p = fmaf(x, -2.48015873e-05f, 1.98412698e-04f);   // -1/8!, 1/7!
-  p = fmaf(x, p, -1.38888889e-03f);                        // -1/6!
-  p = fmaf(x, p, 8.33333333e-03f);                         //  1/5!
-  p = fmaf(x, p, -4.16666667e-02f);                        // -1/4!
-  p = fmaf(x, p, 1.66666667e-01f);                         //  1/3!
+  float p = fmaf(x, -4.16666667e-02f, 1.66666667e-01f);   // -1/4!, 1/3!
   p = fmaf(x, p, -0.5f);
   p = fmaf(x, p, 1.f);
-  return x < 0.5f ? p * x : 1.f - E;
+  return x < 0.0625f ? p * x : 1.f - E;
 }
 // the same for a pixel pair (FFMA2 lanes; each lane bitwise the scalar opacity_x)
 __device__ __forceinline__ float2 opacity_x2(float2 x, float2 E) {
-  float2 p = ffma2(x, bc(-2.48015873e-05f), bc(1.98412698e-04f));
-  p = ffma2(x, p, bc(-1.38888889e-03f));
-  p = ffma2(x, p, bc(8.33333333e-03f));
-  p = ffma2(x, p, bc(-4.16666667e-02f));
-  p = ffma2(x, p, bc(1.66666667e-01f));
+  float2 p = ffma2(x, bc(-4.16666667e-02f), bc(1.66666667e-01f));
   p = ffma2(x, p, bc(-0.5f));
   p = ffma2(x, p, bc(1.f));
   p = fmul2(p, x);
   const float2 q = fsub2(bc(1.f), E);
-  return make_float2(x.x < 0.5f ? p.x : q.x, x.y < 0.5f ? p.y : q.y);
+  return make_float2(x.x < 0.0625f ? p.x : q.x, x.y < 0.0625f ? p.y : q.y);
 }
 
 // smallest stop threshold the raster uses: t_stop below it is raised to it (reading 28).

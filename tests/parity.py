@@ -88,6 +88,23 @@ def grad_close(name, got, ref, flagged=None, rtol=GRAD_RTOL, atol_rel=GRAD_ATOL_
                                  f"scale {scale:.3g} bound {0.0 if bound is None else np.asarray(bound)[idx]:.3g}"), n_cond
 
 
+# ray-space centre / offsets this far from the pixels (in pixels): the fp32 pixel offsets r - c_r of the
+# primitive carry >= 2^-10 px of rounding, which its moment -> vertex chain (M^-1 of offsets ~1e5 px)
+# amplifies; such primitives (near the camera plane, off-screen centres) are flagged
+SCREEN_SCALE = 8192.0
+
+
+def screen_flags(pre, exact=False):
+    """Primitives whose ray-space geometry spans >= SCREEN_SCALE pixels (ray-space mode only)."""
+    if exact:
+        return np.zeros(len(pre.flag), bool)
+    K = (pre.geom.shape[1] - 3) // 3
+    xy = [np.abs(pre.geom[:, 0]), np.abs(pre.geom[:, 1])]
+    for j in range(K):
+        xy += [np.abs(pre.geom[:, 3 + 3 * j]), np.abs(pre.geom[:, 4 + 3 * j])]
+    return (np.max(xy, axis=0) >= SCREEN_SCALE) & (pre.flag == 0)
+
+
 CLAMP_MARGIN = 1e-6     # |SH colour before max(0, .)| below this: the clamp may flip in fp32 (both valid; seen: 9.5e-9)
 
 

@@ -104,16 +104,19 @@ def test_fullsize_sampled_parity(cfg, exact, view, parity_log):
     fb = oracle.render(osc, cam, pre, vals, ranges, pix=pix, dL_dimage=G, exact=exact, bounds=True)
     g = oracle.preprocess_bwd(osc, cam, pre, fb, exact=exact)
     gb = oracle.feature_bounds(osc, cam, pre, fb, exact=exact)
-    flagged = fb.face_margin < PT.FACE_MARGIN
     touched = np.isfinite(fb.face_margin)
+    screen = PT.screen_flags(pre, exact) & touched
+    flagged = (fb.face_margin < PT.FACE_MARGIN) | screen
     ok, worst, reports, n_cond, n_clamp = PT.check_gradients(ds.grad_dict(), g, gb, pre, flagged)
     parity_log(f"fullsize {cfg}{' exact' if exact else ''} view {view}", pixels=int(pix.size),
                masked_px=int(stop_mask.sum()), hit_prims=int(touched.sum()), flagged=int(flagged.sum()),
-               clamp=n_clamp, cond_elems=n_cond, worst=worst)
+               screen_flagged=int(screen.sum()), clamp=n_clamp, cond_elems=n_cond, worst=worst)
     assert ok, "; ".join(reports)
     # SURVEY §8c-5 expects ~7e-4 of the primitives flagged; bound it so a drift in the geometry
     # cannot hide behind the loose bound
-    assert flagged.sum() <= max(3, PT.MAX_FLAGGED_FRAC * touched.sum()), f"flagged {flagged.sum()} of {touched.sum()}"
+    nf = int((fb.face_margin < PT.FACE_MARGIN).sum())
+    assert nf <= max(3, PT.MAX_FLAGGED_FRAC * touched.sum()), f"face-flagged {nf} of {touched.sum()}"
+    assert screen.sum() <= max(3, PT.MAX_FLAGGED_FRAC * touched.sum()), f"screen-flagged {screen.sum()} of {touched.sum()}"
     assert stop_mask.sum() <= PT.MAX_MASKED_FRAC * pix.size, f"masked {stop_mask.sum()} of {pix.size}"
     torch.cuda.empty_cache()
 

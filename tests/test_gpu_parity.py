@@ -78,8 +78,8 @@ def full_parity(scene, cam, kappa=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), seed=0, 
         return
     fb, g = oracle.forward_backward(osc, cam, G, kappa=kappa, t_stop=t_stop, bg=bg, exact=exact, bounds=True)
     gb = oracle.feature_bounds(osc, cam, fb.pre, fb.out, exact=exact)
-    flagged = fb.out.face_margin < PT.FACE_MARGIN
     touched = np.isfinite(fb.out.face_margin)
+    flagged = (fb.out.face_margin < PT.FACE_MARGIN) | (PT.screen_flags(fb.pre, exact) & touched)
     assert flagged.sum() <= max(2, max_flagged * touched.sum()), f"flagged {flagged.sum()} of {touched.sum()}"
     ok, worst, reports, n_cond, n_clamp = PT.check_gradients(ds.grad_dict(), g, gb, fb.pre, flagged, loose=loose)
     import os

@@ -97,6 +97,8 @@ def test_c5_step_vs_oracle(loss, parity_log):
     for k, (b, e) in off.items():
         setattr(g, k, g_o[b:e].reshape(shapes[k]))
         setattr(gb, k, r["bound"][b:e].reshape(shapes[k]))
+    for f in r["fwd"]:
+        r["flagged"] |= PT.screen_flags(f.pre) & (f.pre.tiles_touched > 0)
     ok, worst, reports, n_cond, n_clamp = PT.check_gradients(ds.grad_dict(), g, gb, None, r["flagged"],
                                                              clamp=r["clamp"])
     parity_log(f"c5 step ({loss})", views=len(cams), hit_prims=int(np.isfinite(r["fwd"][0].out.m_face).sum()),
