@@ -115,6 +115,13 @@ typedef struct {
                                  replays only those entries */
   float    *T_last;           /* [H][W] T in front of the entry that stopped the pixel (= T_final if it never
                                  stopped): the backward's first recovered T, never divided by a tiny E */
+  int32_t   deterministic;    /* 1 (frame created with LP_FRAME_DETERMINISTIC): the backward's raster moments are
+                                 written per (tile-list entry, warp) and summed per primitive in a fixed order
+                                 (bitwise reproducible gradients); 0: RED.F32 atomics */
+  uint32_t *emit_prim;        /* [capacity] deterministic frames: primitive of every emitted entry (emission order) */
+  uint32_t *emit_pos;         /* [capacity] deterministic frames: sorted position of every emitted entry */
+  uint32_t *prim_emit;        /* [n] deterministic frames: first emitted entry of every primitive */
+  float    *part;             /* [capacity][4 warps][rgrad_words] deterministic frames: per (entry, warp) moment sums */
   float    *T_ckpt;           /* [tiles + capacity/128 + 2][128][2] the pixels' T in front of every 128-entry
                                  batch of their tile list after the first (forward); the backward restarts its
                                  T = T_after / E recovery from these, so no division chain spans two batches */
@@ -159,13 +166,19 @@ typedef struct {
 int32_t     lp_abi_version(void);
 const char *lp_status_string(lp_status s);
 
-/* Bytes of device workspace for one frame (256-byte aligned inside). */
+/* lp_frame_bytes / lp_frame_init flags */
+enum {
+  LP_FRAME_CANON = 1,         /* keep the canonical fp32 geometry (lp_frame.canon; parity tests) */
+  LP_FRAME_DETERMINISTIC = 2  /* deterministic backward (lp_frame.deterministic): + capacity x (8 + 16 rgrad_words) B */
+};
+
+/* Bytes of device workspace for one frame (256-byte aligned inside); flags: LP_FRAME_* bits. */
 size_t lp_frame_bytes(int32_t kind, int32_t n, int32_t width, int32_t height, int64_t capacity,
-                      int32_t with_canon);
+                      int32_t flags);
 
 /* Carve a frame out of `workspace` (device, >= lp_frame_bytes, 256-byte aligned). Host-only. */
 lp_status lp_frame_init(lp_frame *frame, void *workspace, size_t bytes, int32_t kind, int32_t n,
-                        int32_t width, int32_t height, int64_t capacity, int32_t with_canon);
+                        int32_t width, int32_t height, int64_t capacity, int32_t flags);
 
 /* a1-a3: per primitive, for each view v:
  * vertices from features, view transform, EWA ray space, 2D filter, bbox -> tile rect,

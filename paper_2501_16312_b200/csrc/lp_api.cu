@@ -25,10 +25,11 @@ inline int offsets_k(int kind) { return kind == LP_OCTAHEDRON ? 3 : 4; }
 struct Layout {
   size_t tiles_touched, rect, depth_key, record, prim_key, prim_key_alt, prim_order, prim_order_alt, offsets, tile_key,
       tile_key_alt, entry_val, entry_val_alt, ranges, sort_hist, scan_tmp, counters, T_final, n_proc, rgrad, canon,
-      tile_diff, tile_cursor, hitmask, T_last, T_ckpt, total;
+      tile_diff, tile_cursor, hitmask, T_last, T_ckpt, emit_prim, emit_pos, prim_emit, part, total;
 };
 
-Layout layout(int kind, int64_t n, int w, int h, int64_t cap, int canon) {
+Layout layout(int kind, int64_t n, int w, int h, int64_t cap, int flags) {
+  const bool canon = (flags & LP_FRAME_CANON) != 0, det = (flags & LP_FRAME_DETERMINISTIC) != 0;
   Layout L;
   const int64_t tiles = (int64_t)((w + LP_TILE - 1) / LP_TILE) * ((h + LP_TILE - 1) / LP_TILE);
   const int64_t hw = (int64_t)w * h;
@@ -62,6 +63,10 @@ Layout layout(int kind, int64_t n, int w, int h, int64_t cap, int canon) {
   L.hitmask = take(4 * 4 * hit_words(cc));
   L.T_last = take(4 * hw);
   L.T_ckpt = take(8 * 128 * (size_t)ckpt_slots(tiles, cc));
+  L.emit_prim = det ? take(4 * cc) : 0;
+  L.emit_pos = det ? take(4 * cc) : 0;
+  L.prim_emit = det ? take(4 * nn) : 0;
+  L.part = det ? take(4 * 4 * (size_t)rgrad_words(kind) * cc) : 0;
   L.total = o;
   return L;
 }
@@ -108,17 +113,19 @@ const char *lp_status_string(lp_status s) {
   return "unknown status";
 }
 
-size_t lp_frame_bytes(int32_t kind, int32_t n, int32_t width, int32_t height, int64_t capacity, int32_t with_canon) {
-  if (!valid_kind(kind) || n < 0 || width <= 0 || height <= 0 || capacity < 0) return 0;
-  return layout(kind, n, width, height, capacity, with_canon).total;
+size_t lp_frame_bytes(int32_t kind, int32_t n, int32_t width, int32_t height, int64_t capacity, int32_t flags) {
+  if (!valid_kind(kind) || n < 0 || width <= 0 || height <= 0 || capacity < 0 || (flags & ~3)) return 0;
+  return layout(kind, n, width, height, capacity, flags).total;
 }
 
 lp_status lp_frame_init(lp_frame *F, void *workspace, size_t bytes, int32_t kind, int32_t n, int32_t width,
-                        int32_t height, int64_t capacity, int32_t with_canon) {
-  if (!F || !workspace || !valid_kind(kind) || n < 0 || width <= 0 || height <= 0 || capacity < 0) return LP_ERR_ARG;
+                        int32_t height, int64_t capacity, int32_t flags) {
+  if (!F || !workspace || !valid_kind(kind) || n < 0 || width <= 0 || height <= 0 || capacity < 0 || (flags & ~3))
+    return LP_ERR_ARG;
+  const bool with_canon = (flags & LP_FRAME_CANON) != 0, det = (flags & LP_FRAME_DETERMINISTIC) != 0;
   if ((reinterpret_cast<uintptr_t>(workspace) & (ALIGN - 1)) != 0) return LP_ERR_ARG;
   if (capacity > (int64_t)0xFFFFFFF0u) return LP_ERR_ARG;   // entries are indexed with u32
-  const Layout L = layout(kind, n, width, height, capacity, with_canon);
+  const Layout L = layout(kind, n, width, height, capacity, flags);
   if (bytes < L.total) return LP_ERR_ARG;
   char *b = static_cast<char *>(workspace);
   memset(F, 0, sizeof(*F));
@@ -160,6 +167,11 @@ lp_status lp_frame_init(lp_frame *F, void *workspace, size_t bytes, int32_t kind
   F->hitmask = reinterpret_cast<uint32_t *>(b + L.hitmask);
   F->T_last = reinterpret_cast<float *>(b + L.T_last);
   F->T_ckpt = reinterpret_cast<float *>(b + L.T_ckpt);
+  F->deterministic = det ? 1 : 0;
+  F->emit_prim = det ? reinterpret_cast<uint32_t *>(b + L.emit_prim) : nullptr;
+  F->emit_pos = det ? reinterpret_cast<uint32_t *>(b + L.emit_pos) : nullptr;
+  F->prim_emit = det ? reinterpret_cast<uint32_t *>(b + L.prim_emit) : nullptr;
+  F->part = det ? reinterpret_cast<float *>(b + L.part) : nullptr;
   return LP_OK;
 }
 
@@ -194,6 +206,7 @@ lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, 
   for (int v = 0; v < n_views; ++v) {
     lp_frame &F = frames[v];
     const int n = F.n;
+    if (F.sort_method == LP_SORT_BUCKET && F.deterministic) return LP_ERR_UNSUPPORTED;   // emission order needs radix
     if (F.sort_method == LP_SORT_BUCKET) {
       // counts (2-D prefix of the rect difference grid K1 filled) -> ranges, cursors, E
       launch_tile_counts(F, st);
@@ -246,6 +259,7 @@ lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, 
                                        bits_for(tiles), F.sort_hist, st);
     F.sorted_tile = tflip ? F.tile_key_alt : F.tile_key;
     F.sorted_val = tflip ? F.entry_val_alt : F.entry_val;
+    if (F.deterministic) launch_det_fixup(F, F.sorted_val, st);
     // 5. ranges
     lp_frame Fr = F;
     if (E_host >= 0) Fr.capacity = E_host;

@@ -36,6 +36,10 @@ int radix_sort_pairs(uint32_t *keys, uint32_t *keys_alt, uint32_t *vals, uint32_
 void launch_scan_tiles(const lp_frame &F, int n, cudaStream_t st);   // offsets + E -> counters
 void launch_emit(const lp_frame &F, int n, int64_t max_entries, cudaStream_t st);
 void launch_ranges(const lp_frame &F, const uint32_t *sorted_tile, int tiles, cudaStream_t st);
+// deterministic frames: emission positions + sorted values back to primitive ids (after the tile sort)
+void launch_det_fixup(const lp_frame &F, uint32_t *sorted_val, cudaStream_t st);
+// deterministic frames: per-primitive raster moments summed in a fixed order from the (entry, warp) partials
+void launch_det_gather(const lp_frame &F, cudaStream_t st);
 // LP_SORT_BUCKET path
 void launch_tile_counts(const lp_frame &F, cudaStream_t st);
 void launch_bucket(const lp_frame &F, cudaStream_t st);

@@ -145,13 +145,6 @@ __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_came
   warp_count(F.counters + LP_CNT_FRUSTUM, inb && g.flag == 0);
   warp_count(F.counters + LP_CNT_VISIBLE, inb && g.tiles > 0);
   if (!inb) return;
-  {
-    // the backward's raster-moment row of this (primitive, view) starts at zero (instead of a
-    // separate memset of the whole scratch per view)
-    float4 *row = reinterpret_cast<float4 *>(F.rgrad + (size_t)i * lp_rgs<KIND>());
-#pragma unroll
-    for (int q = 0; q < lp_rgs<KIND>() / 4; ++q) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
 
   const bool ok = g.flag == 0;
   F.tiles_touched[i] = g.tiles;
@@ -172,6 +165,19 @@ __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_came
       for (int a = 0; a < 3; ++a) cn[2 + 3 * j + a] = ok ? g.off[j][a] : 0.f;
   }
   if (g.tiles == 0) return;   // only visible primitives need a record
+  {
+    // the backward's raster-moment row of this (primitive, view) starts at zero (only visible
+    // primitives: K4 and K5 touch no other row).  Whole 32-byte sectors are written -- the row
+    // plus the neighbours' bytes sharing its first / last sector (zeros as well, harmless) -- so
+    // L2 never has to fetch a partially written sector from HBM.
+    constexpr int RB = 4 * lp_rgs<KIND>();
+    const size_t b0 = ((size_t)i * RB) & ~(size_t)31, b1 = ((size_t)i * RB + RB + 31) & ~(size_t)31;
+    float4 *z = reinterpret_cast<float4 *>(reinterpret_cast<char *>(F.rgrad) + b0);
+    const size_t zend = min(b1, (size_t)P.n * RB);
+#pragma unroll
+    for (int q = 0; q < (RB + 64) / 16; ++q)
+      if (b0 + 16 * (size_t)q < zend) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   if (F.sort_method == LP_SORT_BUCKET) {
     // tile rect into the 2-D difference grid of the bucket sort (4 atomics instead of tiles_touched)
     const int cols = F.tiles_x + 1;
@@ -262,9 +268,13 @@ __device__ __forceinline__ void preprocess_view(const lp_prims &P, const lp_came
   rec[KD::RGB + 0] = rgb[0];
   rec[KD::RGB + 1] = rgb[1];
   rec[KD::RGB + 2] = rgb[2];
+  // the whole RS-word row (pad words zero): a partially written 32-byte sector would make L2 read it
+  // from HBM first
   float4 *dst = reinterpret_cast<float4 *>(F.record + (size_t)i * RS);
 #pragma unroll
-  for (int w = 0; w < RW / 4; ++w) dst[w] = make_float4(rec[4 * w], rec[4 * w + 1], rec[4 * w + 2], rec[4 * w + 3]);
+  for (int w = 0; w < RS / 4; ++w)
+    dst[w] = 4 * w < RW ? make_float4(rec[4 * w], rec[4 * w + 1], rec[4 * w + 2], rec[4 * w + 3])
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // =============================================================================================
@@ -704,13 +714,12 @@ __global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, f
     for (int v = 0; v < LP_MAXV; ++v)
       if (v < V.nv && V.tt[v][i] != 0) vis |= 1u << v;
     if (Gs.vis_count && vis) Gs.vis_count[i] += (float)__popc(vis);   // densification denominator
-    // (not gated by vis: the raster scratch of a view is zeroed per frame, so an invisible
-    // primitive's probe is 0 anyway, and the probe loads overlap the tiles_touched loads)
+    // (gated by vis: K1 zeroes the raster rows of visible primitives only)
     float probe[LP_MAXV];
 #pragma unroll
     for (int v = 0; v < LP_MAXV; ++v) {
       probe[v] = 0.f;
-      if (v < V.nv) {
+      if (v < V.nv && ((vis >> v) & 1u)) {
         const float4 rg = *reinterpret_cast<const float4 *>(V.rgrad[v] + (size_t)i * lp_rgs<KIND>());   // dsigma, drgb
         probe[v] = fabsf(rg.x) + fabsf(rg.y) + fabsf(rg.z) + fabsf(rg.w);
       }
@@ -897,6 +906,8 @@ static void bwd_deg(const lp_prims &P, float kappa, const ViewPack &V, int rg, c
 void launch_preprocess_bwd(const lp_prims &P, const lp_camera *cams, float kappa, const lp_frame *frames, int n_views,
                            const lp_grads &G, bool exact, bool assign, cudaStream_t st) {
   if (P.n == 0 || n_views <= 0) return;
+  // deterministic frames: the raster moments from the (entry, warp) partials, in a fixed order
+  for (int v = 0; v < n_views; ++v) launch_det_gather(frames[v], st);
   for (int v0 = 0; v0 < n_views; v0 += LP_MAXV) {
     ViewPack V;
     V.nv = n_views - v0 < LP_MAXV ? n_views - v0 : LP_MAXV;

@@ -723,8 +723,11 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
         if (q + 2 < h) s2 += col[(q + 2) * RGP];
         const float sum = (s0 + s1) + (s2 + s3);
         // the shared row's layout is the rgrad row's (dsigma, drgb | moments): the h-row column sums
-        // land in one primitive's 80 / 96-byte row (3 sectors per RED instruction)
-        if (sum != 0.f) atomicAdd(F.rgrad + (size_t)id * lp_rgs<KIND>() + lane, sum);
+        // land in one primitive's 80 / 96-byte row (3 sectors per RED instruction); deterministic
+        // frames store the (entry, warp) partial instead, summed per primitive in a fixed order by
+        // k_det_gather
+        if (F.deterministic) F.part[((size_t)ej * 4 + w) * lp_rgs<KIND>() + lane] = sum;
+        else if (sum != 0.f) atomicAdd(F.rgrad + (size_t)id * lp_rgs<KIND>() + lane, sum);
       }
       __syncwarp();
     }
@@ -788,6 +791,43 @@ void launch_raster_fwd(const lp_frame &F, const lp_camera &cam, const lp_raster_
     cudaMemsetAsync(F.counters + LP_CNT_WARP_HITS, 0, 8, st);
     k_hit_stats<<<148, 256, 0, st>>>(F.hitmask, hit_words(F.capacity), F.counters);
   }
+}
+
+// deterministic frames: every visible primitive's raster moments = the sum, over its
+// emitted entries in emission order and the four warps in order, of the partials the backward stored
+// for the (entry, warp) pairs the forward's hit bits mark -- a fixed summation order, so the
+// gradients are bitwise reproducible.  One thread per primitive.
+template <int KIND>
+__global__ void __launch_bounds__(128) k_det_gather(lp_frame F) {
+  constexpr int RG = Kind<KIND>::RG, RGS = lp_rgs<KIND>();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= F.n) return;
+  const uint32_t tt = F.tiles_touched[i];
+  if (tt == 0) return;
+  const uint32_t k0 = F.prim_emit[i];
+  const int64_t hw = hit_words(F.capacity);
+  float acc[RG];
+#pragma unroll
+  for (int a = 0; a < RG; ++a) acc[a] = 0.f;
+  for (uint32_t t = 0; t < tt; ++t) {
+    const uint32_t e = F.emit_pos[k0 + t];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      if (((F.hitmask[w * hw + (e >> 5)] >> (e & 31u)) & 1u) == 0u) continue;
+      const float *row = F.part + ((size_t)e * 4 + w) * RGS;
+#pragma unroll
+      for (int a = 0; a < RG; ++a) acc[a] += row[a];
+    }
+  }
+  float *dst = F.rgrad + (size_t)i * RGS;
+#pragma unroll
+  for (int a = 0; a < RGS; ++a) dst[a] = a < RG ? acc[a] : 0.f;
+}
+
+void launch_det_gather(const lp_frame &F, cudaStream_t st) {
+  if (F.n <= 0 || !F.deterministic) return;
+  if (F.kind == LP_OCTAHEDRON) k_det_gather<LP_OCTAHEDRON><<<(F.n + 127) / 128, 128, 0, st>>>(F);
+  else k_det_gather<LP_TETRAHEDRON><<<(F.n + 127) / 128, 128, 0, st>>>(F);
 }
 
 void launch_raster_bwd(const lp_frame &F, const lp_camera &cam, const lp_raster_cfg &cfg, const float *dL,

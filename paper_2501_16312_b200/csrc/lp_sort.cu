@@ -258,9 +258,10 @@ __global__ void __launch_bounds__(1024) k_scan_top(uint32_t *__restrict__ part, 
   }
 }
 
+// prim_emit (deterministic frames, else null): first emitted entry of every primitive
 __global__ void __launch_bounds__(256) k_scan_down(const uint32_t *__restrict__ order, const uint32_t *__restrict__ tt,
                                                    int n, const uint32_t *__restrict__ part,
-                                                   uint32_t *__restrict__ offsets) {
+                                                   uint32_t *__restrict__ offsets, uint32_t *__restrict__ prim_emit) {
   __shared__ uint32_t s_warp[32];
   const int base = blockIdx.x * SCAN_TILE;
   // thread t owns 8 consecutive elements: base + 8t .. 8t+7
@@ -277,7 +278,10 @@ __global__ void __launch_bounds__(256) k_scan_down(const uint32_t *__restrict__ 
 #pragma unroll
   for (int k = 0; k < SCAN_TILE / 256; ++k) {
     const int j = base + threadIdx.x * (SCAN_TILE / 256) + k;
-    if (j < n) offsets[j] = run;
+    if (j < n) {
+      offsets[j] = run;
+      if (prim_emit) prim_emit[order[j]] = run;
+    }
     run += v[k];
   }
 }
@@ -286,7 +290,7 @@ void launch_scan_tiles(const lp_frame &F, int n, cudaStream_t st) {
   const int nb = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (n > 0) k_scan_reduce<<<nb, 256, 0, st>>>(F.prim_order, F.tiles_touched, n, F.scan_tmp);
   k_scan_top<<<1, 1024, 0, st>>>(F.scan_tmp, nb, F.offsets, n, F.counters, F.capacity);
-  if (n > 0) k_scan_down<<<nb, 256, 0, st>>>(F.prim_order, F.tiles_touched, n, F.scan_tmp, F.offsets);
+  if (n > 0) k_scan_down<<<nb, 256, 0, st>>>(F.prim_order, F.tiles_touched, n, F.scan_tmp, F.offsets, F.prim_emit);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -327,7 +331,7 @@ __device__ __forceinline__ int warp_last_leq(const uint32_t *__restrict__ a, int
 __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ order, const uint32_t *__restrict__ offsets,
                                               const ushort4 *__restrict__ rect, int n, int tiles_x, int64_t capacity,
                                               const uint32_t *__restrict__ E_dev, uint32_t *__restrict__ tile_key,
-                                              uint32_t *__restrict__ entry_val) {
+                                              uint32_t *__restrict__ entry_val, uint32_t *__restrict__ emit_prim) {
   __shared__ uint32_t s_off[EMIT_TILE];
   __shared__ uint32_t s_id[EMIT_TILE];
   __shared__ ushort4 s_rect[EMIT_TILE];
@@ -394,15 +398,38 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ order
     const uint32_t rw = (uint32_t)r.z - r.x + 1;
     const uint32_t ty = r.y + k / rw, tx = r.x + k % rw;
     tile_key[e] = ty * (uint32_t)tiles_x + tx;
-    entry_val[e] = s_id[lo];
+    if (emit_prim) {            // deterministic frames: the sort carries the emission index
+      entry_val[e] = (uint32_t)e;
+      emit_prim[e] = s_id[lo];
+    } else {
+      entry_val[e] = s_id[lo];
+    }
   }
+}
+
+// deterministic frames, after the stable tile sort: emit_pos[k] = sorted position of emitted entry k,
+// and the sorted values back to primitive ids (the raster kernels see the usual list)
+__global__ void __launch_bounds__(256) k_det_fixup(uint32_t *__restrict__ sorted_val, const uint32_t *__restrict__ emit_prim,
+                                                   uint32_t *__restrict__ emit_pos, const uint32_t *E_dev, int64_t capacity) {
+  const int64_t E = item_count(E_dev, capacity);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = sorted_val[e];
+    emit_pos[k] = (uint32_t)e;
+    sorted_val[e] = emit_prim[k];
+  }
+}
+
+void launch_det_fixup(const lp_frame &F, uint32_t *sorted_val, cudaStream_t st) {
+  if (F.capacity <= 0) return;
+  k_det_fixup<<<148 * 8, 256, 0, st>>>(sorted_val, F.emit_prim, F.emit_pos, F.counters + LP_CNT_ENTRIES, F.capacity);
 }
 
 void launch_emit(const lp_frame &F, int n, int64_t max_entries, cudaStream_t st) {
   if (n == 0 || max_entries <= 0) return;
   const int64_t grid = (max_entries + EMIT_TILE - 1) / EMIT_TILE;
   k_emit<<<(unsigned)grid, 256, 0, st>>>(F.prim_order, F.offsets, reinterpret_cast<const ushort4 *>(F.rect), n,
-                                         F.tiles_x, F.capacity, F.counters + LP_CNT_ENTRIES, F.tile_key, F.entry_val);
+                                         F.tiles_x, F.capacity, F.counters + LP_CNT_ENTRIES, F.tile_key, F.entry_val,
+                                         F.deterministic ? F.emit_prim : nullptr);
 }
 
 // ---------------------------------------------------------------------------------------------

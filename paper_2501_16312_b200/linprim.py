@@ -25,6 +25,7 @@ LP_CNT_ENTRIES, LP_CNT_OVERFLOW, LP_CNT_INVALID, LP_CNT_FRUSTUM, LP_CNT_VISIBLE 
 LP_CNT_WARP_HITS, LP_CNT_TILE_HITS = 5, 6
 LP_CNT_ITERATED, LP_CNT_INTERSECTED, LP_CNT_INBOX, LP_NUM_COUNTERS = 8, 10, 12, 16
 LP_SORT_BUCKET, LP_SORT_RADIX = 0, 1
+LP_FRAME_CANON, LP_FRAME_DETERMINISTIC = 1, 2
 LP_ABI_VERSION = 4            # include/linprim.h; the loaded library must match the structs below
 
 _p = C.c_void_p
@@ -54,7 +55,8 @@ class lp_frame(C.Structure):
                            "prim_order", "prim_order_alt", "offsets", "tile_key", "tile_key_alt", "entry_val",
                            "entry_val_alt", "sorted_tile", "sorted_val", "ranges", "sort_hist", "scan_tmp",
                            "counters", "T_final", "n_proc", "rgrad", "canon", "tile_diff", "tile_cursor")] + \
-        [("sort_method", C.c_int32), ("hitmask", _p), ("T_last", _p), ("T_ckpt", _p)]
+        [("sort_method", C.c_int32), ("hitmask", _p), ("T_last", _p), ("deterministic", C.c_int32),
+         ("emit_prim", _p), ("emit_pos", _p), ("prim_emit", _p), ("part", _p), ("T_ckpt", _p)]
 
 
 class lp_adam_group(C.Structure):
@@ -131,13 +133,13 @@ def lp_status_string(s) -> str:
     return _lib.lp_status_string(int(s)).decode()
 
 
-def lp_frame_bytes(kind, n, width, height, capacity, with_canon=0) -> int:
-    return int(_lib.lp_frame_bytes(kind, n, width, height, capacity, with_canon))
+def lp_frame_bytes(kind, n, width, height, capacity, flags=0) -> int:
+    return int(_lib.lp_frame_bytes(kind, n, width, height, capacity, flags))
 
 
-def lp_frame_init(frame, workspace, nbytes, kind, n, width, height, capacity, with_canon=0):
+def lp_frame_init(frame, workspace, nbytes, kind, n, width, height, capacity, flags=0):
     return _check(_lib.lp_frame_init(C.byref(frame), _ptr(workspace), nbytes, kind, n, width, height, capacity,
-                                     with_canon), "lp_frame_init")
+                                     flags), "lp_frame_init")
 
 
 def lp_preprocess(prims, cams, cfg, frames, stream):

@@ -82,8 +82,9 @@ class DeviceScene:
 class Frame:
     """One view's scratch: a device workspace carved by lp_frame_init."""
 
-    def __init__(self, kind, n, width, height, capacity, device="cuda", with_canon=False):
-        self.args = (kind, n, width, height, int(capacity), 1 if with_canon else 0)
+    def __init__(self, kind, n, width, height, capacity, device="cuda", with_canon=False, deterministic=False):
+        flags = (L.LP_FRAME_CANON if with_canon else 0) | (L.LP_FRAME_DETERMINISTIC if deterministic else 0)
+        self.args = (kind, n, width, height, int(capacity), flags)
         nbytes = L.lp_frame_bytes(*self.args)
         if nbytes == 0:
             raise L.LinPrimError("lp_frame_bytes: invalid frame arguments")
@@ -128,7 +129,8 @@ class Renderer:
     """Forward / backward of the LinPrim tile rasterizer over a list of views (C-ABI calls only)."""
 
     def __init__(self, scene: DeviceScene, cams, aa_kernel=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), capacity=None,
-                 with_canon=False, count_stats=False, sync_capacity=True, sort_method=None, exact=False):
+                 with_canon=False, count_stats=False, sync_capacity=True, sort_method=None, exact=False,
+                 deterministic=False):
         self.scene = scene
         self.sort_method = L.LP_SORT_RADIX if sort_method is None else int(sort_method)
         self.cam_dicts = list(cams)
@@ -136,6 +138,8 @@ class Renderer:
         # exact: the "no ray space" variant (App. D, lp_raster_cfg.exact)
         self.cfg = L.raster_cfg(aa_kernel, t_stop, bg, count_stats, exact)
         self.with_canon = with_canon
+        # deterministic: bitwise reproducible backward (LP_FRAME_DETERMINISTIC frames)
+        self.deterministic = deterministic
         self.sync_capacity = sync_capacity
         dev = scene.flat.device
         self.frames = []
@@ -146,7 +150,7 @@ class Renderer:
 
     def _new_frame(self, cam, capacity):
         f = Frame(self.scene.kind, self.scene.n, cam["width"], cam["height"], capacity, self.scene.flat.device,
-                  self.with_canon)
+                  self.with_canon, self.deterministic)
         f.c.sort_method = self.sort_method
         return f
 

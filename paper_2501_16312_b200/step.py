@@ -33,7 +33,8 @@ class TrainStep:
 
     def __init__(self, ds: render.DeviceScene, cams, n_views_total, *, targets=None, loss="l1ssim", lam=0.2,
                  streams=4, split_pre=True, assign=True, exact=False, capacity=None, world=1, rank=0,
-                 sharded=False, extent=4.0, betas=(0.9, 0.999), eps=1e-15, loss_slots=256, aa_kernel=None):
+                 sharded=False, extent=4.0, betas=(0.9, 0.999), eps=1e-15, loss_slots=256, aa_kernel=None,
+                 deterministic=False):
         dev = ds.flat.device
         self.ds, self.dev = ds, dev
         self.n_local = len(cams)
@@ -45,7 +46,8 @@ class TrainStep:
         W, H = cams[0]["width"], cams[0]["height"]
         self.W, self.H = W, H
         kappa = (0.0 if exact else 0.1) if aa_kernel is None else aa_kernel
-        self.rend = render.Renderer(ds, cams, capacity=capacity, exact=exact, aa_kernel=kappa, sync_capacity=False)
+        self.rend = render.Renderer(ds, cams, capacity=capacity, exact=exact, aa_kernel=kappa, sync_capacity=False,
+                                    deterministic=deterministic)
         self.img = torch.empty((self.n_local, 3, H, W), dtype=torch.float32, device=dev)
         self.dL = torch.empty_like(self.img)
         self.targets = targets

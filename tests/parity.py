@@ -24,13 +24,14 @@ def log(name, **kw):
 
 
 def gpu_run(scene, cams, G=None, kappa=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), with_canon=True, capacity=None,
-            count_stats=True, filter3d=None, sort_method=None, exact=False):
+            count_stats=True, filter3d=None, sort_method=None, exact=False, deterministic=False):
     import torch
 
     from paper_2501_16312_b200 import render
     ds = render.DeviceScene(scene, filter3d=filter3d)
     r = render.Renderer(ds, cams, aa_kernel=kappa, t_stop=t_stop, bg=bg, with_canon=with_canon,
-                        capacity=capacity, count_stats=count_stats, sort_method=sort_method, exact=exact)
+                        capacity=capacity, count_stats=count_stats, sort_method=sort_method, exact=exact,
+                        deterministic=deterministic)
     img = r.forward()
     if G is not None:
         r.backward(torch.as_tensor(G, device="cuda").reshape(img.shape))

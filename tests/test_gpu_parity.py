@@ -58,14 +58,15 @@ def check_binning(got, pre, cam):
 
 
 def full_parity(scene, cam, kappa=0.1, t_stop=1e-3, bg=(0.0, 0.0, 0.0), seed=0, grads=True, filter3d=None,
-                max_masked=0.01, max_flagged=0.03, exact=False, loose=0.1):
+                max_masked=0.01, max_flagged=0.03, exact=False, loose=0.1, deterministic=False):
     W, H = cam["width"], cam["height"]
     osc = oscene(scene, filter3d)
     f0 = oracle.forward(osc, cam, kappa=kappa, t_stop=t_stop, bg=bg, exact=exact)
     mask = f0.out.m_stop < PT.STOP_MARGIN
     assert mask.mean() <= max_masked, f"too many stop-margin pixels {mask.mean()}"
     G = scenegen.upstream_grad(W, H, seed=seed)[0] * (~mask)[None].astype(np.float32) if grads else None
-    ds, r, img = PT.gpu_run(scene, [cam], G=G, kappa=kappa, t_stop=t_stop, bg=bg, filter3d=filter3d, exact=exact)
+    ds, r, img = PT.gpu_run(scene, [cam], G=G, kappa=kappa, t_stop=t_stop, bg=bg, filter3d=filter3d, exact=exact,
+                            deterministic=deterministic)
     got, pre = check_preprocess(scene, cam, r, kappa=kappa, filter3d=filter3d, exact=exact)
     check_binning(got, pre, cam)
     im = img[0].cpu().numpy()
