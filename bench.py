@@ -67,6 +67,8 @@ def parse(argv=None):
     ap.add_argument("--split-pre", action=argparse.BooleanOptionalAction, default=True,
                     help="preprocess the first --streams views in their own launch so their binning overlaps "
                          "the preprocess of the others")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"], help=argparse.SUPPRESS)
+    ap.add_argument("--shared-gpu", action="store_true", help=argparse.SUPPRESS)   # code-path check: all ranks on cuda:0
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop (ncu --profile-from-start off) and exit")
     return ap.parse_args(argv)
@@ -571,6 +573,9 @@ def main():
             print(json.dumps(out), flush=True)
         return
     import torch
+    if args.shared_gpu:
+        # code-path check only (gloo, every rank on cuda:0): the number it prints is not a bench value
+        local_rank = 0
     if torch.cuda.device_count() < local_rank + 1:
         raise SystemExit(f"rank {rank}: {torch.cuda.device_count()} visible GPUs, local rank {local_rank} has none")
     if world > 1:
@@ -580,7 +585,10 @@ def main():
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     out, ctx = run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
@@ -592,6 +600,8 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             scene, cams, _ = ctx
             out["cpu_baseline"] = cpu_baseline(scene, cams)
+        if args.shared_gpu:
+            out["config"]["code_path_check"] = "all ranks on one GPU over gloo: not a bench value"
         print(json.dumps(out), flush=True)
 
 
