@@ -28,13 +28,18 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+    """variant "checked": liblinprim_checked.so with the device-side bounds checks (-DLP_CHECKED),
+    loaded only when LP_LIB points at it (tests/test_gpu_checked.py)."""
+    lib = LIB if not variant else os.path.join(PKG, f"liblinprim_{variant}.so")
+    if force or not os.path.exists(lib) or any(os.path.getmtime(d) > os.path.getmtime(lib) for d in _deps()):
         nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
         extra = os.environ.get("LP_EXTRA_NVCC_FLAGS", "").split()   # measurement variants only
-        cmd = [nvcc] + NVCC_FLAGS + extra + ["-o", LIB + ".tmp"] + sources()
+        if variant == "checked":
+            extra = extra + ["-DLP_CHECKED"]
+        cmd = [nvcc] + NVCC_FLAGS + extra + ["-o", lib + ".tmp"] + sources()
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(lib + ".tmp", lib)
+    return lib

@@ -16,6 +16,8 @@
 #include "../../include/linprim.h"
 #include "lp_x2.cuh"
 
+#include "lp_check.cuh"
+
 namespace lp {
 
 constexpr int OCTA = LP_OCTAHEDRON;
@@ -761,5 +763,9 @@ __host__ __device__ __forceinline__ int64_t ckpt_slots(int64_t tiles, int64_t ca
 __device__ __forceinline__ float2 *ckpt_at(float *base, int tile, uint32_t start, uint32_t b) {
   return reinterpret_cast<float2 *>(base) + ((size_t)tile + (start >> 7) + ((b - start) >> 7)) * 128;
 }
+// checked builds: the slot of ckpt_at stays inside the frame's checkpoint buffer
+#define LP_CHECK_CKPT(F, tile, start, b)                                                                  \
+  LP_CHECK((int64_t)(tile) + ((start) >> 7) + (((b) - (start)) >> 7) <                                     \
+           ckpt_slots((int64_t)(F).tiles_x * (F).tiles_y, (F).capacity > 0 ? (F).capacity : 1))
 
 }  // namespace lp

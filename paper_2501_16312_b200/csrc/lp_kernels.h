@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include "../../include/linprim.h"
+#include "lp_check.cuh"
 
 namespace lp {
 

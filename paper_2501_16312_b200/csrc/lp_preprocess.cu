@@ -750,6 +750,7 @@ __global__ void __launch_bounds__(64, LP_K5_MINB) k_preprocess_bwd(lp_prims P, f
       const int item = s_items[w][it];
       const int pl = item >> 3, v = item & 7;
       const int ii = base + pl;
+      LP_CHECK(ii < n && v < V.nv && it < 32 * LP_MAXV);
       float gpos[3] = {0.f, 0.f, 0.f}, grot[4] = {0.f, 0.f, 0.f, 0.f}, gdist[4] = {0.f, 0.f, 0.f, 0.f};
       float gop = 0.f, m2d = 0.f, gr[3] = {0.f, 0.f, 0.f}, dir[3] = {0.f, 0.f, 1.f};
       view_feature_grad<KIND, EXACT>(P, s_cam[v], kappa, ii, s_rg[v], gpos, grot, gdist, gop, m2d);

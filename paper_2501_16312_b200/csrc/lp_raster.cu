@@ -188,6 +188,7 @@ extern "C" int lp_debug_bwd_stats(unsigned long long *out, int reset) {
 __device__ __noinline__ void write_hit_word(uint32_t *hitmask, int64_t capacity, int w, uint32_t bit0, uint32_t m) {
   uint32_t *row = hitmask + (size_t)w * hit_words(capacity);
   const uint32_t wd = bit0 >> 5, sh = bit0 & 31u;
+  LP_CHECK((int64_t)wd + (sh ? 1 : 0) < hit_words(capacity));
   atomicOr(row + wd, m << sh);
   if (sh) atomicOr(row + wd + 1, m >> (32u - sh));
 }
@@ -261,10 +262,15 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
   for (uint32_t b = start; b < end; b += NT) {
     if (__syncthreads_and(done[0] && done[1])) break;   // also protects s_rec from the previous batch
     // the pixels' T in front of this batch: the backward restarts its T recovery here
-    if (b > start) *(ckpt_at(F.T_ckpt, tile, start, b) + threadIdx.x) = T2;
+    if (b > start) {
+      LP_CHECK_CKPT(F, tile, start, b);
+      *(ckpt_at(F.T_ckpt, tile, start, b) + threadIdx.x) = T2;
+    }
     const uint32_t e = b + threadIdx.x;
     if (e < end) {
+      LP_CHECK((int64_t)e < F.capacity);
       const uint32_t v = F.sorted_val[e];
+      LP_CHECK(v < (uint32_t)F.n && F.tiles_touched[v] > 0);
       const float4 *src = reinterpret_cast<const float4 *>(F.record + (size_t)v * RS);
       float4 rv[RW4];
 #pragma unroll
@@ -479,7 +485,9 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
     if (be <= start) return false;
     const uint32_t e = bstart_of(be) + threadIdx.x;
     if (e >= be) return false;
+    LP_CHECK((int64_t)e < F.capacity);
     v = F.sorted_val[e];
+    LP_CHECK(v < (uint32_t)F.n);
     return true;
   };
   auto stage = [&](int bf, uint32_t v) {
@@ -515,6 +523,7 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
     // re-anchor the T recovery at the forward's checkpoint in front of the next batch: the
     // divisions T / E never chain across more than one 128-entry batch
     if (after) {
+      LP_CHECK_CKPT(F, tile, start, bend);
       const float2 c = *(ckpt_at(F.T_ckpt, tile, start, bend) + threadIdx.x);
 #pragma unroll
       for (int k = 0; k < PPT; ++k)
@@ -726,6 +735,7 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
         // land in one primitive's 80 / 96-byte row (3 sectors per RED instruction); deterministic
         // frames store the (entry, warp) partial instead, summed per primitive in a fixed order by
         // k_det_gather
+        LP_CHECK((int64_t)ej < F.capacity && id < (uint32_t)F.n);
         if (F.deterministic) F.part[((size_t)ej * 4 + w) * lp_rgs<KIND>() + lane] = sum;
         else if (sum != 0.f) atomicAdd(F.rgrad + (size_t)id * lp_rgs<KIND>() + lane, sum);
       }
@@ -810,7 +820,9 @@ __global__ void __launch_bounds__(128) k_det_gather(lp_frame F) {
 #pragma unroll
   for (int a = 0; a < RG; ++a) acc[a] = 0.f;
   for (uint32_t t = 0; t < tt; ++t) {
+    LP_CHECK((int64_t)k0 + t < F.capacity);
     const uint32_t e = F.emit_pos[k0 + t];
+    LP_CHECK((int64_t)e < F.capacity);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       if (((F.hitmask[w * hw + (e >> 5)] >> (e & 31u)) & 1u) == 0u) continue;

@@ -394,9 +394,11 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ order
   __syncthreads();
   for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     const int lo = s_own[e - e0];
-    const uint32_t k = (uint32_t)e - s_off[lo];    const ushort4 r = s_rect[lo];
+    const uint32_t k = (uint32_t)e - s_off[lo];
+    const ushort4 r = s_rect[lo];
     const uint32_t rw = (uint32_t)r.z - r.x + 1;
     const uint32_t ty = r.y + k / rw, tx = r.x + k % rw;
+    LP_CHECK(tx <= r.z && ty <= r.w && (int64_t)e < capacity);
     tile_key[e] = ty * (uint32_t)tiles_x + tx;
     if (emit_prim) {            // deterministic frames: the sort carries the emission index
       entry_val[e] = (uint32_t)e;
@@ -414,6 +416,7 @@ __global__ void __launch_bounds__(256) k_det_fixup(uint32_t *__restrict__ sorted
   const int64_t E = item_count(E_dev, capacity);
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t k = sorted_val[e];
+    LP_CHECK((int64_t)k < capacity);
     emit_pos[k] = (uint32_t)e;
     sorted_val[e] = emit_prim[k];
   }
@@ -441,6 +444,7 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t *__restrict__ til
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   const uint32_t t = tile[e];
+  LP_CHECK(e == 0 || tile[e - 1] <= t);
   if (e == 0 || tile[e - 1] != t) ranges[2 * (size_t)t] = (uint32_t)e;
   if (e == E - 1 || tile[e + 1] != t) ranges[2 * (size_t)t + 1] = (uint32_t)(e + 1);
 }

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblinprim.so")
+# LP_LIB: an alternative build of the same library (tests only: liblinprim_checked.so, bounds checks)
+LIB_PATH = os.environ.get("LP_LIB") or os.path.join(_HERE, "liblinprim.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
                       "(no CPU fallback exists)")
