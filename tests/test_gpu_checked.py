@@ -25,3 +25,13 @@ def test_checked_build_runs_clean():
                         "tests/test_gpu_deterministic.py::test_deterministic_parity", "tests/test_gpu_exact.py"],
                        capture_output=True, text=True, env=env, cwd=ROOT, timeout=900)
     assert p.returncode == 0 and "LP_CHECK failed" not in p.stdout + p.stderr, (p.stdout[-3000:], p.stderr[-2000:])
+
+
+def test_checked_build_traps_on_a_corrupted_entry():
+    """The checks are live: an out-of-range primitive id in the tile list stops the forward."""
+    from paper_2501_16312_b200 import _build
+    lib = _build.build(variant="checked")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "checked_negative.py")], capture_output=True,
+                       text=True, env=dict(os.environ, LP_LIB=lib), cwd=ROOT, timeout=300)
+    assert p.returncode != 0 and "NOT TRAPPED" not in p.stdout
+    assert "LP_CHECK failed" in p.stdout + p.stderr
