@@ -227,16 +227,22 @@ lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, 
       continue;
     }
     // LP_SORT_RADIX
-    // 1. depth sort of the primitives (stable: ties keep ascending id, reading 11)
-    const int flip = radix_sort_pairs(F.prim_key, F.prim_key_alt, F.prim_order, F.prim_order_alt, n, nullptr, 32,
-                                      F.sort_hist, st);
+    // small frames: steps 1-2 and 4-5 each in one CTA (3 launches instead of ~23)
+    const bool small = small_bin_ok(F);
     lp_frame Fv = F;
-    if (flip) {
-      Fv.prim_key = F.prim_key_alt;
-      Fv.prim_order = F.prim_order_alt;
+    if (small) {
+      launch_small_depth_scan(F, st);
+    } else {
+      // 1. depth sort of the primitives (stable: ties keep ascending id, reading 11)
+      const int flip = radix_sort_pairs(F.prim_key, F.prim_key_alt, F.prim_order, F.prim_order_alt, n, nullptr, 32,
+                                        F.sort_hist, st);
+      if (flip) {
+        Fv.prim_key = F.prim_key_alt;
+        Fv.prim_order = F.prim_order_alt;
+      }
+      // 2. exclusive scan of tiles_touched in depth order -> offsets, E
+      launch_scan_tiles(Fv, n, st);
     }
-    // 2. exclusive scan of tiles_touched in depth order -> offsets, E
-    launch_scan_tiles(Fv, n, st);
     int64_t E_host = -1;
     if (n_entries) {
       uint32_t e32 = 0;
@@ -254,6 +260,13 @@ lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, 
     launch_emit(Fv, n, nmax, st);
     // 4. stable sort by tile id
     const int tiles = F.tiles_x * F.tiles_y;
+    if (small) {   // + 5. ranges, in the same CTA
+      launch_small_tile_sort(F, bits_for(tiles), tiles, st);
+      F.sorted_tile = F.tile_key;
+      F.sorted_val = F.entry_val;
+      if (F.deterministic) launch_det_fixup(F, F.sorted_val, st);
+      continue;
+    }
     const uint32_t *ndev = E_host >= 0 ? nullptr : F.counters + LP_CNT_ENTRIES;
     const int tflip = radix_sort_pairs(F.tile_key, F.tile_key_alt, F.entry_val, F.entry_val_alt, nmax, ndev,
                                        bits_for(tiles), F.sort_hist, st);

@@ -37,6 +37,10 @@ int radix_sort_pairs(uint32_t *keys, uint32_t *keys_alt, uint32_t *vals, uint32_
 void launch_scan_tiles(const lp_frame &F, int n, cudaStream_t st);   // offsets + E -> counters
 void launch_emit(const lp_frame &F, int n, int64_t max_entries, cudaStream_t st);
 void launch_ranges(const lp_frame &F, const uint32_t *sorted_tile, int tiles, cudaStream_t st);
+// small frames (n <= 4096, capacity <= 8192): one-CTA depth sort + scan and tile sort + ranges
+bool small_bin_ok(const lp_frame &F);
+void launch_small_depth_scan(const lp_frame &F, cudaStream_t st);
+void launch_small_tile_sort(const lp_frame &F, int bits, int tiles, cudaStream_t st);
 // deterministic frames: emission positions + sorted values back to primitive ids (after the tile sort)
 void launch_det_fixup(const lp_frame &F, uint32_t *sorted_val, cudaStream_t st);
 // deterministic frames: per-primitive raster moments summed in a fixed order from the (entry, warp) partials

@@ -21,7 +21,7 @@
 namespace lp {
 
 constexpr int RADIX = 256;
-constexpr int RADIX_FUSE_BLOCKS = 64;   // up to this many scatter blocks the per-digit scan is fused in
+constexpr int RADIX_FUSE_BLOCKS = 128;   // up to this many scatter blocks the per-digit scan is fused in
 constexpr int WARPS = SORT_THREADS / 32;
 
 __device__ __forceinline__ int64_t item_count(const uint32_t *n_dev, int64_t n_host) {
@@ -454,6 +454,188 @@ void launch_ranges(const lp_frame &F, const uint32_t *sorted_tile, int tiles, cu
   if (F.capacity <= 0) return;
   const int64_t grid = (F.capacity + 255) / 256;
   k_ranges<<<(unsigned)grid, 256, 0, st>>>(sorted_tile, F.counters + LP_CNT_ENTRIES, F.capacity, F.ranges);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Small problems (C1-sized frames): launch latency, not bandwidth, bounds the ~23-launch pipeline
+// above, so one 1024-thread CTA does the depth sort + scan in shared memory (k_small_depth_scan)
+// and another the tile sort + ranges (k_small_tile_sort): lp_bin_sort becomes 3 launches (with
+// k_emit).  Same stable LSD passes as the multi-block path (match_any ranks in element order),
+// hence the same order bit for bit.
+// ---------------------------------------------------------------------------------------------
+constexpr int SMALL_THREADS = 1024, SMALL_WARPS = SMALL_THREADS / 32;
+
+// one stable 8-bit LSD pass of (key, val) over n <= 32 * 32 * ITEMS elements in shared memory
+template <int ITEMS>
+__device__ void small_radix_pass(const uint32_t *ki, const uint32_t *vi, uint32_t *ko, uint32_t *vo, int n, int shift,
+                                 uint32_t (*s_wcnt)[RADIX], uint32_t *s_local, uint32_t *s_tmp) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int d = lane; d < RADIX; d += 32) s_wcnt[warp][d] = 0;
+  __syncwarp();
+  uint32_t key[ITEMS], val[ITEMS], rank[ITEMS];
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const int li = warp * 32 * ITEMS + r * 32 + lane;
+    const bool valid = li < n;
+    key[r] = valid ? ki[li] : 0u;
+    val[r] = valid ? vi[li] : 0u;
+    const uint32_t d = (key[r] >> shift) & 0xFF;
+    const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0x100u + lane);
+    const int leader = __ffs(peers) - 1;
+    uint32_t b = 0;
+    if (valid && lane == leader) {
+      b = s_wcnt[warp][d];
+      s_wcnt[warp][d] = b + __popc(peers);
+    }
+    b = __shfl_sync(0xffffffffu, b, leader);
+    rank[r] = b + __popc(peers & lt);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit (threads 0..255): exclusive prefix over the warps, then over the digits
+  uint32_t run = 0;
+  if (tid < RADIX) {
+#pragma unroll 4
+    for (int w = 0; w < SMALL_WARPS; ++w) {
+      const uint32_t c = s_wcnt[w][tid];
+      s_wcnt[w][tid] = run;
+      run += c;
+    }
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_tmp[warp] = x;
+    s_local[tid] = x - run;   // exclusive within the warp
+  }
+  __syncthreads();
+  if (tid < RADIX) {
+    uint32_t base = 0;
+    for (int w = 0; w < warp; ++w) base += s_tmp[w];
+    s_local[tid] += base;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const int li = warp * 32 * ITEMS + r * 32 + lane;
+    if (li < n) {
+      const uint32_t d = (key[r] >> shift) & 0xFF;
+      const uint32_t pos = s_local[d] + s_wcnt[warp][d] + rank[r];
+      ko[pos] = key[r];
+      vo[pos] = val[r];
+    }
+  }
+  __syncthreads();
+}
+
+constexpr int SMALL_DEPTH_ITEMS = 4;                                   // n <= 4096 primitives
+constexpr int SMALL_TILE_ITEMS = 8;                                    // E <= 8192 entries
+constexpr int SMALL_N = SMALL_THREADS * SMALL_DEPTH_ITEMS;
+constexpr int SMALL_E = SMALL_THREADS * SMALL_TILE_ITEMS;
+
+// depth sort of the n primitives (keys prim_key: invisible ones 0xFFFFFFFF sort last) + exclusive
+// scan of tiles_touched in that order -> prim_order, offsets[0..n], E, overflow (and prim_emit)
+__global__ void __launch_bounds__(SMALL_THREADS) k_small_depth_scan(lp_frame F, int n) {
+  extern __shared__ __align__(16) uint32_t s_dyn[];
+  uint32_t *kA = s_dyn, *vA = kA + SMALL_N, *kB = vA + SMALL_N, *vB = kB + SMALL_N;
+  __shared__ uint32_t s_wcnt[SMALL_WARPS][RADIX];
+  __shared__ uint32_t s_local[RADIX], s_tmp[SMALL_WARPS];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < n; i += SMALL_THREADS) {
+    kA[i] = F.prim_key[i];
+    vA[i] = (uint32_t)i;
+  }
+  __syncthreads();
+  small_radix_pass<SMALL_DEPTH_ITEMS>(kA, vA, kB, vB, n, 0, s_wcnt, s_local, s_tmp);
+  small_radix_pass<SMALL_DEPTH_ITEMS>(kB, vB, kA, vA, n, 8, s_wcnt, s_local, s_tmp);
+  small_radix_pass<SMALL_DEPTH_ITEMS>(kA, vA, kB, vB, n, 16, s_wcnt, s_local, s_tmp);
+  small_radix_pass<SMALL_DEPTH_ITEMS>(kB, vB, kA, vA, n, 24, s_wcnt, s_local, s_tmp);
+  // exclusive scan of tiles_touched in depth order: thread t owns elements 4t .. 4t+3
+  uint32_t v[SMALL_DEPTH_ITEMS], sum = 0;
+#pragma unroll
+  for (int k = 0; k < SMALL_DEPTH_ITEMS; ++k) {
+    const int j = tid * SMALL_DEPTH_ITEMS + k;
+    v[k] = j < n ? F.tiles_touched[vA[j]] : 0u;
+    sum += v[k];
+  }
+  uint32_t total;
+  uint32_t run = block_exclusive_scan(sum, s_tmp, total);
+#pragma unroll
+  for (int k = 0; k < SMALL_DEPTH_ITEMS; ++k) {
+    const int j = tid * SMALL_DEPTH_ITEMS + k;
+    if (j < n) {
+      F.prim_order[j] = vA[j];
+      F.prim_key[j] = kA[j];
+      F.offsets[j] = run;
+      if (F.prim_emit) F.prim_emit[vA[j]] = run;
+    }
+    run += v[k];
+  }
+  if (tid == 0) {
+    F.offsets[n] = total;
+    F.counters[LP_CNT_ENTRIES] = total;
+    F.counters[LP_CNT_OVERFLOW] = (int64_t)total > F.capacity ? 1u : 0u;
+  }
+}
+
+// stable sort of the E <= capacity <= 8192 emitted (tile, value) pairs by tile (in place in
+// tile_key / entry_val) and the per-tile ranges
+__global__ void __launch_bounds__(SMALL_THREADS) k_small_tile_sort(lp_frame F, int bits, int tiles) {
+  extern __shared__ __align__(16) uint32_t s_dyn[];
+  uint32_t *kA = s_dyn, *vA = kA + SMALL_E, *kB = vA + SMALL_E, *vB = kB + SMALL_E;
+  __shared__ uint32_t s_wcnt[SMALL_WARPS][RADIX];
+  __shared__ uint32_t s_local[RADIX], s_tmp[SMALL_WARPS];
+  const int tid = threadIdx.x;
+  const int E = (int)min((int64_t)F.counters[LP_CNT_ENTRIES], F.capacity);
+  for (int i = tid; i < E; i += SMALL_THREADS) {
+    kA[i] = F.tile_key[i];
+    vA[i] = F.entry_val[i];
+  }
+  for (int t = tid; t < 2 * tiles; t += SMALL_THREADS) F.ranges[t] = 0u;
+  __syncthreads();
+  uint32_t *ki = kA, *vi = vA, *ko = kB, *vo = vB;
+  for (int shift = 0; shift < bits; shift += 8) {
+    small_radix_pass<SMALL_TILE_ITEMS>(ki, vi, ko, vo, E, shift, s_wcnt, s_local, s_tmp);
+    uint32_t *t0 = ki, *t1 = vi;
+    ki = ko;
+    vi = vo;
+    ko = t0;
+    vo = t1;
+  }
+  for (int e = tid; e < E; e += SMALL_THREADS) {
+    const uint32_t t = ki[e];
+    F.tile_key[e] = t;
+    F.entry_val[e] = vi[e];
+    if (e == 0 || ki[e - 1] != t) F.ranges[2 * (size_t)t] = (uint32_t)e;
+    if (e == E - 1 || ki[e + 1] != t) F.ranges[2 * (size_t)t + 1] = (uint32_t)(e + 1);
+  }
+}
+
+bool small_bin_ok(const lp_frame &F) {
+  return F.n <= SMALL_N && F.capacity <= SMALL_E && F.capacity > 0;
+}
+
+void launch_small_depth_scan(const lp_frame &F, cudaStream_t st) {
+  static bool init = false;
+  const int smem = 4 * SMALL_N * 4;
+  if (!init) {
+    cudaFuncSetAttribute(k_small_depth_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = true;
+  }
+  k_small_depth_scan<<<1, SMALL_THREADS, smem, st>>>(F, F.n);
+}
+
+void launch_small_tile_sort(const lp_frame &F, int bits, int tiles, cudaStream_t st) {
+  static bool init = false;
+  const int smem = 4 * SMALL_E * 4;
+  if (!init) {
+    cudaFuncSetAttribute(k_small_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = true;
+  }
+  k_small_tile_sort<<<1, SMALL_THREADS, smem, st>>>(F, bits, tiles);
 }
 
 }  // namespace lp

@@ -284,3 +284,30 @@ def test_oversize_tile_bucket_uses_global_network():
     scene["pos"][1] = 0.0
     scene["pos"][2][10] = scene["pos"][2][11]            # a depth tie inside the big bucket
     full_parity(scene, cam, seed=5, grads=False, max_masked=0.05)
+
+
+@pytest.mark.parametrize("which", ["C1", "small_octa", "small_tetra", "edge"])
+def test_small_frame_binning_path(which):
+    """Frames with n <= 4096 and capacity <= 8192 bin in one CTA per step (k_small_depth_scan,
+    k_small_tile_sort): the sorted lists, ranges and image equal the oracle's and the multi-block
+    path's bit for bit, and the gradients are identical too."""
+    import torch
+    if which == "C1":
+        scene, cams = scenegen.make_scene("C1", seed=0)
+        cam = cams[0]
+    elif which == "edge":
+        scene, cam = scenegen.edge_scene(TETRA, seed=1)
+    else:
+        scene, cam = scenegen.small_scene(OCTA if which == "small_octa" else TETRA, 1500, seed=7, width=150,
+                                          height=100)
+    G = scenegen.upstream_grad(cam["width"], cam["height"], seed=3)[0]
+    pre = oracle.preprocess(oscene(scene), cam)
+    E = int(pre.tiles_touched.astype(np.int64).sum())
+    assert E + 16 <= 8192
+    outs = []
+    for cap in (E + 16, 1 << 16):        # small path, then the multi-block path
+        ds, r, img = PT.gpu_run(scene, [cam], G=G, capacity=cap)
+        got = PT.frame_arrays(r, 0, scene["pos"].shape[1], K_OF[scene["kind"]])
+        check_binning(got, pre, cam)
+        outs.append((img.cpu().numpy(), ds.grad.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])

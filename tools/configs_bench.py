@@ -51,6 +51,7 @@ def run(name, iters, warmup, exact, size_mult=1.0):
     X_ = int(s[10]) | (int(s[11]) << 32)
     B_ = int(s[12]) | (int(s[13]) << 32)
     vis = int(s[L.LP_CNT_VISIBLE])
+    Wh, A_ = int(s[L.LP_CNT_WARP_HITS]), int(s[L.LP_CNT_TILE_HITS])
     del rr
     rend = render.Renderer(ds, [cam], capacity=int(E * 1.3) + 4096, sync_capacity=False, **kw)
     st = torch.cuda.current_stream(dev)
@@ -109,13 +110,22 @@ def run(name, iters, warmup, exact, size_mult=1.0):
                     "iters_per_s": round(1000.0 / fb_ms, 1)})
     out["calls_ms"] = {k: round(v, 4) for k, v in per.items()}
     alu_peak = 148 * 128 * 1965.0 * 1e6
-    out["raster_fwd_alu_frac"] = round(bench.fp32_ops(ds.kind, I_, B_, X_, False) / (per["fwd"] * 1e-3) / alu_peak, 4)
-    if bwd:
-        out["raster_bwd_alu_frac"] = round(bench.fp32_ops(ds.kind, I_, B_, X_, True) / (per["rbwd"] * 1e-3) / alu_peak, 4)
+    cnt = {"I": I_, "B": B_, "X": X_, "Wh": Wh, "A": A_}
+    # the raster kernels' fractions of the nominal ALU peak under SURVEY §8(d)'s work model and the
+    # builder's (bench.raster_work), side by side
+    for key, b in (("fwd", False), ("rbwd", True)):
+        if key == "rbwd" and not bwd:
+            continue
+        sec = per[key] * 1e-3
+        out[f"raster_{'bwd' if b else 'fwd'}_alu_frac"] = round(bench.raster_work(ds.kind, cnt, b, "survey") / sec / alu_peak, 4)
+        out[f"raster_{'bwd' if b else 'fwd'}_alu_frac_builder"] = round(
+            bench.raster_work(ds.kind, cnt, b, "builder") / sec / alu_peak, 4)
+    out["sort_share_of_fwd"] = round(per["sort"] / fwd_ms, 3)
     out["counters"] = {"tile_list_entries": E, "visible_primitives": vis,
                        "iterated_pairs_per_px": round(I_ / (W * H), 2),
                        "in_bbox_pairs_per_px": round(B_ / (W * H), 2),
-                       "intersected_pairs_per_px": round(X_ / (W * H), 2)}
+                       "intersected_pairs_per_px": round(X_ / (W * H), 2),
+                       "warp_hit_pairs": Wh, "tile_hit_pairs": A_}
     out["clocks"] = clocks.summary()
     return out
 
