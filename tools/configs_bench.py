@@ -64,17 +64,25 @@ def run(name, iters, warmup, exact, size_mult=1.0):
     bwd = name not in RENDER_ONLY
     names = ["pre", "sort", "fwd"] + (["rbwd", "pbwd"] if bwd else [])
 
-    def once(ev=None):
+    def once(ev=None, upto=None):
+        st = torch.cuda.current_stream(dev)   # the capture stream inside torch.cuda.graph
+
         def rec(j):
             if ev is not None:
                 ev[j].record(st)
         rec(0)
         L.lp_preprocess(ds.prims, ca, rend.cfg, fa, st)
         rec(1)
+        if upto == "pre":
+            return
         L.lp_bin_sort(ca, fa, st, None)
         rec(2)
+        if upto == "sort":
+            return
         L.lp_render_fwd(ca, rend.cfg, fa, img[0], st)
         rec(3)
+        if upto == "fwd":
+            return
         if bwd:
             L.lp_raster_bwd(ca, rend.cfg, fa, G[0], st)
             rec(4)
@@ -109,6 +117,32 @@ def run(name, iters, warmup, exact, size_mult=1.0):
         out.update({"fwd_bwd_ms": round(fb_ms, 4), "fwd_bwd_mpix_s": round(W * H / (fb_ms * 1e-3) / 1e6, 2),
                     "iters_per_s": round(1000.0 / fb_ms, 1)})
     out["calls_ms"] = {k: round(v, 4) for k, v in per.items()}
+    # the same frame replayed as a CUDA graph (launch gaps of the latency-bound small configs shrink):
+    # medians of --iters replays after an L2 flush, graphs of pre | pre+sort | fwd (| fwd+bwd)
+    gms = {}
+    for upto in ("pre", "sort", "fwd") + (("all",) if bwd else ()):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            once(upto=None if upto == "all" else upto)
+        times = []
+        for k in range(iters + 3):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            g.replay()
+            e1.record(st)
+            torch.cuda.synchronize()
+            if k >= 3:
+                times.append(e0.elapsed_time(e1))
+            ds.grad.zero_()
+        gms[upto] = statistics.median(times)
+        del g
+    out["graph_ms"] = {"pre": round(gms["pre"], 4), "sort": round(gms["sort"] - gms["pre"], 4),
+                       "fwd_total": round(gms["fwd"], 4), "fwd_mpix_s": round(W * H / (gms["fwd"] * 1e-3) / 1e6, 2),
+                       "sort_share_of_fwd": round((gms["sort"] - gms["pre"]) / gms["fwd"], 3)}
+    if bwd:
+        out["graph_ms"].update({"fwd_bwd_total": round(gms["all"], 4),
+                                "fwd_bwd_mpix_s": round(W * H / (gms["all"] * 1e-3) / 1e6, 2)})
     alu_peak = 148 * 128 * 1965.0 * 1e6
     cnt = {"I": I_, "B": B_, "X": X_, "Wh": Wh, "A": A_}
     # the raster kernels' fractions of the nominal ALU peak under SURVEY §8(d)'s work model and the
