@@ -108,8 +108,10 @@ typedef struct {
   float    *canon;            /* [n][2 + 3K] canonical fp32 cr_x, cr_y, offsets (debug; NULL unless requested) */
   int32_t  *tile_diff;        /* [(tiles_y+1)][(tiles_x+1)] 2-D difference counts of the tile rects (bucket sort) */
   uint32_t *tile_cursor;      /* [tiles] bucket fill cursors (bucket sort) */
-  int32_t   sort_method;      /* LP_SORT_RADIX (default set by lp_frame_init) or LP_SORT_BUCKET; caller may change
-                                 before lp_preprocess (K1 fills the bucket method's rect grid only when selected) */
+  int32_t   sort_method;      /* LP_SORT_BUCKET or LP_SORT_RADIX; lp_frame_init picks BUCKET for n <= 300000 (launch-
+                                 latency-bound frames) and RADIX above it and for deterministic frames; the caller
+                                 may change it before lp_preprocess (K1 fills the bucket method's rect grid only
+                                 when selected; deterministic frames require RADIX) */
   uint32_t *hitmask;          /* [4][capacity/32 + 2] per warp of a tile, one bit per tile-list entry: the forward
                                  sets it when the entry intersected one of the warp's pixels; the backward
                                  replays only those entries */

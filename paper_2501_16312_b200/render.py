@@ -132,7 +132,7 @@ class Renderer:
                  with_canon=False, count_stats=False, sync_capacity=True, sort_method=None, exact=False,
                  deterministic=False):
         self.scene = scene
-        self.sort_method = L.LP_SORT_RADIX if sort_method is None else int(sort_method)
+        self.sort_method = None if sort_method is None else int(sort_method)   # None: lp_frame_init's default
         self.cam_dicts = list(cams)
         self.cams = L.cameras(self.cam_dicts)
         # exact: the "no ray space" variant (App. D, lp_raster_cfg.exact)
@@ -151,7 +151,8 @@ class Renderer:
     def _new_frame(self, cam, capacity):
         f = Frame(self.scene.kind, self.scene.n, cam["width"], cam["height"], capacity, self.scene.flat.device,
                   self.with_canon, self.deterministic)
-        f.c.sort_method = self.sort_method
+        if self.sort_method is not None:
+            f.c.sort_method = self.sort_method
         return f
 
     def stream(self):

@@ -291,7 +291,7 @@ def test_small_frame_binning_path(which):
     """Frames with n <= 4096 and capacity <= 8192 bin in one CTA per step (k_small_depth_scan,
     k_small_tile_sort): the sorted lists, ranges and image equal the oracle's and the multi-block
     path's bit for bit, and the (deterministic-mode) gradients are identical too."""
-    import torch
+    from paper_2501_16312_b200 import linprim as L
     if which == "C1":
         scene, cams = scenegen.make_scene("C1", seed=0)
         cam = cams[0]
@@ -306,7 +306,8 @@ def test_small_frame_binning_path(which):
     assert E + 16 <= 8192
     outs = []
     for cap in (E + 16, 1 << 16):        # small path, then the multi-block path
-        ds, r, img = PT.gpu_run(scene, [cam], G=G, capacity=cap, deterministic=True)   # bitwise gradients
+        ds, r, img = PT.gpu_run(scene, [cam], G=G, capacity=cap, deterministic=True,   # bitwise gradients
+                                sort_method=L.LP_SORT_RADIX)
         got = PT.frame_arrays(r, 0, scene["pos"].shape[1], K_OF[scene["kind"]])
         check_binning(got, pre, cam)
         outs.append((img.cpu().numpy(), ds.grad.cpu().numpy()))

@@ -34,7 +34,7 @@ from paper_2501_16312_b200 import render, scenegen  # noqa: E402
 RENDER_ONLY = {"C4"}        # BASELINE configs[3]: "render-only FPS"
 
 
-def run(name, iters, warmup, exact, size_mult=1.0):
+def run(name, iters, warmup, exact, size_mult=1.0, sort_method=None):
     dev = torch.device("cuda", 0)
     scene, cams = scenegen.make_scene(name, seed=0, size_scale=scenegen.DEFAULT_SIZE_SCALE * size_mult)
     cam = cams[0]
@@ -53,7 +53,7 @@ def run(name, iters, warmup, exact, size_mult=1.0):
     vis = int(s[L.LP_CNT_VISIBLE])
     Wh, A_ = int(s[L.LP_CNT_WARP_HITS]), int(s[L.LP_CNT_TILE_HITS])
     del rr
-    rend = render.Renderer(ds, [cam], capacity=int(E * 1.3) + 4096, sync_capacity=False, **kw)
+    rend = render.Renderer(ds, [cam], capacity=int(E * 1.3) + 4096, sync_capacity=False, sort_method=sort_method, **kw)
     st = torch.cuda.current_stream(dev)
     img = torch.empty((1, 3, H, W), dtype=torch.float32, device=dev)
     G = torch.from_numpy(scenegen.upstream_grad(W, H, seed=0)).to(dev).reshape(1, 3, H, W).contiguous()
@@ -171,13 +171,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--sort", default="auto", choices=["auto", "radix", "bucket"],
+                    help="lp_frame.sort_method (auto: lp_frame_init's size-based default)")
     ap.add_argument("--size-mult", type=float, nargs="*", default=[1.0],
                     help="primitive size scale multipliers (SURVEY §8d sensitivity sweep: 0.5 1 2)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     for name in a.configs:
         for sm in a.size_mult:
-            r = run(name, a.iters, a.warmup, a.exact, sm)
+            r = run(name, a.iters, a.warmup, a.exact, sm,
+                    sort_method={"auto": None, "bucket": L.LP_SORT_BUCKET, "radix": L.LP_SORT_RADIX}[a.sort])
+            r["sort_method"] = a.sort
             line = json.dumps(r)
             print(line, flush=True)
             if a.out:
