@@ -167,17 +167,20 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifdef LP_BWD_STATS
 // measurement build only (-DLP_BWD_STATS): warp-level event counts of the backward
 // [0] sublist records, [1] records with a lane in bbox, [2] records with a hit lane, [3] sum of hit lanes,
-// [5] in-bbox lane tests
-__device__ unsigned long long g_bwd_stats[8];
+// [5] in-bbox lane tests, [6] reductions where both pixel rows of the warp hit, [7] hit pixels,
+// [8 + h] reductions with h hit lanes (h = 1..32)
+__device__ unsigned long long g_bwd_stats[48];
 extern "C" int lp_debug_bwd_stats(unsigned long long *out, int reset) {
   cudaMemcpyFromSymbol(out, g_bwd_stats, sizeof(g_bwd_stats));
   if (reset) {
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long z[48] = {};
     cudaMemcpyToSymbol(g_bwd_stats, z, sizeof(z));
   }
   return 0;
 }
-#define BWD_STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_bwd_stats[i], (unsigned long long)(v)); } while (0)
+// counted per CTA in shared memory (s_bst), flushed once per CTA: same-address global atomics from every
+// warp of the grid stall the kernel
+#define BWD_STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&s_bst[i], (unsigned)(v)); } while (0)
 #else
 #define BWD_STAT(i, v) do { } while (0)
 #endif
@@ -427,6 +430,10 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
   __shared__ __align__(16) float s_red[NT / 32][32][RGP];
   __shared__ uint32_t s_id2[2][NT];
   __shared__ uint32_t s_last;
+#ifdef LP_BWD_STATS
+  __shared__ unsigned s_bst[48];
+  if (threadIdx.x < 48) s_bst[threadIdx.x] = 0u;
+#endif
 
   const int tile = blockIdx.x;
   const int tx = tile % F.tiles_x, ty = tile / F.tiles_x;
@@ -607,6 +614,15 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
       if (!hm) continue;
       BWD_STAT(2, 1);
       BWD_STAT(3, __popc(hm));
+      BWD_STAT(8 + __popc(hm), 1);
+#ifdef LP_BWD_STATS
+      {
+        const bool a0 = __any_sync(0xffffffffu, hk[0]), a1 = __any_sync(0xffffffffu, hk[1]);
+        const unsigned np = __popc(__ballot_sync(0xffffffffu, hk[0])) + __popc(__ballot_sync(0xffffffffu, hk[1]));
+        BWD_STAT(6, a0 && a1);
+        BWD_STAT(7, np);
+      }
+#endif
       float *row = &s_red[w][__popc(hm & ((1u << lane) - 1u))][0];
       // sigma and colour into registers once per entry, by every lane (one broadcast load; inside
       // the hit lanes' loop the compiler re-reads them after every shared store to the rows)
@@ -743,6 +759,10 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
     }
     }
   }
+#ifdef LP_BWD_STATS
+  __syncthreads();
+  if (threadIdx.x < 48 && s_bst[threadIdx.x]) atomicAdd(&g_bwd_stats[threadIdx.x], (unsigned long long)s_bst[threadIdx.x]);
+#endif
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -11,10 +11,13 @@ from paper_2501_16312_b200 import linprim as L, render, scenegen  # noqa: E402
 scene, cams = scenegen.make_scene(sys.argv[1] if len(sys.argv) > 1 else "C5", seed=0)
 ds = render.DeviceScene(scene, device=torch.device("cuda", 0))
 r = render.Renderer(ds, cams[:1])
+print("scene ready", flush=True)
 img = r.forward()
+torch.cuda.synchronize()
+print("forward done", flush=True)
 g = torch.rand_like(img)
 f = L._lib.lp_debug_bwd_stats
-out = (ctypes.c_ulonglong * 8)()
+out = (ctypes.c_ulonglong * 48)()
 torch.cuda.synchronize()
 f(out, 1)
 r.backward(g)
@@ -26,3 +29,7 @@ names = ["sublist", "any_bbox", "hit", "hit_lanes", "smem_red", "bbox_lanes"]
 for i, n in enumerate(names):
     print(f"{n:12s} {out[i]:>14d}  per-warp {out[i] / warps:10.1f}")
 print("hit lanes per reduction", out[3] / max(out[2], 1), " smem share", out[4] / max(out[2], 1))
+print("reductions with both pixel rows hit", out[6] / max(out[2], 1), " hit pixels per reduction", out[7] / max(out[2], 1))
+hist = [out[8 + h] for h in range(33)]
+tot = max(sum(hist), 1)
+print("h histogram (share of reductions):", " ".join(f"{h}:{hist[h] / tot:.3f}" for h in range(1, 33)))
