@@ -78,6 +78,15 @@ class TrainStep:
         self.joins = [torch.cuda.Event() for _ in self.streams[1:]]
         self.aux = [torch.cuda.Stream(dev) for _ in range(self.n_str)] if split_pre else []
         self.joins_aux = [torch.cuda.Event() for _ in self.aux]
+        # binning of every local view on its own stream, enqueued before any raster work: the sorts
+        # are chains of small latency-bound kernels and overlap the raster kernels of earlier views
+        # instead of queueing behind them (C5 step 9.61 -> 9.48 ms)
+        # (high priority: the block scheduler hands them SMs as raster CTAs retire, ahead of the queued
+        # raster CTAs, so their short kernels do not wait for a whole raster kernel to drain)
+        lo, hi = torch.cuda.Stream.priority_range()
+        self.sort_streams = [torch.cuda.Stream(dev, priority=hi) for _ in range(n)] if streams > 1 else []
+        self.sorted = [torch.cuda.Event() for _ in range(n)]
+        self.joins_sort = [torch.cuda.Event() for _ in self.sort_streams]
         ns = self.n_str
         self.pre_cams = [rend._cams(list(range(min(ns, n)))), rend._cams(list(range(min(ns, n), n)))]
         self.pre_frames = [render.frames_array([rend.frames[i] for i in range(min(ns, n))]),
@@ -144,6 +153,16 @@ class TrainStep:
             self.fork.record(st)
             for s_ in strs[1:]:
                 s_.wait_event(self.fork)
+        early = not serial and len(self.sort_streams) == n_local
+        if early:
+            for i in range(n_local):
+                ss = self.sort_streams[i]
+                ss.wait_event(self.fork if (not split or i < len(strs)) else self.fork2)
+                ev = events[i] if events is not None else None
+                rec(ev, 0, ss)
+                L_.lp_bin_sort(self.ca_view[i], self.fa_view[i], ss, None)
+                rec(ev, 1, ss)
+                self.sorted[i].record(ss)
         for i in range(n_local):
             sx = strs[i % len(strs)]
             if split:
@@ -151,9 +170,12 @@ class TrainStep:
                 sx.wait_event(self.fork if i < len(strs) else self.fork2)
             ca, fa = self.ca_view[i], self.fa_view[i]
             ev = events[i] if events is not None else None
-            rec(ev, 0, sx)
-            L_.lp_bin_sort(ca, fa, sx, None)
-            rec(ev, 1, sx)
+            if early:
+                sx.wait_event(self.sorted[i])
+            else:
+                rec(ev, 0, sx)
+                L_.lp_bin_sort(ca, fa, sx, None)
+                rec(ev, 1, sx)
             L_.lp_render_fwd(ca, self.rend.cfg, fa, self.img[i], sx)
             rec(ev, 2, sx)
             if tgt_ready is not None:
@@ -166,6 +188,10 @@ class TrainStep:
             L_.lp_raster_bwd(ca, self.rend.cfg, fa, self.dL[i], sx)
             rec(ev, 4, sx)
             self.fa_all[i] = fa[0]
+        if early:
+            for j, s_ in enumerate(self.sort_streams):
+                self.joins_sort[j].record(s_)
+                st.wait_event(self.joins_sort[j])
         if split:
             for j, s_ in enumerate(self.aux):
                 self.joins_aux[j].record(s_)
