@@ -24,6 +24,23 @@ constexpr int RADIX = 256;
 constexpr int RADIX_FUSE_BLOCKS = 128;   // up to this many scatter blocks the per-digit scan is fused in
 constexpr int WARPS = SORT_THREADS / 32;
 
+// lanes of the warp holding the same 8-bit digit d as this lane (valid lanes only): eight ballots, one
+// per digit bit, instead of MATCH.ANY (whose latency grows with the number of distinct values -- up
+// to 32 for the random low bytes of depth keys; measured in the k_radix_scatter stall profile)
+__device__ __forceinline__ unsigned digit_peers(uint32_t d, bool valid) {
+#ifdef LP_SORT_MATCH_ANY
+  return __match_any_sync(0xffffffffu, valid ? d : 0x100u + (threadIdx.x & 31));
+#else
+  unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const unsigned m = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+    peers &= ((d >> b) & 1u) ? m : ~m;
+  }
+  return valid ? peers : (1u << (threadIdx.x & 31));
+#endif
+}
+
 __device__ __forceinline__ int64_t item_count(const uint32_t *n_dev, int64_t n_host) {
   if (!n_dev) return n_host;
   const int64_t n = (int64_t)*n_dev;
@@ -128,7 +145,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(const uint32_t *
     key[r] = valid ? keys_in[start + li] : 0u;
     val[r] = valid ? vals_in[start + li] : 0u;
     const uint32_t d = (key[r] >> shift) & 0xFF;
-    const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0x100u + lane);
+    const unsigned peers = digit_peers(d, valid);
     const int leader = __ffs(peers) - 1;
     uint32_t b = 0;
     if (valid && lane == leader) {
@@ -481,7 +498,7 @@ __device__ void small_radix_pass(const uint32_t *ki, const uint32_t *vi, uint32_
     key[r] = valid ? ki[li] : 0u;
     val[r] = valid ? vi[li] : 0u;
     const uint32_t d = (key[r] >> shift) & 0xFF;
-    const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0x100u + lane);
+    const unsigned peers = digit_peers(d, valid);
     const int leader = __ffs(peers) - 1;
     uint32_t b = 0;
     if (valid && lane == leader) {

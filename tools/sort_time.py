@@ -14,7 +14,7 @@ from paper_2501_16312_b200 import linprim as L, render, scenegen  # noqa: E402
 for cfgname in (sys.argv[1:] or ["C3", "C5"]):
     scene, cams = scenegen.make_scene(cfgname, seed=0)
     ds = render.DeviceScene(scene, device=torch.device("cuda", 0))
-    for method in (L.LP_SORT_BUCKET, L.LP_SORT_RADIX, L.LP_SORT_TILE):
+    for method in (L.LP_SORT_BUCKET, L.LP_SORT_RADIX):
         r = render.Renderer(ds, cams[:1], sort_method=method)
         img = r.forward()
         st = r.stream()
@@ -53,7 +53,7 @@ for cfgname in (sys.argv[1:] or ["C3", "C5"]):
         torch.cuda.synchronize()
         same = bool(torch.equal(img, img2))
         print(json.dumps({"lib": os.path.basename(os.environ.get("LP_LIB", "liblinprim.so")), "cfg": cfgname,
-                          "method": ["bucket", "radix", "tile"][method],
+                          "method": ["bucket", "radix"][method],
                           "pre_ms": round(res["pre"], 4), "sort_ms": round(res["pre_sort"] - res["pre"], 4),
                           "sort_fwd_ms": round(res["pre_sort_fwd"] - res["pre"], 4),
                           "E": int(r.counters(0)[0]), "image_unchanged": same}), flush=True)
