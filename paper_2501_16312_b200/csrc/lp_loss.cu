@@ -35,6 +35,9 @@ constexpr float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
 
 struct Win {
   float g[TAPS];
+  // (g[t - 1], g[t]) for t = 0..TAPS (g outside [0, TAPS) is 0): the coefficient pair of two adjacent
+  // outputs (o + 1, o) of the same input at tap t of output o, one FFMA2 for the scalar map's pair
+  float2 gp[TAPS + 1];
 };
 
 struct LossSmem {
@@ -377,13 +380,11 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__
       constexpr int CH = 6, NCH = RA / CH;
       for (int it = tid; it < RI * NCH; it += LT) {
         const int r = it / NCH, c0 = (it % NCH) * CH;
-        float2 a01[CH], a23[CH];
-        float a4[CH];
+        float2 a01[CH], a23[CH], a4p[CH / 2];   // a4p[q] = xy sums of outputs (2q + 1, 2q)
 #pragma unroll
-        for (int j = 0; j < CH; ++j) {
-          a01[j] = a23[j] = make_float2(0.f, 0.f);
-          a4[j] = 0.f;
-        }
+        for (int j = 0; j < CH; ++j) a01[j] = a23[j] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < CH / 2; ++q) a4p[q] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < CH + TAPS - 1; ++k) {
           const float2 v01 = make_float2(X[r * BW + BX + c0 + k], Y[r * BW + BX + c0 + k]);
@@ -395,15 +396,19 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__
             if (t >= 0 && t < TAPS) {
               a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
               a23[j] = ffma2(bc(win.g[t]), v23, a23[j]);
-              a4[j] = fmaf(win.g[t], v4, a4[j]);
             }
+          }
+#pragma unroll
+          for (int q = 0; q < CH / 2; ++q) {
+            const int t = k - 2 * q;   // tap of output 2q (output 2q + 1 takes t - 1)
+            if (t >= 0 && t <= TAPS) a4p[q] = ffma2(win.gp[t], bc(v4), a4p[q]);
           }
         }
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           S.u.a.h01[r][c0 + j] = a01[j];
           S.u.a.h23[r][c0 + j] = a23[j];
-          S.u.a.h4[r][c0 + j] = a4[j];
+          S.u.a.h4[r][c0 + j] = (j & 1) ? a4p[j / 2].x : a4p[j / 2].y;
         }
       }
     }
@@ -413,13 +418,11 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__
       constexpr int CH = 6, NCH = RA / CH;
       for (int it = tid; it < RA * NCH; it += LT) {
         const int c = it % RA, r0 = (it / RA) * CH;
-        float2 a01[CH], a23[CH];
-        float a4[CH];
+        float2 a01[CH], a23[CH], a4p[CH / 2];   // a4p[q] = xy sums of rows (2q + 1, 2q)
 #pragma unroll
-        for (int j = 0; j < CH; ++j) {
-          a01[j] = a23[j] = make_float2(0.f, 0.f);
-          a4[j] = 0.f;
-        }
+        for (int j = 0; j < CH; ++j) a01[j] = a23[j] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < CH / 2; ++q) a4p[q] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < CH + TAPS - 1; ++k) {
           const float2 v01 = S.u.a.h01[r0 + k][c], v23 = S.u.a.h23[r0 + k][c];
@@ -430,10 +433,17 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__
             if (t >= 0 && t < TAPS) {
               a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
               a23[j] = ffma2(bc(win.g[t]), v23, a23[j]);
-              a4[j] = fmaf(win.g[t], v4, a4[j]);
             }
           }
+#pragma unroll
+          for (int q = 0; q < CH / 2; ++q) {
+            const int t = k - 2 * q;
+            if (t >= 0 && t <= TAPS) a4p[q] = ffma2(win.gp[t], bc(v4), a4p[q]);
+          }
         }
+        float a4[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) a4[j] = (j & 1) ? a4p[j / 2].x : a4p[j / 2].y;
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const int r = r0 + j;
@@ -462,13 +472,11 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__
       constexpr int CH = 4, NCH = TS / CH;
       for (int it = tid; it < RA * NCH; it += LT) {
         const int r = it / NCH, c0 = (it % NCH) * CH;
-        float2 a01[CH];
-        float a2[CH];
+        float2 a01[CH], a2p[CH / 2];
 #pragma unroll
-        for (int j = 0; j < CH; ++j) {
-          a01[j] = make_float2(0.f, 0.f);
-          a2[j] = 0.f;
-        }
+        for (int j = 0; j < CH; ++j) a01[j] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < CH / 2; ++q) a2p[q] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < CH + TAPS - 1; ++k) {
           const float2 v01 = S.g01[r][c0 + k];
@@ -476,16 +484,18 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__
 #pragma unroll
           for (int j = 0; j < CH; ++j) {
             const int t = k - j;
-            if (t >= 0 && t < TAPS) {
-              a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
-              a2[j] = fmaf(win.g[t], v2, a2[j]);
-            }
+            if (t >= 0 && t < TAPS) a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+          }
+#pragma unroll
+          for (int q = 0; q < CH / 2; ++q) {
+            const int t = k - 2 * q;
+            if (t >= 0 && t <= TAPS) a2p[q] = ffma2(win.gp[t], bc(v2), a2p[q]);
           }
         }
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           S.u.b.h01[r][c0 + j] = a01[j];
-          S.u.b.h2[r][c0 + j] = a2[j];
+          S.u.b.h2[r][c0 + j] = (j & 1) ? a2p[j / 2].x : a2p[j / 2].y;
         }
       }
     }
@@ -495,13 +505,11 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__
       constexpr int CH = 4, NCH = TS / CH;
       for (int it = tid; it < TS * NCH; it += LT) {
         const int c = it % TS, r0 = (it / TS) * CH;
-        float2 a01[CH];
-        float a2[CH];
+        float2 a01[CH], a2p[CH / 2];
 #pragma unroll
-        for (int j = 0; j < CH; ++j) {
-          a01[j] = make_float2(0.f, 0.f);
-          a2[j] = 0.f;
-        }
+        for (int j = 0; j < CH; ++j) a01[j] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < CH / 2; ++q) a2p[q] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < CH + TAPS - 1; ++k) {
           const float2 v01 = S.u.b.h01[r0 + k][c];
@@ -509,12 +517,17 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__
 #pragma unroll
           for (int j = 0; j < CH; ++j) {
             const int t = k - j;
-            if (t >= 0 && t < TAPS) {
-              a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
-              a2[j] = fmaf(win.g[t], v2, a2[j]);
-            }
+            if (t >= 0 && t < TAPS) a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+          }
+#pragma unroll
+          for (int q = 0; q < CH / 2; ++q) {
+            const int t = k - 2 * q;
+            if (t >= 0 && t <= TAPS) a2p[q] = ffma2(win.gp[t], bc(v2), a2p[q]);
           }
         }
+        float a2[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) a2[j] = (j & 1) ? a2p[j / 2].x : a2p[j / 2].y;
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const int gy = ty0 + r0 + j, gx = tx0 + c;
@@ -543,6 +556,7 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__
     atomicAdd(loss_sum, scale * t);
   }
 }
+
 
 static bool make_box_map(CUtensorMap *map, const float *base, int planes, int H, int W) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
@@ -575,6 +589,7 @@ void launch_loss_ssim(const float *img, const float *tgt, float *dL, float *loss
     s += g[k];
   }
   for (int k = 0; k < TAPS; ++k) win.g[k] = (float)(g[k] / s);
+  for (int t = 0; t <= TAPS; ++t) win.gp[t] = make_float2(t >= 1 ? win.g[t - 1] : 0.f, t < TAPS ? win.g[t] : 0.f);
   const int tiles_x = (W + TS - 1) / TS, tiles_y = (H + TS - 1) / TS;
   // TMA path: rows 16-byte aligned (W % 4 == 0) and 16-byte aligned bases
   const bool aligned = (W % 4) == 0 && ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(tgt)) & 15) == 0;

@@ -46,7 +46,7 @@ def run(x, y, lam):
 
 
 @pytest.mark.parametrize("V,H,W,seed", [(1, 32, 32, 0), (1, 45, 70, 1), (2, 96, 128, 2), (1, 100, 33, 3),
-                                         (1, 7, 5, 4)])
+                                         (1, 7, 5, 4), (1, 470, 70, 5), (1, 217, 40, 6), (1, 252, 64, 7)])
 @pytest.mark.parametrize("lam", [0.2, 1.0])
 def test_loss_and_grad_vs_oracle(V, H, W, seed, lam):
     x, y = images(V, H, W, seed)

@@ -23,3 +23,12 @@ for _ in range(20):
 e1.record(st)
 torch.cuda.synchronize()
 print("loss kernel ms per 8-view batch", e0.elapsed_time(e1) / 20)
+x1, y1, d1 = x[:1].contiguous(), y[:1].contiguous(), d[:1].contiguous()
+for _ in range(3):
+    L.lp_loss_grad(x1, y1, d1, loss, 0.2, 1.0 / x1.numel(), st)
+e0.record(st)
+for _ in range(50):
+    L.lp_loss_grad(x1, y1, d1, loss, 0.2, 1.0 / x1.numel(), st)
+e1.record(st)
+torch.cuda.synchronize()
+print("loss kernel ms per view (3 planes)", e0.elapsed_time(e1) / 50)
