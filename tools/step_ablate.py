@@ -61,7 +61,7 @@ def _skipped_bin_sort(cams, frames, stream, n_entries=None):
 
 L.lp_bin_sort = _recording_bin_sort
 timed()
-names = sys.argv[1:] or ["lp_bin_sort", "lp_loss_grad", "lp_raster_bwd", "lp_preprocess", "lp_preprocess_bwd_assign",
+names = [a for a in sys.argv[1:] if a != "none"] if sys.argv[1:] else ["lp_bin_sort", "lp_loss_grad", "lp_raster_bwd", "lp_preprocess", "lp_preprocess_bwd_assign",
                          "lp_adam_step"]
 res = {"full": []}
 for rep in range(3):   # interleaved repeats, minimum kept (the step time drifts by ~0.5 ms between runs)
