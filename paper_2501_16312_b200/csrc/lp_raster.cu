@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
   __shared__ float4 s_rec[NT * RW4];
   __shared__ unsigned char s_list[NT / 32][NT];
   __shared__ unsigned char s_wm[NT];
+  __shared__ unsigned char s_hit[NT / 32][NT];   // per warp: batch record j hit one of its pixels
   __shared__ unsigned long long s_stat[3];
   // per-record warp masks (footprint strips) in ray space; the bbox test in the counting and the
   // no-ray-space variants
@@ -230,6 +231,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
   const uint32_t start = F.ranges[2 * tile], end = F.ranges[2 * tile + 1];
   const int W = F.width, H = F.height;
   if (threadIdx.x < 3) s_stat[threadIdx.x] = 0ull;
+  for (int i = threadIdx.x; i < NT * (NT / 32); i += NT) (&s_hit[0][0])[i] = 0;
 
   float fy[PPT], dep[PPT], tlast[PPT];
   float2 T2 = make_float2(1.f, 1.f), C2[3];   // transmittance and colour of the two pixels (lane k = pixel k)
@@ -330,9 +332,10 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
 #pragma unroll
       for (int k = 0; k < PPT; ++k) hk[k] = test[k] && lane_k(ch2, k) > 0.f;
       if (STATS) nbox += (uint32_t)test[0] + (uint32_t)test[1];
-      // the forward's hits of this record -> the warp's hit bits (held by lane j / 32)
+      // the forward's hits of this record -> the warp's hit flags (one byte per batch record; lane 0
+      // writes it, the batch's words are built by ballots after the sub-list)
       if (!__any_sync(0xffffffffu, hk[0] || hk[1])) continue;
-      if (lane == (j >> 5)) hitw |= 1u << (j & 31);
+      if (lane == 0) s_hit[wrp][j] = 1;
       // both pixels composited as f32x2 pairs; a pixel this record does not hit gets chord 0 ->
       // x = 0, E = 1, o = 0, leaving its T and colour bitwise unchanged
       const float2 Tin = T2;
@@ -345,27 +348,43 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
         for (int c = 0; c < 3; ++c) C2[c] = ffma2(wgt, bc(rec[RGB + c]), C2[c]);
         T2 = fmul2(T2, E);
       }
+      if (AUX) {
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        if (!hk[k]) continue;
-        if (AUX && !dset[k] && lane_k(T2, k) < 0.5f) {   // cumulative opacity 1 - T > 0.5 (once per pixel)
-          dset[k] = true;
-          if (EXACT) {
-            dep[k] = enk[k];
-          } else {
-            const uint32_t id = F.sorted_val[b + (uint32_t)j];
-            dep[k] = fa(__uint_as_float(F.depth_key[id]), enk[k]);
+        for (int k = 0; k < PPT; ++k) {
+          if (hk[k] && !dset[k] && lane_k(T2, k) < 0.5f) {   // cumulative opacity 1 - T > 0.5 (once per pixel)
+            dset[k] = true;
+            if (EXACT) {
+              dep[k] = enk[k];
+            } else {
+              const uint32_t id = F.sorted_val[b + (uint32_t)j];
+              dep[k] = fa(__uint_as_float(F.depth_key[id]), enk[k]);
+            }
           }
         }
-        if (STATS) ++nhit;
-        if (lane_k(T2, k) < tstop) {   // include-then-stop (readings 9, 28)
-          done[k] = true;
-          nproc[k] = b + (uint32_t)j - start + 1;
-          tlast[k] = lane_k(Tin, k);   // T in front of the stopping entry (the backward's start)
+      }
+      if (STATS) nhit += (uint32_t)hk[0] + (uint32_t)hk[1];
+      // include-then-stop (readings 9, 28): a pixel stops at most once, so the common path is one
+      // predicate test per pixel pair
+      const bool st0 = hk[0] && T2.x < tstop, st1 = hk[1] && T2.y < tstop;
+      if (st0 || st1) {
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          if (k == 0 ? st0 : st1) {
+            done[k] = true;
+            nproc[k] = b + (uint32_t)j - start + 1;
+            tlast[k] = lane_k(Tin, k);   // T in front of the stopping entry (the backward's start)
+          }
         }
       }
     }
     // this batch's hit bits of the warp -> the global per-warp bit row (entry index = bit index)
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) {
+      const unsigned m = __ballot_sync(0xffffffffu, s_hit[wrp][32 * i + lane] != 0);
+      if (lane == i) hitw = m;
+      s_hit[wrp][32 * i + lane] = 0;
+    }
     if (hitw) write_hit_word(F.hitmask, F.capacity, wrp, b + 32u * (uint32_t)lane, hitw);
   }
 
