@@ -309,6 +309,7 @@ struct LossSmemT {
   float2 g01[RA][RA + 1];
   float g2[RA][RA + 1];
   unsigned long long bar[2];
+  int meta[2][3];                    // per buffer: tile origin x, y and plane of the item it holds
   float red[LT / 32];
 };
 
@@ -355,14 +356,20 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // (the item's tile origin and plane are computed once, by the issuing thread, and read from shared
+  // memory by all: integer divisions by the runtime grid sizes were ~7 % of the instructions)
   auto issue = [&](int item, int buf) {
     const int plane = item / tiles_per_plane, tile = item % tiles_per_plane;
     const int tx0 = (tile % tiles_x) * TS, ty0 = (tile / tiles_x) * TS;
+    S.meta[buf][0] = tx0;
+    S.meta[buf][1] = ty0;
+    S.meta[buf][2] = plane;
     mbar_expect_tx(&S.bar[buf], 2 * BOX_BYTES);
     tma_load_3d(S.box[buf][0], &map_x, tx0 - 2 * RAD - BX, ty0 - 2 * RAD, plane, &S.bar[buf]);
     tma_load_3d(S.box[buf][1], &map_y, tx0 - 2 * RAD - BX, ty0 - 2 * RAD, plane, &S.bar[buf]);
   };
   if (tid == 0 && (int)blockIdx.x < items) issue(blockIdx.x, 0);
+  __syncthreads();   // the first item's metadata
   float lsum = 0.f;
   uint32_t phase[2] = {0u, 0u};
   int buf = 0;
@@ -371,8 +378,7 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__
     mbar_wait(&S.bar[buf], phase[buf]);
     phase[buf] ^= 1u;
     const float *X = S.box[buf][0], *Y = S.box[buf][1];
-    const int plane = item / tiles_per_plane, tile = item % tiles_per_plane;
-    const int tx0 = (tile % tiles_x) * TS, ty0 = (tile / tiles_x) * TS;
+    const int tx0 = S.meta[buf][0], ty0 = S.meta[buf][1], plane = S.meta[buf][2];
     float *D = dL + (size_t)plane * H * W;
 
     // ---- stage 2: horizontal window sums of the five products, 52 rows x 42 cols
