@@ -509,9 +509,13 @@ __device__ __forceinline__ void view_feature_grad(const lp_prims &P, const lp_ca
   // ---- the 2D filter adds constants (fixed extreme index): identity.
   using CT = float;   // the chain below is well conditioned: fp32 (the M^-1 / plane part above is fp64)
   // ---- o_j = J W (dh_j R b_j); c_ray = phi(p), p = W c + t  (fp64 chain)
+  // (one division per distinct denominator -- |q|, p_z, |p| -- and products with its reciprocal:
+  // IEEE divisions were ~a third of K5's instructions; this chain is tolerance-compared, not part
+  // of the bit-exact canonical contract)
   CT q[4] = {qf[0], qf[1], qf[2], qf[3]};
   const CT nq = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-  const CT w = q[0] / nq, x = q[1] / nq, y = q[2] / nq, z = q[3] / nq;
+  const CT inq = 1.0f / nq;
+  const CT w = q[0] * inq, x = q[1] * inq, y = q[2] * inq, z = q[3] * inq;
   const CT R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
                           {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
                           {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
@@ -524,8 +528,9 @@ __device__ __forceinline__ void view_feature_grad(const lp_prims &P, const lp_ca
 #pragma unroll
   for (int r = 0; r < 3; ++r) p[r] = Wm[r][0] * cf[0] + Wm[r][1] * cf[1] + Wm[r][2] * cf[2] + (CT)cam.t[r];
   const CT l = sqrtf(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
-  const CT fx = cam.fx, fy = cam.fy, pz = p[2], pz2 = pz * pz, pz3 = pz2 * pz;
-  const CT J[3][3] = {{fx / pz, 0, -fx * p[0] / pz2}, {0, fy / pz, -fy * p[1] / pz2}, {p[0] / l, p[1] / l, p[2] / l}};
+  const CT fx = cam.fx, fy = cam.fy, pz = p[2];
+  const CT ipz = 1.0f / pz, ipz2 = ipz * ipz, ipz3 = ipz2 * ipz, il = 1.0f / l, il2 = il * il;
+  const CT J[3][3] = {{fx * ipz, 0, -fx * p[0] * ipz2}, {0, fy * ipz, -fy * p[1] * ipz2}, {p[0] * il, p[1] * il, p[2] * il}};
   CT gJ[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, gR[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   CT gdh[4] = {0, 0, 0, 0};
   const CT kk = 0.57735026918962576451f;
@@ -572,16 +577,16 @@ __device__ __forceinline__ void view_feature_grad(const lp_prims &P, const lp_ca
   } else {
 #pragma unroll
   for (int a = 0; a < 3; ++a) gp[a] = J[0][a] * gcr[0] + J[1][a] * gcr[1];   // c_ray.z gets no gradient
-  gp[2] += gJ[0][0] * (-fx / pz2);
-  gp[0] += gJ[0][2] * (-fx / pz2);
-  gp[2] += gJ[0][2] * (2.0f * fx * p[0] / pz3);
-  gp[2] += gJ[1][1] * (-fy / pz2);
-  gp[1] += gJ[1][2] * (-fy / pz2);
-  gp[2] += gJ[1][2] * (2.0f * fy * p[1] / pz3);
+  gp[2] += gJ[0][0] * (-fx * ipz2);
+  gp[0] += gJ[0][2] * (-fx * ipz2);
+  gp[2] += gJ[0][2] * (2.0f * fx * p[0] * ipz3);
+  gp[2] += gJ[1][1] * (-fy * ipz2);
+  gp[1] += gJ[1][2] * (-fy * ipz2);
+  gp[2] += gJ[1][2] * (2.0f * fy * p[1] * ipz3);
 #pragma unroll
   for (int k = 0; k < 3; ++k)
 #pragma unroll
-    for (int mm = 0; mm < 3; ++mm) gp[mm] += gJ[2][k] * (((k == mm) ? 1.0f : 0.0f) - p[k] * p[mm] / (l * l)) / l;
+    for (int mm = 0; mm < 3; ++mm) gp[mm] += gJ[2][k] * (((k == mm) ? 1.0f : 0.0f) - p[k] * p[mm] * il2) * il;
   }
   CT gc[3];
 #pragma unroll
@@ -613,7 +618,7 @@ __device__ __forceinline__ void view_feature_grad(const lp_prims &P, const lp_ca
     const CT qh[4] = {w, x, y, z};
     const CT dot = qh[0] * gq[0] + qh[1] * gq[1] + qh[2] * gq[2] + qh[3] * gq[3];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) grot[a] += (float)((gq[a] - qh[a] * dot) / nq);
+    for (int a = 0; a < 4; ++a) grot[a] += (float)((gq[a] - qh[a] * dot) * inq);
   }
   // ---- opacity: Eq. 1 with the denominator frozen, alpha = sigmoid(logit)
   {
@@ -651,9 +656,10 @@ __device__ __forceinline__ void sh_view_inputs(const lp_prims &P, const lp_camer
   const float cpz = -(cam.W[2] * cam.t[0] + cam.W[5] * cam.t[1] + cam.W[8] * cam.t[2]);
   const float d[3] = {c[0] - cpx, c[1] - cpy, c[2] - cpz};
   const float nv = sqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-  dir[0] = d[0] / nv;
-  dir[1] = d[1] / nv;
-  dir[2] = d[2] / nv;
+  const float inv = 1.0f / nv;
+  dir[0] = d[0] * inv;
+  dir[1] = d[1] * inv;
+  dir[2] = d[2] * inv;
   if constexpr (DEG == 0) return;
   if (gr[0] == 0.f && gr[1] == 0.f && gr[2] == 0.f) return;
   float wk[16];
@@ -669,7 +675,7 @@ __device__ __forceinline__ void sh_view_inputs(const lp_prims &P, const lp_camer
   sh_basis_grad_dot<float>(DEG, dir[0], dir[1], dir[2], wk, gdir);
   const float dd = dir[0] * gdir[0] + dir[1] * gdir[1] + dir[2] * gdir[2];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) gpos[a] += (gdir[a] - dir[a] * dd) / nv;
+  for (int a = 0; a < 3; ++a) gpos[a] += (gdir[a] - dir[a] * dd) * inv;
 }
 
 // per-item result record in shared memory
