@@ -187,9 +187,15 @@ def run_ours(args, rank, world, local_rank):
     tgt_scene["pos"] = (scene["pos"] + rng.normal(0, 0.01, scene["pos"].shape) *
                         scene["dist"].mean(0, keepdims=True)).astype(np.float32)
     tds = render.DeviceScene(tgt_scene, device=dev)
-    targets = render.Renderer(tds, my_cams, exact=args.exact, aa_kernel=kappa).forward()
+    targets_render = render.Renderer(tds, my_cams, exact=args.exact, aa_kernel=kappa).forward()
+    # training targets are 8-bit images (the datasets' PNG / JPEG frames): quantised once here; both the
+    # device-timed loop and the e2e loop train on the same 8-bit targets, e2e ships them as bytes and
+    # expands them on the device (lp_image_from_u8)
+    targets_u8 = (targets_render.clamp(0.0, 1.0) * 255.0).round().to(torch.uint8)
+    targets = torch.empty_like(targets_render)
+    L.lp_image_from_u8(targets_u8, targets, torch.cuda.current_stream(dev))
     torch.cuda.synchronize()
-    del tds
+    del tds, targets_render
 
     # counters pass (untimed): per view E, I, B, X, W_h, A, visible primitives
     rr = render.Renderer(ds, my_cams, count_stats=True, exact=args.exact, aa_kernel=kappa)
@@ -368,8 +374,9 @@ def run_ours(args, rank, world, local_rank):
     # ---------------- e2e: host (pinned) targets copied in and the loss read back every step
     e2e = None
     if not args.no_e2e:
-        host_t = torch.empty(targets.shape, dtype=torch.float32, pin_memory=True)
-        host_t.copy_(targets)
+        host_t = torch.empty(targets_u8.shape, dtype=torch.uint8, pin_memory=True)
+        host_t.copy_(targets_u8)
+        dev_u8 = [torch.empty_like(targets_u8), torch.empty_like(targets_u8)]
         dev_t = [torch.empty_like(targets), torch.empty_like(targets)]
         cp = torch.cuda.Stream(dev)
         copied = [[torch.cuda.Event() for _ in range(n_local)] for _ in range(2)]
@@ -383,7 +390,8 @@ def run_ours(args, rank, world, local_rank):
         def copy_in(b):
             with torch.cuda.stream(cp):
                 for i in range(n_local):
-                    dev_t[b][i].copy_(host_t[i], non_blocking=True)
+                    dev_u8[b][i].copy_(host_t[i], non_blocking=True)
+                    L.lp_image_from_u8(dev_u8[b][i], dev_t[b][i], cp)
                     copied[b][i].record(cp)
 
         barrier()
@@ -415,7 +423,8 @@ def run_ours(args, rank, world, local_rank):
         e2e_step = float(t.item()) / args.steps
         assert all(math.isfinite(x) for x in losses)
         e2e = {"value": round(mpix / (e2e_step * 1e-3), 3), "unit": "Mpixel/s",
-               "h2d_bytes_per_step": int(host_t.numel() * 4 * world), "d2h_bytes_per_step": 4 * world,
+               "h2d_bytes_per_step": int(host_t.numel() * host_t.element_size() * world), "d2h_bytes_per_step": 4 * world,
+               "h2d_format": "8-bit target channels, expanded on the device (lp_image_from_u8)",
                "ms_per_step": round(e2e_step, 3), "loss_last": losses[-1]}
 
     mode = ("sharded Adam (reduce-scatter / all-gather)" if ts.sharded else "one NCCL all_reduce + replicated Adam") \

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 4
+#define LP_ABI_VERSION 5
 #define LP_TILE 16            /* 16 x 16 pixel tiles */
 
 typedef enum {
@@ -269,6 +269,11 @@ lp_status lp_filter3d(const float *pos, int32_t n, const lp_camera *cams_dev, in
 lp_status lp_loss_grad(const float *image, const float *target, float *dL_dimage, float *loss_sum,
                        int32_t n_planes, int32_t height, int32_t width, float lambda, float scale,
                        void *stream);
+
+/* C5 input staging (not part of the method): training images arrive as 8-bit channels (the
+ * datasets' PNG / JPEG targets); dst[i] = src[i] / 255 (IEEE fp32 division, so bitwise
+ * numpy's uint8 -> float32 / 255) for n elements.  src, dst: device pointers; dst written. */
+lp_status lp_image_from_u8(const uint8_t *src, float *dst, int64_t n, void *stream);
 
 /* C5: one fused Adam step over a flat fp32 parameter buffer with per-group learning
  * rates; elements outside every group are left unchanged.  step >= 1 (bias correction). */

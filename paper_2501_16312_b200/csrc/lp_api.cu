@@ -377,6 +377,12 @@ lp_status lp_l1_grad(const float *image, const float *target, float *dL_dimage, 
   return last_error();
 }
 
+lp_status lp_image_from_u8(const uint8_t *src, float *dst, int64_t n, void *stream) {
+  if (n < 0 || (n > 0 && (!src || !dst))) return LP_ERR_ARG;
+  launch_image_from_u8(src, dst, n, static_cast<cudaStream_t>(stream));
+  return last_error();
+}
+
 lp_status lp_filter3d(const float *pos, int32_t n, const lp_camera *cams_dev, int32_t n_cams, float kappa,
                       float *filter3d, void *stream) {
   if (n < 0 || n_cams < 1 || !cams_dev || !filter3d || (n > 0 && !pos) || !(kappa >= 0.f)) return LP_ERR_ARG;

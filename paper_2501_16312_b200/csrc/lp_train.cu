@@ -214,4 +214,35 @@ void launch_adam(float *p, float *g, float *m, float *v, const lp_adam_group *gr
   }
 }
 
+// 8-bit target channels -> fp32 in [0, 1] (16 bytes per thread per iteration)
+__global__ void __launch_bounds__(256) k_image_from_u8(const uint8_t *__restrict__ src, float *__restrict__ dst,
+                                                       int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t n16 = n / 16;
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+    float4 *d4 = reinterpret_cast<float4 *>(dst);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
+      const uint4 w = s4[i];
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        d4[4 * i + q] = make_float4(__fdiv_rn((float)(ww[q] & 0xFFu), 255.f), __fdiv_rn((float)((ww[q] >> 8) & 0xFFu), 255.f),
+                                    __fdiv_rn((float)((ww[q] >> 16) & 0xFFu), 255.f), __fdiv_rn((float)(ww[q] >> 24), 255.f));
+    }
+    done = n16 * 16;
+  }
+  for (int64_t i = done + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = __fdiv_rn((float)src[i], 255.f);
+}
+
+void launch_image_from_u8(const uint8_t *src, float *dst, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  const int64_t want = (n / 16 + 255) / 256;
+  const int grid = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
+  k_image_from_u8<<<grid, 256, 0, st>>>(src, dst, n);
+}
+
 }  // namespace lp

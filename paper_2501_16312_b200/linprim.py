@@ -27,7 +27,7 @@ LP_CNT_WARP_HITS, LP_CNT_TILE_HITS = 5, 6
 LP_CNT_ITERATED, LP_CNT_INTERSECTED, LP_CNT_INBOX, LP_NUM_COUNTERS = 8, 10, 12, 16
 LP_SORT_BUCKET, LP_SORT_RADIX = 0, 1
 LP_FRAME_CANON, LP_FRAME_DETERMINISTIC = 1, 2
-LP_ABI_VERSION = 4            # include/linprim.h; the loaded library must match the structs below
+LP_ABI_VERSION = 5            # include/linprim.h; the loaded library must match the structs below
 
 _p = C.c_void_p
 
@@ -92,6 +92,7 @@ _sig = {
     "lp_frame_counters": (C.c_int, [C.POINTER(lp_frame), C.POINTER(C.c_uint32), _p]),
     "lp_l1_grad": (C.c_int, [_p, _p, _p, _p, C.c_int64, C.c_float, _p]),
     "lp_filter3d": (C.c_int, [_p, C.c_int32, _p, C.c_int32, C.c_float, _p, _p]),
+    "lp_image_from_u8": (C.c_int, [_p, _p, C.c_int64, _p]),
     "lp_loss_grad": (C.c_int, [_p, _p, _p, _p, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_float, _p]),
     "lp_adam_step": (C.c_int, [_p, _p, _p, _p, C.POINTER(lp_adam_group), C.c_int32, C.c_float, C.c_float,
                                C.c_float, C.c_int32, C.c_int32, _p]),
@@ -195,6 +196,13 @@ def lp_frame_counters(frame, stream) -> np.ndarray:
 def lp_l1_grad(image, target, dL, loss_sum, scale, stream):
     return _check(_lib.lp_l1_grad(_ptr(image), _ptr(target), _ptr(dL), _ptr(loss_sum), image.numel(),
                                   C.c_float(scale), _stream(stream)), "lp_l1_grad")
+
+
+def lp_image_from_u8(src_u8, dst, stream):
+    """8-bit target channels -> fp32 / 255 on the device (C5 input staging)."""
+    assert src_u8.numel() == dst.numel()
+    return _check(_lib.lp_image_from_u8(_ptr(src_u8), _ptr(dst), src_u8.numel(), _stream(stream)),
+                  "lp_image_from_u8")
 
 
 def lp_filter3d(pos, n, cams_dev, n_cams, kappa, out, stream):

@@ -75,3 +75,19 @@ def test_identical_images_zero_loss():
     x, _ = images(1, 40, 40, 3)
     L_got, G = run(x, x, 0.2)
     assert abs(L_got) < 1e-6 and np.abs(G).max() < 1e-9
+
+
+def test_image_from_u8_is_numpy_division():
+    """lp_image_from_u8 (the e2e path's 8-bit target staging): bitwise uint8 -> float32 / 255,
+    vectorised body and scalar tail (odd lengths, unaligned tail)."""
+    import torch
+
+    from paper_2501_16312_b200 import linprim as L
+    for n in (1, 15, 16, 17, 4099, 3 * 1060 * 1600):
+        src = np.random.default_rng(n).integers(0, 256, n, dtype=np.uint8)
+        s = torch.as_tensor(src, device="cuda")
+        d = torch.empty(n, dtype=torch.float32, device="cuda")
+        L.lp_image_from_u8(s, d, torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        ref = src.astype(np.float32) / np.float32(255.0)
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), ref.view(np.uint32))
