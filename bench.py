@@ -61,6 +61,8 @@ def parse(argv=None):
     ap.add_argument("--exact", action="store_true",
                     help="the paper's no-ray-space variant (App. D) instead of the EWA ray-space method")
     ap.add_argument("--streams", type=int, default=4, help="CUDA streams the views of a step are spread over")
+    ap.add_argument("--ar-chunks", type=int, default=4,
+                    help="N > 1: the gradient allreduce as this many in-order async chunks, Adam per chunk")
     ap.add_argument("--assign", action=argparse.BooleanOptionalAction, default=True,
                     help="preprocess backward SETS the step's gradient (lp_preprocess_bwd_assign) instead of "
                          "accumulating into a zeroed one")
@@ -212,7 +214,7 @@ def run_ours(args, rank, world, local_rank):
     ts = S.TrainStep(ds, my_cams, n_views, targets=targets, loss=args.loss, streams=args.streams,
                      split_pre=args.split_pre, assign=args.assign, exact=args.exact,
                      capacity=int(max(cnt["E"]) * 1.3) + 4096, world=world, rank=rank, sharded=args.sharded,
-                     loss_slots=2 * (args.warmup + 3 * args.steps) + 64)
+                     loss_slots=2 * (args.warmup + 3 * args.steps) + 64, ar_chunks=args.ar_chunks)
     st = ts.st
     n_local = ts.n_local
     total_steps = args.warmup + args.steps

@@ -6,9 +6,11 @@ Per step:
   per local view, round-robin over `streams` CUDA streams:
       lp_bin_sort -> lp_render_fwd -> lp_loss_grad (3DGS L1 + SSIM) | lp_l1_grad -> lp_raster_bwd
   lp_preprocess_bwd_assign over all local views (the step's gradient is SET: no zeroing pass)
-  N > 1: ONE NCCL all_reduce(SUM) of the flat fp32 gradient (north_star), then the replicated
-         fused Adam (lp_adam_step) -- or, with sharded=True, reduce_scatter + Adam on this rank's
-         chunk + all_gather of the parameters (same wire bytes, 1/N of the Adam work)
+  N > 1: ONE NCCL all_reduce(SUM) of the flat fp32 gradient (north_star; issued as ar_chunks
+         in-order asynchronous chunks so the replicated fused Adam of chunk k (lp_adam_step, groups
+         clipped to the chunk) overlaps the transfer of chunk k + 1) -- or, with sharded=True,
+         reduce_scatter + Adam on this rank's chunk + all_gather of the parameters (same wire bytes,
+         1/N of the Adam work)
 bench.py times exactly this object; tests/test_gpu_step.py compares one step of it with
 oracle/train.py.c5_step.
 """
@@ -34,7 +36,7 @@ class TrainStep:
     def __init__(self, ds: render.DeviceScene, cams, n_views_total, *, targets=None, loss="l1ssim", lam=0.2,
                  streams=4, split_pre=True, assign=True, exact=False, capacity=None, world=1, rank=0,
                  sharded=False, extent=4.0, betas=(0.9, 0.999), eps=1e-15, loss_slots=256, aa_kernel=None,
-                 deterministic=False):
+                 deterministic=False, ar_chunks=4):
         dev = ds.flat.device
         self.ds, self.dev = ds, dev
         self.n_local = len(cams)
@@ -64,6 +66,11 @@ class TrainStep:
         else:
             self.m = torch.zeros(ds.flat.numel(), dtype=torch.float32, device=dev)
         self.v = torch.zeros_like(self.m)
+        # N > 1, single allreduce: issued as `ar_chunks` in-order chunks, each chunk's Adam (groups
+        # clipped to it) waiting only for its own chunk, so the optimizer overlaps the remaining transfer
+        self.ar_bounds = (train.chunk_bounds(ds.total, ar_chunks) if world > 1 and not self.sharded and ar_chunks > 1
+                          else [])
+        self.ar_groups = [train.shard_groups(groups, lo, hi) for lo, hi in self.ar_bounds]
         st = torch.cuda.current_stream(dev)
         self.st = st
         n = self.n_local
@@ -214,6 +221,13 @@ class TrainStep:
             L_.lp_adam_step(ds.flat_padded[self.rank * c:(self.rank + 1) * c], self.gshard, self.m, self.v,
                             self.sgroups, b1, b2, self.eps, t, st, zero_grad=False)
             train.all_gather_params(ds.flat_padded, self.rank, c)
+        elif self.ar_bounds and not serial:
+            works = train.allreduce_gradients_chunked(ds.grad, self.world, self.ar_bounds)
+            rec(S, 3, st)
+            for (lo, hi), grp, work in zip(self.ar_bounds, self.ar_groups, works):
+                work.wait()   # the current stream waits for this chunk's collective only
+                L_.lp_adam_step(ds.flat[lo:hi], ds.grad[lo:hi], self.m[lo:hi], self.v[lo:hi], grp, b1, b2,
+                                self.eps, t, st, zero_grad=not self.assign)
         else:
             train.allreduce_gradients(ds.grad, self.world)
             rec(S, 3, st)

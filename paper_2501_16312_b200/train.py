@@ -50,6 +50,22 @@ def allreduce_gradients(flat_grad, world: int):
     return flat_grad
 
 
+def chunk_bounds(total: int, parts: int, align: int = 4) -> list:
+    """[(lo, hi)] covering [0, total) in `parts` contiguous pieces of about equal size, every lo a
+    multiple of `align` (float4 Adam path); empty pieces dropped."""
+    per = -(-total // max(1, parts))
+    per = -(-per // align) * align
+    return [(lo, min(lo + per, total)) for lo in range(0, total, per)] if total > 0 else []
+
+
+def allreduce_gradients_chunked(flat_grad, world: int, bounds):
+    """The same SUM-allreduce as `allreduce_gradients`, issued as one asynchronous collective per
+    chunk of `bounds` (in order); returns the works.  The caller waits chunk k's work before its
+    optimizer step on chunk k, so Adam on chunk k overlaps the transfer of chunk k + 1."""
+    import torch.distributed as dist
+    return [dist.all_reduce(flat_grad[lo:hi], op=dist.ReduceOp.SUM, async_op=True) for lo, hi in bounds]
+
+
 # ---------------------------------------------------------------------------------------------
 # sharded optimizer (N > 1): reduce-scatter the flat gradient, Adam on the rank's shard only,
 # all-gather the parameters -- the allreduce's wire bytes, 1/N of the Adam work and Adam state

@@ -160,3 +160,51 @@ def test_two_rank_sharded_adam_matches_allreduce_adam(tmp_path):
     _adam_ref(p, g, m, v, train.lr_groups(off, n), step=1)
     assert np.array_equal(p0, p.numpy())
     assert np.abs(p0 - np.linspace(-1, 1, total)).max() > 1e-4   # the step moved the parameters
+
+
+def _chunked_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    scene, cams = _scene()
+    n, kind, deg = scene["pos"].shape[1], scene["kind"], scene["sh_degree"]
+    off = train.flat_offsets(kind, n, deg)
+    total = max(e for _, e in off.values())
+    g = torch.from_numpy(_flat_grad(scene, cams, train.shard_views(N_VIEWS, rank, world))).float()
+    p = torch.linspace(-1, 1, total)
+    m, v = torch.zeros(total), torch.zeros(total)
+    groups = train.lr_groups(off, n)
+    bounds = train.chunk_bounds(total, 4)
+    works = train.allreduce_gradients_chunked(g, world, bounds)
+    for (lo, hi), work in zip(bounds, works):   # TrainStep.run's order: wait chunk k, Adam on chunk k
+        work.wait()
+        _adam_ref(p[lo:hi], g[lo:hi], m[lo:hi], v[lo:hi], train.shard_groups(groups, lo, hi), step=1)
+    np.save(os.path.join(out_dir, f"c{rank}.npy"), p.numpy())
+    dist.destroy_process_group()
+
+
+def test_chunk_bounds_cover_the_buffer():
+    for total, parts in ((0, 4), (1, 4), (7, 4), (1000, 4), (1001, 3), (59 * 1000, 4)):
+        b = train.chunk_bounds(total, parts)
+        assert [x for lo, hi in b for x in range(lo, hi)] == list(range(total))
+        assert all(lo % 4 == 0 and hi > lo for lo, hi in b) and len(b) <= parts
+
+
+def test_two_rank_chunked_allreduce_adam_matches_single(tmp_path):
+    """The chunked allreduce (one async collective per chunk) with Adam per chunk on groups clipped to
+    the chunk == one allreduce + Adam over the whole buffer (TrainStep's N > 1 default)."""
+    world = 2
+    mp.spawn(_chunked_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    c0, c1 = np.load(tmp_path / "c0.npy"), np.load(tmp_path / "c1.npy")
+    assert np.array_equal(c0, c1)
+    scene, cams = _scene()
+    n, kind, deg = scene["pos"].shape[1], scene["kind"], scene["sh_degree"]
+    off = train.flat_offsets(kind, n, deg)
+    total = max(e for _, e in off.values())
+    g = torch.zeros(total, dtype=torch.float32)
+    for r in range(world):
+        g += torch.from_numpy(_flat_grad(scene, cams, train.shard_views(N_VIEWS, r, world))).float()
+    p = torch.linspace(-1, 1, total)
+    m, v = torch.zeros(total), torch.zeros(total)
+    _adam_ref(p, g, m, v, train.lr_groups(off, n), step=1)
+    assert np.array_equal(c0, p.numpy())
