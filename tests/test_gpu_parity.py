@@ -312,3 +312,49 @@ def test_small_frame_binning_path(which):
         check_binning(got, pre, cam)
         outs.append((img.cpu().numpy(), ds.grad.cpu().numpy()))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("kind", [OCTA, TETRA])
+@pytest.mark.parametrize("n_views", [2, 3, 4, 5])
+def test_multi_view_preprocess_equals_single_view_calls(kind, n_views):
+    """One lp_preprocess call over several views (the view-interleaved K1 grid) writes every frame
+    output (tile counts, rects, depth keys, records, canonical geometry) bitwise as one single-view
+    call per view does; the 3D filter and an invalid primitive included."""
+    import torch
+    from paper_2501_16312_b200 import linprim as L
+    from paper_2501_16312_b200 import render
+    n = 5000
+    if kind == OCTA:
+        scene, cams = scenegen.make_scene("C5", seed=2, n=n)
+        cams = [dict(c, width=80, height=64, cx=np.float32(40), cy=np.float32(32),
+                     fx=np.float32(69.3), fy=np.float32(69.3)) for c in cams[:n_views]]
+    else:   # one tetrahedron scene seen through shifted principal points
+        scene, cams = scenegen.make_scene("C2", seed=2, n=n)
+        cams = [dict(cams[0], width=80, height=64, cx=np.float32(40 + 7 * v), cy=np.float32(32 - 3 * v),
+                     fx=np.float32(69.3), fy=np.float32(69.3)) for v in range(n_views)]
+    scene["pos"][0][7] = np.nan
+    f3 = np.random.default_rng(0).uniform(0.0, 0.05, n).astype(np.float32)
+    ds = render.DeviceScene(scene, filter3d=f3)
+    multi = render.Renderer(ds, cams, with_canon=True)
+    singles = [render.Renderer(ds, [c], with_canon=True) for c in cams]
+    st = multi.stream()
+    fa = render.frames_array(multi.frames)
+    L.lp_preprocess(ds.prims, multi._cams(list(range(n_views))), multi.cfg, fa, st)
+    for s_ in singles:
+        fs_ = render.frames_array(s_.frames)
+        L.lp_preprocess(ds.prims, s_._cams([0]), s_.cfg, fs_, st)
+    torch.cuda.synchronize()
+    K = K_OF[scene["kind"]]
+    assert int((multi.frames[0].buf("tiles_touched", n, torch.int32) > 0).sum()) > 100
+    for v in range(n_views):
+        fm_, fs1 = multi.frames[v], singles[v].frames[0]
+        for field, cnt, dt in (("tiles_touched", n, torch.int32), ("rect", 4 * n, torch.int16),
+                               ("depth_key", n, torch.int32), ("record", n * fm_.c.record_words, torch.int32),
+                               ("canon", n * (2 + 3 * K), torch.int32)):
+            a = fm_.buf(field, cnt, dt).cpu().numpy()
+            b = fs1.buf(field, cnt, dt).cpu().numpy()
+            if field == "record":   # records of invisible primitives are not written: compare visible rows
+                vis = fm_.buf("tiles_touched", n, torch.int32).cpu().numpy() > 0
+                a = a.reshape(n, -1)[vis]
+                b = b.reshape(n, -1)[vis]
+            assert np.array_equal(a, b), (field, v)
