@@ -168,7 +168,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // measurement build only (-DLP_BWD_STATS): warp-level event counts of the backward
 // [0] sublist records, [1] records with a lane in bbox, [2] records with a hit lane, [3] sum of hit lanes,
 // [5] in-bbox lane tests, [6] reductions where both pixel rows of the warp hit, [7] hit pixels,
-// [8 + h] reductions with h hit lanes (h = 1..32)
+// [8 + h] reductions with h hit lanes (h = 1..32), [41] / [42] (16x8 half, record) iterations and their
+// active pixel rows under a 2-warps-per-tile, 4-pixels-per-lane mapping
 __device__ unsigned long long g_bwd_stats[48];
 extern "C" int lp_debug_bwd_stats(unsigned long long *out, int reset) {
   cudaMemcpyFromSymbol(out, g_bwd_stats, sizeof(g_bwd_stats));
@@ -451,7 +452,9 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
   __shared__ uint32_t s_last;
 #ifdef LP_BWD_STATS
   __shared__ unsigned s_bst[48];
+  __shared__ unsigned char s_pairs[4][NT];   // per warp and batch record: hit row-pair mask
   if (threadIdx.x < 48) s_bst[threadIdx.x] = 0u;
+  for (int q = threadIdx.x; q < 4 * NT; q += NT) (&s_pairs[0][0])[q] = 0;
 #endif
 
   const int tile = blockIdx.x;
@@ -532,6 +535,19 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
     const uint32_t bstart = bstart_of(bend);
     cp_async_wait_all();
     __syncthreads();   // this batch landed for every thread; every thread is done with the other buffer
+#ifdef LP_BWD_STATS
+    // the previous batch's (16x8 half, record) iterations [41] and their active pixel rows [42] under a
+    // 2-warps-per-tile, 4-pixels-per-lane mapping (halves = warps 0|1 and 2|3)
+    if (threadIdx.x < NT) {
+      const int j = threadIdx.x;
+      const unsigned h0 = s_pairs[0][j] | s_pairs[1][j], h1 = s_pairs[2][j] | s_pairs[3][j];
+      const unsigned it = (h0 != 0u) + (h1 != 0u), rows = __popc(h0) + __popc(h1);
+      if (it) atomicAdd(&s_bst[41], it);
+      if (rows) atomicAdd(&s_bst[42], rows);
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < 4 * NT; q += NT) (&s_pairs[0][0])[q] = 0;
+#endif
     // the next batch's records into the other buffer (their ids were loaded one batch ago), and
     // the id of the batch after it
     if (has_next) stage(buf ^ 1, vnext);
@@ -640,6 +656,16 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
         const unsigned np = __popc(__ballot_sync(0xffffffffu, hk[0])) + __popc(__ballot_sync(0xffffffffu, hk[1]));
         BWD_STAT(6, a0 && a1);
         BWD_STAT(7, np);
+        // row pairs {0,1}, {2,3}, {4,5}, {6,7} of the warp's 8x8 pixels with a hit (a 4-pixels-per-lane
+        // mapping's pixel rows), kept per batch record for the 16x8 half-tile accounting below
+        const unsigned b0 = __ballot_sync(0xffffffffu, hk[0]), b1 = __ballot_sync(0xffffffffu, hk[1]);
+        unsigned pm = 0u;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const unsigned rowbits = ((r < 4 ? b0 : b1) >> (8 * (r & 3))) & 0xFFu;
+          if (rowbits) pm |= 1u << (r >> 1);
+        }
+        if (lane == 0) s_pairs[w][j] = (unsigned char)pm;
       }
 #endif
       float *row = &s_red[w][__popc(hm & ((1u << lane) - 1u))][0];
@@ -779,6 +805,14 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
     }
   }
 #ifdef LP_BWD_STATS
+  __syncthreads();
+  if (threadIdx.x < NT) {
+    const int j = threadIdx.x;
+    const unsigned h0 = s_pairs[0][j] | s_pairs[1][j], h1 = s_pairs[2][j] | s_pairs[3][j];
+    const unsigned it = (h0 != 0u) + (h1 != 0u), rows = __popc(h0) + __popc(h1);
+    if (it) atomicAdd(&s_bst[41], it);
+    if (rows) atomicAdd(&s_bst[42], rows);
+  }
   __syncthreads();
   if (threadIdx.x < 48 && s_bst[threadIdx.x]) atomicAdd(&g_bwd_stats[threadIdx.x], (unsigned long long)s_bst[threadIdx.x]);
 #endif

@@ -30,6 +30,9 @@ for i, n in enumerate(names):
     print(f"{n:12s} {out[i]:>14d}  per-warp {out[i] / warps:10.1f}")
 print("hit lanes per reduction", out[3] / max(out[2], 1), " smem share", out[4] / max(out[2], 1))
 print("reductions with both pixel rows hit", out[6] / max(out[2], 1), " hit pixels per reduction", out[7] / max(out[2], 1))
+print("8x8 warps: (warp, entry) iterations", out[2], " active pixel rows (of 2)", out[2] + out[6])
+print("16x8 halves, 4 pixels per lane: iterations", out[41], " active pixel rows (of 4)", out[42],
+      " rows per iteration", out[42] / max(out[41], 1))
 hist = [out[8 + h] for h in range(33)]
 tot = max(sum(hist), 1)
 print("h histogram (share of reductions):", " ".join(f"{h}:{hist[h] / tot:.3f}" for h in range(1, 33)))
