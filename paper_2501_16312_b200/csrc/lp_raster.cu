@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
       // include-then-stop (readings 9, 28): a pixel stops at most once, so the common path is one
       // predicate test per pixel pair
       const bool st0 = hk[0] && T2.x < tstop, st1 = hk[1] && T2.y < tstop;
-      if (st0 || st1) {
+      if (__any_sync(0xffffffffu, st0 || st1)) {   // warp-uniform: the compiler would predicate a lane branch
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
           if (k == 0 ? st0 : st1) {
