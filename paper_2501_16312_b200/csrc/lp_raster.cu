@@ -721,42 +721,35 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
             const float ax = wt * plane_ik<KIND>(rec, sx, rx, ry), ae = -wt * plane_ik<KIND>(rec, se, rx, ry);
             const float qx0 = fmaf(tx_, rx, -dxp), qx1 = fmaf(tx_, ry, -dyp);
             const float qe0 = fmaf(te, rx, -dxp), qe1 = fmaf(te, ry, -dyp);
-            if (se == sx) {
+            {   // exit then entry plane, one read-modify-write each in order (no branch: se == sx sums too)
               float4 m = slot[sx];
-              m.x += ax + ae;
-              m.y -= ax * qx0 + ae * qe0;
-              m.z -= ax * qx1 + ae * qe1;
-              m.w -= ax * tx_ + ae * te;
-              slot[sx] = m;
-            } else {                                       // distinct slots: both loads first
-              float4 m = slot[sx], n = slot[se];
               m.x += ax;
               m.y -= ax * qx0;
               m.z -= ax * qx1;
               m.w -= ax * tx_;
+              slot[sx] = m;
+              float4 n = slot[se];
               n.x += ae;
               n.y -= ae * qe0;
               n.z -= ae * qe1;
               n.w -= ae * te;
-              slot[sx] = m;
               slot[se] = n;
             }
           } else if (KIND == OCTA) {
             // slab s: (dL/da, dL/db, dL/dc, dL/dhalf) += (w dx, w dy, w, u) with w = gx - gn, u = gx + gn
             const float g = sig * gE, dy = lane_k(dy2, k);   // dL/d exit = g, dL/d entry = -g
-            if (se == sx) {
-              slot[sx].w += g + g;
-            } else {                                       // distinct slots: both loads first
-              float4 m = slot[sx], n = slot[se];
+            {   // exit then entry slab, one read-modify-write each in order (no branch: se == sx sums too)
+              float4 m = slot[sx];
               m.x = fmaf(g, dx, m.x);
               m.y = fmaf(g, dy, m.y);
               m.z += g;
               m.w += g;
+              slot[sx] = m;
+              float4 n = slot[se];
               n.x = fmaf(-g, dx, n.x);
               n.y = fmaf(-g, dy, n.y);
               n.z -= g;
               n.w += g;
-              slot[sx] = m;
               slot[se] = n;
             }
           } else {
