@@ -376,6 +376,8 @@ __global__ void __launch_bounds__(128) k_raster_fwd(lp_frame F, lp_camera cam, l
             tlast[k] = lane_k(Tin, k);   // T in front of the stopping entry (the backward's start)
           }
         }
+        // every pixel of the warp stopped: the rest of its sub-list cannot change them
+        if (__all_sync(0xffffffffu, done[0] && done[1])) break;
       }
     }
     // this batch's hit bits of the warp -> the global per-warp bit row (entry index = bit index)
