@@ -278,12 +278,19 @@ def test_radix_and_bucket_sort_agree(kind):
 
 def test_oversize_tile_bucket_uses_global_network():
     """A tile list longer than the shared-memory capacity (4096) is sorted in place in global memory."""
-    scene, cam = scenegen.small_scene(OCTA, 5000, seed=22, width=16, height=16, size=(0.01, 0.05))
+    from paper_2501_16312_b200 import linprim as L
+    # primitives of a few pixels (smaller ones at the image centre would fall between pixel centres
+    # and touch no tile at all)
+    scene, cam = scenegen.small_scene(OCTA, 5000, seed=22, width=16, height=16, size=(0.3, 0.6))
     scene["pos"][2] = np.random.default_rng(0).uniform(3.0, 8.0, 5000).astype(np.float32)
     scene["pos"][0] = 0.0
     scene["pos"][1] = 0.0
     scene["pos"][2][10] = scene["pos"][2][11]            # a depth tie inside the big bucket
-    full_parity(scene, cam, seed=5, grads=False, max_masked=0.05)
+    pre = oracle.preprocess(oscene(scene), cam)
+    assert int(pre.tiles_touched.sum()) > 4096           # one tile list beyond the shared-memory capacity
+    ds, r, img = PT.gpu_run(scene, [cam], sort_method=L.LP_SORT_BUCKET)
+    check_binning(PT.frame_arrays(r, 0, 5000, K_OF[OCTA]), pre, cam)
+    full_parity(scene, cam, seed=5, grads=False, max_masked=0.05)   # image / T / n_proc (default method)
 
 
 @pytest.mark.parametrize("which", ["C1", "small_octa", "small_tetra", "edge"])
