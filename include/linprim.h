@@ -144,6 +144,7 @@ enum {
   LP_CNT_WARP_HITS = 5,       /* (warp, entry) pairs with a hit: the backward's replayed (warp, primitive) pairs
                                  W_h (count_stats; from lp_render_fwd's hit bits) */
   LP_CNT_TILE_HITS = 6,       /* (tile, entry) pairs hit by any pixel of the tile: A (count_stats) */
+  LP_CNT_SORTED = 7,          /* primitives in lp_bin_sort's depth order (the visible ones; radix method, n > 4096) */
   LP_CNT_ITERATED = 8,        /* words 8-9: u64 (pixel, entry) pairs evaluated by the forward (count_stats) */
   LP_CNT_INTERSECTED = 10,    /* words 10-11: u64 pairs with chord > 0 (count_stats) */
   LP_CNT_INBOX = 12,          /* words 12-13: u64 pairs inside the primitive's screen bbox (count_stats) */

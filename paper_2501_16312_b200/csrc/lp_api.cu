@@ -238,15 +238,16 @@ lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, 
     if (small) {
       launch_small_depth_scan(F, st);
     } else {
-      // 1. depth sort of the primitives (stable: ties keep ascending id, reading 11)
+      // 1. depth sort of the primitives (stable: ties keep ascending id, reading 11); the first pass
+      //    drops the invisible ones (key 0xFFFFFFFF, K1), the other three sort the visible ones only
       const int flip = radix_sort_pairs(F.prim_key, F.prim_key_alt, F.prim_order, F.prim_order_alt, n, nullptr, 32,
-                                        F.sort_hist, st);
+                                        F.sort_hist, st, F.counters + LP_CNT_SORTED);
       if (flip) {
         Fv.prim_key = F.prim_key_alt;
         Fv.prim_order = F.prim_order_alt;
       }
       // 2. exclusive scan of tiles_touched in depth order -> offsets, E
-      launch_scan_tiles(Fv, n, st);
+      launch_scan_tiles(Fv, n, F.counters + LP_CNT_SORTED, st);
     }
     int64_t E_host = -1;
     if (n_entries) {
@@ -262,7 +263,7 @@ lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, 
     }
     // 3. emission in depth order
     const int64_t nmax = E_host >= 0 ? E_host : F.capacity;
-    launch_emit(Fv, n, nmax, st);
+    launch_emit(Fv, n, small ? nullptr : F.counters + LP_CNT_SORTED, nmax, st);
     // 4. stable sort by tile id
     const int tiles = F.tiles_x * F.tiles_y;
     if (small) {   // + 5. ranges, in the same CTA

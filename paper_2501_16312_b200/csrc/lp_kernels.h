@@ -31,11 +31,15 @@ constexpr int SCAN_TILE = 2048;                        // elements per scan bloc
 size_t radix_hist_words(int64_t max_items);
 size_t scan_tmp_words(int64_t max_items);
 // stable LSD radix sort of (key, val) u32 pairs over key bits [0, bits); n from n_dev if non-null
-// else n_host; returns 1 if the result lives in the *_alt buffers.
+// else n_host; returns 1 if the result lives in the *_alt buffers.  kept (non-null): the first pass
+// drops every pair whose key is RADIX_DROP_KEY and writes the number kept to *kept; the later
+// passes (and the caller) sort / use only those (n_dev is then ignored).
+constexpr uint32_t RADIX_DROP_KEY = 0xFFFFFFFFu;
 int radix_sort_pairs(uint32_t *keys, uint32_t *keys_alt, uint32_t *vals, uint32_t *vals_alt, int64_t n_max,
-                     const uint32_t *n_dev, int bits, uint32_t *hist, cudaStream_t st);
-void launch_scan_tiles(const lp_frame &F, int n, cudaStream_t st);   // offsets + E -> counters
-void launch_emit(const lp_frame &F, int n, int64_t max_entries, cudaStream_t st);
+                     const uint32_t *n_dev, int bits, uint32_t *hist, cudaStream_t st, uint32_t *kept = nullptr);
+// n: the host bound; n_dev (nullable): the device count of depth-sorted primitives (<= n)
+void launch_scan_tiles(const lp_frame &F, int n, const uint32_t *n_dev, cudaStream_t st);   // offsets + E -> counters
+void launch_emit(const lp_frame &F, int n, const uint32_t *n_dev, int64_t max_entries, cudaStream_t st);
 void launch_ranges(const lp_frame &F, const uint32_t *sorted_tile, int tiles, cudaStream_t st);
 // small frames (n <= 4096, capacity <= 8192): one-CTA depth sort + scan and tile sort + ranges
 bool small_bin_ok(const lp_frame &F);

@@ -48,6 +48,8 @@ __device__ __forceinline__ int64_t item_count(const uint32_t *n_dev, int64_t n_h
 }
 
 // ---------------------------------------------------------------------------------------------
+// DROP: keys equal to RADIX_DROP_KEY are not counted (and not written by the scatter)
+template <bool DROP>
 __global__ void __launch_bounds__(SORT_THREADS) k_radix_hist(const uint32_t *__restrict__ keys, const uint32_t *n_dev,
                                                              int64_t n_host, int shift, uint32_t *__restrict__ hist,
                                                              int nblk) {
@@ -59,7 +61,10 @@ __global__ void __launch_bounds__(SORT_THREADS) k_radix_hist(const uint32_t *__r
   const int64_t start = (int64_t)blockIdx.x * SORT_TILE;
   if (start < n) {
     const int64_t end = start + SORT_TILE < n ? start + SORT_TILE : n;
-    for (int64_t e = start + tid; e < end; e += SORT_THREADS) atomicAdd(&s_h[warp][(keys[e] >> shift) & 0xFF], 1u);
+    for (int64_t e = start + tid; e < end; e += SORT_THREADS) {
+      const uint32_t k = keys[e];
+      if (!DROP || k != RADIX_DROP_KEY) atomicAdd(&s_h[warp][(k >> shift) & 0xFF], 1u);
+    }
   }
   __syncthreads();
   uint32_t s = 0;
@@ -113,14 +118,17 @@ __global__ void __launch_bounds__(1024) k_radix_scan(uint32_t *__restrict__ hist
 
 // FUSED (few blocks): hist holds the raw per-block digit counts (no k_radix_scan launch); each
 // block sums its own prefix and the digit totals from them (<= RADIX_FUSE_BLOCKS loads per digit).
-template <bool FUSED>
+// DROP: keys equal to RADIX_DROP_KEY are dropped (the output holds the kept pairs in order, their
+// number -> *kept by block 0)
+template <bool FUSED, bool DROP>
 __global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(const uint32_t *__restrict__ keys_in,
                                                                 const uint32_t *__restrict__ vals_in,
                                                                 uint32_t *__restrict__ keys_out,
                                                                 uint32_t *__restrict__ vals_out, const uint32_t *n_dev,
                                                                 int64_t n_host, int shift,
                                                                 const uint32_t *__restrict__ hist,
-                                                                const uint32_t *__restrict__ tot, int nblk) {
+                                                                const uint32_t *__restrict__ tot, int nblk,
+                                                                uint32_t *__restrict__ kept) {
   __shared__ uint32_t s_keys[SORT_TILE];
   __shared__ uint32_t s_vals[SORT_TILE];
   __shared__ uint32_t s_wcnt[WARPS][RADIX];
@@ -137,13 +145,16 @@ __global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(const uint32_t *
   __syncwarp();
   // ---- stable rank within (warp, digit): element index = start + warp*32*ITEMS + r*32 + lane
   uint32_t key[SORT_ITEMS], val[SORT_ITEMS], rank[SORT_ITEMS];
+  unsigned vmask = 0u;   // bit r: key r is kept
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
   for (int r = 0; r < SORT_ITEMS; ++r) {
     const int li = warp * 32 * SORT_ITEMS + r * 32 + lane;
-    const bool valid = li < cnt;
+    bool valid = li < cnt;
     key[r] = valid ? keys_in[start + li] : 0u;
     val[r] = valid ? vals_in[start + li] : 0u;
+    if (DROP) valid = valid && key[r] != RADIX_DROP_KEY;
+    vmask |= valid ? 1u << r : 0u;
     const uint32_t d = (key[r] >> shift) & 0xFF;
     const unsigned peers = digit_peers(d, valid);
     const int leader = __ffs(peers) - 1;
@@ -158,6 +169,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(const uint32_t *
   }
   __syncthreads();
   // ---- per digit: exclusive prefix over warps; block digit counts -> local digit starts
+  uint32_t bkept;   // keys of this block kept (all valid ones unless DROP)
   {
     const int d = tid;   // SORT_THREADS == RADIX
     uint32_t run = 0;
@@ -167,8 +179,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(const uint32_t *
       s_wcnt[w][d] = run;
       run += c;
     }
-    uint32_t total;
-    const uint32_t ex = block_exclusive_scan(run, s_warp, total);
+    const uint32_t ex = block_exclusive_scan(run, s_warp, bkept);
     s_local[d] = ex;
     // global start of digit d = (keys of smaller digits, all blocks) + (digit d, earlier blocks)
     uint32_t tsum, pre;
@@ -188,12 +199,12 @@ __global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(const uint32_t *
     uint32_t gtotal;
     const uint32_t gex = block_exclusive_scan(tsum, s_warp, gtotal);
     s_base[d] = gex + pre;
+    if (DROP && blockIdx.x == 0 && d == 0) *kept = gtotal;
   }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < SORT_ITEMS; ++r) {
-    const int li = warp * 32 * SORT_ITEMS + r * 32 + lane;
-    if (li < cnt) {
+    if ((vmask >> r) & 1u) {
       const uint32_t d = (key[r] >> shift) & 0xFF;
       const uint32_t lp = s_local[d] + s_wcnt[warp][d] + rank[r];
       s_keys[lp] = key[r];
@@ -201,7 +212,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(const uint32_t *
     }
   }
   __syncthreads();
-  for (int i = tid; i < cnt; i += SORT_THREADS) {
+  for (int i = tid; i < (int)bkept; i += SORT_THREADS) {
     const uint32_t k = s_keys[i];
     const uint32_t d = (k >> shift) & 0xFF;
     const uint32_t g = s_base[d] + (uint32_t)i - s_local[d];
@@ -215,22 +226,32 @@ size_t radix_hist_words(int64_t max_items) {
   return (size_t)(nblk > 0 ? nblk : 1) * RADIX + RADIX;
 }
 
+template <bool DROP>
+static void radix_pass(uint32_t *ki, uint32_t *vi, uint32_t *ko, uint32_t *vo, int64_t n_max, const uint32_t *n_dev,
+                       int shift, uint32_t *hist, int nblk, uint32_t *kept, cudaStream_t st) {
+  uint32_t *tot = hist + (size_t)nblk * RADIX;
+  k_radix_hist<DROP><<<nblk, SORT_THREADS, 0, st>>>(ki, n_dev, n_max, shift, hist, nblk);
+  if (nblk <= RADIX_FUSE_BLOCKS) {   // small sorts: two launches per pass instead of three
+    k_radix_scatter<true, DROP><<<nblk, SORT_THREADS, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, hist, tot, nblk,
+                                                               kept);
+  } else {
+    k_radix_scan<<<RADIX, 1024, 0, st>>>(hist, nblk, tot);
+    k_radix_scatter<false, DROP><<<nblk, SORT_THREADS, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, hist, tot, nblk,
+                                                                kept);
+  }
+}
+
 int radix_sort_pairs(uint32_t *keys, uint32_t *keys_alt, uint32_t *vals, uint32_t *vals_alt, int64_t n_max,
-                     const uint32_t *n_dev, int bits, uint32_t *hist, cudaStream_t st) {
+                     const uint32_t *n_dev, int bits, uint32_t *hist, cudaStream_t st, uint32_t *kept) {
+  if (kept && n_max <= 0) cudaMemsetAsync(kept, 0, sizeof(uint32_t), st);
   if (n_max <= 0 || bits <= 0) return 0;
   const int nblk = (int)((n_max + SORT_TILE - 1) / SORT_TILE);
-  uint32_t *tot = hist + (size_t)nblk * RADIX;
   int flip = 0;
   for (int shift = 0; shift < bits; shift += 8) {
     uint32_t *ki = flip ? keys_alt : keys, *vi = flip ? vals_alt : vals;
     uint32_t *ko = flip ? keys : keys_alt, *vo = flip ? vals : vals_alt;
-    k_radix_hist<<<nblk, SORT_THREADS, 0, st>>>(ki, n_dev, n_max, shift, hist, nblk);
-    if (nblk <= RADIX_FUSE_BLOCKS) {   // small sorts: two launches per pass instead of three
-      k_radix_scatter<true><<<nblk, SORT_THREADS, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, hist, tot, nblk);
-    } else {
-      k_radix_scan<<<RADIX, 1024, 0, st>>>(hist, nblk, tot);
-      k_radix_scatter<false><<<nblk, SORT_THREADS, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, hist, tot, nblk);
-    }
+    if (kept && shift == 0) radix_pass<true>(ki, vi, ko, vo, n_max, n_dev, shift, hist, nblk, kept, st);
+    else radix_pass<false>(ki, vi, ko, vo, n_max, kept ? kept : n_dev, shift, hist, nblk, nullptr, st);
     flip ^= 1;
   }
   return flip;
@@ -242,8 +263,9 @@ int radix_sort_pairs(uint32_t *keys, uint32_t *keys_alt, uint32_t *vals, uint32_
 size_t scan_tmp_words(int64_t max_items) { return (size_t)((max_items + SCAN_TILE - 1) / SCAN_TILE) + 32; }
 
 __global__ void __launch_bounds__(256) k_scan_reduce(const uint32_t *__restrict__ order, const uint32_t *__restrict__ tt,
-                                                     int n, uint32_t *__restrict__ part) {
+                                                     int n_host, const uint32_t *n_dev, uint32_t *__restrict__ part) {
   __shared__ uint32_t s_warp[32];
+  const int n = (int)item_count(n_dev, n_host);
   const int base = blockIdx.x * SCAN_TILE;
   uint32_t s = 0;
 #pragma unroll
@@ -257,8 +279,10 @@ __global__ void __launch_bounds__(256) k_scan_reduce(const uint32_t *__restrict_
 }
 
 __global__ void __launch_bounds__(1024) k_scan_top(uint32_t *__restrict__ part, int nb, uint32_t *__restrict__ offsets,
-                                                   int n, uint32_t *__restrict__ counters, int64_t capacity) {
+                                                   int n_host, const uint32_t *n_dev, uint32_t *__restrict__ counters,
+                                                   int64_t capacity) {
   __shared__ uint32_t s_warp[32];
+  const int n = (int)item_count(n_dev, n_host);
   uint32_t carry = 0;
   for (int base = 0; base < nb; base += 1024) {
     const int i = base + threadIdx.x;
@@ -277,10 +301,12 @@ __global__ void __launch_bounds__(1024) k_scan_top(uint32_t *__restrict__ part, 
 
 // prim_emit (deterministic frames, else null): first emitted entry of every primitive
 __global__ void __launch_bounds__(256) k_scan_down(const uint32_t *__restrict__ order, const uint32_t *__restrict__ tt,
-                                                   int n, const uint32_t *__restrict__ part,
+                                                   int n_host, const uint32_t *n_dev, const uint32_t *__restrict__ part,
                                                    uint32_t *__restrict__ offsets, uint32_t *__restrict__ prim_emit) {
   __shared__ uint32_t s_warp[32];
+  const int n = (int)item_count(n_dev, n_host);
   const int base = blockIdx.x * SCAN_TILE;
+  if (base >= n) return;
   // thread t owns 8 consecutive elements: base + 8t .. 8t+7
   uint32_t v[SCAN_TILE / 256];
   uint32_t s = 0;
@@ -303,11 +329,12 @@ __global__ void __launch_bounds__(256) k_scan_down(const uint32_t *__restrict__ 
   }
 }
 
-void launch_scan_tiles(const lp_frame &F, int n, cudaStream_t st) {
+void launch_scan_tiles(const lp_frame &F, int n, const uint32_t *n_dev, cudaStream_t st) {
   const int nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-  if (n > 0) k_scan_reduce<<<nb, 256, 0, st>>>(F.prim_order, F.tiles_touched, n, F.scan_tmp);
-  k_scan_top<<<1, 1024, 0, st>>>(F.scan_tmp, nb, F.offsets, n, F.counters, F.capacity);
-  if (n > 0) k_scan_down<<<nb, 256, 0, st>>>(F.prim_order, F.tiles_touched, n, F.scan_tmp, F.offsets, F.prim_emit);
+  if (n > 0) k_scan_reduce<<<nb, 256, 0, st>>>(F.prim_order, F.tiles_touched, n, n_dev, F.scan_tmp);
+  k_scan_top<<<1, 1024, 0, st>>>(F.scan_tmp, nb, F.offsets, n, n_dev, F.counters, F.capacity);
+  if (n > 0)
+    k_scan_down<<<nb, 256, 0, st>>>(F.prim_order, F.tiles_touched, n, n_dev, F.scan_tmp, F.offsets, F.prim_emit);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -346,7 +373,8 @@ __device__ __forceinline__ int warp_last_leq(const uint32_t *__restrict__ a, int
 }
 
 __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ order, const uint32_t *__restrict__ offsets,
-                                              const ushort4 *__restrict__ rect, int n, int tiles_x, int64_t capacity,
+                                              const ushort4 *__restrict__ rect, int n_host, const uint32_t *n_dev,
+                                              int tiles_x, int64_t capacity,
                                               const uint32_t *__restrict__ E_dev, uint32_t *__restrict__ tile_key,
                                               uint32_t *__restrict__ entry_val, uint32_t *__restrict__ emit_prim) {
   __shared__ uint32_t s_off[EMIT_TILE];
@@ -359,6 +387,7 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ order
   const int64_t e0 = (int64_t)blockIdx.x * EMIT_TILE;
   if (e0 >= E) return;
   const int64_t e1 = e0 + EMIT_TILE < E ? e0 + EMIT_TILE : E;
+  const int n = (int)item_count(n_dev, n_host);
   if (threadIdx.x < 64) {   // warp 0 finds the first primitive of the range, warp 1 the last
     const int j = warp_last_leq(offsets, n, (uint32_t)(threadIdx.x < 32 ? e0 : e1 - 1));
     if (threadIdx.x == 0) s_j0 = j;
@@ -444,10 +473,10 @@ void launch_det_fixup(const lp_frame &F, uint32_t *sorted_val, cudaStream_t st) 
   k_det_fixup<<<148 * 8, 256, 0, st>>>(sorted_val, F.emit_prim, F.emit_pos, F.counters + LP_CNT_ENTRIES, F.capacity);
 }
 
-void launch_emit(const lp_frame &F, int n, int64_t max_entries, cudaStream_t st) {
+void launch_emit(const lp_frame &F, int n, const uint32_t *n_dev, int64_t max_entries, cudaStream_t st) {
   if (n == 0 || max_entries <= 0) return;
   const int64_t grid = (max_entries + EMIT_TILE - 1) / EMIT_TILE;
-  k_emit<<<(unsigned)grid, 256, 0, st>>>(F.prim_order, F.offsets, reinterpret_cast<const ushort4 *>(F.rect), n,
+  k_emit<<<(unsigned)grid, 256, 0, st>>>(F.prim_order, F.offsets, reinterpret_cast<const ushort4 *>(F.rect), n, n_dev,
                                          F.tiles_x, F.capacity, F.counters + LP_CNT_ENTRIES, F.tile_key, F.entry_val,
                                          F.deterministic ? F.emit_prim : nullptr);
 }

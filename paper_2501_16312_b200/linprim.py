@@ -23,7 +23,7 @@ LP_OK, LP_ERR_ARG, LP_ERR_CAPACITY, LP_ERR_CUDA, LP_ERR_UNSUPPORTED = range(5)
 LP_OCTAHEDRON, LP_TETRAHEDRON = 0, 1
 LP_TILE = 16
 LP_CNT_ENTRIES, LP_CNT_OVERFLOW, LP_CNT_INVALID, LP_CNT_FRUSTUM, LP_CNT_VISIBLE = 0, 1, 2, 3, 4
-LP_CNT_WARP_HITS, LP_CNT_TILE_HITS = 5, 6
+LP_CNT_WARP_HITS, LP_CNT_TILE_HITS, LP_CNT_SORTED = 5, 6, 7
 LP_CNT_ITERATED, LP_CNT_INTERSECTED, LP_CNT_INBOX, LP_NUM_COUNTERS = 8, 10, 12, 16
 LP_SORT_BUCKET, LP_SORT_RADIX = 0, 1
 LP_FRAME_CANON, LP_FRAME_DETERMINISTIC = 1, 2
