@@ -263,7 +263,7 @@ lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, 
     }
     // 3. emission in depth order
     const int64_t nmax = E_host >= 0 ? E_host : F.capacity;
-    launch_emit(Fv, n, small ? nullptr : F.counters + LP_CNT_SORTED, nmax, st);
+    const bool hist0 = launch_emit(Fv, n, small ? nullptr : F.counters + LP_CNT_SORTED, nmax, !small, st);
     // 4. stable sort by tile id
     const int tiles = F.tiles_x * F.tiles_y;
     if (small) {   // + 5. ranges, in the same CTA
@@ -275,7 +275,7 @@ lp_status lp_bin_sort(const lp_camera *cams, int32_t n_views, lp_frame *frames, 
     }
     const uint32_t *ndev = E_host >= 0 ? nullptr : F.counters + LP_CNT_ENTRIES;
     const int tflip = radix_sort_pairs(F.tile_key, F.tile_key_alt, F.entry_val, F.entry_val_alt, nmax, ndev,
-                                       bits_for(tiles), F.sort_hist, st);
+                                       bits_for(tiles), F.sort_hist, st, nullptr, hist0);
     F.sorted_tile = tflip ? F.tile_key_alt : F.tile_key;
     F.sorted_val = tflip ? F.entry_val_alt : F.entry_val;
     if (F.deterministic) launch_det_fixup(F, F.sorted_val, st);

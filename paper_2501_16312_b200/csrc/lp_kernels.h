@@ -36,10 +36,12 @@ size_t scan_tmp_words(int64_t max_items);
 // passes (and the caller) sort / use only those (n_dev is then ignored).
 constexpr uint32_t RADIX_DROP_KEY = 0xFFFFFFFFu;
 int radix_sort_pairs(uint32_t *keys, uint32_t *keys_alt, uint32_t *vals, uint32_t *vals_alt, int64_t n_max,
-                     const uint32_t *n_dev, int bits, uint32_t *hist, cudaStream_t st, uint32_t *kept = nullptr);
+                     const uint32_t *n_dev, int bits, uint32_t *hist, cudaStream_t st, uint32_t *kept = nullptr,
+                     bool hist0_ready = false);   // hist0_ready: the first pass's histogram is already in hist
 // n: the host bound; n_dev (nullable): the device count of depth-sorted primitives (<= n)
 void launch_scan_tiles(const lp_frame &F, int n, const uint32_t *n_dev, cudaStream_t st);   // offsets + E -> counters
-void launch_emit(const lp_frame &F, int n, const uint32_t *n_dev, int64_t max_entries, cudaStream_t st);
+// hist0: also write the first tile-sort pass's per-block histogram to F.sort_hist (returns hist0)
+bool launch_emit(const lp_frame &F, int n, const uint32_t *n_dev, int64_t max_entries, bool hist0, cudaStream_t st);
 void launch_ranges(const lp_frame &F, const uint32_t *sorted_tile, int tiles, cudaStream_t st);
 // small frames (n <= 4096, capacity <= 8192): one-CTA depth sort + scan and tile sort + ranges
 bool small_bin_ok(const lp_frame &F);

@@ -228,9 +228,9 @@ size_t radix_hist_words(int64_t max_items) {
 
 template <bool DROP>
 static void radix_pass(uint32_t *ki, uint32_t *vi, uint32_t *ko, uint32_t *vo, int64_t n_max, const uint32_t *n_dev,
-                       int shift, uint32_t *hist, int nblk, uint32_t *kept, cudaStream_t st) {
+                       int shift, uint32_t *hist, int nblk, uint32_t *kept, cudaStream_t st, bool hist_ready = false) {
   uint32_t *tot = hist + (size_t)nblk * RADIX;
-  k_radix_hist<DROP><<<nblk, SORT_THREADS, 0, st>>>(ki, n_dev, n_max, shift, hist, nblk);
+  if (!hist_ready) k_radix_hist<DROP><<<nblk, SORT_THREADS, 0, st>>>(ki, n_dev, n_max, shift, hist, nblk);
   if (nblk <= RADIX_FUSE_BLOCKS) {   // small sorts: two launches per pass instead of three
     k_radix_scatter<true, DROP><<<nblk, SORT_THREADS, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, hist, tot, nblk,
                                                                kept);
@@ -242,7 +242,7 @@ static void radix_pass(uint32_t *ki, uint32_t *vi, uint32_t *ko, uint32_t *vo, i
 }
 
 int radix_sort_pairs(uint32_t *keys, uint32_t *keys_alt, uint32_t *vals, uint32_t *vals_alt, int64_t n_max,
-                     const uint32_t *n_dev, int bits, uint32_t *hist, cudaStream_t st, uint32_t *kept) {
+                     const uint32_t *n_dev, int bits, uint32_t *hist, cudaStream_t st, uint32_t *kept, bool hist0_ready) {
   if (kept && n_max <= 0) cudaMemsetAsync(kept, 0, sizeof(uint32_t), st);
   if (n_max <= 0 || bits <= 0) return 0;
   const int nblk = (int)((n_max + SORT_TILE - 1) / SORT_TILE);
@@ -251,7 +251,8 @@ int radix_sort_pairs(uint32_t *keys, uint32_t *keys_alt, uint32_t *vals, uint32_
     uint32_t *ki = flip ? keys_alt : keys, *vi = flip ? vals_alt : vals;
     uint32_t *ko = flip ? keys : keys_alt, *vo = flip ? vals : vals_alt;
     if (kept && shift == 0) radix_pass<true>(ki, vi, ko, vo, n_max, n_dev, shift, hist, nblk, kept, st);
-    else radix_pass<false>(ki, vi, ko, vo, n_max, kept ? kept : n_dev, shift, hist, nblk, nullptr, st);
+    else radix_pass<false>(ki, vi, ko, vo, n_max, kept ? kept : n_dev, shift, hist, nblk, nullptr, st,
+                           hist0_ready && shift == 0);
     flip ^= 1;
   }
   return flip;
@@ -376,16 +377,22 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ order
                                               const ushort4 *__restrict__ rect, int n_host, const uint32_t *n_dev,
                                               int tiles_x, int64_t capacity,
                                               const uint32_t *__restrict__ E_dev, uint32_t *__restrict__ tile_key,
-                                              uint32_t *__restrict__ entry_val, uint32_t *__restrict__ emit_prim) {
+                                              uint32_t *__restrict__ entry_val, uint32_t *__restrict__ emit_prim,
+                                              uint32_t *__restrict__ hist0, int nblk) {
   __shared__ uint32_t s_off[EMIT_TILE];
   __shared__ uint32_t s_id[EMIT_TILE];
   __shared__ ushort4 s_rect[EMIT_TILE];
   __shared__ int s_own[EMIT_TILE];
   __shared__ int s_wmax[8];
   __shared__ int s_j0, s_cnt;
+  __shared__ uint32_t s_h0[RADIX];   // hist0: this block's low-byte tile-id histogram
   const int64_t E = item_count(E_dev, capacity);
   const int64_t e0 = (int64_t)blockIdx.x * EMIT_TILE;
-  if (e0 >= E) return;
+  if (hist0) s_h0[threadIdx.x] = 0u;   // blockDim == RADIX
+  if (e0 >= E) {
+    if (hist0) hist0[(size_t)threadIdx.x * nblk + blockIdx.x] = 0u;
+    return;
+  }
   const int64_t e1 = e0 + EMIT_TILE < E ? e0 + EMIT_TILE : E;
   const int n = (int)item_count(n_dev, n_host);
   if (threadIdx.x < 64) {   // warp 0 finds the first primitive of the range, warp 1 the last
@@ -445,13 +452,19 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ order
     const uint32_t rw = (uint32_t)r.z - r.x + 1;
     const uint32_t ty = r.y + k / rw, tx = r.x + k % rw;
     LP_CHECK(tx <= r.z && ty <= r.w && (int64_t)e < capacity);
-    tile_key[e] = ty * (uint32_t)tiles_x + tx;
+    const uint32_t tk = ty * (uint32_t)tiles_x + tx;
+    tile_key[e] = tk;
+    if (hist0) atomicAdd(&s_h0[tk & 0xFFu], 1u);
     if (emit_prim) {            // deterministic frames: the sort carries the emission index
       entry_val[e] = (uint32_t)e;
       emit_prim[e] = s_id[lo];
     } else {
       entry_val[e] = s_id[lo];
     }
+  }
+  if (hist0) {   // the first tile-sort pass's histogram column of this block (k_radix_hist not launched)
+    __syncthreads();
+    hist0[(size_t)threadIdx.x * nblk + blockIdx.x] = s_h0[threadIdx.x];
   }
 }
 
@@ -473,12 +486,15 @@ void launch_det_fixup(const lp_frame &F, uint32_t *sorted_val, cudaStream_t st) 
   k_det_fixup<<<148 * 8, 256, 0, st>>>(sorted_val, F.emit_prim, F.emit_pos, F.counters + LP_CNT_ENTRIES, F.capacity);
 }
 
-void launch_emit(const lp_frame &F, int n, const uint32_t *n_dev, int64_t max_entries, cudaStream_t st) {
-  if (n == 0 || max_entries <= 0) return;
+bool launch_emit(const lp_frame &F, int n, const uint32_t *n_dev, int64_t max_entries, bool hist0, cudaStream_t st) {
+  static_assert(EMIT_TILE == SORT_TILE && RADIX == 256, "an emission block is a radix block");
+  if (n == 0 || max_entries <= 0) return false;
   const int64_t grid = (max_entries + EMIT_TILE - 1) / EMIT_TILE;
   k_emit<<<(unsigned)grid, 256, 0, st>>>(F.prim_order, F.offsets, reinterpret_cast<const ushort4 *>(F.rect), n, n_dev,
                                          F.tiles_x, F.capacity, F.counters + LP_CNT_ENTRIES, F.tile_key, F.entry_val,
-                                         F.deterministic ? F.emit_prim : nullptr);
+                                         F.deterministic ? F.emit_prim : nullptr, hist0 ? F.sort_hist : nullptr,
+                                         (int)grid);
+  return hist0;
 }
 
 // ---------------------------------------------------------------------------------------------

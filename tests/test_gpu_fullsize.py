@@ -79,6 +79,10 @@ def test_fullsize_sampled_parity(cfg, exact, view, parity_log):
     # ---- global list properties
     E = got["E"]
     assert E == int(pre.tiles_touched.astype(np.int64).sum())
+    # radix-binned frames (the default above LP_BUCKET_MAX_N primitives): the depth sort kept exactly
+    # the visible primitives (its first pass drops the others)
+    if r.frames[0].c.sort_method == 1:   # LP_SORT_RADIX
+        assert got["counters"][7] == int((pre.tiles_touched > 0).sum()) < n
     st = got["sorted_tile"].astype(np.int64)
     assert np.all(np.diff(st) >= 0)
     k64 = (st.astype(np.uint64) << np.uint64(32)) | got["depth_key"][got["sorted_val"]].astype(np.uint64)

@@ -54,6 +54,8 @@ def check_binning(got, pre, cam):
     # the full 64-bit (tile | depth) key of every entry, reconstructed
     k64 = (got["sorted_tile"].astype(np.uint64) << np.uint64(32)) | got["depth_key"][got["sorted_val"]].astype(np.uint64)
     assert np.array_equal(k64, keys)
+    c = got["counters"]
+    assert c[7] in (0, c[4]), "depth-sorted primitives = visible ones (radix method, n > 4096), else unused"
     return keys, vals, ranges
 
 
