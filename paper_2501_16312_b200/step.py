@@ -117,7 +117,8 @@ class TrainStep:
         F = self.rend.frames[0].c
         tiles = F.tiles_x * F.tiles_y
         tile_passes = math.ceil(max(1, math.ceil(math.log2(tiles))) / 8)
-        per_view = 4 * 3 + 3 + 1 + 3 * tile_passes + 1 + 1 + 1 + 1   # depth sort|scan|emit|tile sort|ranges|fwd|loss|rbwd
+        # depth sort | scan | emit | tile sort (the emission writes its first histogram) | ranges | fwd | loss | rbwd
+        per_view = 4 * 3 + 3 + 1 + (3 * tile_passes - 1) + 1 + 1 + 1 + 1
         n_pre = 2 if (self.split_pre and self.n_local > self.n_str) else math.ceil(self.n_local / 8)
         return self.n_local * per_view + n_pre + math.ceil(self.n_local / 4) + 1
 
