@@ -346,7 +346,8 @@ def run_ours(args, rank, world, local_rank):
                            None, stage_ms["pbwd_all_views"] / n_k5_launch, n_k5_launch),
         "sort": ("lp_bin_sort (K2)", "hbm", (24 + 24 * P) * per_view["E"] + 24 * n, None, stage_ms["sort"], n_local),
         "adam": ("k_adam", "hbm", (28 if args.assign else 32) * params, None, stage_ms["adam"], 1),
-        "loss": (("k_loss_ssim_tma", "alu", 206 * 3 * W * H, None, stage_ms["loss"], n_local) if args.loss == "l1ssim"
+        "loss": (("lp_loss_grad (k_ssim_maps + k_ssim_grad)", "alu", 206 * 3 * W * H, None, stage_ms["loss"], n_local)
+                 if args.loss == "l1ssim"
                  else ("k_l1_grad", "hbm", 12 * 3 * W * H, None, stage_ms["loss"], n_local)),
     }
     rooflines = {}

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 5
+#define LP_ABI_VERSION 6
 #define LP_TILE 16            /* 16 x 16 pixel tiles */
 
 typedef enum {
@@ -261,15 +261,19 @@ lp_status lp_filter3d(const float *pos, int32_t n, const lp_camera *cams_dev, in
 
 /* f1 (#25): the 3DGS loss L = (1 - lambda) L1 + lambda (1 - SSIM) of
  * n_planes fp32 image planes [n_planes][height][width] (n_views * 3 channels, CHW per view) and its
- * gradient, in one kernel.  SSIM: 11 x 11 Gaussian window (sigma 1.5) with zero padding,
- * C1 = 0.01^2, C2 = 0.03^2.
+ * gradient.  SSIM: 11 x 11 Gaussian window (sigma 1.5) with zero padding, C1 = 0.01^2, C2 = 0.03^2.
  * dL_dimage = scale * [(1 - lambda) sign(x - y) - lambda dSumS/dx] (written, not accumulated);
  * loss_sum[0] += scale * sum_p [(1 - lambda)|x_p - y_p| + lambda (1 - S_p)] (device float).
  * scale = 1 / (3 H W n_views) makes both the mean over views of the per-view losses.
- * lambda = 0 reduces to lp_l1_grad. */
+ * lambda = 0 reduces to lp_l1_grad.
+ * workspace: NULL, or device fp32 scratch of 3 * n_planes * height * width floats (16-byte aligned,
+ * caller-owned, contents undefined on return): with it (and width % 4 == 0) the loss runs as two
+ * kernels -- the SSIM maps on each 32 x 32 tile's core into the workspace, then their window sums --
+ * instead of one kernel that recomputes the maps on a 42 x 42 halo region per tile; dL_dimage is
+ * bitwise the same either way, loss_sum differs only in fp32 summation order. */
 lp_status lp_loss_grad(const float *image, const float *target, float *dL_dimage, float *loss_sum,
                        int32_t n_planes, int32_t height, int32_t width, float lambda, float scale,
-                       void *stream);
+                       float *workspace, void *stream);
 
 /* C5 input staging (not part of the method): training images arrive as 8-bit channels (the
  * datasets' PNG / JPEG targets); dst[i] = src[i] / 255 (IEEE fp32 division, so bitwise

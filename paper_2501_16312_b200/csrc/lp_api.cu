@@ -392,11 +392,11 @@ lp_status lp_filter3d(const float *pos, int32_t n, const lp_camera *cams_dev, in
 }
 
 lp_status lp_loss_grad(const float *image, const float *target, float *dL_dimage, float *loss_sum, int32_t n_planes,
-                       int32_t height, int32_t width, float lambda, float scale, void *stream) {
+                       int32_t height, int32_t width, float lambda, float scale, float *workspace, void *stream) {
   if (!image || !target || !dL_dimage || !loss_sum || n_planes < 0 || height < 0 || width < 0 || n_planes > 65535 ||
       !(lambda >= 0.f && lambda <= 1.f))
     return LP_ERR_ARG;
-  launch_loss_ssim(image, target, dL_dimage, loss_sum, n_planes, height, width, lambda, scale,
+  launch_loss_ssim(image, target, dL_dimage, loss_sum, n_planes, height, width, lambda, scale, workspace,
                    static_cast<cudaStream_t>(stream));
   return last_error();
 }

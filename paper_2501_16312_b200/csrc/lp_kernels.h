@@ -70,8 +70,9 @@ void launch_l1_grad(const float *img, const float *tgt, float *dL, float *loss, 
 void launch_filter3d(const float *pos, int n, const lp_camera *cams, int nc, float kappa, float *out,
                      cudaStream_t st);
 // f1 (lp_loss.cu): fused L1 + SSIM loss and gradient over n_planes [H][W] planes
+// ws (nullable): [3][n_planes][H][W] fp32 G-map workspace -> the two-kernel split path
 void launch_loss_ssim(const float *img, const float *tgt, float *dL, float *loss_sum, int n_planes, int H, int W,
-                      float lam, float scale, cudaStream_t st);
+                      float lam, float scale, float *ws, cudaStream_t st);
 void launch_image_from_u8(const uint8_t *src, float *dst, int64_t n, cudaStream_t st);
 void launch_adam(float *p, float *g, float *m, float *v, const lp_adam_group *groups, int ng, float b1,
                  float b2, float eps, int step, bool zero_grad, cudaStream_t st);

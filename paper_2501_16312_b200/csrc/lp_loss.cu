@@ -1,5 +1,6 @@
 // lp_loss.cu -- f1: the 3DGS training loss L = (1 - lam) L1 + lam (1 - SSIM) and its image gradient
-// in ONE kernel (reading 25).
+// (reading 25): one fused kernel, or (given a workspace) the split pair
+// k_ssim_maps + k_ssim_grad at the end of this file.
 //
 // SSIM uses an 11 x 11 Gaussian window (sigma 1.5) with zero padding.  With m = w*x, e = w*(xx),
 // w* the zero-padded window sum, the map S depends on x through m_x, e_xx, e_xy only, and
@@ -564,7 +565,317 @@ __global__ void __launch_bounds__(LT, 2) k_loss_ssim_tma(const __grid_constant__
 }
 
 
-static bool make_box_map(CUtensorMap *map, const float *base, int planes, int H, int W) {
+// ---------------------------------------------------------------------------------------------
+// Split variant (two TMA-fed persistent kernels, with a workspace for the three G maps): the fused
+// kernel above forms S and the G maps on the 42 x 42 region its core's gradient needs (the window
+// sums of the five products on 52 x 42, halo included) -- 1.7x the core.  Here k_ssim_maps forms
+// them on the 32 x 32 core only (window sums on 42 x 32) and stores G_m, G_xy, G_xx to the workspace;
+// k_ssim_grad reads them back with their 5-pixel halo (zero outside the image: the tensor map's OOB
+// fill, exactly the fused kernel's zero padding) and runs the window on them.  Every output is the
+// same sequence of fp32 operations as in the fused kernel (bitwise the same dL/dx); the workspace
+// round trip costs 24 B per pixel-channel of (mostly L2) traffic.
+// ---------------------------------------------------------------------------------------------
+namespace {
+constexpr int SBW = 48;              // box width: columns tx0 - 8 .. tx0 + 39 (16-byte aligned start)
+constexpr int SBX = 3;               // box column of window column 0 (tx0 - 5)
+constexpr int SBF = SBW * RA;        // 2016 floats = 8064 B (63 x 128 B): rows ty0 - 5 .. ty0 + 36
+constexpr int SLT = 384;
+#ifndef LP_SSIM_MINB
+#define LP_SSIM_MINB 3      // resident CTAs per SM of the split kernels (59 / 72 KB shared memory)
+#endif
+struct MapsSmem {
+  float box[2][2][SBF];              // [buffer][x | y]
+  float2 h01[RA][TS];                // horizontal window sums of (x, y) on the box rows, core columns
+  float2 h23[RA][TS];                //                            (xx, yy)
+  float h4[RA][TS];                  //                            xy
+  unsigned long long bar[2];
+  int meta[2][3];
+  float red[SLT / 32];
+};
+struct GradSmem {
+  float gbox[2][3][SBF];             // [buffer][G_m | G_xy | G_xx] with the 5-pixel halo
+  float cbox[2][TS * TS];            // x | y of the current item's core (single buffer, own barrier)
+  float2 h01[RA][TS];                // horizontal window sums of (G_m, G_xy)
+  float h2[RA][TS];                  //                            G_xx
+  unsigned long long bar[2], cbar;
+  int meta[2][3];
+  float red[SLT / 32];
+};
+
+__device__ __forceinline__ void block_loss_add(float lsum, float *red, float *loss_sum, float scale) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < SLT / 32; ++w) t += red[w];
+    atomicAdd(loss_sum, scale * t);
+  }
+}
+}  // namespace
+
+// G maps (workspace [3][planes][H][W]: G_m, G_xy, G_xx) and the SSIM part of the loss
+__global__ void __launch_bounds__(SLT, LP_SSIM_MINB) k_ssim_maps(const __grid_constant__ CUtensorMap map_x,
+                                                      const __grid_constant__ CUtensorMap map_y,
+                                                      float *__restrict__ gmaps, float *__restrict__ loss_sum, int H,
+                                                      int W, int tiles_x, int tiles_per_plane, int items, float lam,
+                                                      float scale, Win win) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  MapsSmem &S = *reinterpret_cast<MapsSmem *>(smem_raw);
+  const int tid = threadIdx.x;
+  constexpr uint32_t BOX_BYTES = SBF * 4;
+  if (tid == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int item, int buf) {
+    const int plane = item / tiles_per_plane, tile = item % tiles_per_plane;
+    const int tx0 = (tile % tiles_x) * TS, ty0 = (tile / tiles_x) * TS;
+    S.meta[buf][0] = tx0;
+    S.meta[buf][1] = ty0;
+    S.meta[buf][2] = plane;
+    mbar_expect_tx(&S.bar[buf], 2 * BOX_BYTES);
+    tma_load_3d(S.box[buf][0], &map_x, tx0 - RAD - SBX, ty0 - RAD, plane, &S.bar[buf]);
+    tma_load_3d(S.box[buf][1], &map_y, tx0 - RAD - SBX, ty0 - RAD, plane, &S.bar[buf]);
+  };
+  if (tid == 0 && (int)blockIdx.x < items) issue(blockIdx.x, 0);
+  __syncthreads();
+  const size_t HW = (size_t)H * W, PHW = (size_t)(items / tiles_per_plane) * HW;
+  float lsum = 0.f;
+  uint32_t phase[2] = {0u, 0u};
+  int buf = 0;
+  for (int item = blockIdx.x; item < items; item += gridDim.x, buf ^= 1) {
+    if (tid == 0 && item + (int)gridDim.x < items) issue(item + gridDim.x, buf ^ 1);
+    mbar_wait(&S.bar[buf], phase[buf]);
+    phase[buf] ^= 1u;
+    const float *X = S.box[buf][0], *Y = S.box[buf][1];
+    const int tx0 = S.meta[buf][0], ty0 = S.meta[buf][1], plane = S.meta[buf][2];
+    // ---- horizontal window sums of the five products: 42 rows x the 32 core columns
+    {
+      constexpr int CH = 4, NCH = TS / CH;
+      for (int it = tid; it < RA * NCH; it += SLT) {
+        const int r = it / NCH, c0 = (it % NCH) * CH;
+        float2 a01[CH], a23[CH], a4p[CH / 2];   // a4p[q] = xy sums of outputs (2q + 1, 2q)
+#pragma unroll
+        for (int j = 0; j < CH; ++j) a01[j] = a23[j] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < CH / 2; ++q) a4p[q] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < CH + TAPS - 1; ++k) {
+          const float2 v01 = make_float2(X[r * SBW + SBX + c0 + k], Y[r * SBW + SBX + c0 + k]);
+          const float2 v23 = fmul2(v01, v01);
+          const float v4 = v01.x * v01.y;
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int t = k - j;
+            if (t >= 0 && t < TAPS) {
+              a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+              a23[j] = ffma2(bc(win.g[t]), v23, a23[j]);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < CH / 2; ++q) {
+            const int t = k - 2 * q;
+            if (t >= 0 && t <= TAPS) a4p[q] = ffma2(win.gp[t], bc(v4), a4p[q]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          S.h01[r][c0 + j] = a01[j];
+          S.h23[r][c0 + j] = a23[j];
+          S.h4[r][c0 + j] = (j & 1) ? a4p[j / 2].x : a4p[j / 2].y;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- vertical sums -> S and the G maps on the core, stored to the workspace
+    {
+      constexpr int CH = 4, NCH = TS / CH;
+      for (int it = tid; it < TS * NCH; it += SLT) {
+        const int c = it % TS, r0 = (it / TS) * CH;
+        float2 a01[CH], a23[CH], a4p[CH / 2];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) a01[j] = a23[j] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < CH / 2; ++q) a4p[q] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < CH + TAPS - 1; ++k) {
+          const float2 v01 = S.h01[r0 + k][c], v23 = S.h23[r0 + k][c];
+          const float v4 = S.h4[r0 + k][c];
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int t = k - j;
+            if (t >= 0 && t < TAPS) {
+              a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+              a23[j] = ffma2(bc(win.g[t]), v23, a23[j]);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < CH / 2; ++q) {
+            const int t = k - 2 * q;
+            if (t >= 0 && t <= TAPS) a4p[q] = ffma2(win.gp[t], bc(v4), a4p[q]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int gy = ty0 + r0 + j, gx = tx0 + c;
+          if (gy < H && gx < W) {
+            const float a4 = (j & 1) ? a4p[j / 2].x : a4p[j / 2].y;
+            const float mx = a01[j].x, my = a01[j].y;
+            const float vx = a23[j].x - mx * mx, vy = a23[j].y - my * my, cxy = a4 - mx * my;
+            const float A1 = 2.f * mx * my + C1, A2 = 2.f * cxy + C2;
+            const float B1 = mx * mx + my * my + C1, B2 = vx + vy + C2;
+            const float iB1 = __fdividef(1.f, B1), iB2 = __fdividef(1.f, B2);
+            const float ssim = A1 * A2 * iB1 * iB2;
+            const size_t o = (size_t)plane * HW + (size_t)gy * W + gx;
+            gmaps[o] = 2.f * my * (A2 - A1) * iB1 * iB2 - 2.f * mx * ssim * (iB1 - iB2);
+            gmaps[PHW + o] = 2.f * A1 * iB1 * iB2;
+            gmaps[2 * PHW + o] = -ssim * iB2;
+            lsum += lam * (1.f - ssim);
+          }
+        }
+      }
+    }
+    __syncthreads();   // every thread is done with box[buf] and the stage buffers
+  }
+  block_loss_add(lsum, S.red, loss_sum, scale);
+}
+
+// dL/dx from the G maps (window sums with their halo) and the L1 part of the loss
+__global__ void __launch_bounds__(SLT, LP_SSIM_MINB) k_ssim_grad(const __grid_constant__ CUtensorMap map_gm,
+                                                      const __grid_constant__ CUtensorMap map_gxy,
+                                                      const __grid_constant__ CUtensorMap map_gxx,
+                                                      const __grid_constant__ CUtensorMap map_cx,
+                                                      const __grid_constant__ CUtensorMap map_cy,
+                                                      float *__restrict__ dL, float *__restrict__ loss_sum, int H,
+                                                      int W, int tiles_x, int tiles_per_plane, int items, float lam,
+                                                      float scale, Win win) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  GradSmem &S = *reinterpret_cast<GradSmem *>(smem_raw);
+  const int tid = threadIdx.x;
+  constexpr uint32_t GBOX_BYTES = SBF * 4, CBOX_BYTES = TS * TS * 4;
+  if (tid == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    mbar_init(&S.cbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int item, int buf) {
+    const int plane = item / tiles_per_plane, tile = item % tiles_per_plane;
+    const int tx0 = (tile % tiles_x) * TS, ty0 = (tile / tiles_x) * TS;
+    S.meta[buf][0] = tx0;
+    S.meta[buf][1] = ty0;
+    S.meta[buf][2] = plane;
+    mbar_expect_tx(&S.bar[buf], 3 * GBOX_BYTES);
+    tma_load_3d(S.gbox[buf][0], &map_gm, tx0 - RAD - SBX, ty0 - RAD, plane, &S.bar[buf]);
+    tma_load_3d(S.gbox[buf][1], &map_gxy, tx0 - RAD - SBX, ty0 - RAD, plane, &S.bar[buf]);
+    tma_load_3d(S.gbox[buf][2], &map_gxx, tx0 - RAD - SBX, ty0 - RAD, plane, &S.bar[buf]);
+  };
+  if (tid == 0 && (int)blockIdx.x < items) issue(blockIdx.x, 0);
+  __syncthreads();
+  float lsum = 0.f;
+  uint32_t phase[2] = {0u, 0u}, cphase = 0u;
+  int buf = 0;
+  for (int item = blockIdx.x; item < items; item += gridDim.x, buf ^= 1) {
+    if (tid == 0 && item + (int)gridDim.x < items) issue(item + gridDim.x, buf ^ 1);
+    const int tx0 = S.meta[buf][0], ty0 = S.meta[buf][1], plane = S.meta[buf][2];
+    if (tid == 0) {   // this item's core (x, y): needed by the last stage only
+      mbar_expect_tx(&S.cbar, 2 * CBOX_BYTES);
+      tma_load_3d(S.cbox[0], &map_cx, tx0, ty0, plane, &S.cbar);
+      tma_load_3d(S.cbox[1], &map_cy, tx0, ty0, plane, &S.cbar);
+    }
+    mbar_wait(&S.bar[buf], phase[buf]);
+    phase[buf] ^= 1u;
+    const float *Gm = S.gbox[buf][0], *Gxy = S.gbox[buf][1], *Gxx = S.gbox[buf][2];
+    float *D = dL + (size_t)plane * H * W;
+    const float *X = S.cbox[0], *Y = S.cbox[1];
+    // ---- horizontal window sums of the G maps: 42 rows x the 32 core columns
+    {
+      constexpr int CH = 4, NCH = TS / CH;
+      for (int it = tid; it < RA * NCH; it += SLT) {
+        const int r = it / NCH, c0 = (it % NCH) * CH;
+        float2 a01[CH], a2p[CH / 2];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) a01[j] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < CH / 2; ++q) a2p[q] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < CH + TAPS - 1; ++k) {
+          const int bi = r * SBW + SBX + c0 + k;
+          const float2 v01 = make_float2(Gm[bi], Gxy[bi]);
+          const float v2 = Gxx[bi];
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int t = k - j;
+            if (t >= 0 && t < TAPS) a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+          }
+#pragma unroll
+          for (int q = 0; q < CH / 2; ++q) {
+            const int t = k - 2 * q;
+            if (t >= 0 && t <= TAPS) a2p[q] = ffma2(win.gp[t], bc(v2), a2p[q]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          S.h01[r][c0 + j] = a01[j];
+          S.h2[r][c0 + j] = (j & 1) ? a2p[j / 2].x : a2p[j / 2].y;
+        }
+      }
+    }
+    __syncthreads();
+    mbar_wait(&S.cbar, cphase);
+    cphase ^= 1u;
+    // ---- vertical sums on the core, combine with L1, write dL/dx
+    {
+      constexpr int CH = 4, NCH = TS / CH;
+      for (int it = tid; it < TS * NCH; it += SLT) {
+        const int c = it % TS, r0 = (it / TS) * CH;
+        float2 a01[CH], a2p[CH / 2];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) a01[j] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < CH / 2; ++q) a2p[q] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < CH + TAPS - 1; ++k) {
+          const float2 v01 = S.h01[r0 + k][c];
+          const float v2 = S.h2[r0 + k][c];
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int t = k - j;
+            if (t >= 0 && t < TAPS) a01[j] = ffma2(bc(win.g[t]), v01, a01[j]);
+          }
+#pragma unroll
+          for (int q = 0; q < CH / 2; ++q) {
+            const int t = k - 2 * q;
+            if (t >= 0 && t <= TAPS) a2p[q] = ffma2(win.gp[t], bc(v2), a2p[q]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int gy = ty0 + r0 + j, gx = tx0 + c;
+          if (gy < H && gx < W) {
+            const float a2 = (j & 1) ? a2p[j / 2].x : a2p[j / 2].y;
+            const float x = X[(r0 + j) * TS + c], y = Y[(r0 + j) * TS + c];
+            const float d = x - y;
+            const float sg = (float)((d > 0.f) - (d < 0.f));
+            const float dS = a01[j].x + y * a01[j].y + 2.f * x * a2;
+            D[(size_t)gy * W + gx] = scale * ((1.f - lam) * sg - lam * dS);
+            lsum += (1.f - lam) * fabsf(d);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  block_loss_add(lsum, S.red, loss_sum, scale);
+}
+
+static bool make_box_map(CUtensorMap *map, const float *base, int planes, int H, int W, int bw = BW, int bh = RI) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -578,7 +889,7 @@ static bool make_box_map(CUtensorMap *map, const float *base, int planes, int H,
   }
   const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)planes};
   const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * H * 4};
-  const cuuint32_t box[3] = {(cuuint32_t)BW, (cuuint32_t)RI, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(base), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -586,7 +897,7 @@ static bool make_box_map(CUtensorMap *map, const float *base, int planes, int H,
 }
 
 void launch_loss_ssim(const float *img, const float *tgt, float *dL, float *loss_sum, int n_planes, int H, int W,
-                      float lam, float scale, cudaStream_t st) {
+                      float lam, float scale, float *ws, cudaStream_t st) {
   if (n_planes <= 0 || H <= 0 || W <= 0) return;
   Win win;
   double g[TAPS], s = 0.0;
@@ -601,6 +912,31 @@ void launch_loss_ssim(const float *img, const float *tgt, float *dL, float *loss
   const bool aligned = (W % 4) == 0 && ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(tgt)) & 15) == 0;
   static const bool tma_off = getenv("LP_LOSS_NO_TMA") != nullptr;   // measurement knob
   CUtensorMap mx, my;
+  if (ws && aligned && !tma_off && (reinterpret_cast<uintptr_t>(ws) & 15) == 0) {
+    const size_t phw = (size_t)n_planes * H * W;
+    CUtensorMap m[7];
+    if (make_box_map(&m[0], img, n_planes, H, W, SBW, RA) && make_box_map(&m[1], tgt, n_planes, H, W, SBW, RA) &&
+        make_box_map(&m[2], ws, n_planes, H, W, SBW, RA) && make_box_map(&m[3], ws + phw, n_planes, H, W, SBW, RA) &&
+        make_box_map(&m[4], ws + 2 * phw, n_planes, H, W, SBW, RA) &&
+        make_box_map(&m[5], img, n_planes, H, W, TS, TS) && make_box_map(&m[6], tgt, n_planes, H, W, TS, TS)) {
+      static bool attr2 = false;
+      if (!attr2) {
+        cudaFuncSetAttribute(k_ssim_maps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MapsSmem));
+        cudaFuncSetAttribute(k_ssim_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GradSmem));
+        attr2 = true;
+      }
+      const int items = tiles_x * tiles_y * n_planes;
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int grid = items < LP_SSIM_MINB * sms ? items : LP_SSIM_MINB * sms;
+      k_ssim_maps<<<grid, SLT, sizeof(MapsSmem), st>>>(m[0], m[1], ws, loss_sum, H, W, tiles_x, tiles_x * tiles_y,
+                                                       items, lam, scale, win);
+      k_ssim_grad<<<grid, SLT, sizeof(GradSmem), st>>>(m[2], m[3], m[4], m[5], m[6], dL, loss_sum, H, W, tiles_x,
+                                                       tiles_x * tiles_y, items, lam, scale, win);
+      return;
+    }
+  }
   if (aligned && !tma_off && make_box_map(&mx, img, n_planes, H, W) && make_box_map(&my, tgt, n_planes, H, W)) {
     const size_t smem = sizeof(LossSmemT);
     static bool attr = false;

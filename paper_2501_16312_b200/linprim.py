@@ -27,7 +27,7 @@ LP_CNT_WARP_HITS, LP_CNT_TILE_HITS, LP_CNT_SORTED = 5, 6, 7
 LP_CNT_ITERATED, LP_CNT_INTERSECTED, LP_CNT_INBOX, LP_NUM_COUNTERS = 8, 10, 12, 16
 LP_SORT_BUCKET, LP_SORT_RADIX = 0, 1
 LP_FRAME_CANON, LP_FRAME_DETERMINISTIC = 1, 2
-LP_ABI_VERSION = 5            # include/linprim.h; the loaded library must match the structs below
+LP_ABI_VERSION = 6            # include/linprim.h; the loaded library must match the structs below
 
 _p = C.c_void_p
 
@@ -93,7 +93,7 @@ _sig = {
     "lp_l1_grad": (C.c_int, [_p, _p, _p, _p, C.c_int64, C.c_float, _p]),
     "lp_filter3d": (C.c_int, [_p, C.c_int32, _p, C.c_int32, C.c_float, _p, _p]),
     "lp_image_from_u8": (C.c_int, [_p, _p, C.c_int64, _p]),
-    "lp_loss_grad": (C.c_int, [_p, _p, _p, _p, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_float, _p]),
+    "lp_loss_grad": (C.c_int, [_p, _p, _p, _p, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_float, _p, _p]),
     "lp_adam_step": (C.c_int, [_p, _p, _p, _p, C.POINTER(lp_adam_group), C.c_int32, C.c_float, C.c_float,
                                C.c_float, C.c_int32, C.c_int32, _p]),
 }
@@ -211,12 +211,16 @@ def lp_filter3d(pos, n, cams_dev, n_cams, kappa, out, stream):
                                    _stream(stream)), "lp_filter3d")
 
 
-def lp_loss_grad(image, target, dL, loss_sum, lam, scale, stream):
-    """image / target / dL: contiguous [..., H, W] fp32 tensors (all leading dims are planes)."""
+def lp_loss_grad(image, target, dL, loss_sum, lam, scale, stream, workspace=None):
+    """image / target / dL: contiguous [..., H, W] fp32 tensors (all leading dims are planes);
+    workspace: None or a contiguous fp32 tensor of >= 3 * image.numel() elements (the split path)."""
     H, W = image.shape[-2], image.shape[-1]
     planes = image.numel() // (H * W) if H * W else 0
+    if workspace is not None and workspace.numel() < 3 * image.numel():
+        raise ValueError("lp_loss_grad workspace needs 3 floats per image element")
     return _check(_lib.lp_loss_grad(_ptr(image), _ptr(target), _ptr(dL), _ptr(loss_sum), planes, H, W,
-                                    C.c_float(lam), C.c_float(scale), _stream(stream)), "lp_loss_grad")
+                                    C.c_float(lam), C.c_float(scale), _ptr(workspace), _stream(stream)),
+                  "lp_loss_grad")
 
 
 def lp_adam_step(param, grad, m, v, groups, beta1, beta2, eps, step, stream, zero_grad=False):

@@ -52,6 +52,9 @@ class TrainStep:
                                     deterministic=deterministic)
         self.img = torch.empty((self.n_local, 3, H, W), dtype=torch.float32, device=dev)
         self.dL = torch.empty_like(self.img)
+        # the split L1 + SSIM path's G-map workspace, one per view (views on different streams run concurrently)
+        self.loss_ws = (torch.empty((self.n_local, 3 * 3 * H * W), dtype=torch.float32, device=dev)
+                        if loss != "l1" else None)
         self.targets = targets
         self.loss_buf = torch.zeros(loss_slots, dtype=torch.float32, device=dev)
         self.scale = 1.0 / (3.0 * W * H * n_views_total)       # mean over views of the per-view means
@@ -118,7 +121,8 @@ class TrainStep:
         tiles = F.tiles_x * F.tiles_y
         tile_passes = math.ceil(max(1, math.ceil(math.log2(tiles))) / 8)
         # depth sort | scan | emit | tile sort (the emission writes its first histogram) | ranges | fwd | loss | rbwd
-        per_view = 4 * 3 + 3 + 1 + (3 * tile_passes - 1) + 1 + 1 + 1 + 1
+        loss = 2 if (self.loss_ws is not None and self.W % 4 == 0) else 1     # the split L1 + SSIM path: 2 kernels
+        per_view = 4 * 3 + 3 + 1 + (3 * tile_passes - 1) + 1 + 1 + loss + 1
         n_pre = 2 if (self.split_pre and self.n_local > self.n_str) else math.ceil(self.n_local / 8)
         return self.n_local * per_view + n_pre + math.ceil(self.n_local / 4) + 1
 
@@ -191,7 +195,8 @@ class TrainStep:
             if self.loss_kind == "l1":
                 L_.lp_l1_grad(self.img[i], tg[i], self.dL[i], self.loss_buf[si:si + 1], self.scale, sx)
             else:
-                L_.lp_loss_grad(self.img[i], tg[i], self.dL[i], self.loss_buf[si:si + 1], self.lam, self.scale, sx)
+                L_.lp_loss_grad(self.img[i], tg[i], self.dL[i], self.loss_buf[si:si + 1], self.lam, self.scale, sx,
+                                workspace=self.loss_ws[i])
             rec(ev, 3, sx)
             L_.lp_raster_bwd(ca, self.rend.cfg, fa, self.dL[i], sx)
             rec(ev, 4, sx)

@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol(L):
 
 
 def test_abi_version_and_status_strings(L):
-    assert L.lp_abi_version() == 5
+    assert L.lp_abi_version() == 6
     assert L.lp_status_string(L.LP_OK) == "ok"
     assert "capacity" in L.lp_status_string(L.LP_ERR_CAPACITY)
 

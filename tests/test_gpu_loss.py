@@ -1,4 +1,5 @@
-"""GPU parity of the fused L1 + SSIM loss kernel (lp_loss_grad) against oracle/loss.py.
+"""GPU parity of the L1 + SSIM loss kernels (lp_loss_grad: fused, or split through a workspace;
+SURVEY §8 f1) against oracle/loss.py.
 
 Tolerances: loss within 1e-5 relative; gradient |err| <= 1e-3 |g| + 1e-5 max|g| (north_star's
 gradient bar), on sizes spanning several 32 x 32 tiles with ragged edges.
@@ -31,7 +32,8 @@ def images(V, H, W, seed):
     return x, y
 
 
-def run(x, y, lam):
+def run(x, y, lam, split=False):
+    """split: pass a G-map workspace (the two-kernel path; W % 4 == 0 only, else the fused kernel)."""
     import torch
 
     from paper_2501_16312_b200 import linprim as L
@@ -40,21 +42,36 @@ def run(x, y, lam):
     D = torch.empty_like(X)
     loss = torch.zeros(1, device="cuda")
     V, C, H, W = x.shape
-    L.lp_loss_grad(X, Y, D, loss, lam, 1.0 / (C * H * W * V), torch.cuda.current_stream())
+    ws = torch.full((3 * X.numel(),), float("nan"), device="cuda") if split else None   # garbage in: must not leak
+    L.lp_loss_grad(X, Y, D, loss, lam, 1.0 / (C * H * W * V), torch.cuda.current_stream(), workspace=ws)
     torch.cuda.synchronize()
     return float(loss.item()), D.cpu().numpy()
 
 
 @pytest.mark.parametrize("V,H,W,seed", [(1, 32, 32, 0), (1, 45, 70, 1), (2, 96, 128, 2), (1, 100, 33, 3),
-                                         (1, 7, 5, 4), (1, 470, 70, 5), (1, 217, 40, 6), (1, 252, 64, 7)])
+                                         (1, 7, 5, 4), (1, 470, 70, 5), (1, 217, 40, 6), (1, 252, 64, 7),
+                                         (1, 33, 36, 8)])
 @pytest.mark.parametrize("lam", [0.2, 1.0])
-def test_loss_and_grad_vs_oracle(V, H, W, seed, lam):
+@pytest.mark.parametrize("split", [False, True])
+def test_loss_and_grad_vs_oracle(V, H, W, seed, lam, split):
     x, y = images(V, H, W, seed)
     L_ref, G_ref = OL.batch_loss_and_grad(x.astype(np.float64), y.astype(np.float64), lam)
-    L_got, G_got = run(x, y, lam)
+    L_got, G_got = run(x, y, lam, split)
     assert abs(L_got - L_ref) <= 1e-5 * abs(L_ref), (L_got, L_ref)
     ok, worst, rep, _ = PT.grad_close("dL/dimage", G_got, G_ref)
     assert ok, rep
+
+
+@pytest.mark.parametrize("V,H,W,seed", [(1, 32, 32, 0), (2, 96, 128, 2), (1, 217, 40, 6), (1, 1060, 1600, 9),
+                                         (3, 61, 100, 10)])
+def test_split_path_is_bitwise_the_fused_kernel(V, H, W, seed):
+    """The two-kernel path (G maps through the workspace) gives the fused kernel's dL/dx bit for bit
+    (the same fp32 operations per output) and its loss within fp32 summation order."""
+    x, y = images(V, H, W, seed)
+    L0, G0 = run(x, y, 0.2, split=False)
+    L1, G1 = run(x, y, 0.2, split=True)
+    assert np.array_equal(G0, G1)
+    assert abs(L1 - L0) <= 1e-6 * abs(L0)
 
 
 def test_lambda_zero_matches_l1_kernel():

@@ -1,7 +1,7 @@
 """Per-kernel launch averages from an ncu metrics pass over ONE bench step (--profile-step):
 gpu__time_duration.sum, dram__bytes_read.sum + dram__bytes_write.sum (traffic) and
 smsp__thread_inst_executed.sum (lane instructions), averaged per launch; the lp_bin_sort kernels are
-also summed per view under "lp_bin_sort".  Output: JSON for profiles/<round>/ncu_kernels.json,
+also summed per view under "lp_bin_sort", the split loss's two kernels under "lp_loss_grad".  Output: JSON for profiles/<round>/ncu_kernels.json,
 which bench.py reads for roofline.traffic and frac_ncu_executed."""
 import collections
 import csv
@@ -54,6 +54,14 @@ def main(path, views=8):
         s[f] = int(s[f])
     s["note"] = "sum of the K2 kernels of one view (per-step totals / %d views)" % views
     out["lp_bin_sort"] = s
+    # the split L1 + SSIM loss: its two kernels per lp_loss_grad call (one call per view)
+    if "k_ssim_maps" in out and "k_ssim_grad" in out:
+        a, b = out["k_ssim_maps"], out["k_ssim_grad"]
+        out["lp_loss_grad"] = {"launches_per_step": a["launches_per_step"] + b["launches_per_step"],
+                               "duration_us": round(a["duration_us"] + b["duration_us"], 2),
+                               **{f: a[f] + b[f] for f in ("traffic_bytes", "dram_read_bytes", "dram_write_bytes",
+                                                           "thread_inst_executed")},
+                               "note": "k_ssim_maps + k_ssim_grad of one lp_loss_grad call (one view)"}
     print(json.dumps(out, indent=1, sort_keys=True))
 
 
