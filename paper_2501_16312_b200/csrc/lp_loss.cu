@@ -579,7 +579,10 @@ namespace {
 constexpr int SBW = 48;              // box width: columns tx0 - 8 .. tx0 + 39 (16-byte aligned start)
 constexpr int SBX = 3;               // box column of window column 0 (tx0 - 5)
 constexpr int SBF = SBW * RA;        // 2016 floats = 8064 B (63 x 128 B): rows ty0 - 5 .. ty0 + 36
-constexpr int SLT = 384;
+#ifndef LP_SSIM_LT
+#define LP_SSIM_LT 384
+#endif
+constexpr int SLT = LP_SSIM_LT;   // threads of the split kernels
 #ifndef LP_SSIM_MINB
 #define LP_SSIM_MINB 3      // resident CTAs per SM of the split kernels (59 / 72 KB shared memory)
 #endif

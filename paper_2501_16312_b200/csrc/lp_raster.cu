@@ -793,7 +793,9 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
         // k_det_gather
         LP_CHECK((int64_t)ej < F.capacity && id < (uint32_t)F.n);
         if (F.deterministic) F.part[((size_t)ej * 4 + w) * lp_rgs<KIND>() + lane] = sum;
-        else if (sum != 0.f) atomicAdd(F.rgrad + (size_t)id * lp_rgs<KIND>() + lane, sum);
+        // (zero column sums are added too: a branch around them diverged inside the 20 lanes and cost
+        // more issue slots than the RED traffic it saved)
+        else atomicAdd(F.rgrad + (size_t)id * lp_rgs<KIND>() + lane, sum);
       }
       __syncwarp();
     }
