@@ -386,6 +386,8 @@ def run_ours(args, rank, world, local_rank):
         freed = [torch.cuda.Event(), torch.cuda.Event()]
         loss_host = torch.zeros(args.steps, dtype=torch.float32, pin_memory=True)
         read = [torch.cuda.Event() for _ in range(args.steps)]
+        done = [torch.cuda.Event() for _ in range(args.steps)]
+        rb = torch.cuda.Stream(dev)   # the loss readback, off the step stream (no copy between two steps)
         base = total_steps + args.steps
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -404,17 +406,24 @@ def run_ours(args, rank, world, local_rank):
         losses = []
         for k in range(args.steps):
             b = k & 1
+            ts.run(base + k, t=args.warmup + args.steps + k + 1, tgt=dev_t[b], tgt_ready=copied[b])
+            freed[b].record(st)
             if k + 1 < args.steps:
+                # the next step's targets: after this step's preprocess (copies under K1 slow it by
+                # ~0.15 ms) into the buffer the previous step has released
+                cp.wait_event(ts.pre_done)
                 if k >= 1:
                     cp.wait_event(freed[1 - b])
                 copy_in(1 - b)
-            ts.run(base + k, t=args.warmup + args.steps + k + 1, tgt=dev_t[b], tgt_ready=copied[b])
-            freed[b].record(st)
-            loss_host[k:k + 1].copy_(ts.loss_buf[base + k:base + k + 1], non_blocking=True)
-            read[k].record(st)
+            done[k].record(st)
+            rb.wait_event(done[k])
+            with torch.cuda.stream(rb):
+                loss_host[k:k + 1].copy_(ts.loss_buf[base + k:base + k + 1], non_blocking=True)
+            read[k].record(rb)
             if k >= 1:
                 read[k - 1].synchronize()
                 losses.append(float(loss_host[k - 1]))
+        st.wait_stream(rb)
         e1.record(st)
         read[args.steps - 1].synchronize()
         losses.append(float(loss_host[args.steps - 1]))

@@ -85,6 +85,9 @@ class TrainStep:
         self.n_str = max(1, min(streams, n))
         self.streams = [st] + [torch.cuda.Stream(dev) for _ in range(self.n_str - 1)]
         self.fork, self.fork2 = torch.cuda.Event(), torch.cuda.Event()
+        # recorded on the main stream once the step's preprocess launches are enqueued: a caller's
+        # host -> device copies for the NEXT step wait for it (copies under K1's HBM traffic slow it)
+        self.pre_done = torch.cuda.Event()
         self.joins = [torch.cuda.Event() for _ in self.streams[1:]]
         self.aux = [torch.cuda.Stream(dev) for _ in range(self.n_str)] if split_pre else []
         self.joins_aux = [torch.cuda.Event() for _ in self.aux]
@@ -161,6 +164,7 @@ class TrainStep:
             for i in range(n_local):
                 self.fa_view[i][0] = self.fa_all[i]
         rec(S, 1, st)
+        self.pre_done.record(st)
         if len(strs) > 1 and not split:
             self.fork.record(st)
             for s_ in strs[1:]:
