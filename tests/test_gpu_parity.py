@@ -154,6 +154,31 @@ def test_empty_and_degenerate_inputs():
     full_parity(scene, cam, seed=1)
 
 
+@pytest.mark.parametrize("culled", ["all", "half"])
+def test_radix_depth_sort_drops_invisible(culled):
+    """The multi-block radix path (n > 4096): the first depth pass drops the invisible primitives and
+    the later passes, the scan and the emission run over the kept ones only (LP_CNT_SORTED); with every
+    primitive culled the list is empty and the image is the background."""
+    import torch
+
+    from paper_2501_16312_b200 import linprim as L
+    n = 6000
+    scene, cam = scenegen.small_scene(OCTA, n, seed=31, width=120, height=90)
+    behind = np.arange(n) % 2 == 0 if culled == "half" else np.ones(n, bool)
+    scene["pos"][2][behind] = -5.0
+    ds, r, img = PT.gpu_run(scene, [cam], sort_method=L.LP_SORT_RADIX, capacity=1 << 16, bg=(0.25, 0.5, 0.75))
+    got = PT.frame_arrays(r, 0, n, K_OF[OCTA])
+    pre = oracle.preprocess(oscene(scene), cam)
+    vis = int((pre.tiles_touched > 0).sum())
+    assert got["counters"][7] == vis and (vis == 0) == (culled == "all")
+    check_binning(got, pre, cam)
+    if culled == "all":
+        assert got["E"] == 0 and torch.allclose(img[0, 2], torch.full_like(img[0, 2], 0.75))
+    else:   # the same lists as the bucket path -> the same image, bit for bit
+        _, _, img_b = PT.gpu_run(scene, [cam], sort_method=L.LP_SORT_BUCKET, bg=(0.25, 0.5, 0.75))
+        assert torch.equal(img, img_b)
+
+
 def test_multi_view_call_and_accumulation():
     """Two views in one Renderer: gradients accumulate (+=) over views."""
     import torch
