@@ -583,6 +583,12 @@ constexpr int SBF = SBW * RA;        // 2016 floats = 8064 B (63 x 128 B): rows 
 #define LP_SSIM_LT 384
 #endif
 constexpr int SLT = LP_SSIM_LT;   // threads of the split kernels
+#ifndef LP_SSIM_CHA
+#define LP_SSIM_CHA 4        // outputs per thread of the horizontal (first) stage of the split kernels
+#endif
+#ifndef LP_SSIM_CHB
+#define LP_SSIM_CHB 4        // outputs per thread of the vertical (second) stage
+#endif
 #ifndef LP_SSIM_MINB
 #define LP_SSIM_MINB 3      // resident CTAs per SM of the split kernels (59 / 72 KB shared memory)
 #endif
@@ -659,7 +665,7 @@ __global__ void __launch_bounds__(SLT, LP_SSIM_MINB) k_ssim_maps(const __grid_co
     const int tx0 = S.meta[buf][0], ty0 = S.meta[buf][1], plane = S.meta[buf][2];
     // ---- horizontal window sums of the five products: 42 rows x the 32 core columns
     {
-      constexpr int CH = 4, NCH = TS / CH;
+      constexpr int CH = LP_SSIM_CHA, NCH = TS / CH;
       for (int it = tid; it < RA * NCH; it += SLT) {
         const int r = it / NCH, c0 = (it % NCH) * CH;
         float2 a01[CH], a23[CH], a4p[CH / 2];   // a4p[q] = xy sums of outputs (2q + 1, 2q)
@@ -697,7 +703,7 @@ __global__ void __launch_bounds__(SLT, LP_SSIM_MINB) k_ssim_maps(const __grid_co
     __syncthreads();
     // ---- vertical sums -> S and the G maps on the core, stored to the workspace
     {
-      constexpr int CH = 4, NCH = TS / CH;
+      constexpr int CH = LP_SSIM_CHB, NCH = TS / CH;
       for (int it = tid; it < TS * NCH; it += SLT) {
         const int c = it % TS, r0 = (it / TS) * CH;
         float2 a01[CH], a23[CH], a4p[CH / 2];
@@ -799,7 +805,7 @@ __global__ void __launch_bounds__(SLT, LP_SSIM_MINB) k_ssim_grad(const __grid_co
     const float *X = S.cbox[0], *Y = S.cbox[1];
     // ---- horizontal window sums of the G maps: 42 rows x the 32 core columns
     {
-      constexpr int CH = 4, NCH = TS / CH;
+      constexpr int CH = LP_SSIM_CHA, NCH = TS / CH;
       for (int it = tid; it < RA * NCH; it += SLT) {
         const int r = it / NCH, c0 = (it % NCH) * CH;
         float2 a01[CH], a2p[CH / 2];
@@ -835,7 +841,7 @@ __global__ void __launch_bounds__(SLT, LP_SSIM_MINB) k_ssim_grad(const __grid_co
     cphase ^= 1u;
     // ---- vertical sums on the core, combine with L1, write dL/dx
     {
-      constexpr int CH = 4, NCH = TS / CH;
+      constexpr int CH = LP_SSIM_CHB, NCH = TS / CH;
       for (int it = tid; it < TS * NCH; it += SLT) {
         const int c = it % TS, r0 = (it / TS) * CH;
         float2 a01[CH], a2p[CH / 2];

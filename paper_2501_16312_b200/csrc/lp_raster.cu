@@ -209,11 +209,15 @@ __device__ __noinline__ void write_hit_word(uint32_t *hitmask, int64_t capacity,
 // lanes, bitwise the scalar chord the backward replays).
 // EXACT: the no-ray-space variant (App. D, reading 27): per-pixel perspective rays
 // r = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1) against the record's camera-space planes.
-#ifndef LP_FWD_BLOCKS
-#define LP_FWD_BLOCKS 1      // measurement knob: resident CTAs per SM asked of the register allocator
+// LP_FWD_BLOCKS (measurement knob): resident CTAs per SM asked of the register allocator.  Unset, the
+// bound names no minimum: ptxas then allocates 64 registers (an explicit minimum of 1 gives 90)
+#ifdef LP_FWD_BLOCKS
+#define LP_FWD_BOUNDS __launch_bounds__(128, LP_FWD_BLOCKS)
+#else
+#define LP_FWD_BOUNDS __launch_bounds__(128)
 #endif
 template <int KIND, bool STATS, bool AUX, bool EXACT>
-__global__ void __launch_bounds__(128, LP_FWD_BLOCKS) k_raster_fwd(lp_frame F, lp_camera cam, lp_raster_cfg cfg,
+__global__ void LP_FWD_BOUNDS k_raster_fwd(lp_frame F, lp_camera cam, lp_raster_cfg cfg,
                                                     float *__restrict__ image, float *__restrict__ depth,
                                                     float *__restrict__ alpha) {
   constexpr int NT = 128, PPT = 2;
