@@ -100,17 +100,30 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *s
   return wbase + x - v;
 }
 
-// one block per digit: exclusive scan over the blocks of hist[d][*]; digit total -> tot[d]
-__global__ void __launch_bounds__(1024) k_radix_scan(uint32_t *__restrict__ hist, int nblk, uint32_t *__restrict__ tot) {
+// one block per digit: exclusive scan over the blocks of hist[d][*]; digit total -> tot[d].  256
+// threads, each owning SCAN_PER consecutive blocks per round (a 1024-thread block per digit spent its
+// time in the 32-warp block scan with most threads idle at these block counts)
+constexpr int SCAN_THREADS = 256, SCAN_PER = 4;
+__global__ void __launch_bounds__(SCAN_THREADS) k_radix_scan(uint32_t *__restrict__ hist, int nblk,
+                                                             uint32_t *__restrict__ tot) {
   __shared__ uint32_t s_warp[32];
   uint32_t *row = hist + (size_t)blockIdx.x * nblk;
   uint32_t carry = 0;
-  for (int base = 0; base < nblk; base += 1024) {
-    const int i = base + threadIdx.x;
-    const uint32_t v = i < nblk ? row[i] : 0;
+  for (int base = 0; base < nblk; base += SCAN_THREADS * SCAN_PER) {
+    const int i0 = base + threadIdx.x * SCAN_PER;
+    uint32_t v[SCAN_PER], s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_PER; ++k) {
+      v[k] = i0 + k < nblk ? row[i0 + k] : 0u;
+      s += v[k];
+    }
     uint32_t total;
-    const uint32_t ex = block_exclusive_scan(v, s_warp, total);
-    if (i < nblk) row[i] = carry + ex;
+    uint32_t run = carry + block_exclusive_scan(s, s_warp, total);
+#pragma unroll
+    for (int k = 0; k < SCAN_PER; ++k) {
+      if (i0 + k < nblk) row[i0 + k] = run;
+      run += v[k];
+    }
     carry += total;
   }
   if (threadIdx.x == 0) tot[blockIdx.x] = carry;
@@ -235,7 +248,7 @@ static void radix_pass(uint32_t *ki, uint32_t *vi, uint32_t *ko, uint32_t *vo, i
     k_radix_scatter<true, DROP><<<nblk, SORT_THREADS, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, hist, tot, nblk,
                                                                kept);
   } else {
-    k_radix_scan<<<RADIX, 1024, 0, st>>>(hist, nblk, tot);
+    k_radix_scan<<<RADIX, SCAN_THREADS, 0, st>>>(hist, nblk, tot);
     k_radix_scatter<false, DROP><<<nblk, SORT_THREADS, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, hist, tot, nblk,
                                                                 kept);
   }
