@@ -938,7 +938,10 @@ void launch_loss_ssim(const float *img, const float *tgt, float *dL, float *loss
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      const int grid = items < LP_SSIM_MINB * sms ? items : LP_SSIM_MINB * sms;
+#ifndef LP_SSIM_GRID
+#define LP_SSIM_GRID LP_SSIM_MINB   // persistent CTAs per SM in the grid (measurement knob)
+#endif
+      const int grid = items < LP_SSIM_GRID * sms ? items : LP_SSIM_GRID * sms;
       k_ssim_maps<<<grid, SLT, sizeof(MapsSmem), st>>>(m[0], m[1], ws, loss_sum, H, W, tiles_x, tiles_x * tiles_y,
                                                        items, lam, scale, win);
       k_ssim_grad<<<grid, SLT, sizeof(GradSmem), st>>>(m[2], m[3], m[4], m[5], m[6], dL, loss_sum, H, W, tiles_x,
