@@ -2,8 +2,9 @@
 rank's views -- host-side sequencing of C-ABI calls only (streams, events, the one collective).
 
 Per step:
-  lp_preprocess of all local views (two launches with split_pre so the first wave bins early)
-  per local view, round-robin over `streams` CUDA streams:
+  lp_preprocess of all local views (one launch for up to 8 views; two with split_pre so the first
+  `wave` views bin early)
+  per local view, round-robin over `streams` CUDA streams (default: one per view):
       lp_bin_sort -> lp_render_fwd -> lp_loss_grad (3DGS L1 + SSIM) | lp_l1_grad -> lp_raster_bwd
   lp_preprocess_bwd_assign over all local views (the step's gradient is SET: no zeroing pass)
   N > 1: ONE NCCL all_reduce(SUM) of the flat fp32 gradient (north_star; issued as ar_chunks
@@ -34,9 +35,9 @@ class TrainStep:
     `n_views_total` views (views[r::N] on rank r)."""
 
     def __init__(self, ds: render.DeviceScene, cams, n_views_total, *, targets=None, loss="l1ssim", lam=0.2,
-                 streams=4, split_pre=True, assign=True, exact=False, capacity=None, world=1, rank=0,
+                 streams=8, split_pre=False, assign=True, exact=False, capacity=None, world=1, rank=0,
                  sharded=False, extent=4.0, betas=(0.9, 0.999), eps=1e-15, loss_slots=256, aa_kernel=None,
-                 deterministic=False, ar_chunks=4):
+                 deterministic=False, ar_chunks=4, wave=4):
         dev = ds.flat.device
         self.ds, self.dev = ds, dev
         self.n_local = len(cams)
@@ -88,6 +89,9 @@ class TrainStep:
         # recorded on the main stream once the step's preprocess launches are enqueued: a caller's
         # host -> device copies for the NEXT step wait for it (copies under K1's HBM traffic slow it)
         self.pre_done = torch.cuda.Event()
+        # recorded after the forward of the middle local view: where a caller's uploads for the NEXT step
+        # cost least (measured: right after the preprocess they slow the step's start; see bench.py)
+        self.mid_done = torch.cuda.Event()
         self.joins = [torch.cuda.Event() for _ in self.streams[1:]]
         self.aux = [torch.cuda.Stream(dev) for _ in range(self.n_str)] if split_pre else []
         self.joins_aux = [torch.cuda.Event() for _ in self.aux]
@@ -100,10 +104,12 @@ class TrainStep:
         self.sort_streams = [torch.cuda.Stream(dev, priority=hi) for _ in range(n)] if streams > 1 else []
         self.sorted = [torch.cuda.Event() for _ in range(n)]
         self.joins_sort = [torch.cuda.Event() for _ in self.sort_streams]
-        ns = self.n_str
-        self.pre_cams = [rend._cams(list(range(min(ns, n)))), rend._cams(list(range(min(ns, n), n)))]
-        self.pre_frames = [render.frames_array([rend.frames[i] for i in range(min(ns, n))]),
-                           render.frames_array([rend.frames[i] for i in range(min(ns, n), n)])]
+        # split_pre: the first `wave` views are preprocessed in their own launch, so their binning starts
+        # while the second launch runs
+        ns = self.wave = min(wave, n)
+        self.pre_cams = [rend._cams(list(range(ns))), rend._cams(list(range(ns, n)))]
+        self.pre_frames = [render.frames_array([rend.frames[i] for i in range(ns)]),
+                           render.frames_array([rend.frames[i] for i in range(ns, n)])]
 
     # ------------------------------------------------------------------------------------------
     @property
@@ -126,7 +132,7 @@ class TrainStep:
         # depth sort | scan | emit | tile sort (the emission writes its first histogram) | ranges | fwd | loss | rbwd
         loss = 2 if (self.loss_ws is not None and self.W % 4 == 0) else 1     # the split L1 + SSIM path: 2 kernels
         per_view = 4 * 3 + 3 + 1 + (3 * tile_passes - 1) + 1 + 1 + loss + 1
-        n_pre = 2 if (self.split_pre and self.n_local > self.n_str) else math.ceil(self.n_local / 8)
+        n_pre = 2 if (self.split_pre and self.n_local > self.wave) else math.ceil(self.n_local / 8)
         return self.n_local * per_view + n_pre + math.ceil(self.n_local / 4) + 1
 
     # ------------------------------------------------------------------------------------------
@@ -150,9 +156,9 @@ class TrainStep:
         for i in range(n_local):
             self.fa_all[i] = self.fa_view[i][0]
         strs = [st] if serial else self.streams
-        split = not serial and self.split_pre and n_local > len(strs)
+        split = not serial and self.split_pre and n_local > self.wave
         if split:
-            nf = len(strs)
+            nf = self.wave
             L_.lp_preprocess(self.ds.prims, self.pre_cams[0], self.rend.cfg, self.pre_frames[0], st)
             self.fork.record(st)
             L_.lp_preprocess(self.ds.prims, self.pre_cams[1], self.rend.cfg, self.pre_frames[1], st)
@@ -173,7 +179,7 @@ class TrainStep:
         if early:
             for i in range(n_local):
                 ss = self.sort_streams[i]
-                ss.wait_event(self.fork if (not split or i < len(strs)) else self.fork2)
+                ss.wait_event(self.fork if (not split or i < self.wave) else self.fork2)
                 ev = events[i] if events is not None else None
                 rec(ev, 0, ss)
                 L_.lp_bin_sort(self.ca_view[i], self.fa_view[i], ss, None)
@@ -183,7 +189,7 @@ class TrainStep:
             sx = strs[i % len(strs)]
             if split:
                 sx = self.aux[i % len(self.aux)]
-                sx.wait_event(self.fork if i < len(strs) else self.fork2)
+                sx.wait_event(self.fork if i < self.wave else self.fork2)
             ca, fa = self.ca_view[i], self.fa_view[i]
             ev = events[i] if events is not None else None
             if early:
@@ -194,6 +200,8 @@ class TrainStep:
                 rec(ev, 1, sx)
             L_.lp_render_fwd(ca, self.rend.cfg, fa, self.img[i], sx)
             rec(ev, 2, sx)
+            if i == (n_local - 1) // 2:
+                self.mid_done.record(sx)
             if tgt_ready is not None:
                 sx.wait_event(tgt_ready[i])
             if self.loss_kind == "l1":

@@ -1,5 +1,6 @@
 """GPU parity of the C5 training step AS BENCH.PY TIMES IT (row a13): the
-TrainStep object (8 views over 4 streams with the split preprocess, lp_loss_grad 3DGS L1 + SSIM,
+TrainStep object (8 views, one stream each -- bench.py's default -- or over 4 streams with the split
+preprocess; lp_loss_grad 3DGS L1 + SSIM,
 lp_raster_bwd, the two-pack lp_preprocess_bwd_assign, the fused Adam with the paper's learning
 rates) against oracle/train.py.c5_step (oracle.forward -> oracle.loss -> oracle.render backward ->
 oracle.preprocess_bwd -> sum -> Adam, fp64), at reduced N and resolution, element by element:
@@ -36,8 +37,9 @@ def _small_c5(seed, n=3000, W=96, H=64):
     return scene, cams
 
 
+@pytest.mark.parametrize("streams,split_pre", [(8, False), (4, True)])   # bench's default, the split variant
 @pytest.mark.parametrize("loss", ["l1ssim", "l1"])
-def test_c5_step_vs_oracle(loss, parity_log):
+def test_c5_step_vs_oracle(loss, streams, split_pre, parity_log):
     import torch
 
     from paper_2501_16312_b200 import step as S
@@ -69,8 +71,8 @@ def test_c5_step_vs_oracle(loss, parity_log):
 
     # ---- the CUDA step, exactly as bench.py runs it
     ds = S.device_scene(scene, "cuda")
-    ts = S.TrainStep(ds, cams, len(cams), targets=torch.from_numpy(targets).cuda(), loss=loss, streams=4,
-                     split_pre=True, assign=True)
+    ts = S.TrainStep(ds, cams, len(cams), targets=torch.from_numpy(targets).cuda(), loss=loss, streams=streams,
+                     split_pre=split_pre, assign=True)
     ts.m.copy_(torch.from_numpy(m0))
     ts.v.copy_(torch.from_numpy(v0))
     p_before = ds.flat.clone()
@@ -101,7 +103,7 @@ def test_c5_step_vs_oracle(loss, parity_log):
         r["flagged"] |= PT.screen_flags(f.pre) & (f.pre.tiles_touched > 0)
     ok, worst, reports, n_cond, n_clamp = PT.check_gradients(ds.grad_dict(), g, gb, None, r["flagged"],
                                                              clamp=r["clamp"])
-    parity_log(f"c5 step ({loss})", views=len(cams), hit_prims=int(np.isfinite(r["fwd"][0].out.m_face).sum()),
+    parity_log(f"c5 step ({loss}, {streams} streams{', split' if split_pre else ''})", views=len(cams), hit_prims=int(np.isfinite(r["fwd"][0].out.m_face).sum()),
                flagged=int(r["flagged"].sum()), clamp=n_clamp, cond_elems=n_cond, worst=dict(worst, dL=worst_dl))
     assert ok, "; ".join(reports)
 
