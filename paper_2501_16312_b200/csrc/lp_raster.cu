@@ -613,14 +613,19 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
       bits &= ~(1u << bt);
       const int j = 32 * wi + bt;
       const uint32_t ej = bstart + (uint32_t)j;
-      // a pixel outside the primitive has chord <= 0; the forward stopped pixel k after last[k]
+      // a pixel outside the primitive has chord <= 0; the forward stopped pixel k after last[k].  (No
+      // vote to skip the entry: the forward set its hit bit for a pixel that had not stopped, so some
+      // pixel of the warp has ej < last.)
       bool test[PPT], any = false;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         test[k] = ej < last[k];
         any = any || test[k];
       }
-      if (!__any_sync(0xffffffffu, any)) continue;
+#ifdef LP_CHECKED
+      LP_CHECK(__any_sync(0xffffffffu, any));
+#endif
+      (void)any;
       BWD_STAT(1, 1);
 #ifdef LP_BWD_STATS
       {
