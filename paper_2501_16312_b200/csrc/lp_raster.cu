@@ -659,8 +659,10 @@ __global__ void __launch_bounds__(NT, BWD_MIN_BLOCKS(KIND, NT)) k_raster_bwd(lp_
         hk[k] = test[k] && lane_k(ch2, k) > 0.f;
         hit = hit || hk[k];
       }
+      // (hm != 0: the chord is bitwise the forward's, which set this entry's hit bit; were it 0, the
+      // entry would only add zero column sums)
       const unsigned hm = __ballot_sync(0xffffffffu, hit);
-      if (!hm) continue;
+      LP_CHECK(hm != 0u);
       BWD_STAT(2, 1);
       BWD_STAT(3, __popc(hm));
       BWD_STAT(8 + __popc(hm), 1);
