@@ -58,6 +58,18 @@ def _free_port():
     return p
 
 
+def _spawn(fn, world, out_dir, tries=3):
+    """mp.spawn on a fresh rendezvous port; a port taken between probing and binding (a race with any
+    other process on the host) is retried on a new one."""
+    for attempt in range(tries):
+        try:
+            mp.spawn(fn, args=(world, _free_port(), out_dir), nprocs=world, join=True)
+            return
+        except mp.ProcessRaisedException:
+            if attempt == tries - 1:
+                raise
+
+
 def test_shard_views():
     assert train.shard_views(8, 0, 1) == list(range(8))
     assert train.shard_views(8, 1, 2) == [1, 3, 5, 7]
@@ -78,7 +90,7 @@ def test_lr_groups_cover_every_parameter_once():
 
 def test_two_rank_gloo_allreduce_matches_single_process(tmp_path):
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    _spawn(_worker, world, str(tmp_path))
     g0 = np.load(tmp_path / "g0.npy")
     g1 = np.load(tmp_path / "g1.npy")
     assert np.array_equal(g0, g1)                          # every rank holds the same sum
@@ -145,7 +157,7 @@ def _zero_worker(rank, world, port, out_dir):
 def test_two_rank_sharded_adam_matches_allreduce_adam(tmp_path):
     """reduce-scatter + Adam on the rank's shard + all-gather == allreduce + replicated Adam."""
     world = 2
-    mp.spawn(_zero_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    _spawn(_zero_worker, world, str(tmp_path))
     p0, p1 = np.load(tmp_path / "p0.npy"), np.load(tmp_path / "p1.npy")
     assert np.array_equal(p0, p1)
     scene, cams = _scene()
@@ -194,7 +206,7 @@ def test_two_rank_chunked_allreduce_adam_matches_single(tmp_path):
     """The chunked allreduce (one async collective per chunk) with Adam per chunk on groups clipped to
     the chunk == one allreduce + Adam over the whole buffer (TrainStep's N > 1 default)."""
     world = 2
-    mp.spawn(_chunked_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    _spawn(_chunked_worker, world, str(tmp_path))
     c0, c1 = np.load(tmp_path / "c0.npy"), np.load(tmp_path / "c1.npy")
     assert np.array_equal(c0, c1)
     scene, cams = _scene()
