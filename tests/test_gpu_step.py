@@ -131,3 +131,28 @@ def test_c5_step_vs_oracle(loss, streams, split_pre, parity_log):
     assert not ((np.abs(v_g - v_o) > tol_v) & ~flag_el).any()
     # the gradient left in the buffer is the step's (assign semantics: nothing zeroes it)
     assert float(ds.grad.abs().max()) > 0
+
+
+def test_kernel_launch_claim_matches_profiler():
+    """bench.py's gpu_launches claim (TrainStep.kernel_launches() per step) equals the liblinprim
+    kernels a CUDA profiler sees in one full-size C5 step (bench's default launch configuration)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    from paper_2501_16312_b200 import linprim as L, render, step as S
+    scene, cams = scenegen.make_scene("C5", seed=0)
+    ds = S.device_scene(scene, "cuda")
+    rr = render.Renderer(ds, cams, count_stats=True)
+    tg = rr.forward().clone()
+    E = max(int(rr.counters(i)[L.LP_CNT_ENTRIES]) for i in range(len(cams)))
+    del rr
+    ts = S.TrainStep(ds, cams, len(cams), targets=tg, capacity=int(E * 1.3) + 4096, loss_slots=16)
+    for i in range(2):
+        ts.run(i)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        ts.run(5)
+        torch.cuda.synchronize()
+    ours = [e.name for e in prof.events()
+            if e.device_type == torch.autograd.DeviceType.CUDA and "lp::k_" in e.name]
+    assert len(ours) == ts.kernel_launches(), (len(ours), ts.kernel_launches())
