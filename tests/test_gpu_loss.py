@@ -74,6 +74,24 @@ def test_split_path_is_bitwise_the_fused_kernel(V, H, W, seed):
     assert abs(L1 - L0) <= 1e-6 * abs(L0)
 
 
+def test_unaligned_workspace_falls_back_to_the_fused_kernel():
+    """A workspace that is not 16-byte aligned (the TMA maps need it) runs the fused kernel: the same
+    dL/dx bit for bit."""
+    import torch
+
+    from paper_2501_16312_b200 import linprim as L
+    x, y = images(1, 96, 128, 11)
+    X, Y = torch.as_tensor(x, device="cuda"), torch.as_tensor(y, device="cuda")
+    outs = []
+    for ws in (None, torch.empty(3 * X.numel() + 1, device="cuda")[1:]):
+        D = torch.empty_like(X)
+        loss = torch.zeros(1, device="cuda")
+        L.lp_loss_grad(X, Y, D, loss, 0.2, 1.0 / X.numel(), torch.cuda.current_stream(), workspace=ws)
+        torch.cuda.synchronize()
+        outs.append(D.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+
+
 def test_lambda_zero_matches_l1_kernel():
     import torch
 
